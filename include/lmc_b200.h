@@ -1,0 +1,138 @@
+/*
+ * lmc_b200.h -- C-ABI of the B200-native LMC hot path (liblmc_b200.so).
+ *
+ * Drop-in boundary for the reference package `lmc` 0.1.0 (pure Python).  Each
+ * entry point below replaces one reference interface; the ctypes binding a
+ * maintainer would add to the reference is shown in INTEGRATION.md.
+ *
+ *   lmcg_compress / lmcg_compress_host
+ *       <- lmc.stream.lmc_compress          (pkg/src/lmc/stream.py:311-341)
+ *       <- lmc.parallel.plmc_compress       (pkg/src/lmc/parallel.py:53-103)
+ *   lmcg_decompress_plan + lmcg_decompress_run / lmcg_decompress_host
+ *       <- lmc.stream.lmc_decompress        (pkg/src/lmc/stream.py:406-423)
+ *       <- lmc.parallel.plmc_decompress     (pkg/src/lmc/parallel.py:106-128)
+ *   lmcg_validate_options
+ *       <- lmc.stream._validate_options     (pkg/src/lmc/stream.py:287-301)
+ *   lmcg_build_codebooks
+ *       <- lmc.huffman.build_codebook       (pkg/src/lmc/huffman.py:79-180), batched
+ *   lmcg_block_info
+ *       per-block (mode, bit count, record size, lengths) of the last compress:
+ *       the values lmc.stream._encode_record (stream.py:161-177) derives.
+ *
+ * Status codes map 1:1 onto the reference exception classes
+ * (pkg/src/lmc/errors.py:8-53); see LMCG_* below.  All device pointers are
+ * plain CUDA device addresses (PyTorch-owned in the Python front-end); the
+ * `cuda_stream` arguments are cudaStream_t values (0 = legacy default).
+ * Functions are reentrant per context; one context must not be used by two
+ * host threads at once.  There is no CPU fallback: without a CUDA device every
+ * compute entry point returns LMCG_ERR_CUDA.
+ */
+#ifndef LMC_B200_H
+#define LMC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes -> reference exception classes (errors.py) */
+#define LMCG_OK 0
+#define LMCG_ERR_UNSUPPORTED 1        /* UnsupportedFormatError (magic/version/short) */
+#define LMCG_ERR_CORRUPT 2            /* CorruptStreamError (any structural failure)  */
+#define LMCG_ERR_INTEGRITY 3          /* IntegrityError (payload CRC mismatch)        */
+#define LMCG_ERR_CONFIG 4             /* ConfigError (block/segment/buffer options)   */
+#define LMCG_ERR_ALIGNMENT 5          /* AlignmentError (length % element width)      */
+#define LMCG_ERR_EMPTY 6              /* EmptyInputError (empty histogram)            */
+#define LMCG_ERR_CUDA 7               /* no device / CUDA runtime failure             */
+#define LMCG_ERR_CAPACITY 8           /* caller buffer too small                      */
+#define LMCG_ERR_ARGUMENT 9           /* bad argument (NULL pointer, n < 0, ...)      */
+
+/* ElementType wire codes (types.py:24-27) */
+#define LMCG_RAW8 0
+#define LMCG_BF16 1
+#define LMCG_FP16 2
+#define LMCG_FP32 3
+
+typedef struct lmcg_ctx lmcg_ctx;
+
+/* One tensor to compress.  `data` (and `prev`) are device pointers. */
+typedef struct {
+    const void* data;      /* payload bytes, or the NEXT step when prev != NULL         */
+    const void* prev;      /* previous step: fused XOR delta (delta.py:18-47), or NULL  */
+    uint64_t nbytes;       /* payload length in bytes                                   */
+    int32_t element_type;  /* LMCG_RAW8 .. LMCG_FP32                                    */
+    int32_t delta;         /* nonzero: header FLAG_DELTA (a DeltaBuffer input)          */
+} lmcg_tensor;
+
+/* lmc_compress keyword options (stream.py:311-318). */
+typedef struct {
+    int32_t byte_group;      /* FLAG_BYTE_GROUPED                          */
+    uint32_t block_size;     /* power of two in [4096, 1048576]            */
+    uint32_t segment_count;  /* >= 1                                       */
+    uint32_t reserved;       /* must be 0                                  */
+    uint64_t buffer_size;    /* window bytes, >= block_size, % width == 0  */
+} lmcg_options;
+
+lmcg_ctx* lmcg_create(int device);
+void lmcg_destroy(lmcg_ctx* ctx);
+const char* lmcg_last_error(lmcg_ctx* ctx);
+int lmcg_version(void); /* stream format version written (1) */
+
+/* stream.py:287-301 plus the TensorBuffer alignment check (types.py:85-90). */
+int lmcg_validate_options(const lmcg_options* opts, int element_type, uint64_t nbytes);
+
+/* Exact upper bound of the packed output of lmcg_compress for these tensors. */
+uint64_t lmcg_compress_bound(const lmcg_tensor* tensors, int n, const lmcg_options* opts);
+/* Device scratch needed by lmcg_compress (pass 0/NULL workspace to let the
+ * context allocate and cache it). */
+uint64_t lmcg_compress_workspace(const lmcg_tensor* tensors, int n, const lmcg_options* opts);
+
+/* Compress n tensors into n independent LMC1 streams packed back to back in
+ * d_out.  d_offsets / d_lengths (device, n x u64) receive each stream's start
+ * and length inside d_out.  Asynchronous on cuda_stream; no host sync. */
+int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* tensors, int n, const lmcg_options* opts,
+                  void* d_out, uint64_t out_capacity, uint64_t* d_offsets, uint64_t* d_lengths,
+                  void* d_workspace, uint64_t workspace_bytes, void* cuda_stream);
+
+/* Decompress, phase 1: parse and validate n device-resident streams
+ * (stream.py:114-142, 358-389).  Synchronises cuda_stream.  Per stream it
+ * returns the original length, element type code, flags and a status
+ * (LMCG_OK, or the error the reference would raise).  The parsed plan stays
+ * in the context for lmcg_decompress_run. */
+int lmcg_decompress_plan(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* stream_lengths,
+                         int n, uint64_t* h_orig_lengths, int32_t* h_element_types, int32_t* h_flags,
+                         int32_t* h_status, void* cuda_stream);
+
+/* Decompress, phase 2: decode the planned streams.  Stream i's payload is
+ * written to d_out + h_out_offsets[i] (capacity h_orig_lengths[i]).  On return
+ * (synchronised) h_status[i] holds LMCG_OK / LMCG_ERR_CORRUPT /
+ * LMCG_ERR_INTEGRITY / LMCG_ERR_UNSUPPORTED per stream. */
+int lmcg_decompress_run(lmcg_ctx* ctx, void* d_out, const uint64_t* h_out_offsets, int32_t* h_status,
+                        void* cuda_stream);
+
+/* Host-buffer conveniences (the call a ctypes binding in lmc.stream makes):
+ * host -> device copy, the GPU path above, device -> host copy. */
+int lmcg_compress_host(lmcg_ctx* ctx, const void* data, uint64_t nbytes, int element_type, int delta,
+                       const lmcg_options* opts, void* out, uint64_t out_capacity, uint64_t* out_len);
+int lmcg_decompress_host(lmcg_ctx* ctx, const void* stream, uint64_t len, void* out, uint64_t out_capacity,
+                         uint64_t* out_len, int32_t* element_type, int32_t* flags);
+
+/* Stage level: code lengths for nhist 256-bin histograms (device u32 [nhist][256]
+ * -> device u8 [nhist][256]); identical to build_codebook including the
+ * package-merge fallback and its tie rules.  Empty histograms yield all zeros
+ * and LMCG_ERR_EMPTY. */
+int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint8_t* d_lengths,
+                         void* cuda_stream);
+
+/* Per-block diagnostics of the most recent lmcg_compress on this context, in
+ * global block order (streams, then windows, then blocks).  Host arrays of
+ * capacity `cap` blocks; any pointer may be NULL.  Returns the block count. */
+int64_t lmcg_block_info(lmcg_ctx* ctx, int32_t* modes, uint32_t* bits, uint32_t* record_sizes,
+                        uint8_t* codebook_wire /* cap x 128 */, uint32_t* pm_flags, int64_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMC_B200_H */

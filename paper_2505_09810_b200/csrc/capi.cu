@@ -1,0 +1,623 @@
+// capi.cu -- extern "C" boundary of liblmc_b200.so (include/lmc_b200.h) and
+// the host orchestration of the compress / decompress kernel pipelines.
+//
+// Single translation unit: the kernels live in compress.cu / decompress.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/lmc_b200.h"
+#include "compress.cu"
+#include "decompress.cu"
+
+using namespace lmcg;
+
+struct lmcg_ctx {
+    int device = 0;
+    std::string err;
+    CrcTables* d_crc = nullptr;
+    // device workspace (grow-only)
+    uint8_t* ws = nullptr;
+    size_t ws_cap = 0;
+    // pinned staging for descriptors
+    uint8_t* pin = nullptr;
+    size_t pin_cap = 0;
+    cudaEvent_t pin_done = nullptr;
+    // last compress (block_info)
+    uint64_t last_nb = 0;
+    const BlockMeta* last_meta = nullptr;
+    const uint8_t* last_wire = nullptr;
+    // host convenience buffers
+    uint8_t* d_in = nullptr;
+    size_t d_in_cap = 0;
+    uint8_t* d_out = nullptr;
+    size_t d_out_cap = 0;
+    // decompress plan
+    std::vector<DecStreamIn> din;
+    std::vector<DecStreamHdr> dhdr;
+    std::vector<DecStreamPlan> dplan;
+    uint8_t* dws = nullptr;   // decompress workspace
+    size_t dws_cap = 0;
+    uint64_t nwin_t = 0, nseg_t = 0, nrec_t = 0, nchunk_t = 0, ntile_t = 0, scratch_t = 0;
+    uint32_t irr_cap = 1u << 16;
+    bool planned = false;
+};
+
+namespace {
+
+int fail(lmcg_ctx* c, int code, const char* fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+    }
+    return code;
+}
+
+#define CK(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) return fail(ctx, LMCG_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+int width_of(int et) { return et == 0 ? 1 : (et == 3 ? 4 : 2); }
+
+// ---- host CRC tables
+uint32_t h_multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = b & 1 ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return p;
+}
+
+void build_crc_tables(CrcTables& t) {
+    for (uint32_t i = 0; i < 256; i++) {
+        uint32_t c = i;
+        for (int k = 0; k < 8; k++) c = (c & 1) ? (c >> 1) ^ 0xEDB88320u : c >> 1;
+        t.slice[0][i] = c;
+    }
+    for (int k = 1; k < 4; k++)
+        for (int i = 0; i < 256; i++) t.slice[k][i] = (t.slice[k - 1][i] >> 8) ^ t.slice[0][t.slice[k - 1][i] & 0xFF];
+    t.x2n[0] = 1u << 30;  // x^1
+    for (int k = 1; k < 64; k++) t.x2n[k] = h_multmodp(t.x2n[k - 1], t.x2n[k - 1]);
+    for (int lvl = 0; lvl < 8; lvl++) {
+        const uint64_t nbytes = 64ull << lvl;
+        // x^(8 nbytes)
+        uint32_t p = 1u << 31;
+        uint64_t n = nbytes;
+        int k = 3;
+        while (n) {
+            if (n & 1) p = h_multmodp(t.x2n[k & 63], p);
+            n >>= 1;
+            k++;
+        }
+        for (int byte = 0; byte < 4; byte++)
+            for (uint32_t b = 0; b < 256; b++) {
+                const uint32_t c = b << (8 * byte);
+                t.shift[lvl][byte][b] = c ? h_multmodp(p, c) : 0;
+            }
+    }
+}
+
+int ensure_ctx(lmcg_ctx* ctx) {
+    CK(cudaSetDevice(ctx->device));
+    return LMCG_OK;
+}
+
+int grow(lmcg_ctx* ctx, uint8_t** buf, size_t* cap, size_t need) {
+    if (need <= *cap) return LMCG_OK;
+    if (*buf) {
+        CK(cudaDeviceSynchronize());
+        CK(cudaFree(*buf));
+        *buf = nullptr;
+        *cap = 0;
+    }
+    size_t n = std::max<size_t>(need, 1 << 20);
+    n = n + n / 4;
+    CK(cudaMalloc(buf, n));
+    *cap = n;
+    return LMCG_OK;
+}
+
+int grow_pinned(lmcg_ctx* ctx, size_t need) {
+    if (ctx->pin_done) CK(cudaEventSynchronize(ctx->pin_done));
+    if (need <= ctx->pin_cap) return LMCG_OK;
+    if (ctx->pin) CK(cudaFreeHost(ctx->pin));
+    size_t n = std::max<size_t>(need, 1 << 16);
+    n = n + n / 4;
+    CK(cudaMallocHost(&ctx->pin, n));
+    ctx->pin_cap = n;
+    return LMCG_OK;
+}
+
+struct Arena {
+    size_t off = 0;
+    template <class T>
+    size_t take(size_t count) {
+        off = (off + 255) & ~size_t(255);
+        size_t o = off;
+        off += count * sizeof(T);
+        return o;
+    }
+};
+
+bool host_valid_block(uint64_t b) { return b >= 4096 && b <= (1u << 20) && (b & (b - 1)) == 0; }
+
+// ---------------------------------------------------------------- compress plan
+struct CPlan {
+    std::vector<StreamDesc> streams;
+    std::vector<WinDesc> wins;
+    uint64_t nb = 0, nslots = 0;
+    uint32_t min_w = 4;
+};
+
+void make_plan(const lmcg_tensor* t, int n, const lmcg_options* o, CPlan& P) {
+    const uint64_t B = o->block_size, buf = o->buffer_size;
+    P.streams.resize(n);
+    for (int i = 0; i < n; i++) {
+        StreamDesc& sd = P.streams[i];
+        const int width = width_of(t[i].element_type);
+        const uint32_t w = o->byte_group ? width : 1;
+        sd.nbytes = t[i].nbytes;
+        sd.blk0 = P.nb;
+        sd.win0 = (uint32_t)P.wins.size();
+        sd.flags = (o->byte_group ? 1u : 0u) | ((t[i].delta || t[i].prev) ? 2u : 0u);
+        sd.et = (uint32_t)t[i].element_type;
+        uint32_t nw = 0;
+        for (uint64_t woff = 0; woff < t[i].nbytes; woff += buf) {
+            WinDesc wd;
+            wd.src = static_cast<const uint8_t*>(t[i].data) + woff;
+            wd.prev = t[i].prev ? static_cast<const uint8_t*>(t[i].prev) + woff : nullptr;
+            wd.W = std::min<uint64_t>(buf, t[i].nbytes - woff);
+            wd.w = w;
+            wd.n = wd.W / w;
+            wd.nblocks = (uint32_t)((wd.W + B - 1) / B);
+            if (w == 1) {
+                wd.nslots = wd.nblocks;
+            } else {
+                uint64_t mx = 0;
+                for (uint32_t g = 0; g < w; g++) {
+                    const uint64_t sg = (g * wd.n + B - 1) / B;
+                    const uint64_t sg1 = (g + 1 == w) ? wd.nblocks : ((g + 1) * wd.n + B - 1) / B;
+                    mx = std::max<uint64_t>(mx, sg1 - sg);
+                }
+                wd.nslots = (uint32_t)(mx * w);
+            }
+            wd.blk0 = P.nb;
+            wd.slot0 = P.nslots;
+            wd.stream = (uint32_t)i;
+            wd.win_local = nw++;
+            const bool al = ((uint64_t)wd.src % 16 == 0) && ((uint64_t)wd.prev % 16 == 0);
+            wd.vec = al && (w == 1 || wd.W % 16 == 0);
+            P.nb += wd.nblocks;
+            P.nslots += wd.nslots;
+            P.min_w = std::min(P.min_w, w);
+            P.wins.push_back(wd);
+        }
+        sd.nwin = nw;
+        sd.nblk = P.nb - sd.blk0;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int lmcg_version(void) { return 1; }
+
+lmcg_ctx* lmcg_create(int device) {
+    lmcg_ctx* ctx = new lmcg_ctx();
+    ctx->device = device;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) {
+        ctx->err = "no CUDA device";
+        return ctx;  // compute calls will fail with LMCG_ERR_CUDA
+    }
+    cudaSetDevice(device);
+    CrcTables* h = new CrcTables();
+    build_crc_tables(*h);
+    if (cudaMalloc(&ctx->d_crc, sizeof(CrcTables)) == cudaSuccess)
+        cudaMemcpy(ctx->d_crc, h, sizeof(CrcTables), cudaMemcpyHostToDevice);
+    delete h;
+    cudaEventCreateWithFlags(&ctx->pin_done, cudaEventDisableTiming);
+    return ctx;
+}
+
+void lmcg_destroy(lmcg_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->d_crc) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->d_crc);
+        if (ctx->ws) cudaFree(ctx->ws);
+        if (ctx->dws) cudaFree(ctx->dws);
+        if (ctx->d_in) cudaFree(ctx->d_in);
+        if (ctx->d_out) cudaFree(ctx->d_out);
+        if (ctx->pin) cudaFreeHost(ctx->pin);
+        if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
+    }
+    delete ctx;
+}
+
+const char* lmcg_last_error(lmcg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int lmcg_validate_options(const lmcg_options* o, int et, uint64_t nbytes) {
+    if (!o || et < 0 || et > 3) return LMCG_ERR_ARGUMENT;
+    if (!host_valid_block(o->block_size)) return LMCG_ERR_CONFIG;
+    if (o->segment_count < 1) return LMCG_ERR_CONFIG;
+    if (o->buffer_size < o->block_size) return LMCG_ERR_CONFIG;
+    if (o->buffer_size % (uint64_t)width_of(et)) return LMCG_ERR_CONFIG;
+    if (nbytes % (uint64_t)width_of(et)) return LMCG_ERR_ALIGNMENT;
+    return LMCG_OK;
+}
+
+uint64_t lmcg_compress_bound(const lmcg_tensor* t, int n, const lmcg_options* o) {
+    if (!t || !o || n < 0 || !host_valid_block(o->block_size) || o->buffer_size < o->block_size || o->segment_count < 1)
+        return 0;
+    uint64_t tot = 0;
+    const uint64_t B = o->block_size, buf = o->buffer_size;
+    for (int i = 0; i < n; i++) {
+        const uint64_t nb = t[i].nbytes;
+        const uint64_t nwin = (nb + buf - 1) / buf;
+        uint64_t blocks = 0;
+        if (nwin) blocks = (nwin - 1) * ((buf + B - 1) / B) + ((nb - (nwin - 1) * buf) + B - 1) / B;
+        tot += kHeader + nwin * kSegEntry * (uint64_t)o->segment_count + nb + 5 * blocks;
+    }
+    return tot;
+}
+
+static size_t compress_layout(const CPlan& P, int n, size_t* offs /* 16 */) {
+    Arena a;
+    const uint64_t nb = P.nb;
+    const uint64_t ntiles = nb / kScanTile + 1;
+    offs[0] = a.take<WinDesc>(P.wins.size() + 1);
+    offs[1] = a.take<StreamDesc>(n + 1);
+    offs[2] = a.take<uint32_t>(P.nslots + 1);
+    offs[3] = a.take<uint32_t>(nb * 256 + 1);
+    offs[4] = a.take<uint32_t>(nb + 1);
+    offs[5] = a.take<BlockMeta>(nb + 1);
+    offs[6] = a.take<uint8_t>(nb * 128 + 1);
+    offs[7] = a.take<uint64_t>(nb + 1);
+    offs[8] = a.take<uint64_t>(ntiles);
+    offs[9] = a.take<uint32_t>(4);   // ticket, pm_count
+    offs[10] = a.take<uint32_t>(nb + 1);
+    offs[11] = a.take<uint64_t>(n + 1);
+    offs[12] = a.take<uint64_t>(n + 1);
+    return a.off + 256;
+}
+
+uint64_t lmcg_compress_workspace(const lmcg_tensor* t, int n, const lmcg_options* o) {
+    if (!t || !o || n < 0) return 0;
+    CPlan P;
+    make_plan(t, n, o, P);
+    size_t offs[16];
+    return compress_layout(P, n, offs);
+}
+
+int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options* o, void* d_out,
+                  uint64_t out_capacity, uint64_t* d_offsets, uint64_t* d_lengths, void* d_workspace,
+                  uint64_t workspace_bytes, void* cuda_stream) {
+    if (!ctx || !o || n < 0 || (n > 0 && !t)) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+    if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
+    if (o->reserved) return fail(ctx, LMCG_ERR_ARGUMENT, "reserved option field must be 0");
+    for (int i = 0; i < n; i++) {
+        int r = lmcg_validate_options(o, t[i].element_type, t[i].nbytes);
+        if (r == LMCG_ERR_CONFIG) return fail(ctx, r, "invalid options (block %u, segments %u, buffer %llu)", o->block_size, o->segment_count, (unsigned long long)o->buffer_size);
+        if (r) return fail(ctx, r, "tensor %d: %llu bytes is not a multiple of the element width", i, (unsigned long long)t[i].nbytes);
+        if (t[i].nbytes && !t[i].data) return fail(ctx, LMCG_ERR_ARGUMENT, "tensor %d: null data", i);
+    }
+    if (int r = ensure_ctx(ctx)) return r;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (out_capacity < lmcg_compress_bound(t, n, o)) return fail(ctx, LMCG_ERR_CAPACITY, "output capacity below lmcg_compress_bound");
+    CPlan P;
+    make_plan(t, n, o, P);
+    size_t offs[16];
+    const size_t need = compress_layout(P, n, offs);
+    uint8_t* ws = static_cast<uint8_t*>(d_workspace);
+    if (!ws) {
+        if (int r = grow(ctx, &ctx->ws, &ctx->ws_cap, need)) return r;
+        ws = ctx->ws;
+    } else if (workspace_bytes < need) {
+        return fail(ctx, LMCG_ERR_CAPACITY, "workspace of %llu bytes < %llu", (unsigned long long)workspace_bytes, (unsigned long long)need);
+    }
+    WinDesc* d_wins = reinterpret_cast<WinDesc*>(ws + offs[0]);
+    StreamDesc* d_streams = reinterpret_cast<StreamDesc*>(ws + offs[1]);
+    uint32_t* d_slot2win = reinterpret_cast<uint32_t*>(ws + offs[2]);
+    uint32_t* d_hist = reinterpret_cast<uint32_t*>(ws + offs[3]);
+    uint32_t* d_crcp = reinterpret_cast<uint32_t*>(ws + offs[4]);
+    BlockMeta* d_meta = reinterpret_cast<BlockMeta*>(ws + offs[5]);
+    uint8_t* d_wire = ws + offs[6];
+    uint64_t* d_scan = reinterpret_cast<uint64_t*>(ws + offs[7]);
+    uint64_t* d_status = reinterpret_cast<uint64_t*>(ws + offs[8]);
+    uint32_t* d_ctr = reinterpret_cast<uint32_t*>(ws + offs[9]);
+    uint32_t* d_pmlist = reinterpret_cast<uint32_t*>(ws + offs[10]);
+    uint64_t* d_soff = d_offsets ? d_offsets : reinterpret_cast<uint64_t*>(ws + offs[11]);
+    uint64_t* d_slen = d_lengths ? d_lengths : reinterpret_cast<uint64_t*>(ws + offs[12]);
+    // descriptors -> device through pinned staging
+    const size_t wbytes = P.wins.size() * sizeof(WinDesc), sbytes = P.streams.size() * sizeof(StreamDesc);
+    if (int r = grow_pinned(ctx, wbytes + sbytes + 64)) return r;
+    if (wbytes) memcpy(ctx->pin, P.wins.data(), wbytes);
+    if (sbytes) memcpy(ctx->pin + wbytes, P.streams.data(), sbytes);
+    if (wbytes) CK(cudaMemcpyAsync(d_wins, ctx->pin, wbytes, cudaMemcpyHostToDevice, st));
+    if (sbytes) CK(cudaMemcpyAsync(d_streams, ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(ctx->pin_done, st));
+    const uint64_t nb = P.nb;
+    const uint64_t ntiles = (nb + kScanTile - 1) / kScanTile;
+    CK(cudaMemsetAsync(d_status, 0, (ntiles + 1) * sizeof(uint64_t), st));
+    CK(cudaMemsetAsync(d_ctr, 0, 4 * sizeof(uint32_t), st));
+    const int nwin = (int)P.wins.size();
+    if (nwin) k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win);
+    if (P.nslots) {
+        k_hist_crc<<<(unsigned)P.nslots, kThreads, 0, st>>>(d_wins, d_slot2win, P.nslots, o->block_size, ctx->d_crc,
+                                                             d_hist, d_crcp, d_meta);
+    }
+    if (nb) {
+        k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
+            d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist);
+        k_pkgmerge<<<296, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr);
+    }
+    k_scan<<<(unsigned)std::max<uint64_t>(ntiles, 1), kScanThreads, 0, st>>>(d_meta, nb, d_scan, d_status, d_ctr);
+    if (n) {
+        k_layout<<<1, 1024, 0, st>>>(d_streams, n, o->segment_count, d_scan, d_soff, d_slen);
+        k_frame<<<n, kThreads, 0, st>>>(d_streams, d_wins, o->block_size, o->segment_count, d_scan, d_crcp,
+                                         ctx->d_crc, d_soff, static_cast<uint8_t*>(d_out));
+    }
+    if (P.nslots) {
+        const uint64_t iterpos = (uint64_t)(kTileBytes / P.min_w) * kWarps;
+        const size_t smem = (size_t)((iterpos * 15) / 32 + 8) * sizeof(uint32_t);
+        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_encode<<<(unsigned)P.nslots, kThreads, smem, st>>>(d_wins, d_slot2win, P.nslots, o->block_size,
+                                                            o->segment_count, d_streams, d_meta, d_wire, d_scan, d_soff,
+                                                            static_cast<uint8_t*>(d_out));
+    }
+    CK(cudaGetLastError());
+    ctx->last_nb = nb;
+    ctx->last_meta = d_meta;
+    ctx->last_wire = d_wire;
+    return LMCG_OK;
+}
+
+int64_t lmcg_block_info(lmcg_ctx* ctx, int32_t* modes, uint32_t* bits, uint32_t* record_sizes, uint8_t* wire,
+                        uint32_t* pm_flags, int64_t cap) {
+    if (!ctx || !ctx->last_meta) return 0;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -LMCG_ERR_CUDA;
+    const uint64_t nb = ctx->last_nb;
+    std::vector<BlockMeta> m(nb);
+    if (nb && cudaMemcpy(m.data(), ctx->last_meta, nb * sizeof(BlockMeta), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return -LMCG_ERR_CUDA;
+    const uint64_t k = std::min<uint64_t>(nb, (uint64_t)std::max<int64_t>(cap, 0));
+    for (uint64_t i = 0; i < k; i++) {
+        if (modes) modes[i] = m[i].mode;
+        if (bits) bits[i] = m[i].bits;
+        if (record_sizes) record_sizes[i] = m[i].recsize;
+        if (pm_flags) pm_flags[i] = m[i].pm;
+    }
+    if (wire && k) cudaMemcpy(wire, ctx->last_wire, k * 128, cudaMemcpyDeviceToHost);
+    return (int64_t)nb;
+}
+
+int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint8_t* d_lengths, void* cuda_stream) {
+    if (!ctx || nhist < 0 || (nhist && (!d_hists || !d_lengths))) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+    if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device");
+    if (int r = ensure_ctx(ctx)) return r;
+    if (!nhist) return LMCG_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const size_t need = 256 + (size_t)nhist * 4 + 64;
+    if (int r = grow(ctx, &ctx->ws, &ctx->ws_cap, need)) return r;
+    uint32_t* d_ctr = reinterpret_cast<uint32_t*>(ctx->ws);
+    uint32_t* d_list = reinterpret_cast<uint32_t*>(ctx->ws + 256);
+    CK(cudaMemsetAsync(d_ctr, 0, 16, st));
+    k_codebook<<<(nhist + kCbWarps - 1) / kCbWarps, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
+                                                                             d_lengths, d_ctr, d_ctr + 1, d_list);
+    k_pkgmerge<<<296, 32, 0, st>>>(d_hists, d_ctr + 1, d_list, nullptr, nullptr, d_lengths);
+    CK(cudaGetLastError());
+    uint32_t flag = 0;
+    CK(cudaMemcpyAsync(&flag, d_ctr, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->last_meta = nullptr;
+    return (flag & 2u) ? LMCG_ERR_EMPTY : LMCG_OK;
+}
+
+// ------------------------------------------------------------------ decompress
+int lmcg_decompress_plan(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
+                         uint64_t* h_orig, int32_t* h_et, int32_t* h_flags, int32_t* h_status, void* cuda_stream) {
+    if (!ctx || n < 0 || (n && (!d_streams || !lens))) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+    if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
+    if (int r = ensure_ctx(ctx)) return r;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    ctx->planned = false;
+    ctx->din.resize(n);
+    for (int i = 0; i < n; i++) ctx->din[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i]};
+    ctx->dhdr.assign(n, DecStreamHdr{});
+    const size_t need = (size_t)n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr)) + 1024;
+    if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, need)) return r;
+    DecStreamIn* d_in = reinterpret_cast<DecStreamIn*>(ctx->dws);
+    DecStreamHdr* d_hdr = reinterpret_cast<DecStreamHdr*>(ctx->dws + ((n * sizeof(DecStreamIn) + 255) & ~size_t(255)));
+    if (n) {
+        CK(cudaMemcpyAsync(d_in, ctx->din.data(), n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
+        k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 1, d_hdr, nullptr, nullptr, nullptr, nullptr);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(ctx->dhdr.data(), d_hdr, n * sizeof(DecStreamHdr), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    ctx->dplan.assign(n, DecStreamPlan{});
+    uint64_t win = 0, seg = 0, rec = 0, chunk = 0, tile = 0, scr = 0;
+    for (int i = 0; i < n; i++) {
+        const DecStreamHdr& h = ctx->dhdr[i];
+        DecStreamPlan& p = ctx->dplan[i];
+        p.win0 = win; p.seg0 = seg; p.rec0 = rec; p.chunk0 = chunk; p.tile0 = tile; p.scratch = scr;
+        if (!h.status) {
+            p.nchunk = (lens[i] + kCandChunk - 1) / kCandChunk + h.nseg;
+            p.ntile = (h.orig + kOutTile - 1) / kOutTile + h.nwin;
+            win += h.nwin; seg += h.nseg; rec += h.nrec; chunk += p.nchunk; tile += p.ntile;
+            scr += ((h.orig + 15) & ~15ull) + 16ull * h.nwin;
+        }
+        if (h_orig) h_orig[i] = h.status ? 0 : h.orig;
+        if (h_et) h_et[i] = (int32_t)h.et;
+        if (h_flags) h_flags[i] = (int32_t)h.flags;
+        if (h_status) h_status[i] = (h.status & ST_UNSUPPORTED) ? LMCG_ERR_UNSUPPORTED : (h.status ? LMCG_ERR_CORRUPT : LMCG_OK);
+    }
+    ctx->nwin_t = win; ctx->nseg_t = seg; ctx->nrec_t = rec; ctx->nchunk_t = chunk; ctx->ntile_t = tile;
+    ctx->scratch_t = scr;
+    ctx->planned = true;
+    return LMCG_OK;
+}
+
+int lmcg_decompress_run(lmcg_ctx* ctx, void* d_out, const uint64_t* h_out_offsets, int32_t* h_status, void* cuda_stream) {
+    if (!ctx || !ctx->planned) return fail(ctx, LMCG_ERR_ARGUMENT, "lmcg_decompress_run without a plan");
+    if (int r = ensure_ctx(ctx)) return r;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    const int n = (int)ctx->din.size();
+    for (int attempt = 0; attempt < 4; attempt++) {
+        for (int i = 0; i < n; i++) ctx->dplan[i].out = h_out_offsets ? h_out_offsets[i] : 0;
+        Arena a;
+        const size_t o_in = a.take<DecStreamIn>(n + 1);
+        const size_t o_hdr = a.take<DecStreamHdr>(n + 1);
+        const size_t o_plan = a.take<DecStreamPlan>(n + 1);
+        const size_t o_win = a.take<DecWin>(ctx->nwin_t + 1);
+        const size_t o_wt0 = a.take<uint64_t>(ctx->nwin_t + 1);
+        const size_t o_seg = a.take<DecSeg>(ctx->nseg_t + 1);
+        const size_t o_cc = a.take<uint32_t>(ctx->nchunk_t + 1);
+        const size_t o_cp = a.take<uint32_t>((ctx->nchunk_t + 1) * kCandCap);
+        const size_t o_rec = a.take<DecRec>(ctx->nrec_t + 1);
+        const size_t o_irr = a.take<DecRec>(ctx->irr_cap);
+        const size_t o_ctr = a.take<uint32_t>(4);
+        const size_t o_st = a.take<uint32_t>(n + 1);
+        const size_t o_tc = a.take<uint32_t>(ctx->ntile_t + 1);
+        const size_t o_te = a.take<uint64_t>(ctx->ntile_t + 1);
+        const size_t o_scr = a.take<uint8_t>(ctx->scratch_t + 64);
+        // keep the parse inputs: they sit at the front of the same buffer
+        std::vector<DecStreamHdr> hdr_keep = ctx->dhdr;
+        if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, a.off + 256)) return r;
+        uint8_t* ws = ctx->dws;
+        auto* d_in = reinterpret_cast<DecStreamIn*>(ws + o_in);
+        auto* d_hdr = reinterpret_cast<DecStreamHdr*>(ws + o_hdr);
+        auto* d_plan = reinterpret_cast<DecStreamPlan*>(ws + o_plan);
+        auto* d_win = reinterpret_cast<DecWin*>(ws + o_win);
+        auto* d_wt0 = reinterpret_cast<uint64_t*>(ws + o_wt0);
+        auto* d_seg = reinterpret_cast<DecSeg*>(ws + o_seg);
+        auto* d_cc = reinterpret_cast<uint32_t*>(ws + o_cc);
+        auto* d_cp = reinterpret_cast<uint32_t*>(ws + o_cp);
+        auto* d_rec = reinterpret_cast<DecRec*>(ws + o_rec);
+        auto* d_irr = reinterpret_cast<DecRec*>(ws + o_irr);
+        auto* d_ctr = reinterpret_cast<uint32_t*>(ws + o_ctr);
+        auto* d_st = reinterpret_cast<uint32_t*>(ws + o_st);
+        auto* d_tc = reinterpret_cast<uint32_t*>(ws + o_tc);
+        auto* d_te = reinterpret_cast<uint64_t*>(ws + o_te);
+        uint8_t* d_scr = ws + o_scr;
+        const size_t hb = n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr) + sizeof(DecStreamPlan)) + 64;
+        if (int r = grow_pinned(ctx, hb)) return r;
+        uint8_t* pp = ctx->pin;
+        if (n) {
+            memcpy(pp, ctx->din.data(), n * sizeof(DecStreamIn));
+            memcpy(pp + n * sizeof(DecStreamIn), hdr_keep.data(), n * sizeof(DecStreamHdr));
+            memcpy(pp + n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr)), ctx->dplan.data(), n * sizeof(DecStreamPlan));
+            CK(cudaMemcpyAsync(d_in, pp, n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_hdr, pp + n * sizeof(DecStreamIn), n * sizeof(DecStreamHdr), cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(d_plan, pp + n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr)), n * sizeof(DecStreamPlan),
+                               cudaMemcpyHostToDevice, st));
+            CK(cudaEventRecord(ctx->pin_done, st));
+        }
+        CK(cudaMemsetAsync(d_ctr, 0, 16, st));
+        CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
+        if (n) k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 2, d_hdr, d_plan, d_win, d_seg, d_wt0);
+        if (ctx->nchunk_t)
+            k_cand<<<(unsigned)ctx->nchunk_t, 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, ctx->nchunk_t, d_cc, d_cp);
+        if (ctx->nseg_t)
+            k_link<<<(unsigned)((ctx->nseg_t + 3) / 4), 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, d_win, d_cc, d_cp, d_rec,
+                                                                       d_irr, d_ctr, ctx->irr_cap, d_st, d_scr);
+        {
+            const unsigned grid = (unsigned)std::min<uint64_t>(std::max<uint64_t>(ctx->nrec_t, 148), 148 * 8);
+            k_decode<<<grid, kThreads, 0, st>>>(d_rec, ctx->nrec_t, d_irr, d_ctr, d_st);
+        }
+        if (ctx->ntile_t)
+            k_ungroup<<<(unsigned)ctx->ntile_t, kThreads, 0, st>>>(d_win, d_wt0, ctx->nwin_t, ctx->ntile_t, d_scr,
+                                                                   static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_te, d_st);
+        if (n) k_finalize<<<n, kThreads, 0, st>>>(d_hdr, d_plan, n, d_tc, d_te, ctx->d_crc, d_st);
+        CK(cudaGetLastError());
+        std::vector<uint32_t> stv(n + 1);
+        CK(cudaMemcpyAsync(stv.data(), d_st, (n + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        bool cap = false;
+        for (int i = 0; i < n; i++) cap |= (stv[i] & ST_CAPACITY) != 0;
+        if (cap) {
+            ctx->irr_cap *= 16;
+            continue;
+        }
+        for (int i = 0; i < n; i++) {
+            const uint32_t s = hdr_keep[i].status | stv[i];
+            int32_t code = LMCG_OK;
+            if (s & ST_UNSUPPORTED) code = LMCG_ERR_UNSUPPORTED;
+            else if (s & ST_CORRUPT) code = LMCG_ERR_CORRUPT;
+            else if (s & ST_INTEGRITY) code = LMCG_ERR_INTEGRITY;
+            if (h_status) h_status[i] = code;
+        }
+        return LMCG_OK;
+    }
+    return fail(ctx, LMCG_ERR_CAPACITY, "irregular record capacity exhausted");
+}
+
+// ------------------------------------------------------------ host wrappers
+int lmcg_compress_host(lmcg_ctx* ctx, const void* data, uint64_t nbytes, int et, int delta, const lmcg_options* o,
+                       void* out, uint64_t out_capacity, uint64_t* out_len) {
+    if (!ctx || !o || (nbytes && !data) || !out || !out_len) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+    if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
+    if (int r = lmcg_validate_options(o, et, nbytes)) return fail(ctx, r, "invalid options or alignment");
+    if (int r = ensure_ctx(ctx)) return r;
+    if (int r = grow(ctx, &ctx->d_in, &ctx->d_in_cap, nbytes + 16)) return r;
+    lmcg_tensor t{ctx->d_in, nullptr, nbytes, et, delta};
+    const uint64_t bound = lmcg_compress_bound(&t, 1, o);
+    if (int r = grow(ctx, &ctx->d_out, &ctx->d_out_cap, bound + 64)) return r;
+    if (nbytes) CK(cudaMemcpy(ctx->d_in, data, nbytes, cudaMemcpyHostToDevice));
+    if (int r = lmcg_compress(ctx, &t, 1, o, ctx->d_out, ctx->d_out_cap, nullptr, nullptr, nullptr, 0, nullptr)) return r;
+    // lengths live in the workspace: recompute pointer by re-deriving the layout
+    CPlan P;
+    make_plan(&t, 1, o, P);
+    size_t offs[16];
+    compress_layout(P, 1, offs);
+    uint64_t len = 0;
+    CK(cudaMemcpy(&len, ctx->ws + offs[12], sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (len > out_capacity) return fail(ctx, LMCG_ERR_CAPACITY, "stream of %llu bytes exceeds capacity", (unsigned long long)len);
+    CK(cudaMemcpy(out, ctx->d_out, len, cudaMemcpyDeviceToHost));
+    *out_len = len;
+    return LMCG_OK;
+}
+
+int lmcg_decompress_host(lmcg_ctx* ctx, const void* stream, uint64_t len, void* out, uint64_t out_capacity,
+                         uint64_t* out_len, int32_t* et, int32_t* flags) {
+    if (!ctx || (len && !stream) || !out_len) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+    if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
+    if (int r = ensure_ctx(ctx)) return r;
+    if (int r = grow(ctx, &ctx->d_in, &ctx->d_in_cap, len + 16)) return r;
+    if (len) CK(cudaMemcpy(ctx->d_in, stream, len, cudaMemcpyHostToDevice));
+    const void* p = ctx->d_in;
+    uint64_t orig = 0;
+    int32_t e = 0, f = 0, s = 0;
+    if (int r = lmcg_decompress_plan(ctx, &p, &len, 1, &orig, &e, &f, &s, nullptr)) return r;
+    if (s) return fail(ctx, s, "stream rejected by the header/table walk");
+    *out_len = orig;
+    if (et) *et = e;
+    if (flags) *flags = f;
+    if (orig > out_capacity) return fail(ctx, LMCG_ERR_CAPACITY, "payload of %llu bytes exceeds capacity", (unsigned long long)orig);
+    if (int r = grow(ctx, &ctx->d_out, &ctx->d_out_cap, orig + 64)) return r;
+    const uint64_t off = 0;
+    if (int r = lmcg_decompress_run(ctx, ctx->d_out, &off, &s, nullptr)) return r;
+    if (s) return fail(ctx, s, s == LMCG_ERR_INTEGRITY ? "payload CRC mismatch" : "corrupt stream");
+    if (orig) CK(cudaMemcpy(out, ctx->d_out, orig, cudaMemcpyDeviceToHost));
+    return LMCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,812 @@
+// compress.cu -- B200 kernels of the LMC compress path.
+//
+//   k_slotmap    slot -> window map (planes interleaved per window)
+//   k_hist_crc   K1: fused XOR delta + byte-group gather + per-block 256-bin
+//                histogram + raw CRC-32 of the plane-0 element range
+//                (entropy.py:53-59, bytegroup.py:39-50, delta.py:18-26,
+//                stream.py:329)
+//   k_codebook   K2: per-block mode + canonical length-limited Huffman lengths
+//                (stream.py:161-177, huffman.py:79-137), one warp per block
+//   k_pkgmerge   K2b: package-merge for blocks whose Huffman tree exceeds 15
+//                bits (huffman.py:140-180), backtracking formulation
+//   k_scan       decoupled look-back exclusive scan of record sizes
+//   k_layout     per-stream totals and stream offsets in the packed output
+//   k_frame      header (with combined CRC) + segment tables (stream.py:100-111,
+//                271-284, 344-355)
+//   k_encode     K4: canonical codes + bit packing of every record straight
+//                from the source tensor (huffman.py:213-255, stream.py:161-177)
+#include "lmc_common.cuh"
+
+namespace lmcg {
+
+// ------------------------------------------------------------------ slotmap
+__global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* __restrict__ slot2win) {
+    int wi = blockIdx.x;
+    if (wi >= nwin) return;
+    const WinDesc wd = wins[wi];
+    for (uint32_t i = threadIdx.x; i < wd.nslots; i += blockDim.x) slot2win[wd.slot0 + i] = (uint32_t)wi;
+}
+
+// -------------------------------------------------------------- K1 hist+crc
+// One CTA per block slot.  Each warp owns 2 KiB warp-tiles of source bytes;
+// lane l holds bytes [64 l, 64 l + 64) of its tile, i.e. 64/w consecutive
+// grouped positions of one plane.  Fast tiles (entirely inside one plane,
+// 16-byte aligned) use 4 x 16-byte loads per lane; other tiles gather byte
+// by byte.  Plane-0 tiles also fold their full elements into the CRC.
+__global__ void __launch_bounds__(kThreads) k_hist_crc(
+    const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
+    const CrcTables* __restrict__ ct, uint32_t* __restrict__ hist_out, uint32_t* __restrict__ crc_out,
+    BlockMeta* __restrict__ meta) {
+    __shared__ uint32_t sh_hist[kWarps][256];
+    __shared__ uint32_t sh_slice[1024];
+    __shared__ uint32_t sh_part[2048];  // per-tile raw CRCs of plane-0 tiles
+    __shared__ uint16_t sh_plen[2048];  // their byte lengths (<= 2048)
+    const uint64_t slot = blockIdx.x;
+    if (slot >= nslots) return;
+    const WinDesc wd = wins[slot2win[slot]];
+    const int64_t kk = slot_to_block(wd, slot - wd.slot0, B);
+    if (kk < 0) return;
+    const uint64_t k = (uint64_t)kk;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < kWarps * 256; i += kThreads) (&sh_hist[0][0])[i] = 0;
+    for (int i = tid; i < 1024; i += kThreads) sh_slice[i] = ct->slice[i >> 8][i & 255];
+    __syncthreads();
+
+    const uint64_t p0 = k * B;
+    const uint64_t p1 = min(wd.W, p0 + B);
+    const uint32_t w = wd.w;
+    const uint64_t T = kTileBytes / w;         // positions per warp-tile
+    const uint64_t ntiles = (p1 - p0 + T - 1) / T;
+    const uint64_t crc_end = min(p1, wd.n);    // plane-0 positions of this block end here
+    uint32_t* hist = sh_hist[warp];
+
+    for (uint64_t t = warp; t < ntiles; t += kWarps) {
+        const uint64_t tp = p0 + t * T;
+        const uint64_t te = min(tp + T, p1);
+        const uint64_t g = (w == 1) ? 0 : tp / wd.n;
+        const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
+        if (fast) {
+            uint32_t v[16], s[16];
+            const uint64_t e0 = tp - g * wd.n;
+            load64(wd.src, wd.prev, e0 * w + (uint64_t)lane * kLaneBytes, v);
+            const int ns = extract_plane(v, w, (uint32_t)g, s);
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+#pragma unroll
+                for (int r = 0; r < 4; r++)
+                    if (4 * q + r < ns) atomicAdd(&hist[(s[q] >> (8 * r)) & 0xFF], 1u);
+            }
+            if (g == 0) {
+                uint32_t c = 0;
+#pragma unroll
+                for (int q = 0; q < 16; q++) c = crc_word(sh_slice, c, v[q]);
+                c = crc_warp_tree(ct, c, lane);
+                if (lane == 0) { sh_part[t] = c; sh_plen[t] = kTileBytes; }
+            }
+        } else {
+            // slow gather: lane owns positions [tp + lane*T/32, ...)
+            const uint64_t per = T / 32;
+            const uint64_t a = tp + lane * per, bnd = min(a + per, te);
+            for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p)], 1u);
+            if (tp < crc_end) {
+                // plane-0 element bytes [tp*w, min(te,n)*w): left-pad to 2 KiB with zeros
+                const uint64_t b0 = tp * w, b1 = min(te, crc_end) * w;
+                const uint64_t L = b1 - b0, Z = kTileBytes - L;
+                uint32_t c = 0;
+                const uint64_t lo = (uint64_t)lane * kLaneBytes, hi = lo + kLaneBytes;
+                for (uint64_t q = max(lo, Z); q < hi; q++) {
+                    uint64_t o = b0 + q - Z;
+                    uint32_t x = wd.src[o];
+                    if (wd.prev) x ^= wd.prev[o];
+                    c = crc_byte(sh_slice, c, x);
+                }
+                c = crc_warp_tree(ct, c, lane);
+                if (lane == 0) { sh_part[t] = c; sh_plen[t] = (uint16_t)L; }
+            }
+        }
+    }
+    __syncthreads();
+    // block histogram
+    const uint64_t b = wd.blk0 + k;
+    {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < kWarps; q++) sum += sh_hist[q][tid];
+        hist_out[b * 256 + tid] = sum;
+    }
+    if (tid == 0) {
+        if (p0 < crc_end) {
+            const uint64_t nct = (crc_end - p0 + T - 1) / T;
+            uint32_t acc = 0;
+            for (uint64_t t = 0; t < nct; t++) {
+                if (sh_plen[t] == kTileBytes) acc = crc_shift_tab(&ct->shift[5][0][0], acc);
+                else acc = crc_shift_generic(ct->x2n, acc, sh_plen[t]);
+                acc ^= sh_part[t];
+            }
+            crc_out[b] = acc;
+        }
+        BlockMeta m;
+        m.len = (uint32_t)(p1 - p0);
+        m.recsize = 0; m.bits = 0; m.mode = 0; m.sym = 0; m.pm = 0; m.pad = 0;
+        meta[b] = m;
+    }
+}
+
+// ------------------------------------------------------------ K2 codebook
+// Warp-level bitonic sort of 256 keys (8 per lane, lane-major), ascending.
+__device__ __forceinline__ void warp_bitonic_sort256(uint64_t key[8], int lane) {
+#pragma unroll
+    for (int kk = 2; kk <= 256; kk <<= 1) {
+#pragma unroll
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+            if (j >= 8) {
+                const int lj = j >> 3;
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const int i = lane * 8 + r;
+                    uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, key[r], lj);
+                    const bool up = (i & kk) == 0;
+                    const bool lower = (i & j) == 0;
+                    // lower element keeps min when ascending
+                    uint64_t mn = min(key[r], other), mx = max(key[r], other);
+                    key[r] = (lower == up) ? mn : mx;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < 8; r++) {
+                    const int partner = r ^ j;
+                    if (partner > r) {
+                        const int i = lane * 8 + r;
+                        const bool up = (i & kk) == 0;
+                        uint64_t a = key[r], c = key[partner];
+                        if ((a > c) == up) { key[r] = c; key[partner] = a; }
+                    }
+                }
+            }
+        }
+    }
+}
+
+struct CbSmem {
+    uint32_t wt[512];     // node weights (leaves sorted, then internal nodes)
+    uint16_t par[512];    // parent / ancestor
+    uint8_t dep[512];     // depth accumulator
+    uint8_t sym[256];     // leaf -> symbol
+    uint8_t lens[256];    // symbol -> code length
+};
+
+// Two-queue Huffman (huffman.py:106-137) on the sorted leaves in s.wt[0..n),
+// then leaf depths by pointer jumping.  Returns the maximum leaf depth.
+__device__ int huffman_depths_warp(CbSmem& s, int n, int lane) {
+    if (lane == 0) {
+        const int total = 2 * n - 1;
+        int leaf = 0, node = n;
+        for (int nxt = n; nxt < total; nxt++) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int q = 0; q < 2; q++) {
+                int child;
+                if (leaf < n && (node >= nxt || s.wt[leaf] <= s.wt[node])) child = leaf++;
+                else child = node++;
+                s.par[child] = (uint16_t)nxt;
+                acc += s.wt[child];
+            }
+            s.wt[nxt] = acc;
+        }
+        s.par[total - 1] = (uint16_t)(total - 1);
+    }
+    __syncwarp();
+    const int total = 2 * n - 1;
+    for (int i = lane; i < total; i += 32) s.dep[i] = (i == total - 1) ? 0 : 1;
+    __syncwarp();
+    // pointer jumping: depth(i) = hops to the root
+    for (int it = 0; it < 9; it++) {
+        uint16_t na[16]; uint8_t nd[16];
+        int c = 0;
+        for (int i = lane; i < total; i += 32, c++) {
+            const int a = s.par[i];
+            na[c] = s.par[a];
+            nd[c] = (uint8_t)(s.dep[i] + s.dep[a]);
+        }
+        __syncwarp();
+        c = 0;
+        for (int i = lane; i < total; i += 32, c++) { s.par[i] = na[c]; s.dep[i] = nd[c]; }
+        __syncwarp();
+    }
+    int mx = 0;
+    for (int i = lane; i < n; i += 32) mx = max(mx, (int)s.dep[i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    return mx;
+}
+
+// Mode, bit cost, record size and 128-byte wire codebook from s.lens
+// (stream.py:170-177, huffman.py:369-377).
+__device__ void finish_block(CbSmem& s, const uint32_t cnt[8], int lane, BlockMeta* __restrict__ meta,
+                             uint8_t* __restrict__ wire, uint64_t b) {
+    uint32_t cost = 0;
+#pragma unroll
+    for (int r = 0; r < 8; r++) cost += cnt[r] * s.lens[lane * 8 + r];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) cost += __shfl_xor_sync(0xFFFFFFFFu, cost, o);
+    const uint32_t len = meta[b].len;
+    const uint32_t hsize = kHuffOverhead + (cost + 7) / 8;
+    const bool huff = hsize <= len;
+    if (huff) {
+        uint32_t wv = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+            wv |= (uint32_t)(s.lens[lane * 8 + 2 * q] | (s.lens[lane * 8 + 2 * q + 1] << 4)) << (8 * q);
+        reinterpret_cast<uint32_t*>(wire + b * 128)[lane] = wv;
+    }
+    if (lane == 0) {
+        BlockMeta m = meta[b];
+        m.mode = huff ? MODE_HUFFMAN : MODE_STORED;
+        m.bits = cost;
+        m.recsize = huff ? 5 + hsize : 5 + len;
+        m.pm = 0;
+        meta[b] = m;
+    }
+}
+
+// Sorted (count, symbol) leaves of one histogram; returns n present.
+__device__ __forceinline__ int sorted_leaves(const uint32_t cnt[8], int lane, uint32_t* wt, uint8_t* sym) {
+    uint64_t key[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) key[r] = cnt[r] ? (((uint64_t)cnt[r] << 8) | (uint64_t)(lane * 8 + r)) : ~0ull;
+    warp_bitonic_sort256(key, lane);
+    int np = 0;
+#pragma unroll
+    for (int r = 0; r < 8; r++) np += cnt[r] ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xFFFFFFFFu, np, o);
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        const int i = lane * 8 + r;
+        if (i < np) { wt[i] = (uint32_t)(key[r] >> 8); sym[i] = (uint8_t)(key[r] & 0xFF); }
+    }
+    __syncwarp();
+    return np;
+}
+
+constexpr int kCbWarps = 4;
+// mode_only: block-level path (stream records).  For the stage-level API
+// (lmcg_build_codebooks) lens_out != null and RLE is not special-cased.
+__global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __restrict__ hist, uint64_t nb,
+                                                          BlockMeta* __restrict__ meta, uint8_t* __restrict__ wire,
+                                                          uint8_t* __restrict__ lens_out, uint32_t* __restrict__ pm_flag,
+                                                          uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list) {
+    __shared__ CbSmem sm[kCbWarps];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t b = (uint64_t)blockIdx.x * kCbWarps + warp;
+    if (b >= nb) return;
+    CbSmem& s = sm[warp];
+    uint32_t cnt[8];
+    {
+        const uint4* h4 = reinterpret_cast<const uint4*>(hist + b * 256 + lane * 8);
+        uint4 a = h4[0], c = h4[1];
+        cnt[0] = a.x; cnt[1] = a.y; cnt[2] = a.z; cnt[3] = a.w;
+        cnt[4] = c.x; cnt[5] = c.y; cnt[6] = c.z; cnt[7] = c.w;
+    }
+    uint32_t mx = 0, total = 0;
+    int arg = 0;
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+        total += cnt[r];
+        if (cnt[r] > mx) { mx = cnt[r]; arg = lane * 8 + r; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        total += __shfl_xor_sync(0xFFFFFFFFu, total, o);
+        uint32_t om = __shfl_xor_sync(0xFFFFFFFFu, mx, o);
+        int oa = __shfl_xor_sync(0xFFFFFFFFu, arg, o);
+        if (om > mx || (om == mx && oa < arg)) { mx = om; arg = oa; }
+    }
+    if (lens_out == nullptr && mx == total) {
+        // monosymbolic block -> RLE record of 6 bytes (stream.py:165-169)
+        if (lane == 0) {
+            BlockMeta m = meta[b];
+            m.mode = MODE_RLE; m.sym = (uint8_t)arg; m.recsize = 6; m.bits = 0; m.pm = 0;
+            meta[b] = m;
+        }
+        return;
+    }
+    for (int i = lane; i < 256; i += 32) s.lens[i] = 0;
+    if (total == 0) {  // empty histogram (stage-level API only)
+        __syncwarp();
+        if (lens_out) reinterpret_cast<uint2*>(lens_out + b * 256)[lane] = make_uint2(0, 0);
+        if (lane == 0 && pm_flag) atomicOr(pm_flag, 2u);
+        return;
+    }
+    const int n = sorted_leaves(cnt, lane, s.wt, s.sym);
+    if (n == 1) {
+        if (lane == 0) s.lens[s.sym[0]] = 1;  // huffman.py:89-91
+    } else {
+        const int mdep = huffman_depths_warp(s, n, lane);
+        if (mdep > kMaxLen) {
+            // package-merge fallback (huffman.py:100-101) runs in k_pkgmerge
+            if (lane == 0) {
+                if (lens_out) { if (pm_flag) atomicOr(pm_flag, 1u); }
+                else { BlockMeta m = meta[b]; m.pm = 1; meta[b] = m; }
+                pm_list[atomicAdd(pm_count, 1u)] = (uint32_t)b;
+            }
+            return;
+        }
+        for (int i = lane; i < n; i += 32) s.lens[s.sym[i]] = s.dep[i];
+    }
+    __syncwarp();
+    if (lens_out) {
+        reinterpret_cast<uint2*>(lens_out + b * 256)[lane] = reinterpret_cast<const uint2*>(s.lens)[lane];
+        return;
+    }
+    finish_block(s, cnt, lane, meta, wire, b);
+}
+
+// ------------------------------------------------------ K2b package-merge
+// Length-limited lengths by package-merge with the reference's tie rules
+// (huffman.py:140-180): packages pair items (2k, 2k+1); merge(leaves,
+// packages) puts a leaf before an equal-weight package; the code length of a
+// leaf is its multiplicity among the first 2n-2 items after 14 rounds.
+// Backtracking form: at the last level take c = 2n-2 items; the leaves among
+// them are the first l leaves; the c-l packages are made of the first
+// 2(c-l) items of the previous level; recurse to level 0.
+struct PmSmem {
+    uint64_t lw[256];        // sorted leaf weights (64-bit: packages can repeat leaves)
+    uint32_t lw32[256];
+    uint8_t sym[256];
+    uint64_t prev[512];      // level t-1 item weights
+    uint64_t cur[512];       // level t item weights
+    uint64_t pk[256];        // packages
+    uint16_t lpos[15][256];  // leaf positions per level
+    uint8_t lens[256];
+};
+
+__global__ void __launch_bounds__(32) k_pkgmerge(const uint32_t* __restrict__ hist, const uint32_t* __restrict__ pm_count,
+                                                 const uint32_t* __restrict__ pm_list, BlockMeta* __restrict__ meta,
+                                                 uint8_t* __restrict__ wire, uint8_t* __restrict__ lens_out) {
+    __shared__ PmSmem s;
+    __shared__ CbSmem cs;
+    const int lane = threadIdx.x;
+    const uint32_t npm = *pm_count;
+    for (uint32_t idx = blockIdx.x; idx < npm; idx += gridDim.x) {
+    const uint64_t b = pm_list[idx];
+    uint32_t cnt[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) cnt[r] = hist[b * 256 + lane * 8 + r];
+    const int n = sorted_leaves(cnt, lane, s.lw32, s.sym);
+    for (int i = lane; i < n; i += 32) { s.lw[i] = s.lw32[i]; s.prev[i] = s.lw32[i]; s.lpos[0][i] = (uint16_t)i; }
+    __syncwarp();
+    int m = n;
+    for (int t = 1; t < kMaxLen; t++) {
+        const int np = m / 2;
+        for (int k = lane; k < np; k += 32) s.pk[k] = s.prev[2 * k] + s.prev[2 * k + 1];
+        __syncwarp();
+        // leaf i -> i + #{packages < w_i}
+        for (int i = lane; i < n; i += 32) {
+            const uint64_t wi = s.lw[i];
+            int lo = 0, hi = np;
+            while (lo < hi) { int mid = (lo + hi) >> 1; if (s.pk[mid] < wi) lo = mid + 1; else hi = mid; }
+            const int pos = i + lo;
+            s.cur[pos] = wi;
+            s.lpos[t][i] = (uint16_t)pos;
+        }
+        // package k -> k + #{leaves <= p_k}
+        for (int k = lane; k < np; k += 32) {
+            const uint64_t pw = s.pk[k];
+            int lo = 0, hi = n;
+            while (lo < hi) { int mid = (lo + hi) >> 1; if (s.lw[mid] <= pw) lo = mid + 1; else hi = mid; }
+            s.cur[k + lo] = pw;
+        }
+        __syncwarp();
+        m = n + np;
+        for (int i = lane; i < m; i += 32) s.prev[i] = s.cur[i];
+        __syncwarp();
+    }
+    // backward pass (all lanes compute the same scalars)
+    for (int i = lane; i < 256; i += 32) s.lens[i] = 0;
+    __syncwarp();
+    int c = min(2 * n - 2, m);
+    uint8_t mylen[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int t = kMaxLen - 1; t >= 0; t--) {
+        int l;
+        if (t == 0) {
+            l = min(c, n);
+        } else {
+            // leaves among the first c items: leaf positions increase with i
+            int lo = 0, hi = n;
+            while (lo < hi) { int mid = (lo + hi) >> 1; if (s.lpos[t][mid] < c) lo = mid + 1; else hi = mid; }
+            l = lo;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; r++) if (lane + 32 * r < l) mylen[r]++;
+        c = 2 * (c - l);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; r++) if (lane + 32 * r < n) s.lens[s.sym[lane + 32 * r]] = mylen[r];
+    __syncwarp();
+    if (lens_out) {
+        reinterpret_cast<uint2*>(lens_out + b * 256)[lane] = reinterpret_cast<const uint2*>(s.lens)[lane];
+    } else {
+        for (int i = lane; i < 256; i += 32) cs.lens[i] = s.lens[i];
+        __syncwarp();
+        finish_block(cs, cnt, lane, meta, wire, b);
+    }
+    __syncwarp();
+    }
+}
+
+// --------------------------------------------------------------- scan
+// Decoupled look-back exclusive scan of meta[i].recsize -> out[i] (u64), with
+// out[n] = total.  status[] (one u64 per tile) and *ticket must be zeroed.
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr uint64_t kFlagAgg = 1ull << 62, kFlagInc = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(const BlockMeta* __restrict__ meta, uint64_t n,
+                                                       uint64_t* __restrict__ out, uint64_t* status,
+                                                       uint32_t* ticket) {
+    __shared__ uint32_t sh_tile;
+    __shared__ uint64_t sh_warp[kScanThreads / 32];
+    __shared__ uint64_t sh_prefix;
+    if (threadIdx.x == 0) sh_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint64_t tile = sh_tile;
+    const uint64_t base = tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+    uint64_t v[kScanItems], sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) {
+        v[i] = (base + i < n) ? meta[base + i].recsize : 0;
+        sum += v[i];
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint64_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) sh_warp[warp] = incl;
+    __syncthreads();
+    uint64_t wpre = 0, agg = 0;
+    for (int q = 0; q < kScanThreads / 32; q++) {
+        if (q < warp) wpre += sh_warp[q];
+        agg += sh_warp[q];
+    }
+    if (threadIdx.x == 0) {
+        if (tile == 0) {
+            st_release(&status[0], kFlagInc | agg);
+            sh_prefix = 0;
+        } else {
+            st_release(&status[tile], kFlagAgg | agg);
+            uint64_t pre = 0;
+            int64_t j = (int64_t)tile - 1;
+            while (j >= 0) {
+                uint64_t st;
+                do { st = ld_acquire(&status[j]); } while ((st >> 62) == 0);
+                pre += st & kValMask;
+                if ((st >> 62) == 2) break;
+                j--;
+            }
+            st_release(&status[tile], kFlagInc | (pre + agg));
+            sh_prefix = pre;
+        }
+    }
+    __syncthreads();
+    uint64_t run = sh_prefix + wpre + incl - sum;
+#pragma unroll
+    for (int i = 0; i < kScanItems; i++) {
+        if (base + i < n) out[base + i] = run;
+        run += v[i];
+    }
+    const uint64_t last_tile = (n == 0) ? 0 : (n - 1) / kScanTile;
+    if (tile == last_tile && threadIdx.x == kScanThreads - 1) out[n] = sh_prefix + agg;
+}
+
+// -------------------------------------------------------------- layout
+// Per-stream totals (28 + nwin*16*S + records) and their exclusive scan.
+__global__ void k_layout(const StreamDesc* __restrict__ streams, int ns, uint32_t segs,
+                         const uint64_t* __restrict__ scan, uint64_t* __restrict__ soff,
+                         uint64_t* __restrict__ slen) {
+    __shared__ uint64_t sh_carry, sh_w[32];
+    if (threadIdx.x == 0) sh_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int base = 0; base < ns; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        uint64_t tot = 0;
+        if (i < ns) {
+            const StreamDesc sd = streams[i];
+            tot = kHeader + (uint64_t)sd.nwin * kSegEntry * segs + (scan[sd.blk0 + sd.nblk] - scan[sd.blk0]);
+            slen[i] = tot;
+        }
+        uint64_t incl = tot;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint64_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) sh_w[warp] = incl;
+        __syncthreads();
+        uint64_t pre = sh_carry, all = 0;
+        for (int q = 0; q < nw; q++) { if (q < warp) pre += sh_w[q]; all += sh_w[q]; }
+        if (i < ns) soff[i] = pre + incl - tot;
+        __syncthreads();
+        if (threadIdx.x == 0) sh_carry += all;
+        __syncthreads();
+    }
+}
+
+// --------------------------------------------------------------- frame
+__device__ __forceinline__ void put_u64(uint8_t* p, uint64_t v) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) p[i] = (uint8_t)(v >> (8 * i));
+}
+__device__ __forceinline__ void put_u32(uint8_t* p, uint32_t v) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) p[i] = (uint8_t)(v >> (8 * i));
+}
+
+// One CTA per stream: combine the per-block raw CRCs into zlib.crc32 of the
+// whole payload, write the 28-byte header and every window's segment table.
+__global__ void __launch_bounds__(kThreads) k_frame(const StreamDesc* __restrict__ streams,
+                                                  const WinDesc* __restrict__ wins, uint32_t B, uint32_t segs,
+                                                  const uint64_t* __restrict__ scan, const uint32_t* __restrict__ crcpart,
+                                                  const CrcTables* __restrict__ ct, const uint64_t* __restrict__ soff,
+                                                  uint8_t* __restrict__ out) {
+    __shared__ uint32_t sh_red[kThreads];
+    const int s = blockIdx.x;
+    const StreamDesc sd = streams[s];
+    const uint64_t base = soff[s];
+    // --- CRC: sum over plane-0 parts of shift(part, bytes after part)
+    uint32_t acc = 0;
+    {
+        uint64_t after_win = sd.nbytes;  // bytes after the current window start... computed per window below
+        uint64_t woff = 0;
+        for (uint32_t wl = 0; wl < sd.nwin; wl++) {
+            const WinDesc wd = wins[sd.win0 + wl];
+            after_win = sd.nbytes - woff - wd.W;  // bytes of later windows
+            const uint64_t nparts = (wd.n + B - 1) / B;  // blocks holding plane-0 positions
+            for (uint64_t k = threadIdx.x; k < nparts; k += blockDim.x) {
+                const uint64_t e1 = min(wd.n, (k + 1) * B);
+                const uint64_t after = (wd.n - e1) * wd.w + after_win;
+                acc ^= crc_shift_generic(ct->x2n, crcpart[wd.blk0 + k], after);
+            }
+            woff += wd.W;
+        }
+    }
+    sh_red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = kThreads / 2; o; o >>= 1) {
+        if (threadIdx.x < o) sh_red[threadIdx.x] ^= sh_red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        uint32_t raw = sh_red[0];
+        uint32_t crc = raw ^ crc_shift_generic(ct->x2n, 0xFFFFFFFFu, sd.nbytes) ^ 0xFFFFFFFFu;
+        uint8_t* h = out + base;
+        h[0] = 'L'; h[1] = 'M'; h[2] = 'C'; h[3] = '1';
+        h[4] = 1; h[5] = (uint8_t)sd.flags; h[6] = (uint8_t)sd.et; h[7] = 0;
+        put_u64(h + 8, sd.nbytes);
+        put_u32(h + 16, B);
+        put_u32(h + 20, segs);
+        put_u32(h + 24, crc);
+    }
+    // --- segment tables (segment_bounds, stream.py:271-284)
+    const uint64_t sb0 = scan[sd.blk0];
+    const uint64_t total_entries = (uint64_t)sd.nwin * segs;
+    for (uint64_t q = threadIdx.x; q < total_entries; q += blockDim.x) {
+        const uint32_t wl = (uint32_t)(q / segs), i = (uint32_t)(q % segs);
+        const WinDesc wd = wins[sd.win0 + wl];
+        const uint64_t nblk = wd.nblocks;
+        const uint64_t ea = min(wd.W, ((uint64_t)i * nblk / segs) * B);
+        const uint64_t eb = (i + 1 == segs) ? wd.W : min(wd.W, ((uint64_t)(i + 1) * nblk / segs) * B);
+        const uint64_t ba = ea / B, bb = (eb == ea) ? ba : (eb + B - 1) / B;
+        const uint64_t comp = scan[wd.blk0 + bb] - scan[wd.blk0 + ba];
+        const uint64_t toff = base + kHeader + (uint64_t)wl * kSegEntry * segs + (scan[wd.blk0] - sb0);
+        put_u64(out + toff + (uint64_t)i * kSegEntry, eb - ea);
+        put_u64(out + toff + (uint64_t)i * kSegEntry + 8, comp);
+    }
+}
+
+// --------------------------------------------------------------- K4 encode
+// One CTA per block slot.  Canonical codes (huffman.py:213-225) are built in
+// shared memory from the wire codebook; every lane packs the codes of its
+// 64/w consecutive symbols MSB-first into a shared staging area laid out on
+// the 4-byte grid of the destination, so complete words leave with plain
+// 32-bit stores and only the two edge words of a record are written bytewise.
+__global__ void __launch_bounds__(kThreads) k_encode(
+    const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
+    uint32_t segs, const StreamDesc* __restrict__ streams, const BlockMeta* __restrict__ meta,
+    const uint8_t* __restrict__ wire, const uint64_t* __restrict__ scan, const uint64_t* __restrict__ soff,
+    uint8_t* __restrict__ out) {
+    extern __shared__ uint32_t stg[];
+    __shared__ uint32_t sh_code[256];
+    __shared__ uint32_t sh_cnt[kWarps][16];
+    __shared__ uint32_t sh_first[16];
+    __shared__ uint32_t sh_wsum[kWarps * 2];
+    const uint64_t slot = blockIdx.x;
+    if (slot >= nslots) return;
+    const WinDesc wd = wins[slot2win[slot]];
+    const int64_t kk = slot_to_block(wd, slot - wd.slot0, B);
+    if (kk < 0) return;
+    const uint64_t k = (uint64_t)kk;
+    const uint64_t b = wd.blk0 + k;
+    const BlockMeta m = meta[b];
+    const StreamDesc sd = streams[wd.stream];
+    const uint64_t rec = soff[wd.stream] + kHeader + (uint64_t)(wd.win_local + 1) * kSegEntry * segs +
+                         (scan[b] - scan[sd.blk0]);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint8_t* rp = out + rec;
+    if (m.mode == MODE_RLE) {
+        if (tid == 0) { rp[0] = MODE_RLE; put_u32(rp + 1, m.len); rp[5] = m.sym; }
+        return;
+    }
+    const bool huff = m.mode == MODE_HUFFMAN;
+    const uint32_t hdr = huff ? 5 + kHuffOverhead : 5;
+    // preamble: mode | len | [codebook | bit count]
+    if (tid < (int)hdr) {
+        uint8_t v;
+        if (tid == 0) v = m.mode;
+        else if (tid < 5) v = (uint8_t)(m.len >> (8 * (tid - 1)));
+        else if (tid < 133) v = wire[b * 128 + (tid - 5)];
+        else v = (uint8_t)(m.bits >> (8 * (tid - 133)));
+        rp[tid] = v;
+    }
+    // canonical code table (huffman.py:213-225): thread t handles symbol t
+    if (tid < kWarps * 16) (&sh_cnt[0][0])[tid] = 0;
+    __syncthreads();
+    uint32_t my_len, my_rank_w;
+    {
+        if (huff) {
+            const uint8_t wb = wire[b * 128 + (tid >> 1)];
+            my_len = (tid & 1) ? (wb >> 4) : (wb & 15);
+        } else {
+            my_len = 8;
+        }
+        const uint32_t mm = __match_any_sync(0xFFFFFFFFu, my_len);
+        my_rank_w = __popc(mm & ((1u << lane) - 1));
+        if (lane == __ffs(mm) - 1) sh_cnt[warp][my_len] = __popc(mm);
+    }
+    __syncthreads();
+    if (tid < 16) {
+        // first left-justified code of each length
+        uint32_t tot[16];
+        for (int l = 0; l < 16; l++) {
+            uint32_t c = 0;
+            for (int q = 0; q < kWarps; q++) c += sh_cnt[q][l];
+            tot[l] = c;
+        }
+        uint32_t start = 0;
+        for (int l = 1; l < 16; l++) {
+            if (l == tid) sh_first[tid] = start;
+            start += tot[l] << (kMaxLen - l);
+        }
+        if (tid == 0) sh_first[0] = 0;
+    }
+    __syncthreads();
+    if (my_len) {
+        uint32_t r = my_rank_w;
+        for (int q = 0; q < warp; q++) r += sh_cnt[q][my_len];
+        const uint32_t code = (sh_first[my_len] >> (kMaxLen - my_len)) + r;
+        sh_code[tid] = (my_len << 16) | code;
+    } else {
+        sh_code[tid] = 0;
+    }
+    // staging
+    const uint32_t w = wd.w;
+    const uint64_t T = kTileBytes / w;
+    const uint64_t iterpos = T * kWarps;
+    const uint32_t stg_words = (uint32_t)((iterpos * (huff ? 15 : 8)) / 32 + 4);
+    for (uint32_t i = tid; i < stg_words; i += kThreads) stg[i] = 0;
+    __syncthreads();
+    const uint64_t gaddr = (uint64_t)(rp + hdr);
+    const uint32_t lead = (uint32_t)(gaddr & 3) * 8;
+    uint32_t* gw = reinterpret_cast<uint32_t*>(gaddr & ~(uint64_t)3);
+    uint64_t bitpos = lead;     // staging coordinate of the next bit (relative to gw)
+    uint64_t base_word = 0;     // global word index (relative to gw) of stg[0]
+    const uint64_t p0 = k * B, p1 = min(wd.W, p0 + B);
+    for (uint64_t it0 = p0; it0 < p1; it0 += iterpos) {
+        const uint64_t tp = it0 + (uint64_t)warp * T;
+        const uint64_t te = min(tp + T, p1);
+        uint32_t s[16];
+        int ns = 0;
+        uint64_t g = 0;
+        if (tp < te) {
+            g = (w == 1) ? 0 : tp / wd.n;
+            const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
+            if (fast) {
+                uint32_t v[16];
+                const uint64_t e0 = tp - g * wd.n;
+                load64(wd.src, wd.prev, e0 * w + (uint64_t)lane * kLaneBytes, v);
+                ns = extract_plane(v, w, (uint32_t)g, s);
+            } else {
+                const uint64_t per = T / 32;
+                const uint64_t a = tp + lane * per, bnd = min(a + per, te);
+#pragma unroll
+                for (int q = 0; q < 16; q++) s[q] = 0;
+                for (uint64_t p = a; p < bnd; p++, ns++) s[ns >> 2] |= gather_byte(wd, p) << (8 * (ns & 3));
+            }
+        }
+        uint32_t nbits = 0;
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+#pragma unroll
+            for (int r = 0; r < 4; r++)
+                if (4 * q + r < ns) nbits += sh_code[(s[q] >> (8 * r)) & 0xFF] >> 16;
+        }
+        // CTA exclusive scan of nbits in (warp, lane) order
+        uint32_t incl = nbits;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) sh_wsum[warp] = incl;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < kWarps; q++) { if (q < warp) wpre += sh_wsum[q]; tot += sh_wsum[q]; }
+        const uint64_t start = bitpos + wpre + incl - nbits - base_word * 32;
+        if (ns) {
+            uint64_t acc = 0;
+            uint32_t nacc = (uint32_t)(start & 31);
+            uint32_t wi = (uint32_t)(start >> 5);
+#pragma unroll
+            for (int q = 0; q < 16; q++) {
+#pragma unroll
+                for (int r = 0; r < 4; r++) {
+                    if (4 * q + r < ns) {
+                        const uint32_t e = sh_code[(s[q] >> (8 * r)) & 0xFF];
+                        const uint32_t l = e >> 16;
+                        acc = (acc << l) | (e & 0xFFFF);
+                        nacc += l;
+                        if (nacc >= 32) {
+                            atomicOr(&stg[wi], (uint32_t)(acc >> (nacc - 32)));
+                            wi++;
+                            nacc -= 32;
+                        }
+                    }
+                }
+            }
+            if (nacc) atomicOr(&stg[wi], (uint32_t)(acc << (32 - nacc)));
+        }
+        __syncthreads();
+        const uint64_t end = bitpos + tot;
+        const uint64_t full = end / 32 - base_word;   // complete words in staging
+        for (uint64_t j = tid; j < full; j += kThreads) {
+            const uint64_t gwi = base_word + j;
+            const uint32_t v = bswap32(stg[j]);
+            if (gwi == 0 && lead) {
+                uint8_t* bp = reinterpret_cast<uint8_t*>(gw);
+                for (uint32_t q = lead / 8; q < 4; q++) bp[q] = (uint8_t)(v >> (8 * q));
+            } else {
+                gw[gwi] = v;
+            }
+        }
+        const uint32_t carry = (tid == 0) ? stg[full] : 0;  // read before anyone clears it
+        __syncthreads();
+        for (uint64_t j = tid; j <= full; j += kThreads) stg[j] = 0;
+        __syncthreads();
+        if (tid == 0) stg[0] = carry;
+        base_word += full;
+        bitpos = end;
+        __syncthreads();
+    }
+    // trailing partial word: bytes up to the record end
+    if (tid == 0 && (bitpos & 31)) {
+        const uint32_t v = bswap32(stg[0]);
+        const uint64_t end_byte = (bitpos + 7) / 8;   // relative to gw
+        uint8_t* bp = reinterpret_cast<uint8_t*>(gw) + base_word * 4;
+        uint32_t q0 = (base_word == 0) ? lead / 8 : 0;
+        for (uint32_t q = q0; q < 4 && base_word * 4 + q < end_byte; q++) bp[q] = (uint8_t)(v >> (8 * q));
+    }
+}
+
+}  // namespace lmcg

@@ -1,0 +1,207 @@
+// lmc_common.cuh -- shared layout, CRC-32 machinery and byte gathers for the
+// B200 LMC kernels.  See DESIGN.md for the HBM layout and the roofline of
+// each kernel.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lmcg {
+
+constexpr int kMaxLen = 15;               // huffman.py:33
+constexpr uint32_t kHeader = 28;          // stream.py:72,77
+constexpr uint32_t kSegEntry = 16;        // stream.py:74
+constexpr uint32_t kHuffOverhead = 132;   // 128-byte codebook + u32 bit count, stream.py:80
+constexpr int kThreads = 256;             // CTA size of the block kernels
+constexpr int kWarps = kThreads / 32;
+constexpr int kLaneBytes = 64;            // contiguous source bytes per lane per warp-tile
+constexpr int kTileBytes = 32 * kLaneBytes;  // source bytes per warp-tile (2 KiB)
+
+enum : uint8_t { MODE_HUFFMAN = 0, MODE_RLE = 1, MODE_STORED = 2 };
+
+// One buffer-size window of one stream (stream.py:332-340).  A window is
+// byte-grouped into w planes of n bytes; its grouped bytes are cut into
+// blocks of B bytes (the last may be short, and when n % B != 0 a block
+// straddles two planes).
+struct WinDesc {
+    const uint8_t* src;   // window start in the (next) payload
+    const uint8_t* prev;  // window start in the previous step (fused XOR) or null
+    uint64_t W;           // window bytes
+    uint64_t n;           // bytes per plane = W / w
+    uint64_t blk0;        // global index of the window's first block
+    uint64_t slot0;       // global index of the window's first CTA slot
+    uint32_t w;           // planes (element width when byte-grouped, else 1)
+    uint32_t nblocks;     // ceil(W / B)
+    uint32_t nslots;      // CTA slots (planes interleaved, see slot_to_block)
+    uint32_t stream;      // owning stream
+    uint32_t win_local;   // window index inside the stream
+    uint32_t vec;         // 16-byte vector loads allowed (alignment of src/prev/W)
+};
+
+// One stream of the batch.
+struct StreamDesc {
+    uint64_t nbytes;      // original_length
+    uint64_t blk0;        // first global block
+    uint64_t nblk;        // blocks in this stream
+    uint32_t win0;        // first global window
+    uint32_t nwin;
+    uint32_t flags;       // FLAG_BYTE_GROUPED | FLAG_DELTA
+    uint32_t et;          // element type wire code
+};
+
+// Per-block result of the codebook stage (stream.py:161-177).
+struct BlockMeta {
+    uint32_t len;      // block bytes
+    uint32_t recsize;  // serialized record bytes (mode u8 | len u32 | payload)
+    uint32_t bits;     // Huffman payload bit count
+    uint8_t mode;      // MODE_*
+    uint8_t sym;       // RLE symbol
+    uint8_t pm;        // 1 = lengths need package-merge (set by k_codebook)
+    uint8_t pad;
+};
+
+// ---------------------------------------------------------------- CRC-32
+// IEEE reflected polynomial 0xEDB88320 (zlib.crc32, stream.py:329).  Kernels
+// compute *raw* CRCs (zero initial register, no final xor) of contiguous
+// pieces and merge them with shift operators: raw(A||B) = shift(raw(A),|B|) ^
+// raw(B); leading zero bytes leave a raw CRC unchanged.  The zlib value of a
+// message of N bytes is raw ^ shift(0xFFFFFFFF, N) ^ 0xFFFFFFFF.
+//
+// Global tables (built once per context, see capi.cu):
+//   crc_slice[4][256]     slice-by-4 tables
+//   crc_shift[k][4][256]  byte-sliced operators "append 64*2^k zero bytes",
+//                         k = 0..7 (64 B .. 8 KiB)
+//   x2n[64]               x^(2^k) mod P for the generic shift
+struct CrcTables {
+    uint32_t slice[4][256];
+    uint32_t shift[8][4][256];
+    uint32_t x2n[64];
+};
+
+__device__ __forceinline__ uint32_t crc_word(const uint32_t* __restrict__ sl, uint32_t crc, uint32_t word) {
+    crc ^= word;
+    return sl[768 + (crc & 0xFF)] ^ sl[512 + ((crc >> 8) & 0xFF)] ^ sl[256 + ((crc >> 16) & 0xFF)] ^
+           sl[crc >> 24];
+}
+__device__ __forceinline__ uint32_t crc_byte(const uint32_t* __restrict__ sl, uint32_t crc, uint32_t b) {
+    return (crc >> 8) ^ sl[(crc ^ b) & 0xFF];
+}
+// shift by 64*2^k bytes through a byte-sliced operator table
+__device__ __forceinline__ uint32_t crc_shift_tab(const uint32_t* __restrict__ t, uint32_t c) {
+    return __ldg(&t[c & 0xFF]) ^ __ldg(&t[256 + ((c >> 8) & 0xFF)]) ^ __ldg(&t[512 + ((c >> 16) & 0xFF)]) ^
+           __ldg(&t[768 + (c >> 24)]);
+}
+// a*b mod P in the reflected representation (zlib multmodp)
+__device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
+    uint32_t m = 1u << 31, p = 0;
+    for (;;) {
+        if (a & m) {
+            p ^= b;
+            if ((a & (m - 1)) == 0) break;
+        }
+        m >>= 1;
+        b = b & 1 ? (b >> 1) ^ 0xEDB88320u : b >> 1;
+    }
+    return p;
+}
+// x^(8*nbytes) mod P
+__device__ __forceinline__ uint32_t x8nmodp(const uint32_t* __restrict__ x2n, uint64_t nbytes) {
+    uint32_t p = 1u << 31;  // x^0
+    int k = 3;
+    uint64_t n = nbytes;
+    while (n) {
+        if (n & 1) p = multmodp(__ldg(&x2n[k & 63]), p);
+        n >>= 1;
+        k++;
+    }
+    return p;
+}
+__device__ __forceinline__ uint32_t crc_shift_generic(const uint32_t* __restrict__ x2n, uint32_t c, uint64_t nbytes) {
+    if (c == 0 || nbytes == 0) return c;
+    return multmodp(x8nmodp(x2n, nbytes), c);
+}
+
+// Warp tree over 32 lane parts of kLaneBytes each (lane order = byte order):
+// returns on lane 0 the raw CRC of the 2 KiB warp-tile.
+__device__ __forceinline__ uint32_t crc_warp_tree(const CrcTables* __restrict__ ct, uint32_t c, int lane) {
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        uint32_t other = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
+        uint32_t shifted = crc_shift_tab(&ct->shift[k][0][0], c);
+        if ((lane & ((2 << k) - 1)) == 0) c = shifted ^ other;
+    }
+    return c;
+}
+
+// ------------------------------------------------------------- gathers
+__device__ __forceinline__ uint4 ldg16(const uint8_t* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
+// 64 contiguous source bytes (16-byte aligned) XOR the previous step.
+__device__ __forceinline__ void load64(const uint8_t* __restrict__ src, const uint8_t* __restrict__ prev,
+                                       uint64_t off, uint32_t v[16]) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        uint4 a = ldg16(src + off + 16 * q);
+        v[4 * q + 0] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+    }
+    if (prev) {
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint4 b = ldg16(prev + off + 16 * q);
+            v[4 * q + 0] ^= b.x; v[4 * q + 1] ^= b.y; v[4 * q + 2] ^= b.z; v[4 * q + 3] ^= b.w;
+        }
+    }
+}
+
+// Plane-g symbols of the 64/w elements held in v (little-endian element
+// bytes), packed 4 per word in position order.  Returns the symbol count.
+__device__ __forceinline__ int extract_plane(const uint32_t v[16], uint32_t w, uint32_t g, uint32_t s[16]) {
+    if (w == 1) {
+#pragma unroll
+        for (int k = 0; k < 16; k++) s[k] = v[k];
+        return 64;
+    }
+    if (w == 2) {
+        const uint32_t sel = g ? 0x7531 : 0x6420;
+#pragma unroll
+        for (int k = 0; k < 8; k++) s[k] = __byte_perm(v[2 * k], v[2 * k + 1], sel);
+        return 32;
+    }
+    const uint32_t sel = g | ((4 + g) << 4);
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        uint32_t lo = __byte_perm(v[4 * k], v[4 * k + 1], sel);
+        uint32_t hi = __byte_perm(v[4 * k + 2], v[4 * k + 3], sel);
+        s[k] = __byte_perm(lo, hi, 0x5410);
+    }
+    return 16;
+}
+
+__device__ __forceinline__ uint32_t sym_at(const uint32_t s[16], int i) {
+    return (s[i >> 2] >> (8 * (i & 3))) & 0xFF;
+}
+
+// Byte of grouped window position p (slow path).
+__device__ __forceinline__ uint32_t gather_byte(const WinDesc& wd, uint64_t p) {
+    uint64_t g = wd.w == 1 ? 0 : p / wd.n;
+    uint64_t e = p - g * wd.n;
+    uint64_t o = e * wd.w + g;
+    uint32_t b = wd.src[o];
+    if (wd.prev) b ^= wd.prev[o];
+    return b;
+}
+
+// Map a CTA slot of a window to its block index, interleaving planes so that
+// the CTAs reading the same source elements run back to back (the second read
+// is then served from L2).  Returns -1 for idle slots.
+__device__ __forceinline__ int64_t slot_to_block(const WinDesc& wd, uint64_t local, uint32_t B) {
+    if (wd.w == 1) return local < wd.nblocks ? (int64_t)local : -1;
+    uint64_t g = local % wd.w, j = local / wd.w;
+    uint64_t sg = (g * wd.n + B - 1) / B;
+    uint64_t sg1 = (g + 1 == wd.w) ? wd.nblocks : ((g + 1) * wd.n + B - 1) / B;
+    uint64_t k = sg + j;
+    return k < sg1 ? (int64_t)k : -1;
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
+
+}  // namespace lmcg

@@ -1,0 +1,419 @@
+"""The LMC codestream on B200: drop-in ``lmc_compress`` / ``lmc_decompress``.
+
+Public surface mirrors the reference ``lmc.stream`` (pkg/src/lmc/stream.py):
+same names, same keyword options, same return types, same exceptions, and
+byte-identical ``LMC1`` streams.  Every byte of compute runs in the CUDA
+kernels of liblmc_b200.so (csrc/); this module only moves buffers, parses the
+28-byte header (host logic, stream.py:114-142) and maps status codes onto the
+reference's exception classes.
+
+Batched, device-resident entry points (``Codec.compress`` / ``Codec.decompress``)
+take CUDA tensors and keep the streams in HBM; the reference-shaped functions
+wrap them with host <-> device copies.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from .errors import (AlignmentError, ConfigError, CorruptStreamError, DeviceError, LmcError,
+                     UnsupportedFormatError, raise_status)
+from .types import DeltaBuffer, ElementType, TensorBuffer, element_code, is_delta
+
+MAGIC = b"LMC1"
+VERSION = 1
+FLAG_BYTE_GROUPED = 0x01
+FLAG_DELTA = 0x02
+DEFAULT_BLOCK_SIZE = 64 * 1024          # entropy.py:22
+MIN_BLOCK_SIZE = 4 * 1024
+MAX_BLOCK_SIZE = 1024 * 1024
+DEFAULT_BUFFER_SIZE = 128 * 1024 * 1024  # stream.py:66
+MODE_HUFFMAN, MODE_RLE, MODE_STORED = 0, 1, 2
+_HEADER = struct.Struct("<4sBBBBQIII")
+HEADER_SIZE = _HEADER.size  # 28
+CODEBOOK_WIRE_SIZE = 128
+
+_WIDTH = {0: 1, 1: 2, 2: 2, 3: 4}
+
+
+# ---------------------------------------------------------------- header
+@dataclass(frozen=True)
+class CodeStreamHeader:
+    """stream.py:83-111."""
+
+    flags: int
+    element_type: ElementType
+    original_length: int
+    block_size: int
+    segment_count: int
+    crc32: int
+
+    @property
+    def byte_grouped(self) -> bool:
+        return bool(self.flags & FLAG_BYTE_GROUPED)
+
+    @property
+    def delta_applied(self) -> bool:
+        return bool(self.flags & FLAG_DELTA)
+
+    def pack(self) -> bytes:
+        return _HEADER.pack(MAGIC, VERSION, self.flags, self.element_type.code, 0, self.original_length,
+                            self.block_size, self.segment_count, self.crc32)
+
+
+def validate_block_size(block_size: int) -> int:
+    """entropy.py:27-37."""
+    if block_size < MIN_BLOCK_SIZE or block_size > MAX_BLOCK_SIZE or block_size & (block_size - 1):
+        raise ConfigError(f"block size must be a power of two in [{MIN_BLOCK_SIZE}, {MAX_BLOCK_SIZE}], got {block_size}")
+    return block_size
+
+
+def parse_header(stream: bytes) -> CodeStreamHeader:
+    """stream.py:114-142 (host-side header parse; the device repeats it)."""
+    if len(stream) < HEADER_SIZE:
+        raise UnsupportedFormatError("stream shorter than a header")
+    magic, version, flags, et_code, reserved, orig_len, block_size, seg_count, crc = _HEADER.unpack_from(stream)
+    if magic != MAGIC:
+        raise UnsupportedFormatError(f"bad magic {magic!r}")
+    if version != VERSION:
+        raise UnsupportedFormatError(f"unsupported version {version}")
+    if flags & ~(FLAG_BYTE_GROUPED | FLAG_DELTA):
+        raise CorruptStreamError(f"unknown flag bits 0x{flags:02x}")
+    if reserved != 0:
+        raise CorruptStreamError("reserved header byte must be zero")
+    try:
+        et = ElementType.from_code(et_code)
+    except ValueError as exc:
+        raise CorruptStreamError(str(exc)) from exc
+    try:
+        validate_block_size(block_size)
+    except ConfigError as exc:
+        raise CorruptStreamError(str(exc)) from exc
+    if seg_count < 1:
+        raise CorruptStreamError("segment count must be >= 1")
+    if orig_len % et.width != 0:
+        raise CorruptStreamError(f"original length {orig_len} is not {et.name}-aligned")
+    return CodeStreamHeader(flags, et, orig_len, block_size, seg_count, crc)
+
+
+def segment_bounds(window_length: int, block_size: int, segment_count: int) -> list[tuple[int, int]]:
+    """stream.py:271-284 (host helper; the device computes the same edges)."""
+    nblocks = (window_length + block_size - 1) // block_size
+    edges = [min(window_length, (i * nblocks // segment_count) * block_size) for i in range(segment_count)]
+    edges.append(window_length)
+    return list(zip(edges[:-1], edges[1:]))
+
+
+def _validate_options(width: int, block_size: int, segment_count: int, buffer_size: int) -> None:
+    """stream.py:287-301."""
+    validate_block_size(block_size)
+    if segment_count < 1:
+        raise ConfigError(f"segment count must be >= 1, got {segment_count}")
+    if buffer_size < block_size:
+        raise ConfigError(f"buffer size {buffer_size} must be >= block size {block_size}")
+    if buffer_size % width != 0:
+        raise ConfigError(f"buffer size {buffer_size} must be a multiple of the element width {width}")
+
+
+def compression_ratio(stream: bytes, original_length: int) -> float:
+    if original_length == 0:
+        return 1.0
+    return len(stream) / original_length
+
+
+# ------------------------------------------------------------ device codec
+_TORCH_ET = None
+
+
+def _torch_et(dtype) -> int:
+    global _TORCH_ET
+    import torch
+
+    if _TORCH_ET is None:
+        _TORCH_ET = {torch.bfloat16: 1, torch.float16: 2, torch.float32: 3, torch.uint8: 0, torch.int8: 0}
+    if dtype not in _TORCH_ET:
+        raise ConfigError(f"no LMC element type for torch dtype {dtype}")
+    return _TORCH_ET[dtype]
+
+
+def _bytes_view(t):
+    import torch
+
+    if not t.is_cuda:
+        raise DeviceError("Codec inputs must be CUDA tensors")
+    if not t.is_contiguous():
+        t = t.contiguous()
+    return t.view(torch.uint8).reshape(-1) if t.numel() else torch.empty(0, dtype=torch.uint8, device=t.device)
+
+
+class CompressedBatch:
+    """Streams packed back to back in one CUDA byte tensor."""
+
+    def __init__(self, data, offsets, lengths):
+        self.data = data          # torch.uint8 [capacity], device
+        self.offsets = offsets    # torch.int64 [n], device
+        self.lengths = lengths    # torch.int64 [n], device
+        self._host = None
+
+    def host_layout(self) -> tuple[list[int], list[int]]:
+        if self._host is None:
+            import torch
+
+            both = torch.stack([self.offsets, self.lengths]).cpu().tolist()
+            self._host = (both[0], both[1])
+        return self._host
+
+    def __len__(self) -> int:
+        return int(self.offsets.numel())
+
+    def stream(self, i: int):
+        off, ln = self.host_layout()
+        return self.data[off[i]: off[i] + ln[i]]
+
+    def total_bytes(self) -> int:
+        off, ln = self.host_layout()
+        return (off[-1] + ln[-1]) if off else 0
+
+    def to_bytes(self) -> list[bytes]:
+        off, ln = self.host_layout()
+        total = self.total_bytes()
+        flat = self.data[:total].cpu().numpy().tobytes() if total else b""
+        return [flat[o: o + n] for o, n in zip(off, ln)]
+
+
+class DecompressedBatch:
+    def __init__(self, data, offsets, lengths, element_types, flags, status):
+        self.data = data
+        self.offsets = offsets
+        self.lengths = lengths
+        self.element_types = element_types
+        self.flags = flags
+        self.status = status
+
+    def __len__(self) -> int:
+        return len(self.offsets)
+
+    def payload(self, i: int):
+        return self.data[self.offsets[i]: self.offsets[i] + self.lengths[i]]
+
+    def raise_for_status(self) -> None:
+        for i, s in enumerate(self.status):
+            if s:
+                raise_status(s, f"stream {i}: " + {1: "unsupported format", 2: "corrupt stream",
+                                                   3: "payload CRC mismatch"}.get(s, f"status {s}"))
+
+
+class Codec:
+    """Batched device-resident LMC codec on one CUDA device.
+
+    ``compress`` takes CUDA tensors (any of bf16/fp16/fp32/uint8, or explicit
+    element type codes) and returns a CompressedBatch whose streams are
+    byte-identical to ``lmc.lmc_compress`` of the same bytes.  ``prev`` turns
+    on the fused XOR delta (delta.py:29-47): the stream then encodes
+    ``prev ^ tensor`` with FLAG_DELTA, exactly like compressing a DeltaBuffer.
+    """
+
+    def __init__(self, device: int | None = None):
+        import torch
+
+        self.ctx = _lib.context(device)
+        self.device = torch.device("cuda", self.ctx.device)
+        self._ws = None
+
+    # -- compress
+    def compress(self, tensors: Sequence, *, element_types: Sequence[int] | None = None, prev: Sequence | None = None,
+                 delta: Sequence[bool] | bool | None = None, byte_group: bool = True,
+                 block_size: int = DEFAULT_BLOCK_SIZE, segment_count: int = 1,
+                 buffer_size: int = DEFAULT_BUFFER_SIZE, out=None, stream=None) -> CompressedBatch:
+        import torch
+
+        n = len(tensors)
+        views, ets = [], []
+        for i, t in enumerate(tensors):
+            et = element_types[i] if element_types is not None else _torch_et(t.dtype)
+            ets.append(int(et))
+            views.append(_bytes_view(t))
+        pviews = [None] * n
+        if prev is not None:
+            for i, p in enumerate(prev):
+                if p is not None:
+                    pv = _bytes_view(p)
+                    if pv.numel() != views[i].numel():
+                        from .errors import ShapeMismatchError
+                        raise ShapeMismatchError(f"length mismatch: {pv.numel()} vs {views[i].numel()}")
+                    pviews[i] = pv
+        if isinstance(delta, bool) or delta is None:
+            dflags = [bool(delta)] * n
+        else:
+            dflags = [bool(d) for d in delta]
+        for et in ets:
+            _validate_options(_WIDTH[et], block_size, segment_count, buffer_size)
+        arr = (_lib.lmcg_tensor * max(n, 1))()
+        for i in range(n):
+            arr[i].data = views[i].data_ptr() if views[i].numel() else 0
+            arr[i].prev = pviews[i].data_ptr() if pviews[i] is not None and pviews[i].numel() else 0
+            arr[i].nbytes = views[i].numel()
+            arr[i].element_type = ets[i]
+            arr[i].delta = int(dflags[i] or pviews[i] is not None)
+            if views[i].numel() % _WIDTH[ets[i]]:
+                raise AlignmentError(f"buffer of {views[i].numel()} bytes is not a multiple of width {_WIDTH[ets[i]]}")
+        opts = _lib.lmcg_options(int(bool(byte_group)), block_size, segment_count, 0, buffer_size)
+        L = self.ctx.lib
+        bound = int(L.lmcg_compress_bound(arr, n, ctypes.byref(opts)))
+        wsb = int(L.lmcg_compress_workspace(arr, n, ctypes.byref(opts)))
+        if self._ws is None or self._ws.numel() < wsb:
+            self._ws = torch.empty(max(wsb, 1 << 20), dtype=torch.uint8, device=self.device)
+        if out is None or out.numel() < bound:
+            out = torch.empty(max(bound, 16), dtype=torch.uint8, device=self.device)
+        meta = torch.empty(2 * max(n, 1), dtype=torch.int64, device=self.device)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = L.lmcg_compress(self.ctx.ptr, arr, n, ctypes.byref(opts), out.data_ptr(), out.numel(),
+                             meta.data_ptr(), meta.data_ptr() + 8 * max(n, 1), self._ws.data_ptr(),
+                             self._ws.numel(), ctypes.c_void_p(s.cuda_stream))
+        self.ctx.check(rc)
+        # keep inputs alive until the work is done
+        batch = CompressedBatch(out, meta[:n], meta[max(n, 1): max(n, 1) + n])
+        batch._keep = (views, pviews)
+        return batch
+
+    def block_info(self) -> dict:
+        """Per-block (mode, bits, record size, wire codebook) of the last compress."""
+        L = self.ctx.lib
+        nb = int(L.lmcg_block_info(self.ctx.ptr, None, None, None, None, None, 0))
+        modes = np.zeros(nb, np.int32)
+        bits = np.zeros(nb, np.uint32)
+        sizes = np.zeros(nb, np.uint32)
+        wire = np.zeros((nb, 128), np.uint8)
+        pm = np.zeros(nb, np.uint32)
+        if nb:
+            L.lmcg_block_info(self.ctx.ptr, modes.ctypes.data, bits.ctypes.data, sizes.ctypes.data,
+                              wire.ctypes.data, pm.ctypes.data, nb)
+        lengths = np.zeros((nb, 256), np.uint8)
+        lengths[:, 0::2] = wire & 0x0F
+        lengths[:, 1::2] = wire >> 4
+        return dict(modes=modes, bits=bits, sizes=sizes, wire=wire, lengths=lengths, pm=pm)
+
+    # -- decompress
+    def plan(self, streams: Sequence, stream=None):
+        """Parse/validate device streams; returns (orig_lengths, element codes, flags, status)."""
+        import torch
+
+        n = len(streams)
+        ptrs = (ctypes.c_void_p * max(n, 1))()
+        lens = (ctypes.c_uint64 * max(n, 1))()
+        keep = []
+        for i, t in enumerate(streams):
+            v = _bytes_view(t)
+            if v.numel() == 0:
+                v = torch.zeros(1, dtype=torch.uint8, device=self.device)
+                lens[i] = 0
+            else:
+                lens[i] = v.numel()
+            keep.append(v)
+            ptrs[i] = v.data_ptr()
+        orig = (ctypes.c_uint64 * max(n, 1))()
+        ets = (ctypes.c_int32 * max(n, 1))()
+        flags = (ctypes.c_int32 * max(n, 1))()
+        st = (ctypes.c_int32 * max(n, 1))()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.ctx.lib.lmcg_decompress_plan(self.ctx.ptr, ptrs, lens, n, orig, ets, flags, st,
+                                               ctypes.c_void_p(s.cuda_stream))
+        self.ctx.check(rc)
+        self._plan_keep = keep
+        return list(orig)[:n], list(ets)[:n], list(flags)[:n], list(st)[:n]
+
+    def decompress(self, streams, *, out=None, stream=None) -> DecompressedBatch:
+        """Decode device streams (a CompressedBatch or a list of CUDA byte tensors)."""
+        import torch
+
+        if isinstance(streams, CompressedBatch):
+            off, ln = streams.host_layout()
+            streams = [streams.data[o: o + n] for o, n in zip(off, ln)]
+        n = len(streams)
+        orig, ets, flags, st0 = self.plan(streams, stream=stream)
+        offs, pos = [], 0
+        for i in range(n):
+            offs.append(pos)
+            pos += (orig[i] + 15) & ~15
+        if out is None or out.numel() < pos:
+            out = torch.empty(max(pos, 16), dtype=torch.uint8, device=self.device)
+        hoff = (ctypes.c_uint64 * max(n, 1))(*offs)
+        st = (ctypes.c_int32 * max(n, 1))()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.ctx.lib.lmcg_decompress_run(self.ctx.ptr, out.data_ptr(), hoff, st, ctypes.c_void_p(s.cuda_stream))
+        self.ctx.check(rc)
+        status = [st0[i] or st[i] for i in range(n)]
+        return DecompressedBatch(out, offs, orig, ets, flags, status)
+
+
+_codecs: dict[int, Codec] = {}
+
+
+def default_codec() -> Codec:
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device: the LMC B200 path has no CPU fallback")
+    d = torch.cuda.current_device()
+    c = _codecs.get(d)
+    if c is None:
+        c = _codecs[d] = Codec(d)
+    return c
+
+
+def _to_device_bytes(data: bytes, device):
+    import torch
+
+    if len(data) == 0:
+        return torch.empty(0, dtype=torch.uint8, device=device)
+    h = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+    return h.pin_memory().to(device, non_blocking=True)
+
+
+# ----------------------------------------------------- reference-shaped API
+def compress_many(bufs: Sequence, *, byte_group: bool = True, block_size: int = DEFAULT_BLOCK_SIZE,
+                  segment_count: int = 1, buffer_size: int = DEFAULT_BUFFER_SIZE) -> list[bytes]:
+    """lmc_compress over many TensorBuffer / DeltaBuffer values in one batch."""
+    codec = default_codec()
+    tens, ets, dflags = [], [], []
+    for b in bufs:
+        et = element_code(b.element_type)
+        _validate_options(_WIDTH[et], block_size, segment_count, buffer_size)
+        tens.append(_to_device_bytes(bytes(b.data), codec.device))
+        ets.append(et)
+        dflags.append(is_delta(b))
+    batch = codec.compress(tens, element_types=ets, delta=dflags, byte_group=byte_group, block_size=block_size,
+                           segment_count=segment_count, buffer_size=buffer_size)
+    return batch.to_bytes()
+
+
+def lmc_compress(buf, *, byte_group: bool = True, block_size: int = DEFAULT_BLOCK_SIZE, segment_count: int = 1,
+                 buffer_size: int = DEFAULT_BUFFER_SIZE) -> bytes:
+    """stream.py:311-341 -- one buffer into a complete LMC1 codestream (GPU)."""
+    return compress_many([buf], byte_group=byte_group, block_size=block_size, segment_count=segment_count,
+                         buffer_size=buffer_size)[0]
+
+
+def decompress_many(streams: Sequence[bytes]) -> list[TensorBuffer]:
+    """lmc_decompress over many streams; raises the first stream's error."""
+    codec = default_codec()
+    dev = [_to_device_bytes(bytes(s), codec.device) for s in streams]
+    res = codec.decompress(dev)
+    res.raise_for_status()
+    out = []
+    host = res.data[: (res.offsets[-1] + res.lengths[-1]) if len(res) else 0].cpu().numpy().tobytes()
+    for i in range(len(res)):
+        o, n = res.offsets[i], res.lengths[i]
+        out.append(TensorBuffer(host[o: o + n], ElementType.from_code(res.element_types[i])))
+    return out
+
+
+def lmc_decompress(stream: bytes) -> TensorBuffer:
+    """stream.py:406-423 -- decode and CRC-verify one codestream (GPU)."""
+    return decompress_many([stream])[0]

@@ -1,0 +1,235 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+golden fixtures produced by the live reference.  Bit-exact everywhere."""
+import numpy as np
+import pytest
+
+from conftest import load_golden_codebooks, load_golden_corruptions, load_golden_streams
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2505_09810_b200 as lmcb  # noqa: E402
+from paper_2505_09810_b200 import synth  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+ET = lmcb.ElementType
+
+
+@pytest.fixture(scope="module")
+def codec():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return lmcb.Codec()
+
+
+def dev_bytes(b: bytes):
+    if not b:
+        return torch.empty(0, dtype=torch.uint8, device="cuda")
+    return torch.frombuffer(bytearray(b), dtype=torch.uint8).cuda()
+
+
+def host_bytes(t) -> bytes:
+    return t.cpu().numpy().tobytes()
+
+
+# ------------------------------------------------------------------ golden
+@pytest.mark.parametrize("case", load_golden_streams(), ids=lambda c: c[0]["name"])
+def test_golden_stream_bytes(codec, case):
+    m, data, stream = case
+    b = codec.compress([dev_bytes(data)], element_types=[m["element_type"]], delta=m["delta"],
+                       byte_group=m["byte_group"], block_size=m["block_size"],
+                       segment_count=m["segment_count"], buffer_size=m["buffer_size"])
+    assert b.to_bytes()[0] == stream
+
+
+@pytest.mark.parametrize("case", load_golden_streams(), ids=lambda c: c[0]["name"])
+def test_golden_stream_decode(codec, case):
+    m, data, stream = case
+    r = codec.decompress([dev_bytes(stream)])
+    assert r.status == [0]
+    assert r.lengths[0] == len(data)
+    assert host_bytes(r.payload(0)) == data
+    assert r.element_types[0] == m["element_type"]
+
+
+def test_golden_codebooks():
+    hists, lengths = load_golden_codebooks()
+    got = lmcb.build_codebooks(hists.astype(np.int64))
+    assert (got == lengths).all()
+
+
+def test_golden_corruption_classes(codec):
+    streams = {m["name"]: (d, s) for m, d, s in load_golden_streams()}
+    cases = load_golden_corruptions()
+    bads, wants = [], []
+    for c in cases:
+        data, s = streams[c["case"]]
+        if c["kind"] == "xor":
+            bad = bytearray(s)
+            bad[c["pos"]] ^= c["val"]
+        elif c["kind"] == "truncate":
+            bad = s[: c["pos"]]
+        else:
+            bad = s + b"\x00"
+        bads.append(bytes(bad))
+        wants.append(c["result"])
+    r = codec.decompress([dev_bytes(b) for b in bads])
+    names = {0: "ok", 1: "UnsupportedFormatError", 2: "CorruptStreamError", 3: "IntegrityError"}
+    got = [names[s] for s in r.status]
+    assert got == wants
+
+
+# ---------------------------------------------------------------- configs
+def _oracle_streams(tensors, ets, **opts):
+    return [O.compress(host_bytes(t.view(torch.uint8).reshape(-1)), et, threads=8, **opts)
+            for t, et in zip(tensors, ets)]
+
+
+def test_cfg1_full_parity(codec):
+    specs, ts = synth.make_checkpoint("cfg1", seed=1)
+    b = codec.compress(ts)
+    got = b.to_bytes()
+    want = _oracle_streams(ts, [1])
+    assert got == want
+    info = codec.block_info()
+    grouped = O.group_bytes(host_bytes(ts[0].view(torch.uint8).reshape(-1)), 2)
+    modes, bits, sizes, lengths, pm = O.analyze_blocks(grouped, 65536)
+    assert (info["modes"] == modes).all()
+    assert (info["sizes"] == sizes).all()
+    huff = modes == 0
+    assert (info["bits"][huff] == bits[huff]).all()
+    assert (info["lengths"][huff] == lengths[huff]).all()
+    assert pm.sum() > 0  # package-merge blocks are part of this config
+    r = codec.decompress(b)
+    assert r.status == [0]
+    assert torch.equal(r.payload(0), ts[0].view(torch.uint8).reshape(-1))
+
+
+def test_cfg2_gpt2_small_parity(codec):
+    specs, ts = synth.make_checkpoint("cfg2", seed=2)
+    assert len(ts) == 148
+    b = codec.compress(ts)
+    got = b.to_bytes()
+    want = _oracle_streams(ts, [1] * len(ts))
+    assert [len(x) for x in got] == [len(x) for x in want]
+    assert got == want
+    r = codec.decompress(b)
+    assert r.status == [0] * len(ts)
+    for i, t in enumerate(ts):
+        assert torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1)), specs[i].name
+
+
+def test_cfg3_rle_heavy_parity(codec):
+    specs, ts = synth.make_checkpoint("cfg3", seed=3)
+    b = codec.compress(ts)
+    got = b.to_bytes()
+    want = _oracle_streams(ts, [1, 1])
+    assert got == want
+    assert len(got[1]) == 236  # 28 + 16 + 32 x 6-byte RLE records
+    r = codec.decompress(b)
+    assert r.status == [0, 0]
+    for i, t in enumerate(ts):
+        assert torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1))
+
+
+def test_cfg4_delta_fused_xor_parity(codec):
+    # three layers of the 1.3B model (embedding window is misaligned: 2 windows)
+    specs, prev = synth.make_checkpoint("cfg4", seed=4, limit=14)
+    nxt = [synth.next_step(w, 4, i) for i, w in enumerate(prev)]
+    b = codec.compress(nxt, prev=prev)
+    got = b.to_bytes()
+    xors = [(p.view(torch.uint8) ^ q.view(torch.uint8)).reshape(-1) for p, q in zip(prev, nxt)]
+    want = [O.compress(host_bytes(x), 1, delta=True, threads=8) for x in xors]
+    assert got == want
+    r = codec.decompress(b)
+    assert r.status == [0] * len(nxt)
+    for i, x in enumerate(xors):
+        assert torch.equal(r.payload(i), x)
+
+
+@pytest.mark.parametrize("segs", [1, 4, 8, 16])
+@pytest.mark.parametrize("bg", [True, False])
+def test_options_matrix(codec, segs, bg):
+    g = torch.Generator(device="cuda").manual_seed(segs * 3 + bg)
+    ts = [
+        (torch.randn(300_001, generator=g, device="cuda") * 0.02).to(torch.bfloat16),
+        torch.randn(70_003, generator=g, device="cuda").to(torch.float32),
+        torch.randn(65_536, generator=g, device="cuda").to(torch.float16),
+        (torch.rand(100_000, generator=g, device="cuda") ** 4 * 255).to(torch.uint8),
+    ]
+    for bs, buf in [(4096, 3 * 4096 + 1000), (65536, 128 << 20), (8192, 8192)]:
+        b = codec.compress(ts, byte_group=bg, block_size=bs, segment_count=segs, buffer_size=buf)
+        got = b.to_bytes()
+        want = [O.compress(host_bytes(t.view(torch.uint8).reshape(-1)), et, byte_group=bg, block_size=bs,
+                           segment_count=segs, buffer_size=buf, threads=8) for t, et in zip(ts, [1, 3, 2, 0])]
+        assert got == want, (bs, buf)
+        r = codec.decompress(b)
+        assert r.status == [0] * len(ts)
+        for i, t in enumerate(ts):
+            assert torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1))
+
+
+def test_unaligned_device_views(codec):
+    base = (torch.randn(200_000, device="cuda") * 0.02).to(torch.bfloat16)
+    t = base[3:150_003]  # 6-byte offset: no 16-byte vector loads
+    b = codec.compress([t])
+    assert b.to_bytes()[0] == O.compress(host_bytes(t.contiguous().view(torch.uint8)), 1)
+
+
+# ------------------------------------------------- reference suite mirrors
+def test_boundary_sizes_round_trip(rng):
+    # test_stream.py:82-96 through the reference-shaped API
+    for size in [0, 1, 4095, 4096, 4097, 65536, 200_000]:
+        data = rng.integers(0, 256, size, dtype=np.uint8).tobytes()
+        for et in (ET.RAW8, ET.FP32):
+            if size % et.width:
+                continue
+            for bg in (True, False):
+                s = lmcb.lmc_compress(lmcb.TensorBuffer(data, et), byte_group=bg, block_size=4096)
+                assert s == O.compress(data, et.code, byte_group=bg, block_size=4096)
+                out = lmcb.lmc_decompress(s)
+                assert out.data == data and out.element_type is et
+
+
+def test_reference_strictness_cases():
+    s = lmcb.lmc_compress(lmcb.TensorBuffer(b"strict header checks", ET.RAW8))
+    for pos, value in [(5, 0x84), (7, 1)]:
+        bad = bytearray(s)
+        bad[pos] = value
+        with pytest.raises(lmcb.CorruptStreamError):
+            lmcb.lmc_decompress(bytes(bad))
+    with pytest.raises(lmcb.UnsupportedFormatError):
+        lmcb.lmc_decompress(b"XLC1" + s[4:])
+    with pytest.raises(lmcb.CorruptStreamError):
+        lmcb.lmc_decompress(s + b"\x00")
+    for et in ET:
+        e = lmcb.lmc_compress(lmcb.TensorBuffer(b"", et))
+        assert len(e) == 28 and lmcb.lmc_decompress(e).data == b""
+
+
+def test_single_byte_corruptions_never_silent(rng):
+    # test_stream.py:170-187
+    data = (rng.random(30_000) ** 2 * 256).astype(np.uint8).tobytes()
+    stream = lmcb.lmc_compress(lmcb.TensorBuffer(data, ET.BF16), block_size=4096)
+    codec = lmcb.stream.default_codec()
+    bads = []
+    for pos in list(range(0, len(stream), 113)) + list(rng.integers(0, len(stream), 120)):
+        bad = bytearray(stream)
+        bad[pos] ^= int(rng.integers(1, 256))
+        bads.append(bytes(bad))
+    r = codec.decompress([dev_bytes(b) for b in bads])
+    for i, b in enumerate(bads):
+        try:
+            O.decompress(b)
+            want = 0
+        except O.OracleError as exc:
+            want = exc.code
+        assert r.status[i] == want
+    assert all(s != 0 for s in r.status)
+
+
+def test_cross_decode_gpu_stream_by_oracle(codec):
+    ts = [(torch.randn(1 << 20, device="cuda") * 0.02).to(torch.bfloat16)]
+    b = codec.compress(ts, segment_count=3)
+    out, et, flags = O.decompress(b.to_bytes()[0])
+    assert out == host_bytes(ts[0].view(torch.uint8)) and et == 1 and flags == 1
