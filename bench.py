@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""LMC hot-path benchmark (BASELINE.json metric on configs[1], GPT-2-small).
+
+One step = compress every tensor of a synthetic GPT-2-small bf16 checkpoint
+(148 tensors, 237 MiB) into LMC1 streams and decompress them again, on each
+rank's GPU.  ``value`` is whole-job GiB/s of uncompressed checkpoint bytes
+through compress + decompress (inputs resident in HBM, streams kept in HBM);
+``e2e`` is the same round trip through the public API with pinned host
+buffers (host->device copy of the checkpoint, device->host copy of the
+streams, and back).  See DESIGN.md "Measurement".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = float(1 << 30)
+METRIC = "lmc compress+decompress round-trip throughput (uncompressed checkpoint GiB/s, whole job)"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks() -> tuple[float, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of `kernel` from the committed ncu summary, or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------ distributed
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------- reference arm
+def run_reference(args, ws, rank):
+    """Time the reference's algorithm on the host cores (C oracle port)."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2505_09810_b200 import synth
+
+    cores = os.cpu_count() or 1
+    specs = synth.CONFIGS[args.config]()
+    raws = _host_checkpoint(specs, seed=1000)
+    nbytes = sum(len(r) for r in raws)
+    # bounded sample: whole checkpoint when it fits ~60 s of total work
+    t0 = time.perf_counter()
+    s = [O.compress(r, 1, threads=cores) for r in raws[:8]]
+    [O.decompress(x, threads=cores) for x in s]
+    probe = time.perf_counter() - t0
+    probe_bytes = sum(len(r) for r in raws[:8])
+    est_step = probe / max(probe_bytes, 1) * nbytes
+    budget = 60.0 / max(args.steps + args.warmup, 1)
+    if est_step > budget:
+        keep, acc = [], 0
+        for r in raws:
+            keep.append(r)
+            acc += len(r)
+            if probe / max(probe_bytes, 1) * acc > budget:
+                break
+        raws = keep
+    sample_bytes = sum(len(r) for r in raws)
+    sample = (f"{args.config} synthetic bf16 checkpoint: {len(raws)} of {len(specs)} tensors, "
+              f"{sample_bytes / 2**20:.1f} MiB per step (compress + decompress, oracle C port, {cores} threads)")
+
+    def step():
+        st = [O.compress(r, 1, threads=cores) for r in raws]
+        for x in st:
+            O.decompress(x, threads=cores)
+        return st
+
+    for _ in range(args.warmup):
+        streams = step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        streams = step()
+    dt = time.perf_counter() - t0
+    value = sample_bytes * args.steps / dt / GIB
+    ratio = sum(len(x) for x in streams) / max(sample_bytes, 1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GiB/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": f"{args.config}: GPT-2-small bf16 checkpoint (148 tensors), every tensor its own "
+                               "LMC1 stream, byte_group=True, block_size=65536, segment_count=1, buffer_size=128MiB",
+                   "sample_tensors": len(raws)},
+        "compression_ratio": round(ratio, 6),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GiB/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GiB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _host_checkpoint(specs, seed):
+    """Host bytes of the synthetic checkpoint (generated with torch, CPU or GPU)."""
+    import torch
+
+    from paper_2505_09810_b200 import synth
+
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    out = []
+    for i, s in enumerate(specs):
+        t = synth.make_tensor(s, seed, i, device=dev)
+        out.append(t.view(torch.uint8).reshape(-1).cpu().numpy().tobytes())
+        del t
+    return out
+
+
+# ----------------------------------------------------------------- ours
+ALGO = {  # algorithmic bytes per launch, as multiples of (N_in, N_stream)
+    "k_encode": (1, 1), "k_hist_crc": (1, 0), "k_decode": (1, 1), "k_ungroup": (2, 0), "k_cand": (0, 1),
+}
+
+
+def run_ours(args, ws, rank, local):
+    import torch
+
+    import paper_2505_09810_b200 as lmcb
+    from paper_2505_09810_b200 import synth
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    specs, ts = synth.make_checkpoint(args.config, seed=1000 + rank, device="cuda")
+    nbytes = sum(t.numel() * t.element_size() for t in ts)
+    codec = lmcb.Codec(local)
+    stream = torch.cuda.current_stream()
+
+    def exchange(batch):
+        # container assembly across ranks: all-gather of per-stream sizes
+        if dist is None:
+            return None
+        lens = batch.lengths
+        g = [torch.empty_like(lens) for _ in range(ws)]
+        dist.all_gather(g, lens)
+        return torch.stack(g)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        b = codec.compress(ts)
+        exchange(b)
+        if ev:
+            ev[1].record(stream)
+        r = codec.decompress(b)
+        if ev:
+            ev[2].record(stream)
+        return b, r
+
+    # correctness gate before timing
+    b, r = step()
+    r.raise_for_status()
+    for i, t in enumerate(ts):
+        if not torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1)):
+            raise SystemExit(f"round trip mismatch on {specs[i].name}")
+    stream_bytes = b.total_bytes()
+    ratio = stream_bytes / nbytes
+    for _ in range(max(args.warmup - 1, 0)):
+        step()
+
+    # per-kernel launch times (separate, untimed pass)
+    codec.ctx.profile(True)
+    nprof = 3
+    for _ in range(nprof):
+        step()
+    prof = codec.ctx.profile_report()
+    codec.ctx.profile(False)
+    launches_per_step = sum(c for c, _ in prof.values()) / nprof
+
+    # timed region
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    if dist is not None:
+        dist.barrier()
+    total_ms = start.elapsed_time(end)
+    comp_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
+    dec_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
+    t = torch.tensor([total_ms, comp_ms, dec_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, comp_ms, dec_ms = t.tolist()
+    value = ws * nbytes * args.steps / (total_ms / 1e3) / GIB
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(codec, ts, args, ws, dist)
+
+    # roofline of the dominant kernel
+    peak, peak_src = measured_peaks()
+    dom = max(prof.items(), key=lambda kv: kv[1][1])
+    dname, (dcnt, dms) = dom
+    avg_ms = dms / dcnt
+    a_in, a_st = ALGO.get(dname, (1, 1))
+    algo_bytes = a_in * nbytes + a_st * stream_bytes   # per launch (one launch per batch)
+    achieved = algo_bytes / (avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": round(avg_ms, 4),
+                "share_of_step": round(dms / sum(v[1] for v in prof.values()), 4)}
+    # pipeline-level fractions (compress: in + stream, decompress: stream + out)
+    comp_s, dec_s = comp_ms / args.steps / 1e3, dec_ms / args.steps / 1e3
+    pipeline = {
+        "compress_gib_s": round(ws * nbytes / comp_s / GIB, 3),
+        "decompress_gib_s": round(ws * nbytes / dec_s / GIB, 3),
+        "compress_hbm_frac": round((nbytes + stream_bytes) / comp_s / 1e9 / peak, 4),
+        "decompress_hbm_frac": round((nbytes + stream_bytes) / dec_s / 1e9 / peak, 4),
+        "compress_ms": round(comp_s * 1e3, 4), "decompress_ms": round(dec_s * 1e3, 4),
+    }
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(ts)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GiB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": f"{args.config}: GPT-2-small bf16 checkpoint (148 tensors, "
+                                   f"{nbytes / 2**20:.1f} MiB per rank), every tensor its own LMC1 stream, "
+                                   "byte_group=True, block_size=65536, segment_count=1, buffer_size=128MiB",
+                       "l2": "inputs 249 MB > 126 MB L2 per step; no flush needed",
+                       "parallelism": f"dp{ws} (independent checkpoints per rank + all-gather of stream sizes)"},
+            "compression_ratio": round(ratio, 6),
+            "pipeline": pipeline,
+            "kernels_ms_per_step": {k: round(v[1] / nprof, 4) for k, v in sorted(prof.items())},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(round(launches_per_step * args.steps)),
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def measure_e2e(codec, ts, args, ws, dist):
+    import torch
+
+    host = [t.view(torch.uint8).reshape(-1).cpu().pin_memory() for t in ts]
+    nbytes = sum(h.numel() for h in host)
+    stream = torch.cuda.current_stream()
+    dev_in = [torch.empty_like(h, device="cuda") for h in host]
+    b = codec.compress(ts)
+    cap = b.total_bytes() + (1 << 20)
+    host_streams = torch.empty(cap, dtype=torch.uint8).pin_memory()
+    dev_streams = torch.empty(cap, dtype=torch.uint8, device="cuda")
+    host_out = torch.empty(nbytes + 16 * len(ts), dtype=torch.uint8).pin_memory()
+
+    def step():
+        for d, h in zip(dev_in, host):
+            d.copy_(h, non_blocking=True)
+        bb = codec.compress([d.view(t.dtype).view(t.shape) for d, t in zip(dev_in, ts)])
+        off, ln = bb.host_layout()  # syncs on the lengths
+        total = off[-1] + ln[-1]
+        host_streams[:total].copy_(bb.data[:total], non_blocking=True)
+        # ... and back: streams host -> device, decompress, payload device -> host
+        dev_streams[:total].copy_(host_streams[:total], non_blocking=True)
+        r = codec.decompress([dev_streams[o: o + n] for o, n in zip(off, ln)])
+        used = r.offsets[-1] + r.lengths[-1]
+        host_out[:used].copy_(r.data[:used], non_blocking=True)
+        return total
+
+    for _ in range(2):
+        step()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        sb = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = ms.item()
+    return {"value": round(ws * nbytes * args.steps / (ms / 1e3) / GIB, 3), "unit": "GiB/s",
+            "h2d_bytes_per_step": nbytes + sb, "d2h_bytes_per_step": sb + nbytes,
+            "path": "pinned host checkpoint -> H2D -> Codec.compress -> D2H streams -> H2D streams -> "
+                    "Codec.decompress -> D2H payload"}
+
+
+def cpu_baseline(ts):
+    """Oracle (C port of the reference algorithm) on the host cores, bounded sample."""
+    import torch
+
+    from oracle import oracle as O
+
+    cores = os.cpu_count() or 1
+    raws = [t.view(torch.uint8).reshape(-1).cpu().numpy().tobytes() for t in ts[2:26]]  # layers 0-1
+    nb = sum(len(r) for r in raws)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        st = [O.compress(r, 1, threads=cores) for r in raws]
+        for x in st:
+            O.decompress(x, threads=cores)
+        reps += 1
+        if time.perf_counter() - t0 > 8.0:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(nb * reps / dt / GIB, 4), "unit": "GiB/s", "cores": cores, "kind": "port",
+            "sample": f"GPT-2 layers 0-1 (24 tensors, {nb / 2**20:.1f} MiB) compress+decompress x{reps} "
+                      f"with the C oracle port, {cores} threads"}
+
+
+def main():
+    args = parse_args()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,13 @@ int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint
 int64_t lmcg_block_info(lmcg_ctx* ctx, int32_t* modes, uint32_t* bits, uint32_t* record_sizes,
                         uint8_t* codebook_wire /* cap x 128 */, uint32_t* pm_flags, int64_t cap);
 
+/* Measurement hooks (bench.py): bracket every kernel launch with CUDA events
+ * while enabled; lmcg_profile_report synchronises, writes lines
+ * "<kernel> <launches> <total_ms>" into buf, clears the counters and returns
+ * the report length. */
+int lmcg_profile(lmcg_ctx* ctx, int enable);
+int64_t lmcg_profile_report(lmcg_ctx* ctx, char* buf, uint64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,7 +42,7 @@ EXPORTS = [
     "lmcg_create", "lmcg_destroy", "lmcg_last_error", "lmcg_version", "lmcg_validate_options",
     "lmcg_compress_bound", "lmcg_compress_workspace", "lmcg_compress", "lmcg_decompress_plan",
     "lmcg_decompress_run", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
-    "lmcg_block_info",
+    "lmcg_block_info", "lmcg_profile", "lmcg_profile_report",
 ]
 
 _lib = None
@@ -87,6 +87,10 @@ def load(path: str = SO_PATH):
         L.lmcg_build_codebooks.argtypes = [vp, vp, ctypes.c_int, vp, vp]
         L.lmcg_block_info.restype = ctypes.c_int64
         L.lmcg_block_info.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int64]
+        L.lmcg_profile.restype = ctypes.c_int
+        L.lmcg_profile.argtypes = [vp, ctypes.c_int]
+        L.lmcg_profile_report.restype = ctypes.c_int64
+        L.lmcg_profile_report.argtypes = [vp, ctypes.c_char_p, u64]
         _lib = L
         return L
 
@@ -100,6 +104,19 @@ class Context:
         self.ptr = self.lib.lmcg_create(device)
         if not self.ptr:
             raise DeviceError("lmcg_create failed")
+
+    def profile(self, enable: bool) -> None:
+        self.lib.lmcg_profile(self.ptr, int(enable))
+
+    def profile_report(self) -> dict:
+        """{kernel: (launches, total_ms)} since the last report."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        self.lib.lmcg_profile_report(self.ptr, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms = line.split()
+            out[name] = (int(cnt), float(ms))
+        return out
 
     def error(self) -> str:
         return self.lib.lmcg_last_error(self.ptr).decode(errors="replace")

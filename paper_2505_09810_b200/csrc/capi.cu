@@ -46,6 +46,11 @@ struct lmcg_ctx {
     uint64_t nwin_t = 0, nseg_t = 0, nrec_t = 0, nchunk_t = 0, ntile_t = 0, scratch_t = 0;
     uint32_t irr_cap = 1u << 16;
     bool planned = false;
+    // per-kernel event timing (lmcg_profile)
+    bool prof = false;
+    std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+    std::vector<cudaEvent_t> prof_pool;
+    std::vector<std::pair<std::string, std::pair<double, uint64_t>>> prof_acc;
 };
 
 namespace {
@@ -154,6 +159,39 @@ struct Arena {
         return o;
     }
 };
+
+cudaEvent_t prof_event(lmcg_ctx* ctx) {
+    if (!ctx->prof_pool.empty()) {
+        cudaEvent_t e = ctx->prof_pool.back();
+        ctx->prof_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Brackets one kernel launch with events when profiling is enabled.
+struct ProfScope {
+    lmcg_ctx* ctx;
+    const char* name;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr;
+    ProfScope(lmcg_ctx* c, const char* n, cudaStream_t s) : ctx(c), name(n), st(s) {
+        if (ctx->prof) {
+            a = prof_event(ctx);
+            cudaEventRecord(a, st);
+        }
+    }
+    ~ProfScope() {
+        if (ctx->prof) {
+            cudaEvent_t b = prof_event(ctx);
+            cudaEventRecord(b, st);
+            ctx->prof_pending.push_back({name, {a, b}});
+        }
+    }
+};
+#define PROF(name) ProfScope prof_scope_##name(ctx, #name, st)
 
 bool host_valid_block(uint64_t b) { return b >= 4096 && b <= (1u << 20) && (b & (b - 1)) == 0; }
 
@@ -359,35 +397,70 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options
     CK(cudaMemsetAsync(d_status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     CK(cudaMemsetAsync(d_ctr, 0, 4 * sizeof(uint32_t), st));
     const int nwin = (int)P.wins.size();
-    if (nwin) k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win);
+    if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win); }
     if (P.nslots) {
-        k_hist_crc<<<(unsigned)P.nslots, kThreads, 0, st>>>(d_wins, d_slot2win, P.nslots, o->block_size, ctx->d_crc,
-                                                             d_hist, d_crcp, d_meta);
+        { PROF(k_hist_crc); k_hist_crc<<<(unsigned)P.nslots, kThreads, 0, st>>>(d_wins, d_slot2win, P.nslots, o->block_size, ctx->d_crc,
+                                                             d_hist, d_crcp, d_meta); }
     }
     if (nb) {
-        k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
-            d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist);
-        k_pkgmerge<<<296, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr);
+        { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
+            d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist); }
+        { PROF(k_pkgmerge); k_pkgmerge<<<296, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr); }
     }
-    k_scan<<<(unsigned)std::max<uint64_t>(ntiles, 1), kScanThreads, 0, st>>>(d_meta, nb, d_scan, d_status, d_ctr);
+    { PROF(k_scan); k_scan<<<(unsigned)std::max<uint64_t>(ntiles, 1), kScanThreads, 0, st>>>(d_meta, nb, d_scan, d_status, d_ctr); }
     if (n) {
-        k_layout<<<1, 1024, 0, st>>>(d_streams, n, o->segment_count, d_scan, d_soff, d_slen);
-        k_frame<<<n, kThreads, 0, st>>>(d_streams, d_wins, o->block_size, o->segment_count, d_scan, d_crcp,
-                                         ctx->d_crc, d_soff, static_cast<uint8_t*>(d_out));
+        { PROF(k_layout); k_layout<<<1, 1024, 0, st>>>(d_streams, n, o->segment_count, d_scan, d_soff, d_slen); }
+        { PROF(k_frame); k_frame<<<n, kThreads, 0, st>>>(d_streams, d_wins, o->block_size, o->segment_count, d_scan, d_crcp,
+                                         ctx->d_crc, d_soff, static_cast<uint8_t*>(d_out)); }
     }
     if (P.nslots) {
         const uint64_t iterpos = (uint64_t)(kTileBytes / P.min_w) * kWarps;
         const size_t smem = (size_t)((iterpos * 15) / 32 + 8) * sizeof(uint32_t);
         if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_encode<<<(unsigned)P.nslots, kThreads, smem, st>>>(d_wins, d_slot2win, P.nslots, o->block_size,
+        { PROF(k_encode); k_encode<<<(unsigned)P.nslots, kThreads, smem, st>>>(d_wins, d_slot2win, P.nslots, o->block_size,
                                                             o->segment_count, d_streams, d_meta, d_wire, d_scan, d_soff,
-                                                            static_cast<uint8_t*>(d_out));
+                                                            static_cast<uint8_t*>(d_out)); }
     }
     CK(cudaGetLastError());
     ctx->last_nb = nb;
     ctx->last_meta = d_meta;
     ctx->last_wire = d_wire;
     return LMCG_OK;
+}
+
+int lmcg_profile(lmcg_ctx* ctx, int enable) {
+    if (!ctx) return LMCG_ERR_ARGUMENT;
+    ctx->prof = enable != 0;
+    return LMCG_OK;
+}
+
+int64_t lmcg_profile_report(lmcg_ctx* ctx, char* buf, uint64_t cap) {
+    if (!ctx) return -LMCG_ERR_ARGUMENT;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -LMCG_ERR_CUDA;
+    for (auto& pe : ctx->prof_pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pe.second.first, pe.second.second);
+        bool found = false;
+        for (auto& a : ctx->prof_acc)
+            if (a.first == pe.first) { a.second.first += ms; a.second.second++; found = true; break; }
+        if (!found) ctx->prof_acc.push_back({pe.first, {ms, 1}});
+        ctx->prof_pool.push_back(pe.second.first);
+        ctx->prof_pool.push_back(pe.second.second);
+    }
+    ctx->prof_pending.clear();
+    std::string out;
+    for (auto& a : ctx->prof_acc) {
+        char line[160];
+        snprintf(line, sizeof line, "%s %llu %.6f\n", a.first.c_str(), (unsigned long long)a.second.second, a.second.first);
+        out += line;
+    }
+    if (buf && cap) {
+        const size_t k = std::min<size_t>(out.size(), cap - 1);
+        memcpy(buf, out.data(), k);
+        buf[k] = 0;
+    }
+    ctx->prof_acc.clear();
+    return (int64_t)out.size();
 }
 
 int64_t lmcg_block_info(lmcg_ctx* ctx, int32_t* modes, uint32_t* bits, uint32_t* record_sizes, uint8_t* wire,
@@ -420,9 +493,9 @@ int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint
     uint32_t* d_ctr = reinterpret_cast<uint32_t*>(ctx->ws);
     uint32_t* d_list = reinterpret_cast<uint32_t*>(ctx->ws + 256);
     CK(cudaMemsetAsync(d_ctr, 0, 16, st));
-    k_codebook<<<(nhist + kCbWarps - 1) / kCbWarps, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
-                                                                             d_lengths, d_ctr, d_ctr + 1, d_list);
-    k_pkgmerge<<<296, 32, 0, st>>>(d_hists, d_ctr + 1, d_list, nullptr, nullptr, d_lengths);
+    { PROF(k_codebook); k_codebook<<<(nhist + kCbWarps - 1) / kCbWarps, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
+                                                                             d_lengths, d_ctr, d_ctr + 1, d_list); }
+    { PROF(k_pkgmerge); k_pkgmerge<<<296, 32, 0, st>>>(d_hists, d_ctr + 1, d_list, nullptr, nullptr, d_lengths); }
     CK(cudaGetLastError());
     uint32_t flag = 0;
     CK(cudaMemcpyAsync(&flag, d_ctr, 4, cudaMemcpyDeviceToHost, st));
@@ -448,7 +521,7 @@ int lmcg_decompress_plan(lmcg_ctx* ctx, const void* const* d_streams, const uint
     DecStreamHdr* d_hdr = reinterpret_cast<DecStreamHdr*>(ctx->dws + ((n * sizeof(DecStreamIn) + 255) & ~size_t(255)));
     if (n) {
         CK(cudaMemcpyAsync(d_in, ctx->din.data(), n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
-        k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 1, d_hdr, nullptr, nullptr, nullptr, nullptr);
+        { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 1, d_hdr, nullptr, nullptr, nullptr, nullptr); }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(ctx->dhdr.data(), d_hdr, n * sizeof(DecStreamHdr), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -533,20 +606,20 @@ int lmcg_decompress_run(lmcg_ctx* ctx, void* d_out, const uint64_t* h_out_offset
         }
         CK(cudaMemsetAsync(d_ctr, 0, 16, st));
         CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
-        if (n) k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 2, d_hdr, d_plan, d_win, d_seg, d_wt0);
+        if (n) { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 2, d_hdr, d_plan, d_win, d_seg, d_wt0); }
         if (ctx->nchunk_t)
-            k_cand<<<(unsigned)ctx->nchunk_t, 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, ctx->nchunk_t, d_cc, d_cp);
+            { PROF(k_cand); k_cand<<<(unsigned)ctx->nchunk_t, 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, ctx->nchunk_t, d_cc, d_cp); }
         if (ctx->nseg_t)
-            k_link<<<(unsigned)((ctx->nseg_t + 3) / 4), 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, d_win, d_cc, d_cp, d_rec,
-                                                                       d_irr, d_ctr, ctx->irr_cap, d_st, d_scr);
+            { PROF(k_link); k_link<<<(unsigned)((ctx->nseg_t + 3) / 4), 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, d_win, d_cc, d_cp, d_rec,
+                                                                       d_irr, d_ctr, ctx->irr_cap, d_st, d_scr); }
         {
             const unsigned grid = (unsigned)std::min<uint64_t>(std::max<uint64_t>(ctx->nrec_t, 148), 148 * 8);
-            k_decode<<<grid, kThreads, 0, st>>>(d_rec, ctx->nrec_t, d_irr, d_ctr, d_st);
+            { PROF(k_decode); k_decode<<<grid, kThreads, 0, st>>>(d_rec, ctx->nrec_t, d_irr, d_ctr, d_st); }
         }
         if (ctx->ntile_t)
-            k_ungroup<<<(unsigned)ctx->ntile_t, kThreads, 0, st>>>(d_win, d_wt0, ctx->nwin_t, ctx->ntile_t, d_scr,
-                                                                   static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_te, d_st);
-        if (n) k_finalize<<<n, kThreads, 0, st>>>(d_hdr, d_plan, n, d_tc, d_te, ctx->d_crc, d_st);
+            { PROF(k_ungroup); k_ungroup<<<(unsigned)ctx->ntile_t, kThreads, 0, st>>>(d_win, d_wt0, ctx->nwin_t, ctx->ntile_t, d_scr,
+                                                                   static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_te, d_st); }
+        if (n) { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_hdr, d_plan, n, d_tc, d_te, ctx->d_crc, d_st); }
         CK(cudaGetLastError());
         std::vector<uint32_t> stv(n + 1);
         CK(cudaMemcpyAsync(stv.data(), d_st, (n + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
