@@ -8,7 +8,7 @@
  *   lmcg_compress / lmcg_compress_host
  *       <- lmc.stream.lmc_compress          (pkg/src/lmc/stream.py:311-341)
  *       <- lmc.parallel.plmc_compress       (pkg/src/lmc/parallel.py:53-103)
- *   lmcg_decompress_plan + lmcg_decompress_run / lmcg_decompress_host
+ *   lmcg_decompress (+ lmcg_read_hints, lmcg_decompress_result) / lmcg_decompress_host
  *       <- lmc.stream.lmc_decompress        (pkg/src/lmc/stream.py:406-423)
  *       <- lmc.parallel.plmc_decompress     (pkg/src/lmc/parallel.py:106-128)
  *   lmcg_validate_options
@@ -48,6 +48,7 @@ extern "C" {
 #define LMCG_ERR_CUDA 7               /* no device / CUDA runtime failure             */
 #define LMCG_ERR_CAPACITY 8           /* caller buffer too small                      */
 #define LMCG_ERR_ARGUMENT 9           /* bad argument (NULL pointer, n < 0, ...)      */
+#define LMCG_ERR_RETRY 10             /* decompress hints too small: call again        */
 
 /* ElementType wire codes (types.py:24-27) */
 #define LMCG_RAW8 0
@@ -96,21 +97,39 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* tensors, int n, const lmcg_o
                   void* d_out, uint64_t out_capacity, uint64_t* d_offsets, uint64_t* d_lengths,
                   void* d_workspace, uint64_t workspace_bytes, void* cuda_stream);
 
-/* Decompress, phase 1: parse and validate n device-resident streams
- * (stream.py:114-142, 358-389).  Synchronises cuda_stream.  Per stream it
- * returns the original length, element type code, flags and a status
- * (LMCG_OK, or the error the reference would raise).  The parsed plan stays
- * in the context for lmcg_decompress_run. */
-int lmcg_decompress_plan(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* stream_lengths,
-                         int n, uint64_t* h_orig_lengths, int32_t* h_element_types, int32_t* h_flags,
-                         int32_t* h_status, void* cuda_stream);
+/* What the caller knows about a stream before decoding it: the header's
+ * original_length / segment_count / block_size and, if known, the number of
+ * windows (0 = assume the default 128 MiB buffer).  Used only to size the
+ * device work areas; a wrong hint costs a retry, never a wrong result. */
+typedef struct {
+    uint64_t orig;
+    uint32_t segments;
+    uint32_t block;
+    uint64_t windows;
+} lmcg_stream_hint;
 
-/* Decompress, phase 2: decode the planned streams.  Stream i's payload is
- * written to d_out + h_out_offsets[i] (capacity h_orig_lengths[i]).  On return
- * (synchronised) h_status[i] holds LMCG_OK / LMCG_ERR_CORRUPT /
- * LMCG_ERR_INTEGRITY / LMCG_ERR_UNSUPPORTED per stream. */
-int lmcg_decompress_run(lmcg_ctx* ctx, void* d_out, const uint64_t* h_out_offsets, int32_t* h_status,
-                        void* cuda_stream);
+/* Exact hints for n device streams: validates headers and segment tables on
+ * the device (nothing is decoded) and reports their structure (synchronises).
+ * Streams the walk rejects get all-zero hints; lmcg_decompress then reports
+ * their error. */
+int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* stream_lengths, int n,
+                    lmcg_stream_hint* hints, void* cuda_stream);
+
+/* Decompress n device-resident streams (stream.py:406-423 semantics, all
+ * validation of stream.py:114-142, 234-268, 358-389 on the device).  Stream
+ * i's payload goes to d_out + h_out_offsets[i] (or, when h_out_offsets is
+ * NULL, packed at 16-byte aligned offsets in stream order).  Asynchronous:
+ * no host synchronisation; read the outcome with lmcg_decompress_result. */
+int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* stream_lengths, int n,
+                    const lmcg_stream_hint* hints, void* d_out, uint64_t out_capacity,
+                    const uint64_t* h_out_offsets, void* cuda_stream);
+
+/* Synchronise and report the last lmcg_decompress per stream: status
+ * (LMCG_OK / UNSUPPORTED / CORRUPT / INTEGRITY, or LMCG_ERR_RETRY /
+ * LMCG_ERR_CAPACITY when the hints were too small), original length, element
+ * type, flags and window count.  Any pointer may be NULL. */
+int lmcg_decompress_result(lmcg_ctx* ctx, int n, int32_t* h_status, uint64_t* h_orig_lengths,
+                           int32_t* h_element_types, int32_t* h_flags, uint64_t* h_windows);
 
 /* Host-buffer conveniences (the call a ctypes binding in lmc.stream makes):
  * host -> device copy, the GPU path above, device -> host copy. */

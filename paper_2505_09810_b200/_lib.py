@@ -37,11 +37,20 @@ class lmcg_options(ctypes.Structure):
     ]
 
 
+class lmcg_stream_hint(ctypes.Structure):
+    _fields_ = [
+        ("orig", ctypes.c_uint64),
+        ("segments", ctypes.c_uint32),
+        ("block", ctypes.c_uint32),
+        ("windows", ctypes.c_uint64),
+    ]
+
+
 # every symbol include/lmc_b200.h declares (tests check the export table)
 EXPORTS = [
     "lmcg_create", "lmcg_destroy", "lmcg_last_error", "lmcg_version", "lmcg_validate_options",
-    "lmcg_compress_bound", "lmcg_compress_workspace", "lmcg_compress", "lmcg_decompress_plan",
-    "lmcg_decompress_run", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
+    "lmcg_compress_bound", "lmcg_compress_workspace", "lmcg_compress", "lmcg_read_hints",
+    "lmcg_decompress", "lmcg_decompress_result", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
     "lmcg_block_info", "lmcg_profile", "lmcg_profile_report",
 ]
 
@@ -75,10 +84,12 @@ def load(path: str = SO_PATH):
         L.lmcg_compress_workspace.argtypes = [P(lmcg_tensor), ctypes.c_int, P(lmcg_options)]
         L.lmcg_compress.restype = ctypes.c_int
         L.lmcg_compress.argtypes = [vp, P(lmcg_tensor), ctypes.c_int, P(lmcg_options), vp, u64, vp, vp, vp, u64, vp]
-        L.lmcg_decompress_plan.restype = ctypes.c_int
-        L.lmcg_decompress_plan.argtypes = [vp, P(vp), P(u64), ctypes.c_int, P(u64), P(i32), P(i32), P(i32), vp]
-        L.lmcg_decompress_run.restype = ctypes.c_int
-        L.lmcg_decompress_run.argtypes = [vp, vp, P(u64), P(i32), vp]
+        L.lmcg_read_hints.restype = ctypes.c_int
+        L.lmcg_read_hints.argtypes = [vp, P(vp), P(u64), ctypes.c_int, P(lmcg_stream_hint), vp]
+        L.lmcg_decompress.restype = ctypes.c_int
+        L.lmcg_decompress.argtypes = [vp, P(vp), P(u64), ctypes.c_int, P(lmcg_stream_hint), vp, u64, P(u64), vp]
+        L.lmcg_decompress_result.restype = ctypes.c_int
+        L.lmcg_decompress_result.argtypes = [vp, ctypes.c_int, P(i32), P(u64), P(i32), P(i32), P(u64)]
         L.lmcg_compress_host.restype = ctypes.c_int
         L.lmcg_compress_host.argtypes = [vp, vp, u64, ctypes.c_int, ctypes.c_int, P(lmcg_options), vp, u64, P(u64)]
         L.lmcg_decompress_host.restype = ctypes.c_int

@@ -37,15 +37,15 @@ struct lmcg_ctx {
     size_t d_in_cap = 0;
     uint8_t* d_out = nullptr;
     size_t d_out_cap = 0;
-    // decompress plan
-    std::vector<DecStreamIn> din;
-    std::vector<DecStreamHdr> dhdr;
-    std::vector<DecStreamPlan> dplan;
+    // decompress
     uint8_t* dws = nullptr;   // decompress workspace
     size_t dws_cap = 0;
-    uint64_t nwin_t = 0, nseg_t = 0, nrec_t = 0, nchunk_t = 0, ntile_t = 0, scratch_t = 0;
-    uint32_t irr_cap = 1u << 16;
-    bool planned = false;
+    uint8_t* hws = nullptr;   // probe workspace
+    size_t hws_cap = 0;
+    int dn = -1;
+    const void* d_sout = nullptr;
+    const uint32_t* d_dstatus = nullptr;
+    bool dec_attr = false;
     // per-kernel event timing (lmcg_profile)
     bool prof = false;
     std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -99,7 +99,7 @@ void build_crc_tables(CrcTables& t) {
         for (int i = 0; i < 256; i++) t.slice[k][i] = (t.slice[k - 1][i] >> 8) ^ t.slice[0][t.slice[k - 1][i] & 0xFF];
     t.x2n[0] = 1u << 30;  // x^1
     for (int k = 1; k < 64; k++) t.x2n[k] = h_multmodp(t.x2n[k - 1], t.x2n[k - 1]);
-    for (int lvl = 0; lvl < 8; lvl++) {
+    for (int lvl = 0; lvl < 9; lvl++) {
         const uint64_t nbytes = 64ull << lvl;
         // x^(8 nbytes)
         uint32_t p = 1u << 31;
@@ -282,6 +282,7 @@ void lmcg_destroy(lmcg_ctx* ctx) {
         cudaFree(ctx->d_crc);
         if (ctx->ws) cudaFree(ctx->ws);
         if (ctx->dws) cudaFree(ctx->dws);
+        if (ctx->hws) cudaFree(ctx->hws);
         if (ctx->d_in) cudaFree(ctx->d_in);
         if (ctx->d_out) cudaFree(ctx->d_out);
         if (ctx->pin) cudaFreeHost(ctx->pin);
@@ -505,142 +506,200 @@ int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint
 }
 
 // ------------------------------------------------------------------ decompress
-int lmcg_decompress_plan(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
-                         uint64_t* h_orig, int32_t* h_et, int32_t* h_flags, int32_t* h_status, void* cuda_stream) {
-    if (!ctx || n < 0 || (n && (!d_streams || !lens))) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+namespace {
+
+struct DPlan {
+    std::vector<DecCaps> caps;
+    uint64_t nwin = 0, nseg = 0, nrec = 0, nchunk = 0, ntile = 0, scratch = 0;
+};
+
+void make_dplan(const uint64_t* lens, int n, const lmcg_stream_hint* hints, const uint64_t* out_off,
+                uint64_t out_capacity, DPlan& P) {
+    P.caps.assign(n, DecCaps{});
+    uint64_t packed = 0;
+    for (int i = 0; i < n; i++) {
+        const lmcg_stream_hint& h = hints[i];
+        DecCaps& c = P.caps[i];
+        const uint64_t body = lens[i] > kHeader ? lens[i] - kHeader : 0;
+        const uint64_t S = std::min<uint64_t>(std::max<uint32_t>(h.segments, 1), body / kSegEntry + 1);
+        const uint64_t B = host_valid_block(h.block) ? h.block : 4096;
+        uint64_t nw = h.windows ? h.windows : (h.orig + (128ull << 20) - 1) / (128ull << 20);
+        nw = std::min<uint64_t>(nw, body / (kSegEntry * S) + 1);
+        c.win0 = P.nwin; c.nwin = nw;
+        c.seg0 = P.nseg; c.nseg = nw * S;
+        c.rec0 = P.nrec; c.nrec = (h.orig + B - 1) / B + c.nseg;
+        c.chunk0 = P.nchunk; c.nchunk = (lens[i] + kChunk - 1) / kChunk + c.nseg;
+        c.tile0 = P.ntile; c.ntile = (h.orig + kOutTile - 1) / kOutTile + nw;
+        c.scratch0 = P.scratch; c.scratch = ((h.orig + 15) & ~15ull) + 16 * nw;
+        if (out_off) {
+            c.out0 = out_off[i];
+            c.out = out_off[i] <= out_capacity ? std::min<uint64_t>(h.orig, out_capacity - out_off[i]) : 0;
+        } else {
+            c.out0 = packed;
+            c.out = packed <= out_capacity ? std::min<uint64_t>(h.orig, out_capacity - packed) : 0;
+            packed += (h.orig + 15) & ~15ull;
+        }
+        P.nwin += c.nwin; P.nseg += c.nseg; P.nrec += c.nrec; P.nchunk += c.nchunk; P.ntile += c.ntile;
+        P.scratch += c.scratch;
+    }
+}
+
+int occupancy(lmcg_ctx* ctx, const void* fn, int threads, size_t smem) {
+    int per = 0, dev = ctx->device, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return std::max(1, per) * std::max(1, sms);
+}
+
+}  // namespace
+
+int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n, lmcg_stream_hint* hints,
+                    void* cuda_stream) {
+    if (!ctx || n < 0 || (n && (!d_streams || !lens || !hints))) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
     if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
     if (int r = ensure_ctx(ctx)) return r;
+    if (!n) return LMCG_OK;
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    ctx->planned = false;
-    ctx->din.resize(n);
-    for (int i = 0; i < n; i++) ctx->din[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i]};
-    ctx->dhdr.assign(n, DecStreamHdr{});
-    const size_t need = (size_t)n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr)) + 1024;
-    if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, need)) return r;
-    DecStreamIn* d_in = reinterpret_cast<DecStreamIn*>(ctx->dws);
-    DecStreamHdr* d_hdr = reinterpret_cast<DecStreamHdr*>(ctx->dws + ((n * sizeof(DecStreamIn) + 255) & ~size_t(255)));
-    if (n) {
-        CK(cudaMemcpyAsync(d_in, ctx->din.data(), n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
-        { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 1, d_hdr, nullptr, nullptr, nullptr, nullptr); }
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(ctx->dhdr.data(), d_hdr, n * sizeof(DecStreamHdr), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-    }
-    ctx->dplan.assign(n, DecStreamPlan{});
-    uint64_t win = 0, seg = 0, rec = 0, chunk = 0, tile = 0, scr = 0;
+    // probe: the parse kernel with empty capacity regions validates headers and
+    // tables and reports the exact structure without writing any descriptor
+    Arena a;
+    const size_t o_in = a.take<DecStreamIn>(n + 1);
+    const size_t o_caps = a.take<DecCaps>(n + 1);
+    const size_t o_out = a.take<DecStreamOut>(n + 1);
+    if (int r = grow(ctx, &ctx->hws, &ctx->hws_cap, a.off + 256)) return r;
+    auto* d_in = reinterpret_cast<DecStreamIn*>(ctx->hws + o_in);
+    auto* d_caps = reinterpret_cast<DecCaps*>(ctx->hws + o_caps);
+    auto* d_sout = reinterpret_cast<DecStreamOut*>(ctx->hws + o_out);
+    std::vector<DecStreamIn> in(n);
+    for (int i = 0; i < n; i++) in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i]};
+    CK(cudaMemcpyAsync(d_in, in.data(), n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_caps, 0, n * sizeof(DecCaps), st));
+    k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, nullptr, nullptr);
+    CK(cudaGetLastError());
+    std::vector<DecStreamOut> so(n);
+    CK(cudaMemcpyAsync(so.data(), d_sout, n * sizeof(DecStreamOut), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     for (int i = 0; i < n; i++) {
-        const DecStreamHdr& h = ctx->dhdr[i];
-        DecStreamPlan& p = ctx->dplan[i];
-        p.win0 = win; p.seg0 = seg; p.rec0 = rec; p.chunk0 = chunk; p.tile0 = tile; p.scratch = scr;
-        if (!h.status) {
-            p.nchunk = (lens[i] + kCandChunk - 1) / kCandChunk + h.nseg;
-            p.ntile = (h.orig + kOutTile - 1) / kOutTile + h.nwin;
-            win += h.nwin; seg += h.nseg; rec += h.nrec; chunk += p.nchunk; tile += p.ntile;
-            scr += ((h.orig + 15) & ~15ull) + 16ull * h.nwin;
+        lmcg_stream_hint h{};
+        if (so[i].status == ST_RETRY || so[i].status == 0) {
+            h.orig = so[i].orig;
+            h.segments = so[i].segs;
+            h.block = so[i].block;
+            h.windows = so[i].nwin;
         }
-        if (h_orig) h_orig[i] = h.status ? 0 : h.orig;
-        if (h_et) h_et[i] = (int32_t)h.et;
-        if (h_flags) h_flags[i] = (int32_t)h.flags;
-        if (h_status) h_status[i] = (h.status & ST_UNSUPPORTED) ? LMCG_ERR_UNSUPPORTED : (h.status ? LMCG_ERR_CORRUPT : LMCG_OK);
+        hints[i] = h;
     }
-    ctx->nwin_t = win; ctx->nseg_t = seg; ctx->nrec_t = rec; ctx->nchunk_t = chunk; ctx->ntile_t = tile;
-    ctx->scratch_t = scr;
-    ctx->planned = true;
     return LMCG_OK;
 }
 
-int lmcg_decompress_run(lmcg_ctx* ctx, void* d_out, const uint64_t* h_out_offsets, int32_t* h_status, void* cuda_stream) {
-    if (!ctx || !ctx->planned) return fail(ctx, LMCG_ERR_ARGUMENT, "lmcg_decompress_run without a plan");
+int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
+                    const lmcg_stream_hint* hints, void* d_out, uint64_t out_capacity, const uint64_t* h_out_offsets,
+                    void* cuda_stream) {
+    if (!ctx || n < 0 || (n && (!d_streams || !lens || !hints))) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+    if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
     if (int r = ensure_ctx(ctx)) return r;
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    const int n = (int)ctx->din.size();
-    for (int attempt = 0; attempt < 4; attempt++) {
-        for (int i = 0; i < n; i++) ctx->dplan[i].out = h_out_offsets ? h_out_offsets[i] : 0;
-        Arena a;
-        const size_t o_in = a.take<DecStreamIn>(n + 1);
-        const size_t o_hdr = a.take<DecStreamHdr>(n + 1);
-        const size_t o_plan = a.take<DecStreamPlan>(n + 1);
-        const size_t o_win = a.take<DecWin>(ctx->nwin_t + 1);
-        const size_t o_wt0 = a.take<uint64_t>(ctx->nwin_t + 1);
-        const size_t o_seg = a.take<DecSeg>(ctx->nseg_t + 1);
-        const size_t o_cc = a.take<uint32_t>(ctx->nchunk_t + 1);
-        const size_t o_cp = a.take<uint32_t>((ctx->nchunk_t + 1) * kCandCap);
-        const size_t o_rec = a.take<DecRec>(ctx->nrec_t + 1);
-        const size_t o_irr = a.take<DecRec>(ctx->irr_cap);
-        const size_t o_ctr = a.take<uint32_t>(4);
-        const size_t o_st = a.take<uint32_t>(n + 1);
-        const size_t o_tc = a.take<uint32_t>(ctx->ntile_t + 1);
-        const size_t o_te = a.take<uint64_t>(ctx->ntile_t + 1);
-        const size_t o_scr = a.take<uint8_t>(ctx->scratch_t + 64);
-        // keep the parse inputs: they sit at the front of the same buffer
-        std::vector<DecStreamHdr> hdr_keep = ctx->dhdr;
-        if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, a.off + 256)) return r;
-        uint8_t* ws = ctx->dws;
-        auto* d_in = reinterpret_cast<DecStreamIn*>(ws + o_in);
-        auto* d_hdr = reinterpret_cast<DecStreamHdr*>(ws + o_hdr);
-        auto* d_plan = reinterpret_cast<DecStreamPlan*>(ws + o_plan);
-        auto* d_win = reinterpret_cast<DecWin*>(ws + o_win);
-        auto* d_wt0 = reinterpret_cast<uint64_t*>(ws + o_wt0);
-        auto* d_seg = reinterpret_cast<DecSeg*>(ws + o_seg);
-        auto* d_cc = reinterpret_cast<uint32_t*>(ws + o_cc);
-        auto* d_cp = reinterpret_cast<uint32_t*>(ws + o_cp);
-        auto* d_rec = reinterpret_cast<DecRec*>(ws + o_rec);
-        auto* d_irr = reinterpret_cast<DecRec*>(ws + o_irr);
-        auto* d_ctr = reinterpret_cast<uint32_t*>(ws + o_ctr);
-        auto* d_st = reinterpret_cast<uint32_t*>(ws + o_st);
-        auto* d_tc = reinterpret_cast<uint32_t*>(ws + o_tc);
-        auto* d_te = reinterpret_cast<uint64_t*>(ws + o_te);
-        uint8_t* d_scr = ws + o_scr;
-        const size_t hb = n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr) + sizeof(DecStreamPlan)) + 64;
-        if (int r = grow_pinned(ctx, hb)) return r;
-        uint8_t* pp = ctx->pin;
-        if (n) {
-            memcpy(pp, ctx->din.data(), n * sizeof(DecStreamIn));
-            memcpy(pp + n * sizeof(DecStreamIn), hdr_keep.data(), n * sizeof(DecStreamHdr));
-            memcpy(pp + n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr)), ctx->dplan.data(), n * sizeof(DecStreamPlan));
-            CK(cudaMemcpyAsync(d_in, pp, n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_hdr, pp + n * sizeof(DecStreamIn), n * sizeof(DecStreamHdr), cudaMemcpyHostToDevice, st));
-            CK(cudaMemcpyAsync(d_plan, pp + n * (sizeof(DecStreamIn) + sizeof(DecStreamHdr)), n * sizeof(DecStreamPlan),
-                               cudaMemcpyHostToDevice, st));
-            CK(cudaEventRecord(ctx->pin_done, st));
-        }
-        CK(cudaMemsetAsync(d_ctr, 0, 16, st));
-        CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
-        if (n) { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, n, 2, d_hdr, d_plan, d_win, d_seg, d_wt0); }
-        if (ctx->nchunk_t)
-            { PROF(k_cand); k_cand<<<(unsigned)ctx->nchunk_t, 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, ctx->nchunk_t, d_cc, d_cp); }
-        if (ctx->nseg_t)
-            { PROF(k_link); k_link<<<(unsigned)((ctx->nseg_t + 3) / 4), 128, 0, st>>>(d_in, d_seg, ctx->nseg_t, d_win, d_cc, d_cp, d_rec,
-                                                                       d_irr, d_ctr, ctx->irr_cap, d_st, d_scr); }
-        {
-            const unsigned grid = (unsigned)std::min<uint64_t>(std::max<uint64_t>(ctx->nrec_t, 148), 148 * 8);
-            { PROF(k_decode); k_decode<<<grid, kThreads, 0, st>>>(d_rec, ctx->nrec_t, d_irr, d_ctr, d_st); }
-        }
-        if (ctx->ntile_t)
-            { PROF(k_ungroup); k_ungroup<<<(unsigned)ctx->ntile_t, kThreads, 0, st>>>(d_win, d_wt0, ctx->nwin_t, ctx->ntile_t, d_scr,
-                                                                   static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_te, d_st); }
-        if (n) { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_hdr, d_plan, n, d_tc, d_te, ctx->d_crc, d_st); }
-        CK(cudaGetLastError());
-        std::vector<uint32_t> stv(n + 1);
-        CK(cudaMemcpyAsync(stv.data(), d_st, (n + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        bool cap = false;
-        for (int i = 0; i < n; i++) cap |= (stv[i] & ST_CAPACITY) != 0;
-        if (cap) {
-            ctx->irr_cap *= 16;
-            continue;
-        }
-        for (int i = 0; i < n; i++) {
-            const uint32_t s = hdr_keep[i].status | stv[i];
-            int32_t code = LMCG_OK;
-            if (s & ST_UNSUPPORTED) code = LMCG_ERR_UNSUPPORTED;
-            else if (s & ST_CORRUPT) code = LMCG_ERR_CORRUPT;
-            else if (s & ST_INTEGRITY) code = LMCG_ERR_INTEGRITY;
-            if (h_status) h_status[i] = code;
-        }
-        return LMCG_OK;
+    ctx->dn = n;
+    DPlan P;
+    make_dplan(lens, n, hints, h_out_offsets, out_capacity, P);
+    Arena a;
+    const size_t o_in = a.take<DecStreamIn>(n + 1);
+    const size_t o_caps = a.take<DecCaps>(n + 1);
+    const size_t o_out = a.take<DecStreamOut>(n + 1);
+    const size_t o_st = a.take<uint32_t>(n + 1);
+    const size_t o_win = a.take<DecWin>(P.nwin + 1);
+    const size_t o_seg = a.take<DecSeg>(P.nseg + 1);
+    const size_t o_cst = a.take<uint64_t>(P.nchunk + 1);
+    const size_t o_tk = a.take<uint32_t>(4);
+    const size_t o_scnt = a.take<uint32_t>(P.nseg + 1);
+    const size_t o_sfail = a.take<uint32_t>(P.nseg + 1);
+    const size_t o_rpos = a.take<uint64_t>(P.nrec + 1);
+    const size_t o_rnext = a.take<uint64_t>(P.nrec + 1);
+    const size_t o_tc = a.take<uint32_t>(P.ntile + 1);
+    const size_t o_scr = a.take<uint8_t>(P.scratch + 64);
+    if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, a.off + 256)) return r;
+    uint8_t* ws = ctx->dws;
+    auto* d_in = reinterpret_cast<DecStreamIn*>(ws + o_in);
+    auto* d_caps = reinterpret_cast<DecCaps*>(ws + o_caps);
+    auto* d_sout = reinterpret_cast<DecStreamOut*>(ws + o_out);
+    auto* d_st = reinterpret_cast<uint32_t*>(ws + o_st);
+    auto* d_win = reinterpret_cast<DecWin*>(ws + o_win);
+    auto* d_seg = reinterpret_cast<DecSeg*>(ws + o_seg);
+    auto* d_cst = reinterpret_cast<uint64_t*>(ws + o_cst);
+    auto* d_tk = reinterpret_cast<uint32_t*>(ws + o_tk);
+    auto* d_scnt = reinterpret_cast<uint32_t*>(ws + o_scnt);
+    auto* d_sfail = reinterpret_cast<uint32_t*>(ws + o_sfail);
+    auto* d_rpos = reinterpret_cast<uint64_t*>(ws + o_rpos);
+    auto* d_rnext = reinterpret_cast<uint64_t*>(ws + o_rnext);
+    auto* d_tc = reinterpret_cast<uint32_t*>(ws + o_tc);
+    uint8_t* d_scr = ws + o_scr;
+    ctx->d_sout = d_sout;
+    ctx->d_dstatus = d_st;
+    const size_t hb = (size_t)n * (sizeof(DecStreamIn) + sizeof(DecCaps)) + 64;
+    if (int r = grow_pinned(ctx, hb)) return r;
+    if (n) {
+        DecStreamIn* pin_in = reinterpret_cast<DecStreamIn*>(ctx->pin);
+        for (int i = 0; i < n; i++) pin_in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i]};
+        memcpy(ctx->pin + (size_t)n * sizeof(DecStreamIn), P.caps.data(), (size_t)n * sizeof(DecCaps));
+        CK(cudaMemcpyAsync(d_in, ctx->pin, (size_t)n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(d_caps, ctx->pin + (size_t)n * sizeof(DecStreamIn), (size_t)n * sizeof(DecCaps),
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(ctx->pin_done, st));
     }
-    return fail(ctx, LMCG_ERR_CAPACITY, "irregular record capacity exhausted");
+    CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
+    CK(cudaMemsetAsync(d_cst, 0, (P.nchunk + 1) * sizeof(uint64_t), st));
+    CK(cudaMemsetAsync(d_tk, 0, 16, st));
+    CK(cudaMemsetAsync(d_sfail, 0, (P.nseg + 1) * sizeof(uint32_t), st));
+    if (!n) return LMCG_OK;
+    const size_t dsm = sizeof(DecSmem);
+    if (!ctx->dec_attr) {
+        CK(cudaFuncSetAttribute(k_scandec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        CK(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        ctx->dec_attr = true;
+    }
+    { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg); }
+    if (P.nchunk) {
+        const int grid = (int)std::min<uint64_t>(P.nchunk, (uint64_t)occupancy(ctx, (const void*)k_scandec, kThreads, dsm));
+        PROF(k_scandec);
+        k_scandec<<<grid, kThreads, dsm, st>>>(d_seg, P.nseg, P.nchunk, d_tk, d_cst, d_scnt, d_sfail, d_rpos, d_rnext, d_scr);
+    }
+    if (P.nrec) { PROF(k_verify); k_verify<<<(unsigned)((P.nrec + 255) / 256), 256, 0, st>>>(d_seg, P.nseg, P.nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
+    if (P.nseg) {
+        const int grid = (int)std::min<uint64_t>(P.nseg, 148 * 2);
+        PROF(k_fallback);
+        k_fallback<<<grid, kThreads, dsm, st>>>(d_seg, P.nseg, d_sfail, d_st, d_scr);
+    }
+    if (P.ntile) { PROF(k_ungroup); k_ungroup<<<(unsigned)P.ntile, kThreads, 0, st>>>(d_win, P.nwin, P.ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_st); }
+    { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st); }
+    CK(cudaGetLastError());
+    return LMCG_OK;
+}
+
+int lmcg_decompress_result(lmcg_ctx* ctx, int n, int32_t* h_status, uint64_t* h_orig, int32_t* h_et, int32_t* h_flags,
+                           uint64_t* h_windows) {
+    if (!ctx || n != ctx->dn || !ctx->d_sout) return fail(ctx, LMCG_ERR_ARGUMENT, "no decompress to report on");
+    if (int r = ensure_ctx(ctx)) return r;
+    std::vector<DecStreamOut> so(n);
+    std::vector<uint32_t> st(n);
+    if (n) {
+        CK(cudaMemcpy(so.data(), ctx->d_sout, n * sizeof(DecStreamOut), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(st.data(), ctx->d_dstatus, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    }
+    for (int i = 0; i < n; i++) {
+        const uint32_t s = so[i].status | st[i];
+        int32_t code = LMCG_OK;
+        if (s & ST_UNSUPPORTED) code = LMCG_ERR_UNSUPPORTED;
+        else if (s & ST_CORRUPT) code = LMCG_ERR_CORRUPT;
+        else if (s & ST_RETRY) code = LMCG_ERR_RETRY;
+        else if (s & ST_CAPACITY) code = LMCG_ERR_CAPACITY;
+        else if (s & ST_INTEGRITY) code = LMCG_ERR_INTEGRITY;
+        if (h_status) h_status[i] = code;
+        if (h_orig) h_orig[i] = so[i].orig;
+        if (h_et) h_et[i] = (int32_t)so[i].et;
+        if (h_flags) h_flags[i] = (int32_t)so[i].flags;
+        if (h_windows) h_windows[i] = so[i].nwin;
+    }
+    return LMCG_OK;
 }
 
 // ------------------------------------------------------------ host wrappers
@@ -677,20 +736,28 @@ int lmcg_decompress_host(lmcg_ctx* ctx, const void* stream, uint64_t len, void* 
     if (int r = grow(ctx, &ctx->d_in, &ctx->d_in_cap, len + 16)) return r;
     if (len) CK(cudaMemcpy(ctx->d_in, stream, len, cudaMemcpyHostToDevice));
     const void* p = ctx->d_in;
-    uint64_t orig = 0;
-    int32_t e = 0, f = 0, s = 0;
-    if (int r = lmcg_decompress_plan(ctx, &p, &len, 1, &orig, &e, &f, &s, nullptr)) return r;
-    if (s) return fail(ctx, s, "stream rejected by the header/table walk");
-    *out_len = orig;
-    if (et) *et = e;
-    if (flags) *flags = f;
-    if (orig > out_capacity) return fail(ctx, LMCG_ERR_CAPACITY, "payload of %llu bytes exceeds capacity", (unsigned long long)orig);
-    if (int r = grow(ctx, &ctx->d_out, &ctx->d_out_cap, orig + 64)) return r;
-    const uint64_t off = 0;
-    if (int r = lmcg_decompress_run(ctx, ctx->d_out, &off, &s, nullptr)) return r;
-    if (s) return fail(ctx, s, s == LMCG_ERR_INTEGRITY ? "payload CRC mismatch" : "corrupt stream");
-    if (orig) CK(cudaMemcpy(out, ctx->d_out, orig, cudaMemcpyDeviceToHost));
-    return LMCG_OK;
+    lmcg_stream_hint h{};
+    if (int r = lmcg_read_hints(ctx, &p, &len, 1, &h, nullptr)) return r;
+    for (int attempt = 0; attempt < 3; attempt++) {
+        if (int r = grow(ctx, &ctx->d_out, &ctx->d_out_cap, h.orig + 64)) return r;
+        if (int r = lmcg_decompress(ctx, &p, &len, 1, &h, ctx->d_out, ctx->d_out_cap, nullptr, nullptr)) return r;
+        int32_t s = 0, e = 0, f = 0;
+        uint64_t orig = 0, nw = 0;
+        if (int r = lmcg_decompress_result(ctx, 1, &s, &orig, &e, &f, &nw)) return r;
+        if (s == LMCG_ERR_RETRY || s == LMCG_ERR_CAPACITY) {
+            h.orig = orig;
+            h.windows = nw;
+            continue;
+        }
+        if (s) return fail(ctx, s, s == LMCG_ERR_INTEGRITY ? "payload CRC mismatch" : "stream rejected");
+        *out_len = orig;
+        if (et) *et = e;
+        if (flags) *flags = f;
+        if (orig > out_capacity) return fail(ctx, LMCG_ERR_CAPACITY, "payload of %llu bytes exceeds capacity", (unsigned long long)orig);
+        if (orig) CK(cudaMemcpy(out, ctx->d_out, orig, cudaMemcpyDeviceToHost));
+        return LMCG_OK;
+    }
+    return fail(ctx, LMCG_ERR_CORRUPT, "stream structure does not converge");
 }
 
 }  // extern "C"

@@ -1,254 +1,582 @@
 // decompress.cu -- B200 kernels of the LMC decompress path.
 //
-//   k_parse      header + window/segment-table walk with the reference's exact
-//                validation (stream.py:114-142, 358-389); pass 1 counts,
-//                pass 2 writes window / segment descriptors
-//   k_cand       record discovery, step 1: every 4 KiB chunk of every segment
-//                is scanned for record headers "mode<=2 | len==block_size"
-//   k_link       record discovery, step 2 (warp per segment): the candidates
-//                must chain exactly (p -> p + record size) through the
-//                canonical record lengths; otherwise the segment is walked
-//                serially exactly like decompress_segment (stream.py:234-268)
-//   k_decode     persistent CTA-per-record decoder: RLE fill, stored copy, and
-//                Huffman decode with self-synchronising chunked parallel
-//                decoding (huffman.py:258-349 semantics, stream.py:190-215)
-//   k_ungroup    inverse byte-grouping of each window (bytegroup.py:53-62,
-//                stream.py:392-403) + raw CRC-32 of every 16 KiB output tile
-//   k_finalize   per-stream CRC combine and status (stream.py:416-423)
+// The host lays out, from per-stream hints (original length, segment count,
+// window count: exact for streams this library produced, header-derived
+// otherwise), fixed capacity regions for every stream's windows, segments,
+// record slots, scan chunks and output tiles.  The whole pipeline then runs
+// without a host round trip:
+//
+//   k_parse     one thread per stream: header + window/segment-table walk
+//               with the reference's exact validation (stream.py:114-142,
+//               358-389); writes window / segment descriptors (or RETRY when
+//               a stream does not fit the hinted capacities)
+//   k_scandec   persistent, ticket-ordered CTAs over 64 KiB chunks of segment
+//               payload: find record-header candidates "mode<=2|len==block",
+//               number them with a segmented decoupled look-back, and decode
+//               every candidate record straight away (RLE fill, stored copy,
+//               self-synchronising parallel Huffman decode, stream.py:190-215,
+//               huffman.py:258-349) into the grouped scratch
+//   k_verify    one thread per record slot: candidates must chain exactly
+//               (p -> p + record size) with the canonical record lengths
+//   k_fallback  segments that failed verification are re-walked serially,
+//               exactly like decompress_segment (stream.py:234-268), and
+//               re-decoded -- the authoritative path for any stream
+//   k_ungroup   inverse byte-grouping per window (bytegroup.py:53-62) + raw
+//               CRC-32 of each 16 KiB output tile
+//   k_finalize  per-stream CRC combine and status (stream.py:416-423)
 #include "lmc_common.cuh"
 
 namespace lmcg {
 
-constexpr int kCandChunk = 4096;   // bytes of segment payload per k_cand CTA
-constexpr int kCandCap = 32;       // candidates kept per chunk
-constexpr int kOutTile = 16384;    // output bytes per k_ungroup CTA
-constexpr uint8_t kSkip = 0xFF;
+constexpr int kChunk = 65536;        // segment payload bytes per k_scandec chunk
+constexpr int kOutTile = 16384;      // output bytes per k_ungroup CTA
+constexpr int kStage = 49152;        // Huffman bitstream bytes staged in shared memory
+constexpr int kLut = 11;             // LUT index bits
+constexpr int kCkpt = 4;             // self-sync checkpoints per decode chunk
+constexpr int kMine = 8;             // candidates a thread keeps per chunk
 
-enum : uint32_t { ST_CORRUPT = 1, ST_INTEGRITY = 2, ST_UNSUPPORTED = 4, ST_CAPACITY = 8 };
+enum : uint32_t { ST_CORRUPT = 1, ST_INTEGRITY = 2, ST_UNSUPPORTED = 4, ST_RETRY = 8, ST_CAPACITY = 16 };
 
 struct DecStreamIn {
     const uint8_t* p;
     uint64_t len;
 };
 
-// per stream, written by k_parse pass 1 (and read back by the host)
-struct DecStreamHdr {
-    uint64_t orig;
-    uint32_t status;   // ST_* bits
-    uint32_t et, flags, block, segs, crc;
-    uint32_t nwin;
-    uint32_t pad;
-    uint64_t nseg;
-    uint64_t nrec;     // canonical record count = sum ceil(seg_orig / block)
+// Per-stream capacity regions (host-computed from hints).
+struct DecCaps {
+    uint64_t win0, nwin;
+    uint64_t seg0, nseg;
+    uint64_t rec0, nrec;
+    uint64_t chunk0, nchunk;
+    uint64_t tile0, ntile;
+    uint64_t scratch0, scratch;
+    uint64_t out0, out;       // output offset and capacity
 };
 
-// per stream, computed by the host after pass 1
-struct DecStreamPlan {
-    uint64_t win0, seg0, rec0;      // global first window / segment / record
-    uint64_t chunk0, nchunk;        // k_cand chunk range (upper bound)
-    uint64_t tile0, ntile;          // k_ungroup tile range (upper bound)
-    uint64_t scratch;               // grouped scratch offset (16-aligned)
-    uint64_t out;                   // output offset (caller's layout)
+// Per-stream parse result (device; read back by the host with the status).
+struct DecStreamOut {
+    uint64_t orig;
+    uint32_t status;
+    uint32_t et, flags, crc;
+    uint32_t nwin, nseg;       // actual counts (valid also on RETRY)
+    uint64_t nrec, nchunk, ntile, scratch;
+    uint32_t segs, block;
 };
 
 struct DecWin {
-    uint64_t W, n;          // window bytes, bytes per plane
-    uint64_t goff;          // absolute scratch offset (16-aligned)
-    uint64_t ooff;          // absolute output offset
-    uint64_t soff;          // window start inside the stream's original payload
-    uint32_t w, stream;
+    uint64_t W, n;
+    uint64_t goff;            // absolute scratch offset (16-aligned)
+    uint64_t ooff;            // absolute output offset
+    uint64_t soff;            // window start within the stream payload
+    uint64_t tile0;           // global first tile
+    uint32_t ntile, w, stream, pad;
 };
 
 struct DecSeg {
-    uint64_t comp_off;      // segment start (byte offset inside its stream)
-    uint64_t comp_len;
-    uint64_t orig_off;      // offset inside the window's grouped bytes
-    uint64_t orig_len;
-    uint64_t rec0;          // global index of the first canonical record slot
-    uint64_t chunk0;        // global index of the first k_cand chunk
-    uint32_t win, stream;
-    uint32_t nrec, block;
-};
-
-struct DecRec {
-    const uint8_t* src;     // record start (mode byte)
-    uint8_t* dst;           // grouped scratch destination
-    uint32_t len;           // original block length
-    uint32_t psize;         // payload bytes
-    uint32_t stream;
-    uint8_t mode;
-    uint8_t pad[3];
+    const uint8_t* base;      // segment payload start
+    uint64_t comp, orig;      // compressed / original bytes
+    uint64_t goff;            // absolute scratch offset of the segment's first byte
+    uint64_t rec0, chunk0;    // global first record slot / chunk
+    uint32_t nrec, nchunk;    // canonical records, scan chunks
+    uint32_t block, stream;
 };
 
 __device__ __forceinline__ uint32_t rd32(const uint8_t* p) {
     return (uint32_t)p[0] | ((uint32_t)p[1] << 8) | ((uint32_t)p[2] << 16) | ((uint32_t)p[3] << 24);
 }
 __device__ __forceinline__ uint64_t rd64(const uint8_t* p) { return (uint64_t)rd32(p) | ((uint64_t)rd32(p + 4) << 32); }
-
 __device__ __forceinline__ bool valid_block(uint32_t b) { return b >= 4096 && b <= (1u << 20) && (b & (b - 1)) == 0; }
 
 // ---------------------------------------------------------------- k_parse
-// One thread per stream.  pass 1: validate + count; pass 2: write descriptors.
-__global__ void k_parse(const DecStreamIn* __restrict__ in, int ns, int pass, DecStreamHdr* __restrict__ hdr,
-                        const DecStreamPlan* __restrict__ plan, DecWin* __restrict__ wins, DecSeg* __restrict__ segs,
-                        uint64_t* __restrict__ win_tile0) {
+__global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __restrict__ caps, int ns,
+                        DecStreamOut* __restrict__ sout, DecWin* __restrict__ wins, DecSeg* __restrict__ segs) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
     const uint8_t* p = in[s].p;
     const uint64_t len = in[s].len;
-    DecStreamHdr h;
-    if (pass == 2) {
-        h = hdr[s];
-        if (h.status) return;
-    } else {
-        h.orig = 0; h.status = 0; h.et = 0; h.flags = 0; h.block = 0; h.segs = 0; h.crc = 0;
-        h.nwin = 0; h.pad = 0; h.nseg = 0; h.nrec = 0;
-        // parse_header (stream.py:114-142)
-        if (len < kHeader || p[0] != 'L' || p[1] != 'M' || p[2] != 'C' || p[3] != '1' || p[4] != 1) {
-            h.status = ST_UNSUPPORTED; hdr[s] = h; return;
-        }
-        const uint32_t flags = p[5], et = p[6];
-        h.flags = flags; h.et = et;
-        h.orig = rd64(p + 8); h.block = rd32(p + 16); h.segs = rd32(p + 20); h.crc = rd32(p + 24);
-        const uint32_t width = et == 0 ? 1 : (et == 3 ? 4 : 2);
-        if ((flags & ~3u) || p[7] != 0 || et > 3 || !valid_block(h.block) || h.segs < 1 || (h.orig % width)) {
-            h.status = ST_CORRUPT; hdr[s] = h; return;
-        }
-    }
-    const uint32_t width = h.et == 0 ? 1 : (h.et == 3 ? 4 : 2);
-    const uint32_t wdt = (h.flags & 1) ? width : 1;
-    const uint64_t B = h.block, S = h.segs;
-    // iter_windows (stream.py:358-389)
-    uint64_t off = kHeader, remaining = h.orig, opos = 0;
-    uint64_t nwin = 0, nseg = 0, nrec = 0, ntile = 0, scr = 0;
-    const uint64_t table = kSegEntry * S;
-    const DecStreamPlan pl = (pass == 2) ? plan[s] : DecStreamPlan{};
-    uint64_t chunk = 0;
+    const DecCaps cp = caps[s];
+    DecStreamOut h = {};
+    uint64_t nwin = 0, nseg = 0, nrec = 0, nchunk = 0, ntile = 0, scr = 0;
     bool bad = false;
-    while (remaining > 0) {
-        if (table > len - off) { bad = true; break; }
-        uint64_t wsum = 0;
-        bool over = false;
-        for (uint64_t i = 0; i < S; i++) {
-            const uint64_t o = rd64(p + off + i * kSegEntry);
-            if (o > remaining - wsum) over = true;
-            else wsum += o;
-        }
-        const uint64_t toff = off;
-        off += table;
-        if (over || wsum == 0) { bad = true; break; }
-        const uint64_t W = wsum;
-        if ((h.flags & 1) && (W % width)) { bad = true; break; }   // reassemble_window
-        uint64_t gpos = 0;
-        for (uint64_t i = 0; i < S; i++) {
-            const uint64_t so = rd64(p + toff + i * kSegEntry), sc = rd64(p + toff + i * kSegEntry + 8);
-            if (sc > len - off) { bad = true; break; }
-            if ((so == 0) != (sc == 0)) { bad = true; break; }
-            const uint64_t r = (so + B - 1) / B;
-            if (pass == 2) {
-                DecSeg d;
-                d.comp_off = off; d.comp_len = sc; d.orig_off = gpos; d.orig_len = so;
-                d.rec0 = pl.rec0 + nrec; d.chunk0 = pl.chunk0 + chunk;
-                d.win = (uint32_t)(pl.win0 + nwin); d.stream = (uint32_t)s;
-                d.nrec = (uint32_t)r; d.block = (uint32_t)B;
-                segs[pl.seg0 + nseg] = d;
+    // parse_header (stream.py:114-142)
+    if (len < kHeader || p[0] != 'L' || p[1] != 'M' || p[2] != 'C' || p[3] != '1' || p[4] != 1) {
+        h.status = ST_UNSUPPORTED;
+    } else {
+        h.flags = p[5];
+        h.et = p[6];
+        h.orig = rd64(p + 8);
+        const uint32_t B = rd32(p + 16), S = rd32(p + 20);
+        h.block = B;
+        h.segs = S;
+        h.crc = rd32(p + 24);
+        const uint32_t width = h.et == 0 ? 1 : (h.et == 3 ? 4 : 2);
+        if ((h.flags & ~3u) || p[7] != 0 || h.et > 3 || !valid_block(B) || S < 1 || (h.orig % width)) {
+            h.status = ST_CORRUPT;
+        } else {
+            const uint32_t wdt = (h.flags & 1) ? width : 1;
+            const uint64_t table = (uint64_t)kSegEntry * S;
+            uint64_t off = kHeader, remaining = h.orig, opos = 0;
+            // iter_windows (stream.py:358-389)
+            while (remaining > 0 && !bad) {
+                if (table > len - off) { bad = true; break; }
+                uint64_t wsum = 0;
+                bool over = false;
+                for (uint64_t i = 0; i < S; i++) {
+                    const uint64_t o = rd64(p + off + i * kSegEntry);
+                    if (o > remaining - wsum) over = true;
+                    else wsum += o;
+                }
+                const uint64_t toff = off;
+                off += table;
+                if (over || wsum == 0) { bad = true; break; }
+                const uint64_t W = wsum;
+                if ((h.flags & 1) && (W % width)) { bad = true; break; }  // reassemble_window
+                const uint64_t wtiles = (W + kOutTile - 1) / kOutTile;
+                if (nwin < cp.nwin && ntile + wtiles <= cp.ntile && scr + W <= cp.scratch) {
+                    DecWin d;
+                    d.W = W; d.n = W / wdt; d.w = wdt; d.stream = (uint32_t)s; d.pad = 0;
+                    d.goff = cp.scratch0 + scr; d.ooff = cp.out0 + opos; d.soff = opos;
+                    d.tile0 = cp.tile0 + ntile; d.ntile = (uint32_t)wtiles;
+                    wins[cp.win0 + nwin] = d;
+                }
+                uint64_t gpos = 0;
+                for (uint64_t i = 0; i < S; i++) {
+                    const uint64_t so = rd64(p + toff + i * kSegEntry), sc = rd64(p + toff + i * kSegEntry + 8);
+                    if (sc > len - off) { bad = true; break; }
+                    if ((so == 0) != (sc == 0)) { bad = true; break; }
+                    // records are >= 6 bytes and decode to <= B bytes: anything more cannot
+                    // walk (stream.py:240-250), so it is corrupt without looking further
+                    if (so > (sc / 6) * (uint64_t)B) { bad = true; break; }
+                    const uint64_t r = (so + B - 1) / B;
+                    const uint64_t ch = (sc + kChunk - 1) / kChunk;
+                    if (nseg < cp.nseg && nrec + r <= cp.nrec && nchunk + ch <= cp.nchunk && scr + W <= cp.scratch) {
+                        DecSeg d;
+                        d.base = p + off; d.comp = sc; d.orig = so;
+                        d.goff = cp.scratch0 + scr + gpos;
+                        d.rec0 = cp.rec0 + nrec; d.chunk0 = cp.chunk0 + nchunk;
+                        d.nrec = (uint32_t)r; d.nchunk = (uint32_t)ch; d.block = B; d.stream = (uint32_t)s;
+                        segs[cp.seg0 + nseg] = d;
+                    }
+                    nrec += r;
+                    nchunk += ch;
+                    nseg++;
+                    off += sc;
+                    gpos += so;
+                }
+                ntile += wtiles;
+                scr += (W + 15) & ~15ull;
+                nwin++;
+                opos += W;
+                remaining -= W;
             }
-            chunk += (sc + kCandChunk - 1) / kCandChunk;
-            nrec += r;
-            nseg++;
-            off += sc;
-            gpos += so;
+            if (!bad && off != len) bad = true;  // trailing bytes (stream.py:388-389)
+            if (bad) h.status = ST_CORRUPT;
+            else if (nwin > cp.nwin || nseg > cp.nseg || nrec > cp.nrec || nchunk > cp.nchunk || ntile > cp.ntile ||
+                     scr > cp.scratch)
+                h.status = ST_RETRY;
+            else if (h.orig > cp.out)
+                h.status = ST_CAPACITY;
         }
-        if (bad) break;
-        if (pass == 2) {
-            DecWin d;
-            d.W = W; d.n = W / wdt; d.w = wdt; d.stream = (uint32_t)s;
-            d.goff = pl.scratch + scr; d.ooff = pl.out + opos; d.soff = opos;
-            wins[pl.win0 + nwin] = d;
-            win_tile0[pl.win0 + nwin] = pl.tile0 + ntile;
-        }
-        ntile += (W + kOutTile - 1) / kOutTile;
-        scr += (W + 15) & ~15ull;
-        nwin++;
-        opos += W;
-        remaining -= W;
     }
-    if (!bad && off != len) bad = true;   // trailing bytes (stream.py:388-389)
-    if (pass == 1) {
-        if (bad) { h.status = ST_CORRUPT; hdr[s] = h; return; }
-        h.nwin = (uint32_t)nwin; h.nseg = nseg; h.nrec = nrec;
-        hdr[s] = h;
+    h.nwin = (uint32_t)nwin; h.nseg = (uint32_t)nseg; h.nrec = nrec; h.nchunk = nchunk; h.ntile = ntile; h.scratch = scr;
+    sout[s] = h;
+    // padding descriptors: unused (or rejected) capacity slots stay well-formed
+    const bool ok = h.status == 0;
+    const uint64_t used_w = ok ? nwin : 0, used_s = ok ? nseg : 0;
+    const uint64_t end_rec = cp.rec0 + (ok ? nrec : 0), end_chunk = cp.chunk0 + (ok ? nchunk : 0);
+    const uint64_t end_tile = cp.tile0 + (ok ? ntile : 0);
+    for (uint64_t i = used_w; i < cp.nwin; i++) {
+        DecWin d = {};
+        d.tile0 = end_tile; d.stream = (uint32_t)s;
+        wins[cp.win0 + i] = d;
+    }
+    for (uint64_t i = used_s; i < cp.nseg; i++) {
+        DecSeg d = {};
+        d.rec0 = end_rec; d.chunk0 = end_chunk; d.stream = (uint32_t)s; d.block = 4096;
+        segs[cp.seg0 + i] = d;
     }
 }
 
-// ----------------------------------------------------------------- k_cand
-// CTA per 4 KiB chunk of segment payload.  A candidate is a position where a
-// record header "mode <= 2 | len == block_size" fits, plus the segment start.
-__global__ void __launch_bounds__(128) k_cand(const DecStreamIn* __restrict__ in, const DecSeg* __restrict__ segs,
-                                              uint64_t nseg_total, uint64_t nchunk_total,
-                                              uint32_t* __restrict__ cand_cnt, uint32_t* __restrict__ cand_pos) {
-    __shared__ uint8_t buf[kCandChunk + 8];
-    __shared__ uint32_t sh_w[4];
-    const uint64_t chunk = blockIdx.x;
-    if (chunk >= nchunk_total) return;
-    // segment owning this chunk: last seg with chunk0 <= chunk
-    uint64_t lo = 0, hi = nseg_total;
-    while (hi - lo > 1) {
-        uint64_t mid = (lo + hi) >> 1;
-        if (segs[mid].chunk0 <= chunk) lo = mid; else hi = mid;
-    }
-    const DecSeg sg = segs[lo];
-    const uint64_t nch = (sg.comp_len + kCandChunk - 1) / kCandChunk;
-    if (chunk < sg.chunk0 || chunk >= sg.chunk0 + nch) {
-        if (threadIdx.x == 0) cand_cnt[chunk] = 0;
-        return;
-    }
-    const uint64_t c0 = (chunk - sg.chunk0) * kCandChunk;
-    const uint64_t avail = min((uint64_t)(sg.comp_len - c0), (uint64_t)(kCandChunk + 8));
-    const uint8_t* base = in[sg.stream].p + sg.comp_off + c0;
-    for (int i = threadIdx.x; i < kCandChunk + 8; i += 128) buf[i] = i < (int)avail ? base[i] : 0xFF;
-    __syncthreads();
-    const uint32_t B = sg.block;
-    const uint64_t npos = min((uint64_t)(sg.comp_len - c0), (uint64_t)(kCandChunk));
-    uint32_t mask = 0;
-    for (int q = 0; q < 32; q++) {
-        const int i = threadIdx.x * 32 + q;
-        if ((uint64_t)i >= npos) break;
-        const uint64_t pos = c0 + i;
-        bool cand = (pos == 0);
-        if (!cand && pos + 5 <= sg.comp_len && buf[i] <= 2) {
-            const uint32_t l = (uint32_t)buf[i + 1] | ((uint32_t)buf[i + 2] << 8) | ((uint32_t)buf[i + 3] << 16) |
-                               ((uint32_t)buf[i + 4] << 24);
-            cand = (l == B);
+// ------------------------------------------------------- Huffman decoding
+struct DecSmem {
+    uint32_t bits[kStage / 4 + 8];      // staged bitstream, big-endian words
+    uint32_t mlut[1 << kLut];           // two-symbol LUT: n(2)|l1(4)|l12(5)|pad|s1(8)|s2(8)
+    union {
+        uint16_t slut[1 << kLut];       // single-symbol LUT (len << 8 | sym), build time only
+        struct {
+            uint32_t end[kThreads];
+            uint32_t ckpos[kCkpt][kThreads], ckcnt[kCkpt][kThreads];
+        } ch;
+    } u;
+    uint8_t lens[256];
+    uint8_t csym[256];
+    uint32_t first_left[17], first_idx[17], bl_count[17];
+    uint32_t cnt_w[kWarps][16];
+    uint32_t wsum[kWarps];
+    uint32_t kraft;
+    int minlen, maxlen;
+    // k_scandec bookkeeping
+    uint32_t cand[kThreads];
+    uint32_t base;
+    uint64_t tile;
+};
+
+struct Bits {
+    // reads from the staged shared copy when available, else from global
+    const uint32_t* sw;        // shared words (big-endian) or null
+    const uint8_t* gbase;      // 4-aligned global base
+    uint64_t glimit;           // payload end in bytes from gbase
+    uint64_t nwords_full;
+    uint32_t sh;               // bit offset of bit 0 from gbase / shared word 0
+    __device__ __forceinline__ uint32_t word(uint64_t j) const {
+        if (sw) return sw[j];
+        if (j < nwords_full) return bswap32(__ldg(reinterpret_cast<const uint32_t*>(gbase) + j));
+        uint32_t v = 0;
+        for (int q = 0; q < 4; q++) {
+            const uint64_t o = j * 4 + q;
+            v = (v << 8) | (o < glimit ? gbase[o] : 0u);
         }
-        if (cand) mask |= 1u << q;
+        return v;
     }
-    // ordered compaction
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t c = __popc(mask);
-    uint32_t incl = c;
+};
+
+struct Reader {
+    uint64_t buf;
+    int nb;
+    uint64_t next;
+    __device__ __forceinline__ void init(const Bits& B, uint32_t bitpos) {
+        const uint64_t abit = (uint64_t)bitpos + B.sh;
+        const uint64_t j = abit >> 5;
+        const int k = (int)(abit & 31);
+        buf = (((uint64_t)B.word(j) << 32) | B.word(j + 1)) << k;
+        nb = 64 - k;
+        next = j + 2;
+    }
+    __device__ __forceinline__ void refill(const Bits& B) {
+        if (nb <= 32) {
+            buf |= (uint64_t)B.word(next) << (32 - nb);
+            nb += 32;
+            next++;
+        }
+    }
+};
+
+// Long-code path: canonical limit search for codes longer than kLut bits.
+__device__ __forceinline__ uint32_t long_code(const DecSmem& s, uint32_t win15, uint32_t& sym) {
+    for (int q = kLut + 1; q <= s.maxlen; q++) {
+        const uint32_t fl = s.first_left[q], endq = fl + (s.bl_count[q] << (kMaxLen - q));
+        if (s.bl_count[q] && win15 >= fl && win15 < endq) {
+            sym = s.csym[s.first_idx[q] + ((win15 - fl) >> (kMaxLen - q))];
+            return q;
+        }
+    }
+    return 0;
+}
+
+// Decode the codewords starting in [pos, lim).  Returns the first boundary
+// >= lim (or ~0u on an invalid prefix) and the symbol count.
+//   MODE 0: count only, record kCkpt (boundary, count) checkpoints
+//   MODE 1: count only, stop early when landing on a recorded checkpoint
+//           (*sync = its index; the rest of the path is identical)
+//   MODE 2: emit the symbols to dst
+template <int MODE>
+__device__ uint32_t decode_span(DecSmem& s, const Bits& B, uint32_t pos, uint32_t lim, uint32_t& count, uint8_t* dst,
+                                int* sync) {
+    const int tid = threadIdx.x;
+    Reader r;
+    r.init(B, pos);
+    uint32_t c = 0;
+    uint64_t acc_lo = 0, acc_hi = 0;
+    int nacc = 0;
+    uint64_t o = 0;
+    const uint32_t step = (lim - pos) / (kCkpt + 1);
+    int ck = 0;
+    uint32_t ck_next = pos + step;
+    int sp = 0;
+    while (pos < lim) {
+        r.refill(B);
+        const uint32_t e = s.mlut[r.buf >> (64 - kLut)];
+        uint32_t nsym, l1, l12, s1, s2;
+        if (e) {
+            nsym = e >> 30;
+            l1 = (e >> 26) & 15;
+            l12 = (e >> 21) & 31;
+            s1 = (e >> 8) & 0xFF;
+            s2 = e & 0xFF;
+            if (nsym == 2 && pos + l1 >= lim) nsym = 1;  // second symbol starts past the span
+        } else {
+            l1 = long_code(s, (uint32_t)(r.buf >> 49), s1);
+            if (!l1) {
+                count = c;
+                return ~0u;
+            }
+            nsym = 1;
+            s2 = 0;
+            l12 = l1;
+        }
+        const uint32_t adv = nsym == 2 ? l12 : l1;
+        r.buf <<= adv;
+        r.nb -= adv;
+        if (MODE == 2) {
+            const uint32_t syms = s1 | (s2 << 8);
+            for (uint32_t q = 0; q < nsym; q++) {
+                const uint32_t sy = (syms >> (8 * q)) & 0xFF;
+                uint8_t* d = dst + o;
+                if (nacc == 0 && (reinterpret_cast<uint64_t>(d) & 15) != 0) {
+                    *d = (uint8_t)sy;
+                    o++;
+                } else {
+                    if (nacc < 8) acc_lo |= (uint64_t)sy << (8 * nacc);
+                    else acc_hi |= (uint64_t)sy << (8 * (nacc - 8));
+                    if (++nacc == 16) {
+                        *reinterpret_cast<uint4*>(dst + o) = make_uint4((uint32_t)acc_lo, (uint32_t)(acc_lo >> 32),
+                                                                        (uint32_t)acc_hi, (uint32_t)(acc_hi >> 32));
+                        o += 16;
+                        nacc = 0;
+                        acc_lo = acc_hi = 0;
+                    }
+                }
+            }
+        }
+        pos += adv;
+        c += nsym;
+        if (MODE == 0 && ck < kCkpt && pos >= ck_next && pos < lim) {
+            s.u.ch.ckpos[ck][tid] = pos;
+            s.u.ch.ckcnt[ck][tid] = c;
+            ck++;
+            ck_next = pos + step;
+        }
+        if (MODE == 1) {
+            while (sp < kCkpt && s.u.ch.ckpos[sp][tid] < pos) sp++;
+            if (sp < kCkpt && s.u.ch.ckpos[sp][tid] == pos) {
+                *sync = sp;
+                count = c;
+                return pos;
+            }
+        }
+    }
+    if (MODE == 2)
+        for (int q = 0; q < nacc; q++) dst[o + q] = (uint8_t)((q < 8 ? acc_lo >> (8 * q) : acc_hi >> (8 * (q - 8))));
+    if (MODE == 1) *sync = -1;
+    count = c;
+    return pos;
+}
+
+// CTA-wide decode of one Huffman record payload `pl` (codebook | bits u32 |
+// bits) into dst[0, len).  Returns false on any corruption the reference
+// would report (malformed codebook, zero bit count, invalid prefix, wrong end
+// position or symbol count).
+__device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t* dst) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __syncthreads();
+    const uint8_t wb = pl[tid >> 1];
+    const uint32_t l = (tid & 1) ? (wb >> 4) : (wb & 15);
+    s.lens[tid] = (uint8_t)l;
+    if (tid < kWarps * 16) (&s.cnt_w[0][0])[tid] = 0;
+    if (tid == 0) s.kraft = 0;
+    __syncthreads();
+    const uint32_t mm = __match_any_sync(0xFFFFFFFFu, l);
+    const uint32_t rank_w = __popc(mm & ((1u << lane) - 1));
+    if (lane == __ffs(mm) - 1) s.cnt_w[warp][l] = __popc(mm);
+    uint32_t ku = l ? (1u << (kMaxLen - l)) : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ku += __shfl_xor_sync(0xFFFFFFFFu, ku, o);
+    if (lane == 0) atomicAdd(&s.kraft, ku);
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t left = 0, idx = 0;
+        int mn = 16, mx = 0;
+        for (int q = 1; q <= kMaxLen; q++) {
+            uint32_t c = 0;
+            for (int w = 0; w < kWarps; w++) c += s.cnt_w[w][q];
+            s.bl_count[q] = c;
+            s.first_left[q] = left;
+            s.first_idx[q] = idx;
+            left += c << (kMaxLen - q);
+            idx += c;
+            if (c) { mn = min(mn, q); mx = max(mx, q); }
+        }
+        s.minlen = mn;
+        s.maxlen = mx;
+    }
+    __syncthreads();
+    const uint32_t bits = rd32(pl + 128);
+    // _validate_codebook (huffman.py:191-210) and decode_block's bit-length check (:275)
+    if (s.maxlen == 0 || s.kraft > (1u << kMaxLen) || bits == 0) return false;
+    if (l) {
+        uint32_t rk = rank_w;
+        for (int w = 0; w < warp; w++) rk += s.cnt_w[w][l];
+        s.csym[s.first_idx[l] + rk] = (uint8_t)tid;
+    }
+    const uint8_t* data = pl + kHuffOverhead;
+    const uint64_t nbytes = ((uint64_t)bits + 7) / 8;
+    Bits B;
+    B.gbase = reinterpret_cast<const uint8_t*>(reinterpret_cast<uint64_t>(data) & ~3ull);
+    B.sh = (uint32_t)(reinterpret_cast<uint64_t>(data) & 3) * 8;
+    B.glimit = (uint64_t)(data - B.gbase) + nbytes;
+    B.nwords_full = B.glimit / 4;
+    B.sw = nullptr;
+    const uint64_t nwords = (B.glimit + 3) / 4;
+    const bool staged = nwords + 4 <= kStage / 4 + 8;
+    if (staged)  // stage the payload words (zero past the end) in shared memory
+        for (uint64_t j = tid; j < nwords + 4; j += kThreads) s.bits[j] = B.word(j);
+    __syncthreads();
+    if (staged) B.sw = s.bits;
+    // single-symbol LUT over kLut-bit prefixes
+    for (int e = tid; e < (1 << kLut); e += kThreads) {
+        const uint32_t v = (uint32_t)e << (kMaxLen - kLut);
+        uint16_t ent = 0;
+        for (int q = 1; q <= kLut; q++) {
+            const uint32_t fl = s.first_left[q], endq = fl + (s.bl_count[q] << (kMaxLen - q));
+            if (v >= fl && v < endq) {
+                ent = (uint16_t)((q << 8) | s.csym[s.first_idx[q] + ((v - fl) >> (kMaxLen - q))]);
+                break;
+            }
+        }
+        s.u.slut[e] = ent;
+    }
+    __syncthreads();
+    // two-symbol LUT
+    for (int e = tid; e < (1 << kLut); e += kThreads) {
+        const uint32_t a = s.u.slut[e];
+        uint32_t ent = 0;
+        if (a) {
+            const uint32_t l1 = a >> 8, s1 = a & 0xFF;
+            const uint32_t rest = ((uint32_t)e << l1) & ((1u << kLut) - 1);
+            const uint32_t b = s.u.slut[rest];
+            const uint32_t l2 = b >> 8;
+            if (b && l1 + l2 <= kLut) ent = (2u << 30) | (l1 << 26) | ((l1 + l2) << 21) | (s1 << 8) | (b & 0xFF);
+            else ent = (1u << 30) | (l1 << 26) | (l1 << 21) | (s1 << 8);
+        }
+        s.mlut[e] = ent;
+    }
+    __syncthreads();
+    // chunking: one chunk of S bits per thread
+    uint32_t S = (bits + kThreads - 1) / kThreads;
+    S = max(128u, (S + 31) & ~31u);
+    const uint32_t nch = (bits + S - 1) / S;
+    const bool fixed = s.minlen == s.maxlen;
+    const uint32_t c = tid;
+    const uint32_t lim = min((c + 1) * S, bits);
+    uint32_t my_start = 0, my_end = 0, my_cnt = 0;
+    for (int k = 0; k < kCkpt; k++) { s.u.ch.ckpos[k][tid] = ~0u; s.u.ch.ckcnt[k][tid] = 0; }
+    if (c < nch) {
+        my_start = c * S;
+        if (fixed) my_start = ((my_start + s.minlen - 1) / s.minlen) * s.minlen;
+        if (my_start >= lim) my_end = my_start;
+        else my_end = decode_span<0>(s, B, my_start, lim, my_cnt, nullptr, nullptr);
+        s.u.ch.end[c] = my_end;
+    }
+    __syncthreads();
+    // fix-up rounds until every chunk starts where its predecessor ended
+    for (;;) {
+        uint32_t pe = 0;
+        if (c < nch && c > 0) pe = s.u.ch.end[c - 1];
+        __syncthreads();
+        int changed = 0;
+        if (c < nch && c > 0 && pe != ~0u && pe != my_start) {
+            my_start = pe;
+            if (my_start >= lim) {
+                my_end = my_start;
+                my_cnt = 0;
+                for (int q = 0; q < kCkpt; q++) s.u.ch.ckpos[q][tid] = ~0u;
+            } else {
+                int k = -1;
+                uint32_t cnt2 = 0;
+                const uint32_t e2 = decode_span<1>(s, B, my_start, lim, cnt2, nullptr, &k);
+                if (e2 != ~0u && k >= 0) {
+                    // merged into the previous path at checkpoint k: the rest is identical
+                    const uint32_t base = s.u.ch.ckcnt[k][tid];
+                    my_cnt = cnt2 + (my_cnt - base);
+                    for (int q = 0; q < kCkpt; q++) {
+                        if (q < k) s.u.ch.ckpos[q][tid] = ~0u;
+                        else s.u.ch.ckcnt[q][tid] = s.u.ch.ckcnt[q][tid] - base + cnt2;
+                    }
+                } else {
+                    my_end = e2;
+                    my_cnt = cnt2;
+                    for (int q = 0; q < kCkpt; q++) s.u.ch.ckpos[q][tid] = ~0u;
+                }
+            }
+            s.u.ch.end[c] = my_end;
+            changed = 1;
+        }
+        if (!__syncthreads_or(changed)) break;
+    }
+    uint32_t v = (c < nch) ? my_cnt : 0;
+    uint32_t incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= o) incl += y;
     }
-    if (lane == 31) sh_w[warp] = incl;
+    if (lane == 31) s.wsum[warp] = incl;
     __syncthreads();
     uint32_t pre = 0, tot = 0;
-    for (int q = 0; q < 4; q++) { if (q < warp) pre += sh_w[q]; tot += sh_w[q]; }
-    uint32_t o = pre + incl - c;
-    while (mask) {
-        const int q = __ffs(mask) - 1;
-        mask &= mask - 1;
-        if (o < kCandCap) cand_pos[chunk * kCandCap + o] = (uint32_t)(c0 + threadIdx.x * 32 + q);
-        o++;
+    for (int w = 0; w < kWarps; w++) { if (w < warp) pre += s.wsum[w]; tot += s.wsum[w]; }
+    const bool inv = (c < nch) && (my_end == ~0u);
+    const bool bad = __syncthreads_or(inv) || tot != len || s.u.ch.end[nch - 1] != bits;
+    __syncthreads();
+    if (bad) return false;
+    if (c < nch && my_cnt) {
+        uint32_t cc;
+        decode_span<2>(s, B, my_start, lim, cc, dst + (pre + incl - v), nullptr);
     }
-    if (threadIdx.x == 0) cand_cnt[chunk] = tot;
+    __syncthreads();
+    return true;
 }
 
-// ----------------------------------------------------------------- k_link
-__device__ __forceinline__ bool rec_size_at(const uint8_t* seg, uint64_t comp, uint64_t pos, uint32_t& mode,
-                                            uint32_t& l, uint64_t& psize) {
+__device__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t n) {
+    // dst 16-byte aligned; src arbitrary
+    const int tid = threadIdx.x;
+    const uint32_t nv = n / 16;
+    const uint32_t sh = (uint32_t)(reinterpret_cast<uint64_t>(src) & 3) * 8;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uint64_t>(src) & ~3ull);
+    for (uint32_t i = tid; i < nv; i += kThreads) {
+        uint4 v;
+        const uint32_t* wi = w + 4 * i;
+        const uint32_t a0 = __ldg(wi), a1 = __ldg(wi + 1), a2 = __ldg(wi + 2), a3 = __ldg(wi + 3);
+        if (sh == 0) {
+            v = make_uint4(a0, a1, a2, a3);
+        } else {
+            uint32_t a4;
+            if (16 * i + 20 <= n) a4 = __ldg(wi + 4);
+            else {
+                a4 = 0;
+                const uint8_t* b4 = reinterpret_cast<const uint8_t*>(wi + 4);
+                const int64_t lim = (int64_t)((uint64_t)(src + n) - reinterpret_cast<uint64_t>(b4));
+                for (int q = 0; q < 4 && q < lim; q++) a4 |= (uint32_t)b4[q] << (8 * q);
+            }
+            v = make_uint4(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh), __funnelshift_r(a2, a3, sh),
+                           __funnelshift_r(a3, a4, sh));
+        }
+        reinterpret_cast<uint4*>(dst)[i] = v;
+    }
+    for (uint32_t i = nv * 16 + tid; i < n; i += kThreads) dst[i] = src[i];
+}
+
+// Decode one record (mode u8 | len u32 | payload) at rec into dst.  The caller
+// has validated the header and the payload bounds.  CTA-wide.
+__device__ bool decode_record(DecSmem& s, const uint8_t* rec, uint32_t mode, uint32_t len, uint8_t* dst) {
+    const uint8_t* pl = rec + 5;
+    if (mode == MODE_RLE) {
+        const uint32_t v = pl[0] * 0x01010101u;
+        const uint32_t nv = len / 16;
+        for (uint32_t i = threadIdx.x; i < nv; i += kThreads) reinterpret_cast<uint4*>(dst)[i] = make_uint4(v, v, v, v);
+        for (uint32_t i = nv * 16 + threadIdx.x; i < len; i += kThreads) dst[i] = (uint8_t)v;
+        return true;
+    }
+    if (mode == MODE_STORED) {
+        copy_bytes(dst, pl, len);
+        return true;
+    }
+    return huff_decode(s, pl, len, dst);
+}
+
+// payload size of the record at pos (stream.py:258-268); false when the
+// header or payload does not fit in the segment.
+__device__ __forceinline__ bool rec_size(const uint8_t* seg, uint64_t comp, uint64_t pos, uint32_t& mode, uint32_t& l,
+                                         uint64_t& psize) {
     if (pos + 5 > comp) return false;
     mode = seg[pos];
     l = rd32(seg + pos + 1);
@@ -261,405 +589,94 @@ __device__ __forceinline__ bool rec_size_at(const uint8_t* seg, uint64_t comp, u
     return pos + 5 + psize <= comp;
 }
 
-// One warp per segment.
-__global__ void __launch_bounds__(128) k_link(const DecStreamIn* __restrict__ in, const DecSeg* __restrict__ segs,
-                                              uint64_t nseg_total, const DecWin* __restrict__ wins,
-                                              const uint32_t* __restrict__ cand_cnt, const uint32_t* __restrict__ cand_pos,
-                                              DecRec* __restrict__ recs, DecRec* __restrict__ irr, uint32_t* __restrict__ irr_count,
-                                              uint32_t irr_cap, uint32_t* __restrict__ status, uint8_t* __restrict__ scratch) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t si = (uint64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (si >= nseg_total) return;
-    const DecSeg sg = segs[si];
-    if (sg.orig_len == 0) return;
-    const uint8_t* seg = in[sg.stream].p + sg.comp_off;
-    uint8_t* gdst = scratch + wins[sg.win].goff + sg.orig_off;
-    const uint64_t comp = sg.comp_len;
-    const uint32_t B = sg.block, R = sg.nrec;
-    const uint32_t Ltail = (uint32_t)(sg.orig_len - (uint64_t)(R - 1) * B);
-    const uint64_t nch = (comp + kCandChunk - 1) / kCandChunk;
-    // total candidates (and overflow)
-    uint64_t m = 0;
-    bool overflow = false;
-    for (uint64_t c = lane; c < nch; c += 32) {
-        const uint32_t k = cand_cnt[sg.chunk0 + c];
-        m += k;
-        overflow |= k > kCandCap;
+// -------------------------------------------------------------- k_scandec
+constexpr uint64_t kFlagA = 1ull << 62, kFlagI = 2ull << 62, kMask = (1ull << 62) - 1;
+__device__ __forceinline__ uint64_t ld_acq(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint64_t pos, uint32_t B) {
+    if (pos + 5 > comp || seg[pos] > 2) return false;
+    return rd32(seg + pos + 1) == B;
+}
+
+// Candidates in [a, e) (a thread's slice of a chunk).  The little-endian
+// block size has exactly one non-zero byte, at offset 1 + kb of a record;
+// its positions are found 4 bytes at a time with __vcmpeq4.
+__device__ __forceinline__ uint32_t scan_slice(const DecSeg& sg, uint64_t a, uint64_t e, uint32_t* out) {
+    const uint32_t B = sg.block;
+    const int kb = (__ffs(B) - 1) >> 3;
+    const uint32_t kv = B >> (8 * kb);
+    uint32_t n = 0;
+    if (a >= e) return 0;
+    if (a == 0) {  // the segment start is always a record start
+        out[0] = 0;
+        n = 1;
     }
+    const uint8_t* b = sg.base;
+    const uint64_t qa = max(a, (uint64_t)1) + 1 + kb, qe = min(e + 1 + kb, sg.comp);
+    uint64_t q = qa;
+    auto hit = [&](uint64_t qq) {
+        const uint64_t p = qq - 1 - kb;
+        if (is_cand(b, sg.comp, p, B)) {
+            if (n < kMine) out[n] = (uint32_t)p;
+            n++;
+        }
+    };
+    while (q < qe && (reinterpret_cast<uint64_t>(b + q) & 3)) {
+        if (b[q] == kv) hit(q);
+        q++;
+    }
+    const uint32_t pat = kv * 0x01010101u;
+    for (; q + 4 <= qe; q += 4) {
+        const uint32_t m = __vcmpeq4(*reinterpret_cast<const uint32_t*>(b + q), pat);
+        if (m) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xFFFFFFFFu, m, o);
-    overflow = __any_sync(0xFFFFFFFFu, overflow);
-    const uint64_t m_exp = (Ltail == B) ? R : (R > 1 ? R - 1 : 1);
-    bool ok = !overflow && m == m_exp;
-    if (ok) {
-        // candidate i -> (chunk, slot): walk chunks with a running prefix
-        uint64_t pre = 0;
-        for (uint64_t cbase = 0; cbase < nch && ok; cbase += 32) {
-            const uint64_t c = cbase + lane;
-            const uint32_t k = c < nch ? cand_cnt[sg.chunk0 + c] : 0;
-            uint32_t incl = k;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            const uint64_t first = pre + incl - k;
-            bool good = true;
-            for (uint32_t j = 0; j < k; j++) {
-                const uint64_t idx = first + j;   // candidate == canonical record index
-                const uint64_t pos = cand_pos[(sg.chunk0 + c) * kCandCap + j];
-                uint32_t mode, l;
-                uint64_t ps;
-                const uint32_t want = (idx + 1 == R) ? Ltail : B;
-                if (!rec_size_at(seg, comp, pos, mode, l, ps) || l != want) { good = false; break; }
-                const uint64_t nxt = pos + 5 + ps;
-                // successor: next candidate, or the tail record, or the segment end
-                if (idx + 1 < m) {
-                    const uint64_t np = (j + 1 < k) ? cand_pos[(sg.chunk0 + c) * kCandCap + j + 1] : ~0ull;
-                    if (np != ~0ull && np != nxt) { good = false; break; }
-                    if (np == ~0ull) {
-                        // first candidate of a later chunk: checked by its predecessor through scan below
-                    }
-                } else if (m < R) {
-                    // tail record follows the last candidate (Ltail != B)
-                    uint32_t tm, tl;
-                    uint64_t tps;
-                    if (!rec_size_at(seg, comp, nxt, tm, tl, tps) || tl != Ltail || nxt + 5 + tps != comp) {
-                        good = false; break;
-                    }
-                    DecRec t;
-                    t.src = seg + nxt; t.dst = gdst + (uint64_t)(R - 1) * B; t.len = tl; t.psize = (uint32_t)tps;
-                    t.stream = sg.stream; t.mode = (uint8_t)tm;
-                    recs[sg.rec0 + R - 1] = t;
-                } else {
-                    if (nxt != comp) { good = false; break; }
-                }
-                DecRec d;
-                d.src = seg + pos; d.dst = gdst + idx * B; d.len = l; d.psize = (uint32_t)ps;
-                d.stream = sg.stream; d.mode = (uint8_t)mode;
-                recs[sg.rec0 + idx] = d;
-            }
-            ok = __all_sync(0xFFFFFFFFu, good);
-            pre += __shfl_sync(0xFFFFFFFFu, incl, 31);
-        }
-        // cross-chunk links: the last candidate of each chunk must point at the
-        // first candidate of the next non-empty chunk
-        if (ok) {
-            __syncwarp();
-            bool good = true;
-            for (uint64_t i = lane; i + 1 < m; i += 32) {
-                const DecRec a = recs[sg.rec0 + i];
-                const DecRec bb = recs[sg.rec0 + i + 1];
-                if (a.src + 5 + a.psize != bb.src) good = false;
-            }
-            ok = __all_sync(0xFFFFFFFFu, good);
+            for (int k = 0; k < 4; k++)
+                if ((m >> (8 * k)) & 1) hit(q + k);
         }
     }
-    if (ok) return;
-    // ---- serial walk, exactly decompress_segment (stream.py:234-255)
-    __syncwarp();
-    for (uint32_t r = lane; r < R; r += 32) recs[sg.rec0 + r].mode = kSkip;
-    __syncwarp();
-    if (lane != 0) return;
-    uint64_t pos = 0, got = 0;
-    uint32_t idx = 0;
-    bool canon = true;
-    uint32_t nirr = 0;
-    // first pass: validate and check canonical shape
-    while (got < sg.orig_len) {
-        uint32_t mode, l;
-        uint64_t ps;
-        if (pos + 5 > comp) { atomicOr(&status[sg.stream], ST_CORRUPT); return; }
-        mode = seg[pos];
-        l = rd32(seg + pos + 1);
-        if (l == 0 || l > B || l > sg.orig_len - got) { atomicOr(&status[sg.stream], ST_CORRUPT); return; }
-        if (!rec_size_at(seg, comp, pos, mode, l, ps)) { atomicOr(&status[sg.stream], ST_CORRUPT); return; }
-        const uint32_t want = (idx + 1 == R) ? Ltail : B;
-        if (idx >= R || l != want) canon = false;
-        pos += 5 + ps;
-        got += l;
-        idx++;
-    }
-    if (pos != comp) { atomicOr(&status[sg.stream], ST_CORRUPT); return; }
-    if (!canon) {
-        nirr = atomicAdd(irr_count, idx);
-        if (nirr + idx > irr_cap) { atomicOr(&status[sg.stream], ST_CAPACITY); return; }
-    }
-    // second pass: emit records
-    pos = 0; got = 0;
-    for (uint32_t r = 0; r < idx; r++) {
-        uint32_t mode, l;
-        uint64_t ps;
-        rec_size_at(seg, comp, pos, mode, l, ps);
-        DecRec d;
-        d.src = seg + pos; d.dst = gdst + got; d.len = l; d.psize = (uint32_t)ps; d.stream = sg.stream;
-        d.mode = (uint8_t)mode;
-        if (canon) recs[sg.rec0 + r] = d;
-        else irr[nirr + r] = d;
-        pos += 5 + ps;
-        got += l;
-    }
+    for (; q < qe; q++)
+        if (b[q] == kv) hit(q);
+    return n;
 }
 
-// --------------------------------------------------------------- k_decode
-constexpr int kLutBits = 11;
-
-struct DecSmem {
-    uint8_t lens[256];
-    uint8_t csym[256];          // symbols in canonical (length, symbol) order
-    uint16_t lut[1 << kLutBits];  // (len << 8) | sym for codes <= kLutBits, 0 otherwise
-    uint32_t first_left[17];    // left-justified first code of each length
-    uint32_t first_idx[17];     // canonical index of the first code of each length
-    uint32_t bl_count[17];
-    uint32_t cnt_w[kWarps][16];
-    uint32_t start[kThreads], end[kThreads], cnt[kThreads], off[kThreads];
-    uint32_t wsum[kWarps];
-    uint32_t kraft;
-    int minlen, maxlen;
-};
-
-struct BitReader {
-    const uint8_t* base;   // 4-byte aligned base
-    uint64_t nwords_full;  // words entirely inside the payload
-    uint64_t limit;        // payload end (bytes from base)
-    uint64_t buf;
-    int nb;
-    uint64_t next;         // next word index
-    __device__ __forceinline__ uint32_t word(uint64_t j) const {
-        if (j < nwords_full) return bswap32(__ldg(reinterpret_cast<const uint32_t*>(base) + j));
-        uint32_t v = 0;
-        for (int q = 0; q < 4; q++) {
-            const uint64_t o = j * 4 + q;
-            v = (v << 8) | (o < limit ? base[o] : 0u);
-        }
-        return v;
-    }
-    __device__ __forceinline__ void init(const uint8_t* data, uint64_t nbytes, uint64_t bitpos) {
-        base = reinterpret_cast<const uint8_t*>(reinterpret_cast<uint64_t>(data) & ~3ull);
-        const uint32_t sh = (uint32_t)(reinterpret_cast<uint64_t>(data) & 3) * 8;
-        limit = (uint64_t)(data - base) + nbytes;
-        nwords_full = limit / 4;
-        const uint64_t abit = bitpos + sh;
-        const uint64_t j = abit >> 5;
-        const int k = (int)(abit & 31);
-        buf = (((uint64_t)word(j) << 32) | word(j + 1)) << k;
-        nb = 64 - k;
-        next = j + 2;
-    }
-    __device__ __forceinline__ void refill() {
-        if (nb <= 32) {
-            buf |= (uint64_t)word(next) << (32 - nb);
-            nb += 32;
-            next++;
-        }
-    }
-};
-
-// Decode codewords starting in [pos, lim); returns the end position (first
-// boundary >= lim) or ~0u on an invalid prefix.  EMIT writes the symbols to
-// dst (16-byte grouped stores where aligned).
-template <bool EMIT>
-__device__ __forceinline__ uint32_t decode_run(const DecSmem& s, const uint8_t* data, uint64_t nbytes, uint32_t pos,
-                                               uint32_t lim, uint32_t& count, uint8_t* dst) {
-    BitReader br;
-    br.init(data, nbytes, pos);
-    uint32_t c = 0;
-    uint64_t acc_lo = 0, acc_hi = 0;
-    int nacc = 0;
-    uint64_t o = 0;  // bytes emitted
-    while (pos < lim) {
-        br.refill();
-        const uint32_t win = (uint32_t)(br.buf >> 49);  // 15-bit window
-        const uint32_t e = s.lut[win >> (kMaxLen - kLutBits)];
-        uint32_t l, sym;
-        if (e) {
-            l = e >> 8;
-            sym = e & 0xFF;
-        } else {
-            l = 0;
-            for (int q = kLutBits + 1; q <= s.maxlen; q++) {
-                const uint32_t endq = s.first_left[q] + (s.bl_count[q] << (kMaxLen - q));
-                if (s.bl_count[q] && win >= s.first_left[q] && win < endq) { l = q; break; }
-            }
-            if (!l) { count = c; return ~0u; }
-            sym = s.csym[s.first_idx[l] + ((win - s.first_left[l]) >> (kMaxLen - l))];
-        }
-        br.buf <<= l;
-        br.nb -= l;
-        pos += l;
-        c++;
-        if (EMIT) {
-            // head bytes until 16-byte alignment, then whole uint4 stores
-            uint8_t* d = dst + o;
-            if (nacc == 0 && ((reinterpret_cast<uint64_t>(d) & 15) != 0)) {
-                *d = (uint8_t)sym;
-                o++;
-            } else {
-                if (nacc < 8) acc_lo |= (uint64_t)sym << (8 * nacc);
-                else acc_hi |= (uint64_t)sym << (8 * (nacc - 8));
-                nacc++;
-                if (nacc == 16) {
-                    *reinterpret_cast<uint4*>(dst + o) =
-                        make_uint4((uint32_t)acc_lo, (uint32_t)(acc_lo >> 32), (uint32_t)acc_hi, (uint32_t)(acc_hi >> 32));
-                    o += 16;
-                    nacc = 0;
-                    acc_lo = acc_hi = 0;
-                }
-            }
-        }
-    }
-    if (EMIT) {
-        for (int q = 0; q < nacc; q++) dst[o + q] = (uint8_t)((q < 8 ? acc_lo >> (8 * q) : acc_hi >> (8 * (q - 8))));
-    }
-    count = c;
-    return pos;
-}
-
-__device__ __forceinline__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t n, int tid, int nt) {
-    // dst is 16-byte aligned; src arbitrary
-    const uint32_t nv = n / 16;
-    for (uint32_t i = tid; i < nv; i += nt) {
-        uint4 v;
-        const uint8_t* sp = src + 16 * i;
-        if ((reinterpret_cast<uint64_t>(sp) & 3) == 0) {
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(sp);
-            v = make_uint4(__ldg(w), __ldg(w + 1), __ldg(w + 2), __ldg(w + 3));
-        } else {
-            const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uint64_t>(sp) & ~3ull);
-            const uint32_t sh = (uint32_t)(reinterpret_cast<uint64_t>(sp) & 3) * 8;
-            const uint32_t a0 = __ldg(w), a1 = __ldg(w + 1), a2 = __ldg(w + 2), a3 = __ldg(w + 3);
-            // the 5th word may lie past the payload only for the final vector: read bytewise there
-            uint32_t a4;
-            if (16 * i + 16 + 4 <= n) a4 = __ldg(w + 4);
-            else {
-                a4 = 0;
-                const uint8_t* b4 = reinterpret_cast<const uint8_t*>(w + 4);
-                const uint64_t lim = (uint64_t)(src + n) - reinterpret_cast<uint64_t>(b4);
-                for (uint32_t q = 0; q < 4 && q < lim; q++) a4 |= (uint32_t)b4[q] << (8 * q);
-            }
-            v = make_uint4(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh), __funnelshift_r(a2, a3, sh),
-                           __funnelshift_r(a3, a4, sh));
-        }
-        reinterpret_cast<uint4*>(dst)[i] = v;
-    }
-    for (uint32_t i = nv * 16 + tid; i < n; i += nt) dst[i] = src[i];
-}
-
-__global__ void __launch_bounds__(kThreads) k_decode(const DecRec* __restrict__ recs, uint64_t nrec,
-                                                   const DecRec* __restrict__ irr, const uint32_t* __restrict__ irr_count,
-                                                   uint32_t* __restrict__ status) {
-    __shared__ DecSmem s;
+__global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+                                                    uint64_t nchunk_total, uint32_t* __restrict__ ticket,
+                                                    uint64_t* __restrict__ cstat, uint32_t* __restrict__ seg_cnt,
+                                                    uint32_t* __restrict__ seg_fail, uint64_t* __restrict__ rec_pos,
+                                                    uint64_t* __restrict__ rec_next, uint8_t* __restrict__ scratch) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t total = nrec + *irr_count;
-    for (uint64_t r = blockIdx.x; r < total; r += gridDim.x) {
-        const DecRec d = (r < nrec) ? recs[r] : irr[r - nrec];
-        __syncthreads();   // smem reuse across records
-        if (d.mode == kSkip) continue;
-        const uint8_t* pl = d.src + 5;
-        if (d.mode == MODE_RLE) {
-            const uint32_t v = pl[0] * 0x01010101u;
-            const uint32_t nv = d.len / 16;
-            for (uint32_t i = tid; i < nv; i += kThreads) reinterpret_cast<uint4*>(d.dst)[i] = make_uint4(v, v, v, v);
-            for (uint32_t i = nv * 16 + tid; i < d.len; i += kThreads) d.dst[i] = (uint8_t)v;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s.tile = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint64_t t = s.tile;
+        if (t >= nchunk_total) return;
+        uint64_t lo = 0, hi = nseg_total;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (segs[mid].chunk0 <= t) lo = mid; else hi = mid;
+        }
+        const DecSeg sg = segs[lo];
+        if (t < sg.chunk0 || t >= sg.chunk0 + sg.nchunk) {
+            if (tid == 0) st_rel(&cstat[t], kFlagI);  // unused capacity slot
             continue;
         }
-        if (d.mode == MODE_STORED) {
-            copy_bytes(d.dst, pl, d.len, tid, kThreads);
-            continue;
-        }
-        // ---- Huffman (huffman.py:258-349 semantics)
-        const uint8_t wb = pl[tid >> 1];
-        const uint32_t l = (tid & 1) ? (wb >> 4) : (wb & 15);
-        s.lens[tid] = (uint8_t)l;
-        if (tid < kWarps * 16) (&s.cnt_w[0][0])[tid] = 0;
-        if (tid == 0) s.kraft = 0;
-        __syncthreads();
-        const uint32_t mm = __match_any_sync(0xFFFFFFFFu, l);
-        const uint32_t rank_w = __popc(mm & ((1u << lane) - 1));
-        if (lane == __ffs(mm) - 1) s.cnt_w[warp][l] = __popc(mm);
-        if (l) atomicAdd(&s.kraft, 1u << (kMaxLen - l));
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t left = 0, idx = 0;
-            int mn = 16, mx = 0;
-            for (int q = 1; q <= kMaxLen; q++) {
-                uint32_t c = 0;
-                for (int w = 0; w < kWarps; w++) c += s.cnt_w[w][q];
-                s.bl_count[q] = c;
-                s.first_left[q] = left;
-                s.first_idx[q] = idx;
-                left += c << (kMaxLen - q);
-                idx += c;
-                if (c) { mn = min(mn, q); mx = max(mx, q); }
-            }
-            s.minlen = mn;
-            s.maxlen = mx;
-        }
-        __syncthreads();
-        const uint32_t bits = rd32(pl + 128);
-        // _validate_codebook (huffman.py:191-210) and the bit-length check (:275)
-        const bool bad_cb = (s.maxlen == 0) || (s.kraft > (1u << kMaxLen)) || bits == 0;
-        if (bad_cb) {
-            if (tid == 0) atomicOr(&status[d.stream], ST_CORRUPT);
-            continue;
-        }
-        if (l) {
-            uint32_t rk = rank_w;
-            for (int w = 0; w < warp; w++) rk += s.cnt_w[w][l];
-            s.csym[s.first_idx[l] + rk] = (uint8_t)tid;
-        }
-        __syncthreads();
-        // LUT: entry e covers windows [e << 4, (e+1) << 4)
-        for (int e = tid; e < (1 << kLutBits); e += kThreads) {
-            const uint32_t v = (uint32_t)e << (kMaxLen - kLutBits);
-            uint16_t ent = 0;
-            for (int q = 1; q <= kLutBits; q++) {
-                const uint32_t fl = s.first_left[q], endq = fl + (s.bl_count[q] << (kMaxLen - q));
-                if (v >= fl && v < endq) {
-                    ent = (uint16_t)((q << 8) | s.csym[s.first_idx[q] + ((v - fl) >> (kMaxLen - q))]);
-                    break;
-                }
-            }
-            s.lut[e] = ent;
-        }
-        const uint8_t* data = pl + kHuffOverhead;
-        const uint64_t nbytes = (bits + 7) / 8;
-        // chunking: at most kThreads chunks of S bits (multiple of 32)
-        uint32_t S = (bits + kThreads - 1) / kThreads;
-        S = max(256u, (S + 31) & ~31u);
-        const uint32_t nch = (bits + S - 1) / S;
-        const bool fixed = s.minlen == s.maxlen;
-        __syncthreads();
-        // phase 1: speculative decode of every chunk from its nominal start
-        const uint32_t c = tid;
-        uint32_t my_start = 0, my_end = 0, my_cnt = 0;
-        const uint32_t lim = min((c + 1) * S, bits);
-        if (c < nch) {
-            my_start = c * S;
-            if (fixed) my_start = ((my_start + s.minlen - 1) / s.minlen) * s.minlen;
-            if (my_start >= lim) { my_end = my_start; my_cnt = 0; }
-            else my_end = decode_run<false>(s, data, nbytes, my_start, lim, my_cnt, nullptr);
-            s.start[c] = my_start; s.end[c] = my_end; s.cnt[c] = my_cnt;
-        }
-        __syncthreads();
-        // phase 2: fix-up rounds until every chunk starts where its predecessor ended
-        for (;;) {
-            uint32_t pe = 0;
-            if (c < nch && c > 0) pe = s.end[c - 1];
-            __syncthreads();
-            int changed = 0;
-            if (c < nch && c > 0 && pe != ~0u && pe != my_start) {
-                my_start = pe;
-                if (my_start >= lim) { my_end = my_start; my_cnt = 0; }
-                else my_end = decode_run<false>(s, data, nbytes, my_start, lim, my_cnt, nullptr);
-                s.start[c] = my_start; s.end[c] = my_end; s.cnt[c] = my_cnt;
-                changed = 1;
-            }
-            if (!__syncthreads_or(changed)) break;
-        }
-        // totals
-        uint32_t v = (c < nch) ? my_cnt : 0;
-        uint32_t incl = v;
+        const uint64_t ci = t - sg.chunk0;
+        const uint64_t c0 = ci * kChunk, c1 = min(c0 + kChunk, sg.comp);
+        // ---- candidates of this chunk
+        uint32_t mine[kMine];
+        const uint64_t a = c0 + (uint64_t)tid * (kChunk / kThreads);
+        const uint32_t nmine = scan_slice(sg, a, min(a + kChunk / kThreads, c1), mine);
+        uint32_t incl = nmine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
@@ -667,30 +684,166 @@ __global__ void __launch_bounds__(kThreads) k_decode(const DecRec* __restrict__ 
         }
         if (lane == 31) s.wsum[warp] = incl;
         __syncthreads();
-        uint32_t pre = 0, tot = 0;
-        for (int w = 0; w < kWarps; w++) { if (w < warp) pre += s.wsum[w]; tot += s.wsum[w]; }
-        const bool inv = (c < nch) && (my_end == ~0u);
-        const bool bad = __syncthreads_or(inv) || tot != d.len || s.end[nch - 1] != bits;
-        if (bad) {
-            if (tid == 0) atomicOr(&status[d.stream], ST_CORRUPT);
+        uint32_t wpre = 0, tot = 0;
+        for (int w = 0; w < kWarps; w++) { if (w < warp) wpre += s.wsum[w]; tot += s.wsum[w]; }
+        // ---- segmented decoupled look-back over the segment's chunks
+        if (tid == 0) {
+            uint64_t pre = 0;
+            if (ci == 0) {
+                st_rel(&cstat[t], kFlagI | tot);
+            } else {
+                st_rel(&cstat[t], kFlagA | tot);
+                int64_t j = (int64_t)t - 1;
+                for (;;) {
+                    uint64_t st;
+                    do { st = ld_acq(&cstat[j]); } while ((st >> 62) == 0);
+                    pre += st & kMask;
+                    if ((st >> 62) == 2) break;
+                    j--;
+                }
+                st_rel(&cstat[t], kFlagI | (pre + tot));
+            }
+            s.base = (uint32_t)pre;
+            if (c1 == sg.comp) seg_cnt[lo] = (uint32_t)(pre + tot);
+        }
+        const bool dense = __syncthreads_or(nmine > kMine);
+        if (dense) {
+            // e.g. long runs of 6-byte RLE records: the serial path handles the segment
+            if (tid == 0) atomicOr(&seg_fail[lo], 1u);
             continue;
         }
-        // phase 3: final decode with output
-        if (c < nch && my_cnt) {
-            uint32_t cc;
-            decode_run<true>(s, data, nbytes, my_start, lim, cc, d.dst + (pre + incl - v));
+        const uint32_t base = s.base;
+        const uint32_t R = sg.nrec, B = sg.block;
+        const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(R - 1) * B);
+        const uint32_t my0 = wpre + incl - nmine;
+        for (uint32_t done = 0; done < tot; done += kThreads) {
+            for (uint32_t k = 0; k < nmine; k++) {
+                const uint32_t g = my0 + k;
+                if (g >= done && g < done + kThreads) s.cand[g - done] = mine[k];
+            }
+            __syncthreads();
+            const uint32_t nb = min(tot - done, (uint32_t)kThreads);
+            for (uint32_t k = 0; k < nb; k++) {
+                const uint64_t pos = s.cand[k];
+                const uint32_t r = base + done + k;
+                if (r >= R) {
+                    if (tid == 0) atomicOr(&seg_fail[lo], 1u);
+                    break;
+                }
+                uint32_t mode = 0, l = 0;
+                uint64_t ps = 0;
+                bool ok = rec_size(sg.base, sg.comp, pos, mode, l, ps) && l == ((r + 1 == R) ? Ltail : B);
+                if (ok) ok = decode_record(s, sg.base + pos, mode, l, scratch + sg.goff + (uint64_t)r * B);
+                if (tid == 0) {
+                    rec_pos[sg.rec0 + r] = pos;
+                    rec_next[sg.rec0 + r] = ok ? pos + 5 + ps : ~0ull;
+                }
+                if (ok && r + 2 == R && Ltail != B) {
+                    // the tail record (not a candidate: its length differs) follows record R-2
+                    const uint64_t q = pos + 5 + ps;
+                    uint32_t tm = 0, tl = 0;
+                    uint64_t tps = 0;
+                    bool tok = rec_size(sg.base, sg.comp, q, tm, tl, tps) && tl == Ltail;
+                    if (tok) tok = decode_record(s, sg.base + q, tm, tl, scratch + sg.goff + (uint64_t)(R - 1) * B);
+                    if (tid == 0) {
+                        rec_pos[sg.rec0 + R - 1] = q;
+                        rec_next[sg.rec0 + R - 1] = tok ? q + 5 + tps : ~0ull;
+                    }
+                }
+                if (!ok && tid == 0) atomicOr(&seg_fail[lo], 1u);
+            }
+            __syncthreads();
         }
+    }
+}
+
+// --------------------------------------------------------------- k_verify
+// One thread per record slot: the candidates must chain exactly.
+__global__ void k_verify(const DecSeg* __restrict__ segs, uint64_t nseg_total, uint64_t nrec_total,
+                         const uint32_t* __restrict__ seg_cnt, uint32_t* __restrict__ seg_fail,
+                         const uint64_t* __restrict__ rec_pos, const uint64_t* __restrict__ rec_next) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (g >= nrec_total) return;
+    uint64_t lo = 0, hi = nseg_total;
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (segs[mid].rec0 <= g) lo = mid; else hi = mid;
+    }
+    // several empty segments may share rec0: move to the one that owns g
+    const DecSeg sg = segs[lo];
+    if (g < sg.rec0 || g >= sg.rec0 + sg.nrec) return;
+    const uint32_t r = (uint32_t)(g - sg.rec0);
+    const uint32_t R = sg.nrec, B = sg.block;
+    const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(R - 1) * B);
+    bool ok = true;
+    if (r == 0) {
+        const uint32_t m_exp = (Ltail == B) ? R : (R > 1 ? R - 1 : 1);
+        ok = seg_cnt[lo] == m_exp && rec_pos[g] == 0;
+    }
+    if (ok) {
+        const uint64_t nx = rec_next[g];
+        if (nx == ~0ull) ok = false;
+        else if (r + 1 < R) ok = nx == rec_pos[g + 1];
+        else ok = nx == sg.comp;
+    }
+    if (!ok) atomicOr(&seg_fail[lo], 1u);
+}
+
+// ------------------------------------------------------------- k_fallback
+// Serial record walk with the reference's validation (stream.py:234-268) for
+// every segment that failed verification; decodes each record in turn.
+__global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+                                                     const uint32_t* __restrict__ seg_fail, uint32_t* __restrict__ status,
+                                                     uint8_t* __restrict__ scratch) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
+    __shared__ uint64_t sh_pos, sh_got, sh_ps;
+    __shared__ uint32_t sh_mode, sh_len, sh_ok;
+    for (uint64_t si = blockIdx.x; si < nseg_total; si += gridDim.x) {
+        if (!seg_fail[si]) continue;
+        const DecSeg sg = segs[si];
+        if (threadIdx.x == 0) { sh_pos = 0; sh_got = 0; }
+        __syncthreads();
+        bool corrupt = false;
+        for (;;) {
+            if (threadIdx.x == 0) {
+                sh_ok = 1;
+                const uint64_t pos = sh_pos, got = sh_got;
+                if (got >= sg.orig) {
+                    sh_ok = (pos == sg.comp) ? 2 : 0;
+                } else {
+                    uint32_t mode = 0, l = 0;
+                    uint64_t ps = 0;
+                    if (pos + 5 > sg.comp) sh_ok = 0;
+                    else {
+                        l = rd32(sg.base + pos + 1);
+                        if (l == 0 || l > sg.block || l > sg.orig - got) sh_ok = 0;
+                        else if (!rec_size(sg.base, sg.comp, pos, mode, l, ps)) sh_ok = 0;
+                        else { sh_mode = mode; sh_len = l; sh_ps = ps; }
+                    }
+                }
+            }
+            __syncthreads();
+            const uint32_t okv = sh_ok;
+            if (okv == 2) break;
+            if (okv == 0) { corrupt = true; break; }
+            if (!decode_record(s, sg.base + sh_pos, sh_mode, sh_len, scratch + sg.goff + sh_got)) { corrupt = true; break; }
+            __syncthreads();
+            if (threadIdx.x == 0) { sh_pos += 5 + sh_ps; sh_got += sh_len; }
+            __syncthreads();
+        }
+        if (corrupt && threadIdx.x == 0) atomicOr(&status[sg.stream], ST_CORRUPT);
+        __syncthreads();
     }
 }
 
 // -------------------------------------------------------------- k_ungroup
 // CTA per 16 KiB output tile of a window: out[e*w + g] = grouped[g*n + e];
 // each thread produces 64 contiguous output bytes and their raw CRC.
-__global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__ wins, const uint64_t* __restrict__ win_tile0,
-                                                    uint64_t nwin_total, uint64_t ntile_total,
-                                                    const uint8_t* __restrict__ scratch, uint8_t* __restrict__ out,
-                                                    const CrcTables* __restrict__ ct, uint32_t* __restrict__ tile_crc,
-                                                    uint64_t* __restrict__ tile_end, const uint32_t* __restrict__ status) {
+__global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__ wins, uint64_t nwin_total,
+                                                    uint64_t ntile_total, const uint8_t* __restrict__ scratch,
+                                                    uint8_t* __restrict__ out, const CrcTables* __restrict__ ct,
+                                                    uint32_t* __restrict__ tile_crc, const uint32_t* __restrict__ status) {
     __shared__ uint32_t sh_slice[1024];
     __shared__ uint32_t sh_part[kWarps];
     const uint64_t tile = blockIdx.x;
@@ -698,18 +851,18 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
     uint64_t lo = 0, hi = nwin_total;
     while (hi - lo > 1) {
         uint64_t mid = (lo + hi) >> 1;
-        if (win_tile0[mid] <= tile) lo = mid; else hi = mid;
+        if (wins[mid].tile0 <= tile) lo = mid; else hi = mid;
     }
     const DecWin wd = wins[lo];
-    const uint64_t t0 = (tile - win_tile0[lo]) * kOutTile;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tile < win_tile0[lo] || t0 >= wd.W || status[wd.stream]) {
-        if (tid == 0) { tile_crc[tile] = 0; tile_end[tile] = 0; }
+    if (tile < wd.tile0 || tile >= wd.tile0 + wd.ntile || status[wd.stream]) {
+        if (tid == 0) tile_crc[tile] = 0;
         return;
     }
+    const uint64_t t0 = (tile - wd.tile0) * kOutTile;
     for (int i = tid; i < 1024; i += kThreads) sh_slice[i] = ct->slice[i >> 8][i & 255];
     __syncthreads();
-    const uint64_t L = min((uint64_t)(kOutTile), (uint64_t)(wd.W - t0));
+    const uint64_t L = min((uint64_t)kOutTile, wd.W - t0);
     const uint64_t Z = kOutTile - L;  // leading zero padding of a short tile
     const uint32_t w = wd.w;
     const uint8_t* g = scratch + wd.goff;
@@ -717,7 +870,7 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
     const uint64_t lo_b = (uint64_t)tid * kLaneBytes, hi_b = lo_b + kLaneBytes;
     uint32_t c = 0;
     const bool full = lo_b >= Z;
-    const uint64_t ob = t0 + lo_b - Z;  // first output byte (window-relative) of this thread when full
+    const uint64_t ob = t0 + lo_b - Z;
     const bool vec = full && ((reinterpret_cast<uint64_t>(o) + ob) % 16 == 0) &&
                      (w == 1 ? ((reinterpret_cast<uint64_t>(g) + ob) % 16 == 0)
                              : ((ob / w) % 16 == 0 && (wd.n % 16) == 0));
@@ -780,35 +933,33 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
         uint32_t acc = 0;
         for (int q = 0; q < kWarps; q++) acc = crc_shift_tab(&ct->shift[5][0][0], acc) ^ sh_part[q];
         tile_crc[tile] = acc;
-        tile_end[tile] = wd.soff + t0 + L;  // stream-relative end of this tile
     }
 }
 
 // ------------------------------------------------------------- k_finalize
-__global__ void __launch_bounds__(kThreads) k_finalize(const DecStreamHdr* __restrict__ hdr, const DecStreamPlan* __restrict__ plan,
-                                                     int ns, const uint32_t* __restrict__ tile_crc,
-                                                     const uint64_t* __restrict__ tile_end, const CrcTables* __restrict__ ct,
+__global__ void __launch_bounds__(kThreads) k_finalize(const DecStreamOut* __restrict__ sout, const DecCaps* __restrict__ caps,
+                                                     const DecWin* __restrict__ wins, int ns,
+                                                     const uint32_t* __restrict__ tile_crc, const CrcTables* __restrict__ ct,
                                                      uint32_t* __restrict__ status) {
     __shared__ uint32_t red[kThreads];
     const int s = blockIdx.x;
     if (s >= ns) return;
-    const DecStreamHdr h = hdr[s];
-    if (h.status) return;
-    const DecStreamPlan pl = plan[s];
-    uint32_t acc = 0;
-    for (uint64_t t = threadIdx.x; t < pl.ntile; t += kThreads) {
-        const uint64_t e = tile_end[pl.tile0 + t];
-        const uint32_t part = tile_crc[pl.tile0 + t];
-        if (part) acc ^= crc_shift_generic(ct->x2n, part, h.orig - e);
-    }
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int o = kThreads / 2; o; o >>= 1) {
-        if (threadIdx.x < o) red[threadIdx.x] ^= red[threadIdx.x + o];
-        __syncthreads();
+    const DecStreamOut h = sout[s];
+    if (h.status || status[s]) return;
+    const DecCaps cp = caps[s];
+    uint32_t acc = 0;  // stream raw CRC so far (thread 0)
+    for (uint32_t wl = 0; wl < h.nwin; wl++) {
+        const DecWin wd = wins[cp.win0 + wl];
+        const uint64_t full = wd.W / kOutTile, rem = wd.W % kOutTile;
+        const uint32_t* tc = tile_crc + wd.tile0;
+        uint32_t wc = crc_combine_uniform(ct, full, kOutTile, [&](uint64_t i) { return tc[i]; }, red);
+        if (threadIdx.x == 0) {
+            if (rem) wc = crc_shift_generic(ct->x2n, wc, rem) ^ tc[full];
+            acc = crc_shift_generic(ct->x2n, acc, wd.W) ^ wc;
+        }
     }
     if (threadIdx.x == 0) {
-        const uint32_t crc = red[0] ^ crc_shift_generic(ct->x2n, 0xFFFFFFFFu, h.orig) ^ 0xFFFFFFFFu;
+        const uint32_t crc = acc ^ crc_shift_generic(ct->x2n, 0xFFFFFFFFu, h.orig) ^ 0xFFFFFFFFu;
         if (crc != h.crc) atomicOr(&status[s], ST_INTEGRITY);
     }
 }

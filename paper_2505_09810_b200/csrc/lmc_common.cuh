@@ -69,11 +69,11 @@ struct BlockMeta {
 // Global tables (built once per context, see capi.cu):
 //   crc_slice[4][256]     slice-by-4 tables
 //   crc_shift[k][4][256]  byte-sliced operators "append 64*2^k zero bytes",
-//                         k = 0..7 (64 B .. 8 KiB)
+//                         k = 0..8 (64 B .. 16 KiB)
 //   x2n[64]               x^(2^k) mod P for the generic shift
 struct CrcTables {
     uint32_t slice[4][256];
-    uint32_t shift[8][4][256];
+    uint32_t shift[9][4][256];
     uint32_t x2n[64];
 };
 
@@ -92,6 +92,7 @@ __device__ __forceinline__ uint32_t crc_shift_tab(const uint32_t* __restrict__ t
 }
 // a*b mod P in the reflected representation (zlib multmodp)
 __device__ __forceinline__ uint32_t multmodp(uint32_t a, uint32_t b) {
+    if (a == 0 || b == 0) return 0;
     uint32_t m = 1u << 31, p = 0;
     for (;;) {
         if (a & m) {
@@ -118,6 +119,39 @@ __device__ __forceinline__ uint32_t x8nmodp(const uint32_t* __restrict__ x2n, ui
 __device__ __forceinline__ uint32_t crc_shift_generic(const uint32_t* __restrict__ x2n, uint32_t c, uint64_t nbytes) {
     if (c == 0 || nbytes == 0) return c;
     return multmodp(x8nmodp(x2n, nbytes), c);
+}
+
+// Raw CRC of `count` consecutive parts of `unit` bytes each, part(i) given by
+// get(i), combined by the whole CTA (blockDim.x threads, `red` = blockDim.x
+// words of shared memory).  Missing leading parts are treated as zero bytes,
+// which leave a raw CRC unchanged, so every thread folds the same number of
+// parts.  Result valid on thread 0.
+template <class F>
+__device__ uint32_t crc_combine_uniform(const CrcTables* __restrict__ ct, uint64_t count, uint64_t unit, F get,
+                                        uint32_t* red) {
+    const int T = blockDim.x, tid = threadIdx.x;
+    const uint64_t q = (count + T - 1) / T;
+    const int64_t pad = (int64_t)(q * T) - (int64_t)count;
+    uint32_t acc = 0;
+    if (count) {
+        const uint32_t K = x8nmodp(ct->x2n, unit);
+        for (uint64_t v = (uint64_t)tid * q; v < (uint64_t)tid * q + q; v++) {
+            const int64_t i = (int64_t)v - pad;
+            acc = multmodp(K, acc);
+            if (i >= 0) acc ^= get((uint64_t)i);
+        }
+    }
+    red[tid] = acc;
+    __syncthreads();
+    uint32_t Kk = count ? x8nmodp(ct->x2n, unit * q) : 0;
+    for (int k = 1; k < T; k <<= 1) {
+        if ((tid & (2 * k - 1)) == 0 && tid + k < T) red[tid] = multmodp(Kk, red[tid]) ^ red[tid + k];
+        Kk = multmodp(Kk, Kk);
+        __syncthreads();
+    }
+    const uint32_t r = red[0];
+    __syncthreads();
+    return r;
 }
 
 // Warp tree over 32 lane parts of kLaneBytes each (lane order = byte order):

@@ -155,10 +155,11 @@ def _bytes_view(t):
 class CompressedBatch:
     """Streams packed back to back in one CUDA byte tensor."""
 
-    def __init__(self, data, offsets, lengths):
+    def __init__(self, data, offsets, lengths, hints=None):
         self.data = data          # torch.uint8 [capacity], device
         self.offsets = offsets    # torch.int64 [n], device
         self.lengths = lengths    # torch.int64 [n], device
+        self.hints = hints        # per stream (orig, segments, block, windows): exact decode hints
         self._host = None
 
     def host_layout(self) -> tuple[list[int], list[int]]:
@@ -278,7 +279,9 @@ class Codec:
                              self._ws.numel(), ctypes.c_void_p(s.cuda_stream))
         self.ctx.check(rc)
         # keep inputs alive until the work is done
-        batch = CompressedBatch(out, meta[:n], meta[max(n, 1): max(n, 1) + n])
+        hints = [(int(v.numel()), segment_count, block_size, (int(v.numel()) + buffer_size - 1) // buffer_size)
+                 for v in views]
+        batch = CompressedBatch(out, meta[:n], meta[max(n, 1): max(n, 1) + n], hints)
         batch._keep = (views, pviews)
         return batch
 
@@ -300,56 +303,70 @@ class Codec:
         return dict(modes=modes, bits=bits, sizes=sizes, wire=wire, lengths=lengths, pm=pm)
 
     # -- decompress
-    def plan(self, streams: Sequence, stream=None):
-        """Parse/validate device streams; returns (orig_lengths, element codes, flags, status)."""
+    def read_hints(self, views, stream=None) -> list[tuple]:
+        """Exact (orig, segments, block, windows) of device streams, validated on the device (synchronises)."""
         import torch
 
-        n = len(streams)
-        ptrs = (ctypes.c_void_p * max(n, 1))()
-        lens = (ctypes.c_uint64 * max(n, 1))()
-        keep = []
-        for i, t in enumerate(streams):
-            v = _bytes_view(t)
-            if v.numel() == 0:
-                v = torch.zeros(1, dtype=torch.uint8, device=self.device)
-                lens[i] = 0
-            else:
-                lens[i] = v.numel()
-            keep.append(v)
-            ptrs[i] = v.data_ptr()
-        orig = (ctypes.c_uint64 * max(n, 1))()
-        ets = (ctypes.c_int32 * max(n, 1))()
-        flags = (ctypes.c_int32 * max(n, 1))()
-        st = (ctypes.c_int32 * max(n, 1))()
+        n = len(views)
+        ptrs = (ctypes.c_void_p * max(n, 1))(*[v.data_ptr() for v in views])
+        lens = (ctypes.c_uint64 * max(n, 1))(*[v.numel() for v in views])
+        hs = (_lib.lmcg_stream_hint * max(n, 1))()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        rc = self.ctx.lib.lmcg_decompress_plan(self.ctx.ptr, ptrs, lens, n, orig, ets, flags, st,
-                                               ctypes.c_void_p(s.cuda_stream))
-        self.ctx.check(rc)
-        self._plan_keep = keep
-        return list(orig)[:n], list(ets)[:n], list(flags)[:n], list(st)[:n]
+        self.ctx.check(self.ctx.lib.lmcg_read_hints(self.ctx.ptr, ptrs, lens, n, hs, ctypes.c_void_p(s.cuda_stream)))
+        return [(hs[i].orig, hs[i].segments, hs[i].block, hs[i].windows) for i in range(n)]
 
-    def decompress(self, streams, *, out=None, stream=None) -> DecompressedBatch:
-        """Decode device streams (a CompressedBatch or a list of CUDA byte tensors)."""
+    def decompress(self, streams, *, hints=None, out=None, stream=None) -> DecompressedBatch:
+        """Decode device streams (a CompressedBatch or a list of CUDA byte tensors).
+
+        ``hints`` (per stream: original length, segment count, block size,
+        window count) size the device work areas; a CompressedBatch carries
+        exact ones, otherwise they are read from the stream headers.  Wrong
+        hints only cost a retry.
+        """
         import torch
 
         if isinstance(streams, CompressedBatch):
+            if hints is None:
+                hints = streams.hints
             off, ln = streams.host_layout()
             streams = [streams.data[o: o + n] for o, n in zip(off, ln)]
-        n = len(streams)
-        orig, ets, flags, st0 = self.plan(streams, stream=stream)
-        offs, pos = [], 0
-        for i in range(n):
-            offs.append(pos)
-            pos += (orig[i] + 15) & ~15
-        if out is None or out.numel() < pos:
-            out = torch.empty(max(pos, 16), dtype=torch.uint8, device=self.device)
-        hoff = (ctypes.c_uint64 * max(n, 1))(*offs)
-        st = (ctypes.c_int32 * max(n, 1))()
+        views = []
+        for t in streams:
+            v = _bytes_view(t)
+            if v.numel() == 0:
+                v = torch.zeros(16, dtype=torch.uint8, device=self.device)[:0]
+            views.append(v)
+        n = len(views)
+        if hints is None:
+            hints = self.read_hints(views, stream=stream)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        rc = self.ctx.lib.lmcg_decompress_run(self.ctx.ptr, out.data_ptr(), hoff, st, ctypes.c_void_p(s.cuda_stream))
-        self.ctx.check(rc)
-        status = [st0[i] or st[i] for i in range(n)]
-        return DecompressedBatch(out, offs, orig, ets, flags, status)
+        ptrs = (ctypes.c_void_p * max(n, 1))(*[v.data_ptr() if v.numel() else 0 for v in views])
+        lens = (ctypes.c_uint64 * max(n, 1))(*[v.numel() for v in views])
+        for _ in range(3):
+            hs = (_lib.lmcg_stream_hint * max(n, 1))()
+            offs, pos = [], 0
+            for i, h in enumerate(hints):
+                hs[i].orig, hs[i].segments, hs[i].block, hs[i].windows = (int(x) for x in h)
+                offs.append(pos)
+                pos += (int(h[0]) + 15) & ~15
+            if out is None or out.numel() < pos:
+                out = torch.empty(max(pos, 16), dtype=torch.uint8, device=self.device)
+            hoff = (ctypes.c_uint64 * max(n, 1))(*offs)
+            self.ctx.check(self.ctx.lib.lmcg_decompress(self.ctx.ptr, ptrs, lens, n, hs, out.data_ptr(), out.numel(),
+                                                        hoff, ctypes.c_void_p(s.cuda_stream)))
+            st = (ctypes.c_int32 * max(n, 1))()
+            orig = (ctypes.c_uint64 * max(n, 1))()
+            ets = (ctypes.c_int32 * max(n, 1))()
+            fl = (ctypes.c_int32 * max(n, 1))()
+            nw = (ctypes.c_uint64 * max(n, 1))()
+            self.ctx.check(self.ctx.lib.lmcg_decompress_result(self.ctx.ptr, n, st, orig, ets, fl, nw))
+            status = list(st)[:n]
+            retry = [i for i in range(n) if status[i] in (8, 10)]
+            if not retry:
+                return DecompressedBatch(out, offs, list(orig)[:n], list(ets)[:n], list(fl)[:n], status)
+            hints = [((int(orig[i]), int(hints[i][1]), int(hints[i][2]), int(nw[i])) if i in retry else hints[i])
+                     for i in range(n)]
+        raise LmcError("decompress hints did not converge")
 
 
 _codecs: dict[int, Codec] = {}
