@@ -760,4 +760,15 @@ int lmcg_decompress_host(lmcg_ctx* ctx, const void* stream, uint64_t len, void* 
     return fail(ctx, LMCG_ERR_CORRUPT, "stream structure does not converge");
 }
 
+#ifdef LMCG_DEBUG
+int lmcg_debug_counters(unsigned long long* out, int reset) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, lmcg::lmcg_dbg, sizeof(unsigned long long) * 32);
+    if (reset) {
+        unsigned long long z[32] = {0};
+        cudaMemcpyToSymbol(lmcg::lmcg_dbg, z, sizeof z);
+    }
+    return 0;
+}
+#endif
 }  // extern "C"

@@ -30,10 +30,18 @@ namespace lmcg {
 
 constexpr int kChunk = 65536;        // segment payload bytes per k_scandec chunk
 constexpr int kOutTile = 16384;      // output bytes per k_ungroup CTA
-constexpr int kStage = 49152;        // Huffman bitstream bytes staged in shared memory
 constexpr int kLut = 11;             // LUT index bits
-constexpr int kCkpt = 4;             // self-sync checkpoints per decode chunk
-constexpr int kMine = 8;             // candidates a thread keeps per chunk
+
+#ifdef LMCG_DEBUG
+__device__ unsigned long long lmcg_dbg[32];
+#define DBG_ADD(i, v) atomicAdd(&lmcg_dbg[i], (unsigned long long)(v))
+#define DBG_T0(var) unsigned long long var = clock64()
+#define DBG_TADD(i, var) do { if (threadIdx.x == 0) atomicAdd(&lmcg_dbg[i], clock64() - var); } while (0)
+#else
+#define DBG_ADD(i, v) ((void)0)
+#define DBG_T0(var) ((void)0)
+#define DBG_TADD(i, var) ((void)0)
+#endif
 
 enum : uint32_t { ST_CORRUPT = 1, ST_INTEGRITY = 2, ST_UNSUPPORTED = 4, ST_RETRY = 8, ST_CAPACITY = 16 };
 
@@ -198,16 +206,22 @@ __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __res
 }
 
 // ------------------------------------------------------- Huffman decoding
+// Each record is decoded by one CTA: the bitstream is cut into one chunk of
+// S bits per thread.  Pass 0 decodes every chunk from its nominal start
+// (counting symbols, and marking the codeword boundaries of its first 64
+// bits in a bitmap); a fix-up pass re-decodes a chunk from the end of its
+// predecessor until it lands on one of those boundaries (Huffman codes
+// self-synchronise within a few codewords); pass 2 re-decodes every chunk
+// from its exact start and writes the symbols.  The decoder consumes up to
+// three symbols per table lookup.
+constexpr int kStage = 40960;  // bitstream bytes staged in shared memory (longer ones are read from global)
+
 struct DecSmem {
-    uint32_t bits[kStage / 4 + 8];      // staged bitstream, big-endian words
-    uint32_t mlut[1 << kLut];           // two-symbol LUT: n(2)|l1(4)|l12(5)|pad|s1(8)|s2(8)
-    union {
-        uint16_t slut[1 << kLut];       // single-symbol LUT (len << 8 | sym), build time only
-        struct {
-            uint32_t end[kThreads];
-            uint32_t ckpos[kCkpt][kThreads], ckcnt[kCkpt][kThreads];
-        } ch;
-    } u;
+    uint32_t bits[kStage / 4 + 4];      // staged bitstream, big-endian words
+    uint32_t lut3[1 << kLut];           // n(2)|tl(4)|pad(2)|s3(8)|s2(8)|s1(8); n == 0: slow path
+    uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0
+    uint32_t bm[2][kThreads];           // pass-0 boundary bitmaps (first 64 bits of each chunk)
+    uint32_t end[kThreads];
     uint8_t lens[256];
     uint8_t csym[256];
     uint32_t first_left[17], first_idx[17], bl_count[17];
@@ -216,20 +230,22 @@ struct DecSmem {
     uint32_t kraft;
     int minlen, maxlen;
     // k_scandec bookkeeping
-    uint32_t cand[kThreads];
+    uint32_t wcand[kWarps][64];
+    uint32_t wcnt[kWarps];
     uint32_t base;
     uint64_t tile;
 };
 
-struct Bits {
-    // reads from the staged shared copy when available, else from global
-    const uint32_t* sw;        // shared words (big-endian) or null
+// Payload bit source: big-endian words, bit i of the payload is bit
+// 31 - ((i + sh) & 31) of word (i + sh) >> 5; staged in shared memory when
+// it fits (sw != null), else read from global memory.
+struct Src {
+    const uint32_t* sw;
     const uint8_t* gbase;      // 4-aligned global base
     uint64_t glimit;           // payload end in bytes from gbase
     uint64_t nwords_full;
-    uint32_t sh;               // bit offset of bit 0 from gbase / shared word 0
-    __device__ __forceinline__ uint32_t word(uint64_t j) const {
-        if (sw) return sw[j];
+    uint32_t sh;
+    __device__ __forceinline__ uint32_t gword(uint64_t j) const {
         if (j < nwords_full) return bswap32(__ldg(reinterpret_cast<const uint32_t*>(gbase) + j));
         uint32_t v = 0;
         for (int q = 0; q < 4; q++) {
@@ -238,31 +254,30 @@ struct Bits {
         }
         return v;
     }
-};
-
-struct Reader {
-    uint64_t buf;
-    int nb;
-    uint64_t next;
-    __device__ __forceinline__ void init(const Bits& B, uint32_t bitpos) {
-        const uint64_t abit = (uint64_t)bitpos + B.sh;
-        const uint64_t j = abit >> 5;
-        const int k = (int)(abit & 31);
-        buf = (((uint64_t)B.word(j) << 32) | B.word(j + 1)) << k;
-        nb = 64 - k;
-        next = j + 2;
-    }
-    __device__ __forceinline__ void refill(const Bits& B) {
-        if (nb <= 32) {
-            buf |= (uint64_t)B.word(next) << (32 - nb);
-            nb += 32;
-            next++;
+    // the 32 payload bits starting at bit pos (zeros past the end)
+    __device__ __forceinline__ uint32_t peek(uint32_t pos) const {
+        const uint32_t a = pos + sh;
+        const uint32_t j = a >> 5;
+        uint32_t w0, w1;
+        if (sw) {
+            w0 = sw[j];
+            w1 = sw[j + 1];
+        } else {
+            w0 = gword(j);
+            w1 = gword(j + 1);
         }
+        return __funnelshift_l(w1, w0, a & 31);
     }
 };
 
-// Long-code path: canonical limit search for codes longer than kLut bits.
-__device__ __forceinline__ uint32_t long_code(const DecSmem& s, uint32_t win15, uint32_t& sym) {
+// One codeword at the window: returns its length (0 = invalid prefix).
+__device__ __forceinline__ uint32_t step1(const DecSmem& s, uint32_t win, uint32_t& sym) {
+    const uint32_t e = s.lut1[win >> (32 - kLut)];
+    if (e) {
+        sym = e & 0xFF;
+        return e >> 8;
+    }
+    const uint32_t win15 = win >> 17;
     for (int q = kLut + 1; q <= s.maxlen; q++) {
         const uint32_t fl = s.first_left[q], endq = fl + (s.bl_count[q] << (kMaxLen - q));
         if (s.bl_count[q] && win15 >= fl && win15 < endq) {
@@ -273,93 +288,212 @@ __device__ __forceinline__ uint32_t long_code(const DecSmem& s, uint32_t win15, 
     return 0;
 }
 
-// Decode the codewords starting in [pos, lim).  Returns the first boundary
-// >= lim (or ~0u on an invalid prefix) and the symbol count.
-//   MODE 0: count only, record kCkpt (boundary, count) checkpoints
-//   MODE 1: count only, stop early when landing on a recorded checkpoint
-//           (*sync = its index; the rest of the path is identical)
-//   MODE 2: emit the symbols to dst
-template <int MODE>
-__device__ uint32_t decode_span(DecSmem& s, const Bits& B, uint32_t pos, uint32_t lim, uint32_t& count, uint8_t* dst,
-                                int* sync) {
+// Decode the codewords that start in [pos, lim).  Returns the first boundary
+// >= lim (~0u on an invalid prefix) and the symbol count.
+//   bm == 1: mark the boundaries within [p0, p0 + 64) in this thread's bitmap
+//   bm == 2: stop as soon as a boundary hits that bitmap (*hit = the old
+//            path's symbol count at that boundary, else ~0u)
+//   EMIT:    write the symbols to dst
+// The bulk loop is branch-free apart from codes longer than kLut bits:
+// one 32-bit window (two word reads + funnel shift), one table lookup, up to
+// three symbols.
+template <bool EMIT>
+__device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32_t lim, uint32_t p0, int bm,
+                                uint32_t& count, uint8_t* dst, uint32_t* hit) {
+    // Lanes decode different chunks with different trip counts: every loop is
+    // driven by a warp vote so the warp re-converges each iteration (instead of
+    // drifting into independently scheduled, divergent lanes).
+    const unsigned mask = __activemask();
     const int tid = threadIdx.x;
-    Reader r;
-    r.init(B, pos);
     uint32_t c = 0;
-    uint64_t acc_lo = 0, acc_hi = 0;
-    int nacc = 0;
-    uint64_t o = 0;
-    const uint32_t step = (lim - pos) / (kCkpt + 1);
-    int ck = 0;
-    uint32_t ck_next = pos + step;
-    int sp = 0;
-    while (pos < lim) {
-        r.refill(B);
-        const uint32_t e = s.mlut[r.buf >> (64 - kLut)];
-        uint32_t nsym, l1, l12, s1, s2;
-        if (e) {
-            nsym = e >> 30;
-            l1 = (e >> 26) & 15;
-            l12 = (e >> 21) & 31;
-            s1 = (e >> 8) & 0xFF;
-            s2 = e & 0xFF;
-            if (nsym == 2 && pos + l1 >= lim) nsym = 1;  // second symbol starts past the span
-        } else {
-            l1 = long_code(s, (uint32_t)(r.buf >> 49), s1);
-            if (!l1) {
-                count = c;
-                return ~0u;
-            }
-            nsym = 1;
-            s2 = 0;
-            l12 = l1;
-        }
-        const uint32_t adv = nsym == 2 ? l12 : l1;
-        r.buf <<= adv;
-        r.nb -= adv;
-        if (MODE == 2) {
-            const uint32_t syms = s1 | (s2 << 8);
-            for (uint32_t q = 0; q < nsym; q++) {
-                const uint32_t sy = (syms >> (8 * q)) & 0xFF;
-                uint8_t* d = dst + o;
-                if (nacc == 0 && (reinterpret_cast<uint64_t>(d) & 15) != 0) {
-                    *d = (uint8_t)sy;
-                    o++;
+    bool bad = false, done = false;
+    if (!EMIT) {
+        // (every lane of the mask runs this loop's votes, also those with bm == 0)
+        uint32_t m0 = 0, m1 = 0;
+        if (bm == 2) { m0 = s.bm[0][tid]; m1 = s.bm[1][tid]; }
+        bool act = bm != 0 && pos < lim && pos < p0 + 64;
+        while (__any_sync(mask, act)) {
+            if (act) {
+                uint32_t sym;
+                const uint32_t l = step1(s, src.peek(pos), sym);
+                if (!l) {
+                    bad = true;
                 } else {
-                    if (nacc < 8) acc_lo |= (uint64_t)sy << (8 * nacc);
-                    else acc_hi |= (uint64_t)sy << (8 * (nacc - 8));
-                    if (++nacc == 16) {
-                        *reinterpret_cast<uint4*>(dst + o) = make_uint4((uint32_t)acc_lo, (uint32_t)(acc_lo >> 32),
-                                                                        (uint32_t)acc_hi, (uint32_t)(acc_hi >> 32));
-                        o += 16;
-                        nacc = 0;
-                        acc_lo = acc_hi = 0;
+                    pos += l;
+                    c++;
+                    const uint32_t rel = pos - p0;
+                    if (rel < 64) {
+                        const uint32_t bit = 1u << (rel & 31);
+                        if (bm == 1) {
+                            if (rel < 32) m0 |= bit; else m1 |= bit;
+                        } else if ((rel < 32 ? m0 : m1) & bit) {
+                            // synchronised: old count at this boundary = boundaries at or below rel
+                            *hit = rel < 32 ? __popc(m0 & (bit | (bit - 1))) : __popc(m0) + __popc(m1 & (bit | (bit - 1)));
+                            done = true;
+                        }
                     }
                 }
+                act = !bad && !done && pos < lim && pos < p0 + 64;
             }
         }
-        pos += adv;
-        c += nsym;
-        if (MODE == 0 && ck < kCkpt && pos >= ck_next && pos < lim) {
-            s.u.ch.ckpos[ck][tid] = pos;
-            s.u.ch.ckcnt[ck][tid] = c;
-            ck++;
-            ck_next = pos + step;
-        }
-        if (MODE == 1) {
-            while (sp < kCkpt && s.u.ch.ckpos[sp][tid] < pos) sp++;
-            if (sp < kCkpt && s.u.ch.ckpos[sp][tid] == pos) {
-                *sync = sp;
-                count = c;
-                return pos;
+        if (bm == 1) { s.bm[0][tid] = m0; s.bm[1][tid] = m1; }
+    }
+    uint8_t* d = dst;
+    if (EMIT) {
+        // head: single symbols until the destination is 8-byte aligned
+        bool act = pos < lim && (reinterpret_cast<uint64_t>(d) & 7);
+        while (__any_sync(mask, act)) {
+            if (act) {
+                uint32_t sym;
+                const uint32_t l = step1(s, src.peek(pos), sym);
+                if (!l) {
+                    bad = true;
+                } else {
+                    pos += l;
+                    c++;
+                    *d++ = (uint8_t)sym;
+                }
+                act = !bad && pos < lim && (reinterpret_cast<uint64_t>(d) & 7);
             }
         }
     }
-    if (MODE == 2)
-        for (int q = 0; q < nacc; q++) dst[o + q] = (uint8_t)((q < 8 ? acc_lo >> (8 * q) : acc_hi >> (8 * (q - 8))));
-    if (MODE == 1) *sync = -1;
+    uint64_t* w = reinterpret_cast<uint64_t*>(d);
+    uint64_t acc = 0;
+    uint32_t nacc = 0;
+    bool act = !bad && !done && pos + kLut <= lim;
+    while (__any_sync(mask, act)) {
+        if (act) {
+            const uint32_t win = src.peek(pos);
+            const uint32_t e = s.lut3[win >> (32 - kLut)];
+            uint32_t n = e >> 30, tl = (e >> 26) & 15, packed = e & 0xFFFFFF;
+            if (n == 0) {
+                uint32_t sym;
+                tl = step1(s, win, sym);
+                n = 1;
+                packed = sym;
+                bad = tl == 0;
+            }
+            pos += tl;
+            c += n;
+            if (EMIT) {
+                acc |= (uint64_t)packed << (8 * nacc);
+                const uint32_t nn = nacc + n;
+                const bool full = nn >= 8;
+                if (full) *w = acc;
+                w += full ? 1 : 0;
+                acc = full ? (nacc ? ((uint64_t)packed >> (8 * (8 - nacc))) : 0ull) : acc;
+                nacc = full ? nn - 8 : nn;
+            }
+            act = !bad && pos + kLut <= lim;
+        }
+    }
+    act = !bad && !done && pos < lim;
+    while (__any_sync(mask, act)) {
+        if (act) {
+            uint32_t sym;
+            const uint32_t l = step1(s, src.peek(pos), sym);
+            if (!l) {
+                bad = true;
+            } else {
+                pos += l;
+                c++;
+                if (EMIT) {
+                    acc |= (uint64_t)sym << (8 * nacc);
+                    if (++nacc == 8) {
+                        *w++ = acc;
+                        acc = 0;
+                        nacc = 0;
+                    }
+                }
+            }
+            act = !bad && pos < lim;
+        }
+    }
+    if (EMIT && !bad) {
+        uint8_t* b = reinterpret_cast<uint8_t*>(w);
+        for (uint32_t q = 0; q < nacc; q++) b[q] = (uint8_t)(acc >> (8 * q));
+    }
+    if (bm == 2 && !done) *hit = ~0u;
+    DBG_ADD(EMIT ? 4 : bm * 2, 1);
+    DBG_ADD((EMIT ? 4 : bm * 2) + 1, c);
     count = c;
-    return pos;
+    return bad ? ~0u : pos;
+}
+
+// All passes over the chunks of one record (see huff_decode).
+__device__ bool huff_passes(DecSmem& s, const Src& src, uint32_t bits, uint32_t len, uint8_t* dst) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t S = (bits + kThreads - 1) / kThreads;
+    S = max(128u, (S + 31) & ~31u);
+    const uint32_t nch = (bits + S - 1) / S;
+    const bool fixed = s.minlen == s.maxlen;
+    const uint32_t c = tid;
+    const uint32_t lim = min((c + 1) * S, bits);
+    uint32_t p0 = 0, my_start = 0, my_end = 0, my_cnt = 0;
+    DBG_T0(t_p0);
+    if (c < nch) {
+        p0 = c * S;
+        if (fixed) p0 = ((p0 + s.minlen - 1) / s.minlen) * s.minlen;
+        my_start = p0;
+        if (my_start >= lim) { my_end = my_start; s.bm[0][tid] = 0; s.bm[1][tid] = 0; }
+        else my_end = decode_span<false>(s, src, my_start, lim, p0, 1, my_cnt, nullptr, nullptr);
+        s.end[c] = my_end;
+    }
+    __syncthreads();
+    DBG_TADD(18, t_p0);
+    DBG_T0(t_fix);
+    // fix-up rounds until every chunk starts where its predecessor ended
+    for (;;) {
+        uint32_t pe = 0;
+        if (c < nch && c > 0) pe = s.end[c - 1];
+        __syncthreads();
+        int changed = 0;
+        if (c < nch && c > 0 && pe != ~0u && pe != my_start) {
+            const bool first_fix = my_start == p0;
+            my_start = pe;
+            if (my_start >= lim) {
+                my_end = my_start;
+                my_cnt = 0;
+            } else {
+                uint32_t h = ~0u, cnt2 = 0;
+                const uint32_t e2 = decode_span<false>(s, src, my_start, lim, p0, first_fix ? 2 : 0, cnt2, nullptr, &h);
+                if (first_fix && e2 != ~0u && h != ~0u) {
+                    my_cnt = cnt2 + (my_cnt - h);  // the rest of the path is the pass-0 path
+                } else {
+                    my_end = e2;
+                    my_cnt = cnt2;
+                }
+            }
+            s.end[c] = my_end;
+            changed = 1;
+        }
+        DBG_ADD(8, (tid == 0));
+        if (!__syncthreads_or(changed)) break;
+    }
+    uint32_t v = (c < nch) ? my_cnt : 0;
+    uint32_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s.wsum[warp] = incl;
+    __syncthreads();
+    uint32_t pre = 0, tot = 0;
+    for (int w = 0; w < kWarps; w++) { if (w < warp) pre += s.wsum[w]; tot += s.wsum[w]; }
+    const bool inv = (c < nch) && (my_end == ~0u);
+    const bool bad = __syncthreads_or(inv) || tot != len || s.end[nch - 1] != bits;
+    __syncthreads();
+    DBG_TADD(19, t_fix);
+    if (bad) return false;
+    DBG_T0(t_emit);
+    if (c < nch && my_cnt) {
+        uint32_t cc;
+        decode_span<true>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
+    }
+    __syncthreads();
+    DBG_TADD(20, t_emit);
+    return true;
 }
 
 // CTA-wide decode of one Huffman record payload `pl` (codebook | bits u32 |
@@ -368,6 +502,7 @@ __device__ uint32_t decode_span(DecSmem& s, const Bits& B, uint32_t pos, uint32_
 // position or symbol count).
 __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t* dst) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    DBG_T0(t_setup);
     __syncthreads();
     const uint8_t wb = pl[tid >> 1];
     const uint32_t l = (tid & 1) ? (wb >> 4) : (wb & 15);
@@ -410,120 +545,52 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     }
     const uint8_t* data = pl + kHuffOverhead;
     const uint64_t nbytes = ((uint64_t)bits + 7) / 8;
-    Bits B;
-    B.gbase = reinterpret_cast<const uint8_t*>(reinterpret_cast<uint64_t>(data) & ~3ull);
-    B.sh = (uint32_t)(reinterpret_cast<uint64_t>(data) & 3) * 8;
-    B.glimit = (uint64_t)(data - B.gbase) + nbytes;
-    B.nwords_full = B.glimit / 4;
-    B.sw = nullptr;
-    const uint64_t nwords = (B.glimit + 3) / 4;
-    const bool staged = nwords + 4 <= kStage / 4 + 8;
+    Src G;
+    G.sw = nullptr;
+    G.gbase = reinterpret_cast<const uint8_t*>(reinterpret_cast<uint64_t>(data) & ~3ull);
+    G.sh = (uint32_t)(reinterpret_cast<uint64_t>(data) & 3) * 8;
+    G.glimit = (uint64_t)(data - G.gbase) + nbytes;
+    G.nwords_full = G.glimit / 4;
+    const uint64_t nwords = (G.glimit + 3) / 4;
+    const bool staged = nwords + 3 <= kStage / 4 + 4;
     if (staged)  // stage the payload words (zero past the end) in shared memory
-        for (uint64_t j = tid; j < nwords + 4; j += kThreads) s.bits[j] = B.word(j);
+        for (uint64_t j = tid; j < nwords + 3; j += kThreads) s.bits[j] = G.gword(j);
     __syncthreads();
-    if (staged) B.sw = s.bits;
     // single-symbol LUT over kLut-bit prefixes
     for (int e = tid; e < (1 << kLut); e += kThreads) {
         const uint32_t v = (uint32_t)e << (kMaxLen - kLut);
         uint16_t ent = 0;
-        for (int q = 1; q <= kLut; q++) {
+        for (int q = s.minlen; q <= min(s.maxlen, kLut); q++) {
             const uint32_t fl = s.first_left[q], endq = fl + (s.bl_count[q] << (kMaxLen - q));
-            if (v >= fl && v < endq) {
-                ent = (uint16_t)((q << 8) | s.csym[s.first_idx[q] + ((v - fl) >> (kMaxLen - q))]);
+            if (v < endq) {
+                if (v >= fl) ent = (uint16_t)((q << 8) | s.csym[s.first_idx[q] + ((v - fl) >> (kMaxLen - q))]);
                 break;
             }
         }
-        s.u.slut[e] = ent;
+        s.lut1[e] = ent;
     }
     __syncthreads();
-    // two-symbol LUT
+    // three-symbol LUT: greedy codewords fully inside the kLut-bit prefix
     for (int e = tid; e < (1 << kLut); e += kThreads) {
-        const uint32_t a = s.u.slut[e];
-        uint32_t ent = 0;
-        if (a) {
-            const uint32_t l1 = a >> 8, s1 = a & 0xFF;
-            const uint32_t rest = ((uint32_t)e << l1) & ((1u << kLut) - 1);
-            const uint32_t b = s.u.slut[rest];
-            const uint32_t l2 = b >> 8;
-            if (b && l1 + l2 <= kLut) ent = (2u << 30) | (l1 << 26) | ((l1 + l2) << 21) | (s1 << 8) | (b & 0xFF);
-            else ent = (1u << 30) | (l1 << 26) | (l1 << 21) | (s1 << 8);
+        uint32_t ent = 0, n = 0, tl = 0, syms = 0;
+        uint32_t rest = (uint32_t)e;
+        while (n < 3) {
+            const uint32_t a = s.lut1[rest & ((1u << kLut) - 1)];
+            const uint32_t la = a >> 8;
+            if (!a || tl + la > kLut) break;
+            syms |= (a & 0xFF) << (8 * n);
+            n++;
+            tl += la;
+            rest = (uint32_t)e << tl;
         }
-        s.mlut[e] = ent;
+        if (n) ent = (n << 30) | (tl << 26) | syms;
+        s.lut3[e] = ent;
     }
     __syncthreads();
-    // chunking: one chunk of S bits per thread
-    uint32_t S = (bits + kThreads - 1) / kThreads;
-    S = max(128u, (S + 31) & ~31u);
-    const uint32_t nch = (bits + S - 1) / S;
-    const bool fixed = s.minlen == s.maxlen;
-    const uint32_t c = tid;
-    const uint32_t lim = min((c + 1) * S, bits);
-    uint32_t my_start = 0, my_end = 0, my_cnt = 0;
-    for (int k = 0; k < kCkpt; k++) { s.u.ch.ckpos[k][tid] = ~0u; s.u.ch.ckcnt[k][tid] = 0; }
-    if (c < nch) {
-        my_start = c * S;
-        if (fixed) my_start = ((my_start + s.minlen - 1) / s.minlen) * s.minlen;
-        if (my_start >= lim) my_end = my_start;
-        else my_end = decode_span<0>(s, B, my_start, lim, my_cnt, nullptr, nullptr);
-        s.u.ch.end[c] = my_end;
-    }
-    __syncthreads();
-    // fix-up rounds until every chunk starts where its predecessor ended
-    for (;;) {
-        uint32_t pe = 0;
-        if (c < nch && c > 0) pe = s.u.ch.end[c - 1];
-        __syncthreads();
-        int changed = 0;
-        if (c < nch && c > 0 && pe != ~0u && pe != my_start) {
-            my_start = pe;
-            if (my_start >= lim) {
-                my_end = my_start;
-                my_cnt = 0;
-                for (int q = 0; q < kCkpt; q++) s.u.ch.ckpos[q][tid] = ~0u;
-            } else {
-                int k = -1;
-                uint32_t cnt2 = 0;
-                const uint32_t e2 = decode_span<1>(s, B, my_start, lim, cnt2, nullptr, &k);
-                if (e2 != ~0u && k >= 0) {
-                    // merged into the previous path at checkpoint k: the rest is identical
-                    const uint32_t base = s.u.ch.ckcnt[k][tid];
-                    my_cnt = cnt2 + (my_cnt - base);
-                    for (int q = 0; q < kCkpt; q++) {
-                        if (q < k) s.u.ch.ckpos[q][tid] = ~0u;
-                        else s.u.ch.ckcnt[q][tid] = s.u.ch.ckcnt[q][tid] - base + cnt2;
-                    }
-                } else {
-                    my_end = e2;
-                    my_cnt = cnt2;
-                    for (int q = 0; q < kCkpt; q++) s.u.ch.ckpos[q][tid] = ~0u;
-                }
-            }
-            s.u.ch.end[c] = my_end;
-            changed = 1;
-        }
-        if (!__syncthreads_or(changed)) break;
-    }
-    uint32_t v = (c < nch) ? my_cnt : 0;
-    uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s.wsum[warp] = incl;
-    __syncthreads();
-    uint32_t pre = 0, tot = 0;
-    for (int w = 0; w < kWarps; w++) { if (w < warp) pre += s.wsum[w]; tot += s.wsum[w]; }
-    const bool inv = (c < nch) && (my_end == ~0u);
-    const bool bad = __syncthreads_or(inv) || tot != len || s.u.ch.end[nch - 1] != bits;
-    __syncthreads();
-    if (bad) return false;
-    if (c < nch && my_cnt) {
-        uint32_t cc;
-        decode_span<2>(s, B, my_start, lim, cc, dst + (pre + incl - v), nullptr);
-    }
-    __syncthreads();
-    return true;
+    DBG_TADD(16, t_setup);
+    DBG_ADD(17, staged ? 1 : 0);
+    if (staged) G.sw = s.bits;
+    return huff_passes(s, G, bits, len, dst);
 }
 
 __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t n) {
@@ -605,45 +672,72 @@ __device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint6
     return rd32(seg + pos + 1) == B;
 }
 
-// Candidates in [a, e) (a thread's slice of a chunk).  The little-endian
-// block size has exactly one non-zero byte, at offset 1 + kb of a record;
-// its positions are found 4 bytes at a time with __vcmpeq4.
-__device__ __forceinline__ uint32_t scan_slice(const DecSeg& sg, uint64_t a, uint64_t e, uint32_t* out) {
+// Candidates of positions [pa, pe) of a segment, found by one warp with
+// coalesced 16-byte loads: the little-endian block size has exactly one
+// non-zero byte (at offset 1 + kb of a record header), so anchors are the
+// bytes equal to it, compared 4 at a time with __vcmpeq4.  Appends the
+// candidates in increasing order to list[0..*cnt); returns false on overflow.
+__device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* list, uint32_t* cnt, int lane) {
     const uint32_t B = sg.block;
     const int kb = (__ffs(B) - 1) >> 3;
     const uint32_t kv = B >> (8 * kb);
-    uint32_t n = 0;
-    if (a >= e) return 0;
-    if (a == 0) {  // the segment start is always a record start
-        out[0] = 0;
-        n = 1;
-    }
-    const uint8_t* b = sg.base;
-    const uint64_t qa = max(a, (uint64_t)1) + 1 + kb, qe = min(e + 1 + kb, sg.comp);
-    uint64_t q = qa;
-    auto hit = [&](uint64_t qq) {
-        const uint64_t p = qq - 1 - kb;
-        if (is_cand(b, sg.comp, p, B)) {
-            if (n < kMine) out[n] = (uint32_t)p;
-            n++;
-        }
-    };
-    while (q < qe && (reinterpret_cast<uint64_t>(b + q) & 3)) {
-        if (b[q] == kv) hit(q);
-        q++;
-    }
     const uint32_t pat = kv * 0x01010101u;
-    for (; q + 4 <= qe; q += 4) {
-        const uint32_t m = __vcmpeq4(*reinterpret_cast<const uint32_t*>(b + q), pat);
-        if (m) {
-#pragma unroll
-            for (int k = 0; k < 4; k++)
-                if ((m >> (8 * k)) & 1) hit(q + k);
+    const uint8_t* b = sg.base;
+    const uint64_t qa = max(pa, (uint64_t)1) + 1 + kb;
+    const uint64_t qe = min(pe + 1 + kb, sg.comp);
+    if (qa >= qe) return true;
+    const uint64_t A = (reinterpret_cast<uint64_t>(b) + qa) & ~15ull;   // aligned absolute start
+    const uint64_t Aend = reinterpret_cast<uint64_t>(b) + qe;
+    const uint64_t segend = reinterpret_cast<uint64_t>(b) + sg.comp;
+    bool ok = true;
+    for (uint64_t g0 = A; g0 < Aend; g0 += 512) {
+        const uint64_t g = g0 + 16ull * lane;
+        uint32_t w4[4] = {0, 0, 0, 0};
+        if (g < Aend) {
+            if (g + 16 <= segend) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(g));
+                w4[0] = v.x; w4[1] = v.y; w4[2] = v.z; w4[3] = v.w;
+            } else {
+                for (int q = 0; q < 16; q++)
+                    if (g + q < segend) w4[q >> 2] |= (uint32_t)(*reinterpret_cast<const uint8_t*>(g + q)) << (8 * (q & 3));
+            }
         }
+        uint32_t found[4];
+        uint32_t k = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            uint32_t m = __vcmpeq4(w4[q], pat);
+            while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= ~(0xFFu << (bit & ~7));
+                const uint64_t abs_q = g + 4 * q + (bit >> 3);
+                if (abs_q >= reinterpret_cast<uint64_t>(b) + qa && abs_q < Aend) {
+                    const uint64_t p = abs_q - reinterpret_cast<uint64_t>(b) - 1 - kb;
+                    if (is_cand(b, sg.comp, p, B)) {
+                        if (k < 4) found[k] = (uint32_t)p;
+                        k++;
+                    }
+                }
+            }
+        }
+        if (k > 4) ok = false;
+        const uint32_t kk = min(k, 4u);
+        uint32_t incl = kk;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t base = *cnt + incl - kk;
+        for (uint32_t i = 0; i < kk; i++)
+            if (base + i < 64) list[base + i] = found[i];
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        __syncwarp();
+        if (lane == 0) *cnt += tot;
+        __syncwarp();
+        if (*cnt > 64) ok = false;
     }
-    for (; q < qe; q++)
-        if (b[q] == kv) hit(q);
-    return n;
+    return __all_sync(0xFFFFFFFFu, ok);
 }
 
 __global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__ segs, uint64_t nseg_total,
@@ -672,41 +766,61 @@ __global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__
         }
         const uint64_t ci = t - sg.chunk0;
         const uint64_t c0 = ci * kChunk, c1 = min(c0 + kChunk, sg.comp);
-        // ---- candidates of this chunk
-        uint32_t mine[kMine];
-        const uint64_t a = c0 + (uint64_t)tid * (kChunk / kThreads);
-        const uint32_t nmine = scan_slice(sg, a, min(a + kChunk / kThreads, c1), mine);
-        uint32_t incl = nmine;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
+        DBG_T0(t_scan);
+        DBG_ADD(21, tid == 0);
+        // ---- candidates of this chunk: warp w scans positions [c0 + w*8K, ...)
+        constexpr uint64_t kWarpSpan = kChunk / kWarps;
+        const uint64_t pa = c0 + warp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
+        if (lane == 0) {
+            s.wcnt[warp] = 0;
+            if (pa == 0 && pa < pe) {  // the segment start is always a record start
+                s.wcand[warp][0] = 0;
+                s.wcnt[warp] = 1;
+            }
         }
-        if (lane == 31) s.wsum[warp] = incl;
-        __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-        for (int w = 0; w < kWarps; w++) { if (w < warp) wpre += s.wsum[w]; tot += s.wsum[w]; }
-        // ---- segmented decoupled look-back over the segment's chunks
-        if (tid == 0) {
+        __syncwarp();
+        bool ok = true;
+        if (pa < pe) ok = warp_scan(sg, pa, pe, s.wcand[warp], &s.wcnt[warp], lane);
+        const bool dense = __syncthreads_or(!ok);
+        uint32_t tot = 0, wpre[kWarps];
+#pragma unroll
+        for (int w = 0; w < kWarps; w++) { wpre[w] = tot; tot += s.wcnt[w]; }
+        DBG_TADD(22, t_scan);
+        DBG_T0(t_lb);
+        // ---- segmented decoupled look-back over the segment's chunks (warp 0,
+        // 32 predecessors per round trip)
+        if (warp == 0) {
             uint64_t pre = 0;
             if (ci == 0) {
-                st_rel(&cstat[t], kFlagI | tot);
+                if (lane == 0) st_rel(&cstat[t], kFlagI | tot);
             } else {
-                st_rel(&cstat[t], kFlagA | tot);
-                int64_t j = (int64_t)t - 1;
+                if (lane == 0) st_rel(&cstat[t], kFlagA | tot);
+                int64_t j = (int64_t)t - 1;  // next predecessor to look at (lane 0's slot)
                 for (;;) {
-                    uint64_t st;
-                    do { st = ld_acq(&cstat[j]); } while ((st >> 62) == 0);
-                    pre += st & kMask;
-                    if ((st >> 62) == 2) break;
-                    j--;
+                    const int64_t jj = j - lane;
+                    uint64_t st = jj >= 0 ? ld_acq(&cstat[jj]) : kFlagI;
+                    // wait until the 32 slots are published
+                    while (__any_sync(0xFFFFFFFFu, (st >> 62) == 0)) {
+                        if ((st >> 62) == 0) st = ld_acq(&cstat[jj]);
+                    }
+                    const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (st >> 62) == 2);
+                    const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
+                    uint64_t v = (lane <= first && lane < 32) ? (st & kMask) : 0;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+                    pre += v;
+                    if (inc) break;
+                    j -= 32;
                 }
-                st_rel(&cstat[t], kFlagI | (pre + tot));
+                if (lane == 0) st_rel(&cstat[t], kFlagI | (pre + tot));
             }
-            s.base = (uint32_t)pre;
-            if (c1 == sg.comp) seg_cnt[lo] = (uint32_t)(pre + tot);
+            if (lane == 0) {
+                s.base = (uint32_t)pre;
+                if (c1 == sg.comp) seg_cnt[lo] = (uint32_t)(pre + tot);
+            }
         }
-        const bool dense = __syncthreads_or(nmine > kMine);
+        __syncthreads();
+        DBG_TADD(23, t_lb);
         if (dense) {
             // e.g. long runs of 6-byte RLE records: the serial path handles the segment
             if (tid == 0) atomicOr(&seg_fail[lo], 1u);
@@ -715,44 +829,34 @@ __global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__
         const uint32_t base = s.base;
         const uint32_t R = sg.nrec, B = sg.block;
         const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(R - 1) * B);
-        const uint32_t my0 = wpre + incl - nmine;
-        for (uint32_t done = 0; done < tot; done += kThreads) {
-            for (uint32_t k = 0; k < nmine; k++) {
-                const uint32_t g = my0 + k;
-                if (g >= done && g < done + kThreads) s.cand[g - done] = mine[k];
+        int w = 0;
+        for (uint32_t k = 0; k < tot; k++) {
+            while (k >= wpre[w] + s.wcnt[w]) w++;
+            uint64_t pos = s.wcand[w][k - wpre[w]];
+            uint32_t r = base + k;
+            if (r >= R) {
+                if (tid == 0) atomicOr(&seg_fail[lo], 1u);
+                break;
             }
-            __syncthreads();
-            const uint32_t nb = min(tot - done, (uint32_t)kThreads);
-            for (uint32_t k = 0; k < nb; k++) {
-                const uint64_t pos = s.cand[k];
-                const uint32_t r = base + done + k;
-                if (r >= R) {
-                    if (tid == 0) atomicOr(&seg_fail[lo], 1u);
-                    break;
-                }
+            // the candidate record, then (after record R-2) the tail record, which is
+            // not a candidate because its length differs from the block size
+            for (int part = 0; part < 2; part++) {
                 uint32_t mode = 0, l = 0;
                 uint64_t ps = 0;
-                bool ok = rec_size(sg.base, sg.comp, pos, mode, l, ps) && l == ((r + 1 == R) ? Ltail : B);
-                if (ok) ok = decode_record(s, sg.base + pos, mode, l, scratch + sg.goff + (uint64_t)r * B);
+                bool rok = rec_size(sg.base, sg.comp, pos, mode, l, ps) && l == ((r + 1 == R) ? Ltail : B);
+                DBG_T0(t_rec);
+                if (rok) rok = decode_record(s, sg.base + pos, mode, l, scratch + sg.goff + (uint64_t)r * B);
+                DBG_TADD(24 + (mode & 3), t_rec);
+                DBG_ADD(28 + (mode & 3), tid == 0);
                 if (tid == 0) {
                     rec_pos[sg.rec0 + r] = pos;
-                    rec_next[sg.rec0 + r] = ok ? pos + 5 + ps : ~0ull;
+                    rec_next[sg.rec0 + r] = rok ? pos + 5 + ps : ~0ull;
+                    if (!rok) atomicOr(&seg_fail[lo], 1u);
                 }
-                if (ok && r + 2 == R && Ltail != B) {
-                    // the tail record (not a candidate: its length differs) follows record R-2
-                    const uint64_t q = pos + 5 + ps;
-                    uint32_t tm = 0, tl = 0;
-                    uint64_t tps = 0;
-                    bool tok = rec_size(sg.base, sg.comp, q, tm, tl, tps) && tl == Ltail;
-                    if (tok) tok = decode_record(s, sg.base + q, tm, tl, scratch + sg.goff + (uint64_t)(R - 1) * B);
-                    if (tid == 0) {
-                        rec_pos[sg.rec0 + R - 1] = q;
-                        rec_next[sg.rec0 + R - 1] = tok ? q + 5 + tps : ~0ull;
-                    }
-                }
-                if (!ok && tid == 0) atomicOr(&seg_fail[lo], 1u);
+                if (!(rok && part == 0 && r + 2 == R && Ltail != B)) break;
+                pos += 5 + ps;
+                r = R - 1;
             }
-            __syncthreads();
         }
     }
 }
