@@ -667,9 +667,34 @@ __device__ __forceinline__ void st_rel(uint64_t* p, uint64_t v) {
     asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint64_t pos, uint32_t B) {
-    if (pos + 5 > comp || seg[pos] > 2) return false;
-    return rd32(seg + pos + 1) == B;
+__device__ __forceinline__ bool rec_size_dev(const uint8_t* seg, uint64_t comp, uint64_t pos, uint32_t& mode,
+                                             uint32_t& l, uint64_t& psize) {
+    if (pos + 5 > comp) return false;
+    mode = seg[pos];
+    l = rd32(seg + pos + 1);
+    if (mode == MODE_RLE) psize = 1;
+    else if (mode == MODE_STORED) psize = l;
+    else if (mode == MODE_HUFFMAN) {
+        if (pos + 5 + kHuffOverhead > comp) return false;
+        psize = kHuffOverhead + ((uint64_t)rd32(seg + pos + 5 + 128) + 7) / 8;
+    } else return false;
+    return pos + 5 + psize <= comp;
+}
+
+// A record header "mode <= 2 | len == B" whose payload fits and whose
+// successor is the segment end or another plausible header (len B, or the
+// segment's tail length).  False positives inside payload bytes would have to
+// pass both tests; any that does is caught by k_verify.
+__device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint64_t pos, uint32_t B, uint32_t Ltail) {
+    if (pos + 5 > comp || seg[pos] > 2 || rd32(seg + pos + 1) != B) return false;
+    uint32_t mode, l;
+    uint64_t ps;
+    if (!rec_size_dev(seg, comp, pos, mode, l, ps)) return false;
+    const uint64_t q = pos + 5 + ps;
+    if (q == comp) return true;
+    if (q + 5 > comp || seg[q] > 2) return false;
+    const uint32_t l2 = rd32(seg + q + 1);
+    return l2 == B || l2 == Ltail;
 }
 
 // Candidates of positions [pa, pe) of a segment, found by one warp with
@@ -679,6 +704,7 @@ __device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint6
 // candidates in increasing order to list[0..*cnt); returns false on overflow.
 __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* list, uint32_t* cnt, int lane) {
     const uint32_t B = sg.block;
+    const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(sg.nrec - 1) * B);
     const int kb = (__ffs(B) - 1) >> 3;
     const uint32_t kv = B >> (8 * kb);
     const uint32_t pat = kv * 0x01010101u;
@@ -713,7 +739,7 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* 
                 const uint64_t abs_q = g + 4 * q + (bit >> 3);
                 if (abs_q >= reinterpret_cast<uint64_t>(b) + qa && abs_q < Aend) {
                     const uint64_t p = abs_q - reinterpret_cast<uint64_t>(b) - 1 - kb;
-                    if (is_cand(b, sg.comp, p, B)) {
+                    if (is_cand(b, sg.comp, p, B, Ltail)) {
                         if (k < 4) found[k] = (uint32_t)p;
                         k++;
                     }
@@ -823,6 +849,7 @@ __global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__
         DBG_TADD(23, t_lb);
         if (dense) {
             // e.g. long runs of 6-byte RLE records: the serial path handles the segment
+            DBG_ADD(12, tid == 0);
             if (tid == 0) atomicOr(&seg_fail[lo], 1u);
             continue;
         }
@@ -835,6 +862,7 @@ __global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__
             uint64_t pos = s.wcand[w][k - wpre[w]];
             uint32_t r = base + k;
             if (r >= R) {
+                DBG_ADD(13, tid == 0);
                 if (tid == 0) atomicOr(&seg_fail[lo], 1u);
                 break;
             }
@@ -851,7 +879,7 @@ __global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__
                 if (tid == 0) {
                     rec_pos[sg.rec0 + r] = pos;
                     rec_next[sg.rec0 + r] = rok ? pos + 5 + ps : ~0ull;
-                    if (!rok) atomicOr(&seg_fail[lo], 1u);
+                    if (!rok) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(14, 1); }
                 }
                 if (!(rok && part == 0 && r + 2 == R && Ltail != B)) break;
                 pos += 5 + ps;
@@ -890,7 +918,7 @@ __global__ void k_verify(const DecSeg* __restrict__ segs, uint64_t nseg_total, u
         else if (r + 1 < R) ok = nx == rec_pos[g + 1];
         else ok = nx == sg.comp;
     }
-    if (!ok) atomicOr(&seg_fail[lo], 1u);
+    if (!ok) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(15, 1); }
 }
 
 // ------------------------------------------------------------- k_fallback
@@ -905,6 +933,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
     __shared__ uint32_t sh_mode, sh_len, sh_ok;
     for (uint64_t si = blockIdx.x; si < nseg_total; si += gridDim.x) {
         if (!seg_fail[si]) continue;
+        DBG_ADD(11, threadIdx.x == 0);
         const DecSeg sg = segs[si];
         if (threadIdx.x == 0) { sh_pos = 0; sh_got = 0; }
         __syncthreads();

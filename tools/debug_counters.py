@@ -12,15 +12,18 @@ import torch
 import paper_2505_09810_b200 as lmcb
 from paper_2505_09810_b200 import synth
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
-specs, ts = synth.make_checkpoint(cfg, seed=5)
+specs, ts = synth.make_checkpoint(cfg, seed=int(sys.argv[2]) if len(sys.argv) > 2 else 5)
 codec = lmcb.Codec()
 b = codec.compress(ts)
 cnt = (ctypes.c_ulonglong * 32)()
 L.lmcg_debug_counters(cnt, 1)
 r = codec.decompress(b)
 L.lmcg_debug_counters(cnt, 1)
-names = ["m0 calls", "m0 syms", "m1 calls", "m1 syms", "m2 calls", "m2 syms", "m3 calls", "m3 syms", "fixup rounds", "-", "-", "-",
-         "-", "-", "-", "-", "huff setup cyc", "staged recs", "pass0 cyc", "fixup cyc", "emit cyc", "chunks", "scan cyc",
+print("first decompress: fallback segs", cnt[11], "dense", cnt[12], "r>=R", cnt[13], "recfail", cnt[14], "verify", cnt[15])
+r = codec.decompress(b)
+L.lmcg_debug_counters(cnt, 1)
+names = ["count calls", "count syms", "rec-bm calls", "rec-bm syms", "emit calls", "emit syms", "chk-bm calls", "chk-bm syms", "fixup rounds", "-", "-", "fallback segs",
+         "dense", "r>=R", "rec fail", "verify fail", "huff setup cyc", "staged recs", "pass0 cyc", "fixup cyc", "emit cyc", "chunks", "scan cyc",
          "lookback cyc", "huff rec cyc", "rle rec cyc", "stored rec cyc", "-", "huff recs", "rle recs", "stored recs"]
 for i, n in enumerate(names):
     print(f"{n:14s} {cnt[i]}")
