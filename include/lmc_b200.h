@@ -131,6 +131,29 @@ int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
 int lmcg_decompress_result(lmcg_ctx* ctx, int n, int32_t* h_status, uint64_t* h_orig_lengths,
                            int32_t* h_element_types, int32_t* h_flags, uint64_t* h_windows);
 
+/* Plans: everything that depends only on shapes/options is validated, laid
+ * out and uploaded once; a run only launches kernels (no host synchronisation,
+ * no allocation), so runs can be captured in a CUDA graph and replayed for
+ * every checkpoint of the same model.
+ *
+ * Compress plan: the tensors' device addresses and sizes are fixed; each run
+ * compresses their current contents (identical bytes to lmcg_compress). */
+typedef struct lmcg_plan lmcg_plan;
+lmcg_plan* lmcg_compress_plan_create(lmcg_ctx* ctx, const lmcg_tensor* tensors, int n, const lmcg_options* opts);
+int lmcg_compress_plan_run(lmcg_ctx* ctx, lmcg_plan* plan, void* d_out, uint64_t out_capacity, uint64_t* d_offsets,
+                           uint64_t* d_lengths, void* cuda_stream);
+/* Decompress plan for n streams whose structure the hints describe exactly
+ * (e.g. those of a compress plan) and whose lengths never exceed len_bounds.
+ * Each run decodes the streams found at d_base + d_offsets[i] (device arrays,
+ * e.g. the output of lmcg_compress_plan_run) into d_out at 16-byte aligned
+ * packed offsets, and writes per-stream LMCG_* codes to d_status (device). */
+lmcg_plan* lmcg_decompress_plan_create(lmcg_ctx* ctx, int n, const lmcg_stream_hint* hints, const uint64_t* len_bounds);
+int lmcg_decompress_plan_run(lmcg_ctx* ctx, lmcg_plan* plan, const void* d_base, const uint64_t* d_offsets,
+                             const uint64_t* d_lengths, void* d_out, int32_t* d_status, void* cuda_stream);
+/* Output bytes a run needs: compress bound / decompressed payload bytes. */
+uint64_t lmcg_plan_output_bytes(const lmcg_plan* plan);
+void lmcg_plan_destroy(lmcg_plan* plan);
+
 /* Host-buffer conveniences (the call a ctypes binding in lmc.stream makes):
  * host -> device copy, the GPU path above, device -> host copy. */
 int lmcg_compress_host(lmcg_ctx* ctx, const void* data, uint64_t nbytes, int element_type, int delta,

@@ -51,7 +51,8 @@ EXPORTS = [
     "lmcg_create", "lmcg_destroy", "lmcg_last_error", "lmcg_version", "lmcg_validate_options",
     "lmcg_compress_bound", "lmcg_compress_workspace", "lmcg_compress", "lmcg_read_hints",
     "lmcg_decompress", "lmcg_decompress_result", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
-    "lmcg_block_info", "lmcg_profile", "lmcg_profile_report",
+    "lmcg_block_info", "lmcg_profile", "lmcg_profile_report", "lmcg_compress_plan_create", "lmcg_compress_plan_run",
+    "lmcg_decompress_plan_create", "lmcg_decompress_plan_run", "lmcg_plan_output_bytes", "lmcg_plan_destroy",
 ]
 
 _lib = None
@@ -102,6 +103,18 @@ def load(path: str = SO_PATH):
         L.lmcg_profile.argtypes = [vp, ctypes.c_int]
         L.lmcg_profile_report.restype = ctypes.c_int64
         L.lmcg_profile_report.argtypes = [vp, ctypes.c_char_p, u64]
+        L.lmcg_compress_plan_create.restype = vp
+        L.lmcg_compress_plan_create.argtypes = [vp, P(lmcg_tensor), ctypes.c_int, P(lmcg_options)]
+        L.lmcg_compress_plan_run.restype = ctypes.c_int
+        L.lmcg_compress_plan_run.argtypes = [vp, vp, vp, u64, vp, vp, vp]
+        L.lmcg_decompress_plan_create.restype = vp
+        L.lmcg_decompress_plan_create.argtypes = [vp, ctypes.c_int, P(lmcg_stream_hint), P(u64)]
+        L.lmcg_decompress_plan_run.restype = ctypes.c_int
+        L.lmcg_decompress_plan_run.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
+        L.lmcg_plan_output_bytes.restype = u64
+        L.lmcg_plan_output_bytes.argtypes = [vp]
+        L.lmcg_plan_destroy.restype = None
+        L.lmcg_plan_destroy.argtypes = [vp]
         _lib = L
         return L
 

@@ -46,6 +46,8 @@ struct lmcg_ctx {
     const void* d_sout = nullptr;
     const uint32_t* d_dstatus = nullptr;
     bool dec_attr = false;
+    int scandec_occ = 1;
+    bool enc_attr = false;
     // per-kernel event timing (lmcg_profile)
     bool prof = false;
     std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -346,9 +348,7 @@ uint64_t lmcg_compress_workspace(const lmcg_tensor* t, int n, const lmcg_options
     return compress_layout(P, n, offs);
 }
 
-int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options* o, void* d_out,
-                  uint64_t out_capacity, uint64_t* d_offsets, uint64_t* d_lengths, void* d_workspace,
-                  uint64_t workspace_bytes, void* cuda_stream) {
+static int check_compress_args(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options* o) {
     if (!ctx || !o || n < 0 || (n > 0 && !t)) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
     if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
     if (o->reserved) return fail(ctx, LMCG_ERR_ARGUMENT, "reserved option field must be 0");
@@ -358,20 +358,15 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options
         if (r) return fail(ctx, r, "tensor %d: %llu bytes is not a multiple of the element width", i, (unsigned long long)t[i].nbytes);
         if (t[i].nbytes && !t[i].data) return fail(ctx, LMCG_ERR_ARGUMENT, "tensor %d: null data", i);
     }
-    if (int r = ensure_ctx(ctx)) return r;
-    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    if (out_capacity < lmcg_compress_bound(t, n, o)) return fail(ctx, LMCG_ERR_CAPACITY, "output capacity below lmcg_compress_bound");
-    CPlan P;
-    make_plan(t, n, o, P);
-    size_t offs[16];
-    const size_t need = compress_layout(P, n, offs);
-    uint8_t* ws = static_cast<uint8_t*>(d_workspace);
-    if (!ws) {
-        if (int r = grow(ctx, &ctx->ws, &ctx->ws_cap, need)) return r;
-        ws = ctx->ws;
-    } else if (workspace_bytes < need) {
-        return fail(ctx, LMCG_ERR_CAPACITY, "workspace of %llu bytes < %llu", (unsigned long long)workspace_bytes, (unsigned long long)need);
-    }
+    return ensure_ctx(ctx);
+}
+
+// Kernel sequence of one compress over descriptors already resident on the
+// device (workspace laid out by compress_layout).  No host synchronisation:
+// capturable in a CUDA graph.
+static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t nslots, uint32_t min_w,
+                           const lmcg_options* o, uint8_t* ws, const size_t* offs, void* d_out, uint64_t* d_offsets,
+                           uint64_t* d_lengths, cudaStream_t st) {
     WinDesc* d_wins = reinterpret_cast<WinDesc*>(ws + offs[0]);
     StreamDesc* d_streams = reinterpret_cast<StreamDesc*>(ws + offs[1]);
     uint32_t* d_slot2win = reinterpret_cast<uint32_t*>(ws + offs[2]);
@@ -385,23 +380,14 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options
     uint32_t* d_pmlist = reinterpret_cast<uint32_t*>(ws + offs[10]);
     uint64_t* d_soff = d_offsets ? d_offsets : reinterpret_cast<uint64_t*>(ws + offs[11]);
     uint64_t* d_slen = d_lengths ? d_lengths : reinterpret_cast<uint64_t*>(ws + offs[12]);
-    // descriptors -> device through pinned staging
-    const size_t wbytes = P.wins.size() * sizeof(WinDesc), sbytes = P.streams.size() * sizeof(StreamDesc);
-    if (int r = grow_pinned(ctx, wbytes + sbytes + 64)) return r;
-    if (wbytes) memcpy(ctx->pin, P.wins.data(), wbytes);
-    if (sbytes) memcpy(ctx->pin + wbytes, P.streams.data(), sbytes);
-    if (wbytes) CK(cudaMemcpyAsync(d_wins, ctx->pin, wbytes, cudaMemcpyHostToDevice, st));
-    if (sbytes) CK(cudaMemcpyAsync(d_streams, ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
-    CK(cudaEventRecord(ctx->pin_done, st));
-    const uint64_t nb = P.nb;
     const uint64_t ntiles = (nb + kScanTile - 1) / kScanTile;
     CK(cudaMemsetAsync(d_status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     CK(cudaMemsetAsync(d_ctr, 0, 4 * sizeof(uint32_t), st));
-    const int nwin = (int)P.wins.size();
     if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win); }
-    if (P.nslots) {
-        { PROF(k_hist_crc); k_hist_crc<<<(unsigned)P.nslots, kThreads, 0, st>>>(d_wins, d_slot2win, P.nslots, o->block_size, ctx->d_crc,
-                                                             d_hist, d_crcp, d_meta); }
+    if (nslots) {
+        PROF(k_hist_crc);
+        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, ctx->d_crc, d_hist,
+                                                          d_crcp, d_meta);
     }
     if (nb) {
         { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
@@ -414,19 +400,122 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options
         { PROF(k_frame); k_frame<<<n, kThreads, 0, st>>>(d_streams, d_wins, o->block_size, o->segment_count, d_scan, d_crcp,
                                          ctx->d_crc, d_soff, static_cast<uint8_t*>(d_out)); }
     }
-    if (P.nslots) {
-        const uint64_t iterpos = (uint64_t)(kTileBytes / P.min_w) * kWarps;
+    if (nslots) {
+        const uint64_t iterpos = (uint64_t)(kTileBytes / min_w) * kWarps;
         const size_t smem = (size_t)((iterpos * 15) / 32 + 8) * sizeof(uint32_t);
-        if (smem > 48 * 1024) CK(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        { PROF(k_encode); k_encode<<<(unsigned)P.nslots, kThreads, smem, st>>>(d_wins, d_slot2win, P.nslots, o->block_size,
-                                                            o->segment_count, d_streams, d_meta, d_wire, d_scan, d_soff,
-                                                            static_cast<uint8_t*>(d_out)); }
+        if (smem > 48 * 1024 && !ctx->enc_attr) {
+            CK(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            ctx->enc_attr = true;
+        }
+        PROF(k_encode);
+        k_encode<<<(unsigned)nslots, kThreads, smem, st>>>(d_wins, d_slot2win, nslots, o->block_size, o->segment_count,
+                                                         d_streams, d_meta, d_wire, d_scan, d_soff,
+                                                         static_cast<uint8_t*>(d_out));
     }
     CK(cudaGetLastError());
     ctx->last_nb = nb;
     ctx->last_meta = d_meta;
     ctx->last_wire = d_wire;
     return LMCG_OK;
+}
+
+int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options* o, void* d_out,
+                  uint64_t out_capacity, uint64_t* d_offsets, uint64_t* d_lengths, void* d_workspace,
+                  uint64_t workspace_bytes, void* cuda_stream) {
+    if (int r = check_compress_args(ctx, t, n, o)) return r;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (out_capacity < lmcg_compress_bound(t, n, o)) return fail(ctx, LMCG_ERR_CAPACITY, "output capacity below lmcg_compress_bound");
+    CPlan P;
+    make_plan(t, n, o, P);
+    size_t offs[16];
+    const size_t need = compress_layout(P, n, offs);
+    uint8_t* ws = static_cast<uint8_t*>(d_workspace);
+    if (!ws) {
+        if (int r = grow(ctx, &ctx->ws, &ctx->ws_cap, need)) return r;
+        ws = ctx->ws;
+    } else if (workspace_bytes < need) {
+        return fail(ctx, LMCG_ERR_CAPACITY, "workspace of %llu bytes < %llu", (unsigned long long)workspace_bytes, (unsigned long long)need);
+    }
+    // descriptors -> device through pinned staging
+    const size_t wbytes = P.wins.size() * sizeof(WinDesc), sbytes = P.streams.size() * sizeof(StreamDesc);
+    if (int r = grow_pinned(ctx, wbytes + sbytes + 64)) return r;
+    if (wbytes) memcpy(ctx->pin, P.wins.data(), wbytes);
+    if (sbytes) memcpy(ctx->pin + wbytes, P.streams.data(), sbytes);
+    if (wbytes) CK(cudaMemcpyAsync(ws + offs[0], ctx->pin, wbytes, cudaMemcpyHostToDevice, st));
+    if (sbytes) CK(cudaMemcpyAsync(ws + offs[1], ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(ctx->pin_done, st));
+    return compress_launch(ctx, n, (int)P.wins.size(), P.nb, P.nslots, P.min_w, o, ws, offs, d_out, d_offsets, d_lengths, st);
+}
+
+// ---------------------------------------------------------------- plans
+struct lmcg_plan {
+    int kind = 0;  // 1 compress, 2 decompress
+    int n = 0;
+    uint8_t* ws = nullptr;
+    size_t ws_bytes = 0;
+    // compress
+    lmcg_options opts{};
+    int nwin = 0;
+    uint64_t nb = 0, nslots = 0, bound = 0;
+    uint32_t min_w = 4;
+    size_t offs[16] = {};
+    // decompress
+    uint64_t dn_win = 0, dn_seg = 0, dn_rec = 0, dn_chunk = 0, dn_tile = 0, out_bytes = 0;
+    size_t doffs[20] = {};
+    int scandec_grid = 0, fallback_grid = 0;
+};
+
+lmcg_plan* lmcg_compress_plan_create(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options* o) {
+    if (check_compress_args(ctx, t, n, o)) return nullptr;
+    lmcg_plan* pl = new lmcg_plan();
+    pl->kind = 1;
+    pl->n = n;
+    pl->opts = *o;
+    CPlan P;
+    make_plan(t, n, o, P);
+    pl->nwin = (int)P.wins.size();
+    pl->nb = P.nb;
+    pl->nslots = P.nslots;
+    pl->min_w = P.min_w;
+    pl->bound = lmcg_compress_bound(t, n, o);
+    pl->ws_bytes = compress_layout(P, n, pl->offs);
+    if (cudaMalloc(&pl->ws, pl->ws_bytes) != cudaSuccess) {
+        fail(ctx, LMCG_ERR_CUDA, "cudaMalloc of %zu bytes for a compress plan failed", pl->ws_bytes);
+        delete pl;
+        return nullptr;
+    }
+    if (!P.wins.empty()) cudaMemcpy(pl->ws + pl->offs[0], P.wins.data(), P.wins.size() * sizeof(WinDesc), cudaMemcpyHostToDevice);
+    if (!P.streams.empty()) cudaMemcpy(pl->ws + pl->offs[1], P.streams.data(), P.streams.size() * sizeof(StreamDesc), cudaMemcpyHostToDevice);
+    if (cudaGetLastError() != cudaSuccess) {
+        cudaFree(pl->ws);
+        delete pl;
+        fail(ctx, LMCG_ERR_CUDA, "uploading compress plan descriptors failed");
+        return nullptr;
+    }
+    return pl;
+}
+
+uint64_t lmcg_plan_output_bytes(const lmcg_plan* pl) {
+    if (!pl) return 0;
+    return pl->kind == 1 ? pl->bound : pl->out_bytes;
+}
+
+int lmcg_compress_plan_run(lmcg_ctx* ctx, lmcg_plan* pl, void* d_out, uint64_t out_capacity, uint64_t* d_offsets,
+                           uint64_t* d_lengths, void* cuda_stream) {
+    if (!ctx || !pl || pl->kind != 1) return fail(ctx, LMCG_ERR_ARGUMENT, "not a compress plan");
+    if (out_capacity < pl->bound) return fail(ctx, LMCG_ERR_CAPACITY, "output capacity below the plan's bound");
+    if (int r = ensure_ctx(ctx)) return r;
+    return compress_launch(ctx, pl->n, pl->nwin, pl->nb, pl->nslots, pl->min_w, &pl->opts, pl->ws, pl->offs, d_out,
+                           d_offsets, d_lengths, static_cast<cudaStream_t>(cuda_stream));
+}
+
+void lmcg_plan_destroy(lmcg_plan* pl) {
+    if (!pl) return;
+    if (pl->ws) {
+        cudaDeviceSynchronize();
+        cudaFree(pl->ws);
+    }
+    delete pl;
 }
 
 int lmcg_profile(lmcg_ctx* ctx, int enable) {
@@ -592,6 +681,82 @@ int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
     return LMCG_OK;
 }
 
+namespace {
+// Workspace layout of one decompress (offsets into the workspace).
+enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CST, D_TK, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_TC, D_SCR, D_NOFF };
+size_t dec_layout(const DPlan& P, int n, size_t* o) {
+    Arena a;
+    o[D_IN] = a.take<DecStreamIn>(n + 1);
+    o[D_CAPS] = a.take<DecCaps>(n + 1);
+    o[D_SOUT] = a.take<DecStreamOut>(n + 1);
+    o[D_ST] = a.take<uint32_t>(n + 1);
+    o[D_WIN] = a.take<DecWin>(P.nwin + 1);
+    o[D_SEG] = a.take<DecSeg>(P.nseg + 1);
+    o[D_CST] = a.take<uint64_t>(P.nchunk + 1);
+    o[D_TK] = a.take<uint32_t>(4);
+    o[D_SCNT] = a.take<uint32_t>(P.nseg + 1);
+    o[D_SFAIL] = a.take<uint32_t>(P.nseg + 1);
+    o[D_RPOS] = a.take<uint64_t>(P.nrec + 1);
+    o[D_RNEXT] = a.take<uint64_t>(P.nrec + 1);
+    o[D_TC] = a.take<uint32_t>(P.ntile + 1);
+    o[D_SCR] = a.take<uint8_t>(P.scratch + 64);
+    return a.off + 256;
+}
+}  // namespace
+
+// Kernel sequence of one decompress; DecStreamIn and DecCaps are already on
+// the device.  No host synchronisation: capturable in a CUDA graph.
+static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg, uint64_t nrec, uint64_t nchunk,
+                             uint64_t ntile, uint8_t* ws, const size_t* o, void* d_out, int32_t* d_codes,
+                             cudaStream_t st) {
+    auto* d_in = reinterpret_cast<DecStreamIn*>(ws + o[D_IN]);
+    auto* d_caps = reinterpret_cast<DecCaps*>(ws + o[D_CAPS]);
+    auto* d_sout = reinterpret_cast<DecStreamOut*>(ws + o[D_SOUT]);
+    auto* d_st = reinterpret_cast<uint32_t*>(ws + o[D_ST]);
+    auto* d_win = reinterpret_cast<DecWin*>(ws + o[D_WIN]);
+    auto* d_seg = reinterpret_cast<DecSeg*>(ws + o[D_SEG]);
+    auto* d_cst = reinterpret_cast<uint64_t*>(ws + o[D_CST]);
+    auto* d_tk = reinterpret_cast<uint32_t*>(ws + o[D_TK]);
+    auto* d_scnt = reinterpret_cast<uint32_t*>(ws + o[D_SCNT]);
+    auto* d_sfail = reinterpret_cast<uint32_t*>(ws + o[D_SFAIL]);
+    auto* d_rpos = reinterpret_cast<uint64_t*>(ws + o[D_RPOS]);
+    auto* d_rnext = reinterpret_cast<uint64_t*>(ws + o[D_RNEXT]);
+    auto* d_tc = reinterpret_cast<uint32_t*>(ws + o[D_TC]);
+    uint8_t* d_scr = ws + o[D_SCR];
+    ctx->d_sout = d_sout;
+    ctx->d_dstatus = d_st;
+    ctx->dn = n;
+    CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
+    CK(cudaMemsetAsync(d_cst, 0, (nchunk + 1) * sizeof(uint64_t), st));
+    CK(cudaMemsetAsync(d_tk, 0, 16, st));
+    CK(cudaMemsetAsync(d_sfail, 0, (nseg + 1) * sizeof(uint32_t), st));
+    if (!n) return LMCG_OK;
+    const size_t dsm = sizeof(DecSmem);
+    if (!ctx->dec_attr) {
+        CK(cudaFuncSetAttribute(k_scandec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        CK(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        ctx->scandec_occ = occupancy(ctx, (const void*)k_scandec, kThreads, dsm);
+        ctx->dec_attr = true;
+    }
+    { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg); }
+    if (nchunk) {
+        const int grid = (int)std::min<uint64_t>(nchunk, (uint64_t)ctx->scandec_occ);
+        PROF(k_scandec);
+        k_scandec<<<grid, kThreads, dsm, st>>>(d_seg, nseg, nchunk, d_tk, d_cst, d_scnt, d_sfail, d_rpos, d_rnext, d_scr);
+    }
+    if (nrec) { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, nseg, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
+    if (nseg) {
+        const int grid = (int)std::min<uint64_t>(nseg, 148 * 2);
+        PROF(k_fallback);
+        k_fallback<<<grid, kThreads, dsm, st>>>(d_seg, nseg, d_sfail, d_st, d_scr);
+    }
+    if (ntile) { PROF(k_ungroup); k_ungroup<<<(unsigned)ntile, kThreads, 0, st>>>(d_win, nwin, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_st); }
+    { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st); }
+    if (d_codes) k_status<<<(n + 255) / 256, 256, 0, st>>>(d_sout, d_st, n, d_codes);
+    CK(cudaGetLastError());
+    return LMCG_OK;
+}
+
 int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
                     const lmcg_stream_hint* hints, void* d_out, uint64_t out_capacity, const uint64_t* h_out_offsets,
                     void* cuda_stream) {
@@ -599,80 +764,59 @@ int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
     if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
     if (int r = ensure_ctx(ctx)) return r;
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-    ctx->dn = n;
     DPlan P;
     make_dplan(lens, n, hints, h_out_offsets, out_capacity, P);
-    Arena a;
-    const size_t o_in = a.take<DecStreamIn>(n + 1);
-    const size_t o_caps = a.take<DecCaps>(n + 1);
-    const size_t o_out = a.take<DecStreamOut>(n + 1);
-    const size_t o_st = a.take<uint32_t>(n + 1);
-    const size_t o_win = a.take<DecWin>(P.nwin + 1);
-    const size_t o_seg = a.take<DecSeg>(P.nseg + 1);
-    const size_t o_cst = a.take<uint64_t>(P.nchunk + 1);
-    const size_t o_tk = a.take<uint32_t>(4);
-    const size_t o_scnt = a.take<uint32_t>(P.nseg + 1);
-    const size_t o_sfail = a.take<uint32_t>(P.nseg + 1);
-    const size_t o_rpos = a.take<uint64_t>(P.nrec + 1);
-    const size_t o_rnext = a.take<uint64_t>(P.nrec + 1);
-    const size_t o_tc = a.take<uint32_t>(P.ntile + 1);
-    const size_t o_scr = a.take<uint8_t>(P.scratch + 64);
-    if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, a.off + 256)) return r;
+    size_t o[D_NOFF];
+    const size_t need = dec_layout(P, n, o);
+    if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, need)) return r;
     uint8_t* ws = ctx->dws;
-    auto* d_in = reinterpret_cast<DecStreamIn*>(ws + o_in);
-    auto* d_caps = reinterpret_cast<DecCaps*>(ws + o_caps);
-    auto* d_sout = reinterpret_cast<DecStreamOut*>(ws + o_out);
-    auto* d_st = reinterpret_cast<uint32_t*>(ws + o_st);
-    auto* d_win = reinterpret_cast<DecWin*>(ws + o_win);
-    auto* d_seg = reinterpret_cast<DecSeg*>(ws + o_seg);
-    auto* d_cst = reinterpret_cast<uint64_t*>(ws + o_cst);
-    auto* d_tk = reinterpret_cast<uint32_t*>(ws + o_tk);
-    auto* d_scnt = reinterpret_cast<uint32_t*>(ws + o_scnt);
-    auto* d_sfail = reinterpret_cast<uint32_t*>(ws + o_sfail);
-    auto* d_rpos = reinterpret_cast<uint64_t*>(ws + o_rpos);
-    auto* d_rnext = reinterpret_cast<uint64_t*>(ws + o_rnext);
-    auto* d_tc = reinterpret_cast<uint32_t*>(ws + o_tc);
-    uint8_t* d_scr = ws + o_scr;
-    ctx->d_sout = d_sout;
-    ctx->d_dstatus = d_st;
     const size_t hb = (size_t)n * (sizeof(DecStreamIn) + sizeof(DecCaps)) + 64;
     if (int r = grow_pinned(ctx, hb)) return r;
     if (n) {
         DecStreamIn* pin_in = reinterpret_cast<DecStreamIn*>(ctx->pin);
         for (int i = 0; i < n; i++) pin_in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i]};
         memcpy(ctx->pin + (size_t)n * sizeof(DecStreamIn), P.caps.data(), (size_t)n * sizeof(DecCaps));
-        CK(cudaMemcpyAsync(d_in, ctx->pin, (size_t)n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(d_caps, ctx->pin + (size_t)n * sizeof(DecStreamIn), (size_t)n * sizeof(DecCaps),
+        CK(cudaMemcpyAsync(ws + o[D_IN], ctx->pin, (size_t)n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(ws + o[D_CAPS], ctx->pin + (size_t)n * sizeof(DecStreamIn), (size_t)n * sizeof(DecCaps),
                            cudaMemcpyHostToDevice, st));
         CK(cudaEventRecord(ctx->pin_done, st));
     }
-    CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
-    CK(cudaMemsetAsync(d_cst, 0, (P.nchunk + 1) * sizeof(uint64_t), st));
-    CK(cudaMemsetAsync(d_tk, 0, 16, st));
-    CK(cudaMemsetAsync(d_sfail, 0, (P.nseg + 1) * sizeof(uint32_t), st));
-    if (!n) return LMCG_OK;
-    const size_t dsm = sizeof(DecSmem);
-    if (!ctx->dec_attr) {
-        CK(cudaFuncSetAttribute(k_scandec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        CK(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        ctx->dec_attr = true;
+    return decompress_launch(ctx, n, P.nwin, P.nseg, P.nrec, P.nchunk, P.ntile, ws, o, d_out, nullptr, st);
+}
+
+lmcg_plan* lmcg_decompress_plan_create(lmcg_ctx* ctx, int n, const lmcg_stream_hint* hints, const uint64_t* len_bounds) {
+    if (!ctx || n < 0 || (n && (!hints || !len_bounds))) { fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments"); return nullptr; }
+    if (!ctx->d_crc) { fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback"); return nullptr; }
+    if (ensure_ctx(ctx)) return nullptr;
+    lmcg_plan* pl = new lmcg_plan();
+    pl->kind = 2;
+    pl->n = n;
+    DPlan P;
+    make_dplan(len_bounds, n, hints, nullptr, ~0ull, P);
+    uint64_t out = 0;
+    for (int i = 0; i < n; i++) out += (hints[i].orig + 15) & ~15ull;
+    pl->out_bytes = out;
+    pl->dn_win = P.nwin; pl->dn_seg = P.nseg; pl->dn_rec = P.nrec; pl->dn_chunk = P.nchunk; pl->dn_tile = P.ntile;
+    pl->ws_bytes = dec_layout(P, n, pl->doffs);
+    if (cudaMalloc(&pl->ws, pl->ws_bytes) != cudaSuccess) {
+        fail(ctx, LMCG_ERR_CUDA, "cudaMalloc of %zu bytes for a decompress plan failed", pl->ws_bytes);
+        delete pl;
+        return nullptr;
     }
-    { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg); }
-    if (P.nchunk) {
-        const int grid = (int)std::min<uint64_t>(P.nchunk, (uint64_t)occupancy(ctx, (const void*)k_scandec, kThreads, dsm));
-        PROF(k_scandec);
-        k_scandec<<<grid, kThreads, dsm, st>>>(d_seg, P.nseg, P.nchunk, d_tk, d_cst, d_scnt, d_sfail, d_rpos, d_rnext, d_scr);
-    }
-    if (P.nrec) { PROF(k_verify); k_verify<<<(unsigned)((P.nrec + 255) / 256), 256, 0, st>>>(d_seg, P.nseg, P.nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
-    if (P.nseg) {
-        const int grid = (int)std::min<uint64_t>(P.nseg, 148 * 2);
-        PROF(k_fallback);
-        k_fallback<<<grid, kThreads, dsm, st>>>(d_seg, P.nseg, d_sfail, d_st, d_scr);
-    }
-    if (P.ntile) { PROF(k_ungroup); k_ungroup<<<(unsigned)P.ntile, kThreads, 0, st>>>(d_win, P.nwin, P.ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_st); }
-    { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st); }
-    CK(cudaGetLastError());
-    return LMCG_OK;
+    if (n) cudaMemcpy(pl->ws + pl->doffs[D_CAPS], P.caps.data(), n * sizeof(DecCaps), cudaMemcpyHostToDevice);
+    return pl;
+}
+
+int lmcg_decompress_plan_run(lmcg_ctx* ctx, lmcg_plan* pl, const void* d_base, const uint64_t* d_offsets,
+                             const uint64_t* d_lengths, void* d_out, int32_t* d_status, void* cuda_stream) {
+    if (!ctx || !pl || pl->kind != 2 || (pl->n && (!d_base || !d_offsets || !d_lengths))) return fail(ctx, LMCG_ERR_ARGUMENT, "not a decompress plan");
+    if (int r = ensure_ctx(ctx)) return r;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    if (pl->n)
+        k_mkin<<<(pl->n + 255) / 256, 256, 0, st>>>(static_cast<const uint8_t*>(d_base), d_offsets, d_lengths, pl->n,
+                                                  reinterpret_cast<DecStreamIn*>(pl->ws + pl->doffs[D_IN]));
+    return decompress_launch(ctx, pl->n, pl->dn_win, pl->dn_seg, pl->dn_rec, pl->dn_chunk, pl->dn_tile, pl->ws,
+                             pl->doffs, d_out, d_status, st);
 }
 
 int lmcg_decompress_result(lmcg_ctx* ctx, int n, int32_t* h_status, uint64_t* h_orig, int32_t* h_et, int32_t* h_flags,

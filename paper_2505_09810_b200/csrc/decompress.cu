@@ -1097,4 +1097,27 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const DecStreamOut* __res
     }
 }
 
+// ----------------------------------------------------- plan helper kernels
+// Stream inputs of a decompress plan: n streams at base + offsets[i].
+__global__ void k_mkin(const uint8_t* __restrict__ base, const uint64_t* __restrict__ offsets,
+                       const uint64_t* __restrict__ lengths, int n, DecStreamIn* __restrict__ in) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) in[i] = DecStreamIn{base + offsets[i], lengths[i]};
+}
+
+// Final per-stream status as C-ABI codes (LMCG_*), written to device memory.
+__global__ void k_status(const DecStreamOut* __restrict__ sout, const uint32_t* __restrict__ status, int n,
+                         int32_t* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t s = sout[i].status | status[i];
+    int32_t code = 0;
+    if (s & ST_UNSUPPORTED) code = 1;
+    else if (s & ST_CORRUPT) code = 2;
+    else if (s & ST_RETRY) code = 10;
+    else if (s & ST_CAPACITY) code = 8;
+    else if (s & ST_INTEGRITY) code = 3;
+    out[i] = code;
+}
+
 }  // namespace lmcg

@@ -189,13 +189,26 @@ class CompressedBatch:
 
 
 class DecompressedBatch:
-    def __init__(self, data, offsets, lengths, element_types, flags, status):
+    """Decoded payloads packed at 16-byte aligned offsets of one CUDA byte tensor.
+
+    ``status`` holds per-stream C-ABI codes (0 = OK; 1/2/3 = the reference's
+    UnsupportedFormat / CorruptStream / Integrity errors).  Plan runs leave
+    it on the device until first read (reading synchronises)."""
+
+    def __init__(self, data, offsets, lengths, element_types, flags, status, status_dev=None):
         self.data = data
         self.offsets = offsets
         self.lengths = lengths
         self.element_types = element_types
         self.flags = flags
-        self.status = status
+        self._status = status
+        self._status_dev = status_dev
+
+    @property
+    def status(self) -> list[int]:
+        if self._status is None:
+            self._status = self._status_dev.cpu().tolist()
+        return self._status
 
     def __len__(self) -> int:
         return len(self.offsets)
@@ -285,6 +298,10 @@ class Codec:
         batch._keep = (views, pviews)
         return batch
 
+    def compress_plan(self, tensors, **kw) -> CompressPlan:
+        """A CompressPlan over these tensors (see CompressPlan)."""
+        return CompressPlan(self, tensors, **kw)
+
     def block_info(self) -> dict:
         """Per-block (mode, bits, record size, wire codebook) of the last compress."""
         L = self.ctx.lib
@@ -367,6 +384,166 @@ class Codec:
             hints = [((int(orig[i]), int(hints[i][1]), int(hints[i][2]), int(nw[i])) if i in retry else hints[i])
                      for i in range(n)]
         raise LmcError("decompress hints did not converge")
+
+
+class CompressPlan:
+    """Repeated compression of the same device tensors (a model's parameters).
+
+    Validation, layout and descriptor upload happen once; ``run()`` only
+    launches the kernels -- optionally replaying a captured CUDA graph -- and
+    returns streams byte-identical to ``lmc_compress`` of the tensors' current
+    contents.  The returned batch aliases the plan's output buffer and stays
+    valid until the next ``run()``.
+    """
+
+    def __init__(self, codec: "Codec", tensors, *, element_types=None, prev=None, delta=None, byte_group=True,
+                 block_size=DEFAULT_BLOCK_SIZE, segment_count=1, buffer_size=DEFAULT_BUFFER_SIZE, graph=False):
+        import torch
+
+        self.codec = codec
+        L = codec.ctx.lib
+        n = len(tensors)
+        self.n = n
+        views = [_bytes_view(t) for t in tensors]
+        ets = [int(element_types[i]) if element_types is not None else _torch_et(t.dtype) for i, t in enumerate(tensors)]
+        pviews = [None] * n if prev is None else [(_bytes_view(p) if p is not None else None) for p in prev]
+        dflags = [bool(delta)] * n if (delta is None or isinstance(delta, bool)) else [bool(d) for d in delta]
+        for et in ets:
+            _validate_options(_WIDTH[et], block_size, segment_count, buffer_size)
+        arr = (_lib.lmcg_tensor * max(n, 1))()
+        bounds = []
+        opts = _lib.lmcg_options(int(bool(byte_group)), block_size, segment_count, 0, buffer_size)
+        for i in range(n):
+            if views[i].numel() % _WIDTH[ets[i]]:
+                raise AlignmentError(f"buffer of {views[i].numel()} bytes is not a multiple of width {_WIDTH[ets[i]]}")
+            if pviews[i] is not None and pviews[i].numel() != views[i].numel():
+                from .errors import ShapeMismatchError
+                raise ShapeMismatchError(f"length mismatch: {pviews[i].numel()} vs {views[i].numel()}")
+            arr[i].data = views[i].data_ptr() if views[i].numel() else 0
+            arr[i].prev = pviews[i].data_ptr() if pviews[i] is not None and pviews[i].numel() else 0
+            arr[i].nbytes = views[i].numel()
+            arr[i].element_type = ets[i]
+            arr[i].delta = int(dflags[i] or pviews[i] is not None)
+            bounds.append(int(L.lmcg_compress_bound(ctypes.byref(arr[i]), 1, ctypes.byref(opts))))
+        self._keep = (views, pviews, arr)
+        self.ptr = L.lmcg_compress_plan_create(codec.ctx.ptr, arr, n, ctypes.byref(opts))
+        if not self.ptr:
+            raise_status(4 if "option" in codec.ctx.error() else 7, codec.ctx.error())
+        self.bound = int(L.lmcg_plan_output_bytes(self.ptr))
+        self.stream_bounds = bounds
+        self.hints = [(int(v.numel()), segment_count, block_size, (int(v.numel()) + buffer_size - 1) // buffer_size)
+                      for v in views]
+        self.out = torch.empty(max(self.bound, 16), dtype=torch.uint8, device=codec.device)
+        self.meta = torch.zeros(2 * max(n, 1), dtype=torch.int64, device=codec.device)
+        self.graph = None
+        if graph:
+            self.graph = _capture(lambda st: self._launch(st))
+
+    def _launch(self, st) -> None:
+        L = self.codec.ctx.lib
+        rc = L.lmcg_compress_plan_run(self.codec.ctx.ptr, self.ptr, self.out.data_ptr(), self.out.numel(),
+                                      self.meta.data_ptr(), self.meta.data_ptr() + 8 * max(self.n, 1),
+                                      ctypes.c_void_p(st.cuda_stream))
+        self.codec.ctx.check(rc)
+
+    def run(self, stream=None) -> CompressedBatch:
+        import torch
+
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch(stream if stream is not None else torch.cuda.current_stream(self.codec.device))
+        n = self.n
+        return CompressedBatch(self.out, self.meta[:n], self.meta[max(n, 1): max(n, 1) + n], self.hints)
+
+    def decompress_plan(self, graph=False) -> "DecompressPlan":
+        """A plan decoding this plan's output (exact structure hints)."""
+        return DecompressPlan(self.codec, self.hints, self.stream_bounds, graph=graph, source=self)
+
+    def __del__(self):
+        try:
+            if getattr(self, "ptr", None):
+                self.codec.ctx.lib.lmcg_plan_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+class DecompressPlan:
+    """Repeated decompression of streams with a known structure (see CompressPlan)."""
+
+    def __init__(self, codec: "Codec", hints, len_bounds, *, graph=False, source: CompressPlan | None = None):
+        import torch
+
+        self.codec = codec
+        L = codec.ctx.lib
+        n = len(hints)
+        self.n = n
+        hs = (_lib.lmcg_stream_hint * max(n, 1))()
+        for i, h in enumerate(hints):
+            hs[i].orig, hs[i].segments, hs[i].block, hs[i].windows = (int(x) for x in h)
+        lb = (ctypes.c_uint64 * max(n, 1))(*[int(x) for x in len_bounds])
+        self.ptr = L.lmcg_decompress_plan_create(codec.ctx.ptr, n, hs, lb)
+        if not self.ptr:
+            raise_status(7, codec.ctx.error())
+        self.out = torch.empty(max(int(L.lmcg_plan_output_bytes(self.ptr)), 16), dtype=torch.uint8, device=codec.device)
+        self.status = torch.zeros(max(n, 1), dtype=torch.int32, device=codec.device)
+        self.offsets, pos = [], 0
+        for h in hints:
+            self.offsets.append(pos)
+            pos += (int(h[0]) + 15) & ~15
+        self.lengths = [int(h[0]) for h in hints]
+        self.source = source
+        self.graph = None
+        if graph:
+            if source is None:
+                raise ValueError("graph capture needs a fixed source buffer (a CompressPlan)")
+            self.graph = _capture(lambda st: self._launch(st, source.out, source.meta[:n], source.meta[max(n, 1):]))
+
+    def _launch(self, st, data, offsets, lengths) -> None:
+        L = self.codec.ctx.lib
+        rc = L.lmcg_decompress_plan_run(self.codec.ctx.ptr, self.ptr, data.data_ptr(), offsets.data_ptr(),
+                                        lengths.data_ptr(), self.out.data_ptr(), self.status.data_ptr(),
+                                        ctypes.c_void_p(st.cuda_stream))
+        self.codec.ctx.check(rc)
+
+    def run(self, batch: CompressedBatch | None = None, stream=None) -> DecompressedBatch:
+        import torch
+
+        if self.graph is not None and (batch is None or batch.data is self.source.out):
+            self.graph.replay()
+        else:
+            if batch is None:
+                raise ValueError("run() needs a CompressedBatch")
+            self._launch(stream if stream is not None else torch.cuda.current_stream(self.codec.device),
+                         batch.data, batch.offsets, batch.lengths)
+        n = self.n
+        return DecompressedBatch(self.out, self.offsets, self.lengths, None, None, None, status_dev=self.status[:n])
+
+    def __del__(self):
+        try:
+            if getattr(self, "ptr", None):
+                self.codec.ctx.lib.lmcg_plan_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+def _capture(launch):
+    """Warm up `launch` on a side stream, then capture it into a CUDA graph."""
+    import torch
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        launch(side)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        launch(torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    return g
 
 
 _codecs: dict[int, Codec] = {}

@@ -233,3 +233,54 @@ def test_cross_decode_gpu_stream_by_oracle(codec):
     b = codec.compress(ts, segment_count=3)
     out, et, flags = O.decompress(b.to_bytes()[0])
     assert out == host_bytes(ts[0].view(torch.uint8)) and et == 1 and flags == 1
+
+
+# ------------------------------------------------------------------- plans
+@pytest.mark.parametrize("graph", [False, True])
+def test_plans_match_oracle_and_round_trip(codec, graph):
+    specs, ts = synth.make_checkpoint("cfg2", seed=7, limit=30)
+    plan = codec.compress_plan(ts, graph=graph)
+    dplan = plan.decompress_plan(graph=graph)
+    for it in range(2):
+        if it == 1:  # new contents, same tensors: replay must pick them up
+            for t in ts:
+                t.mul_(-1.5)
+        b = plan.run()
+        got = b.to_bytes()
+        want = _oracle_streams(ts, [1] * len(ts))
+        assert got == want
+        r = dplan.run(b)
+        assert r.status == [0] * len(ts)
+        for i, t in enumerate(ts):
+            assert torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1))
+
+
+def test_plan_delta_fused(codec):
+    specs, prev = synth.make_checkpoint("cfg4", seed=8, limit=4)
+    nxt = [synth.next_step(w, 8, i) for i, w in enumerate(prev)]
+    plan = codec.compress_plan(nxt, prev=prev)
+    b = plan.run()
+    want = [O.compress(host_bytes((p.view(torch.uint8) ^ q.view(torch.uint8)).reshape(-1)), 1, delta=True, threads=8)
+            for p, q in zip(prev, nxt)]
+    assert b.to_bytes() == want
+
+
+def test_false_candidates_inside_payload(codec):
+    # Raw stored blocks that contain fake record headers "mode|len==block" (and a
+    # fake successor header) must still decode exactly: the scan's candidates
+    # are only hints, verification + the serial walk decide.
+    B = 4096
+    rng = np.random.default_rng(3)
+    data = bytearray(rng.integers(0, 256, 40 * B, dtype=np.uint8).tobytes())
+    fake = bytes([2]) + B.to_bytes(4, "little")
+    for k in range(1, 39, 3):
+        off = k * B + 100
+        data[off: off + 5] = fake                      # fake stored header
+        nxt = off + 5 + B
+        data[nxt: nxt + 5] = bytes([0]) + B.to_bytes(4, "little")  # fake successor
+    data = bytes(data)
+    t = dev_bytes(data)
+    b = codec.compress([t], element_types=[0], byte_group=False, block_size=B)
+    assert b.to_bytes()[0] == O.compress(data, 0, byte_group=False, block_size=B)
+    r = codec.decompress(b)
+    assert r.status == [0] and host_bytes(r.payload(0)) == data
