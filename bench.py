@@ -38,6 +38,7 @@ def parse_args():
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of replaying CUDA graphs")
     return ap.parse_args()
 
 
@@ -218,6 +219,11 @@ def run_ours(args, ws, rank, local):
     nbytes = sum(t.numel() * t.element_size() for t in ts)
     codec = lmcb.Codec(local)
     stream = torch.cuda.current_stream()
+    # The checkpoint's tensors are registered once (CompressPlan): every step
+    # re-compresses their current contents.  Runs replay captured CUDA graphs.
+    cplan = codec.compress_plan(ts, graph=not args.no_graph)
+    dplan = cplan.decompress_plan(graph=not args.no_graph)
+    status_log = torch.zeros((args.steps + args.warmup + 8, len(ts)), dtype=torch.int32, device="cuda")
 
     def exchange(batch):
         # container assembly across ranks: all-gather of per-stream sizes
@@ -228,14 +234,19 @@ def run_ours(args, ws, rank, local):
         dist.all_gather(g, lens)
         return torch.stack(g)
 
+    step_no = [0]
+
     def step(ev=None):
         if ev:
             ev[0].record(stream)
-        b = codec.compress(ts)
+        b = cplan.run()
         exchange(b)
         if ev:
             ev[1].record(stream)
-        r = codec.decompress(b)
+        r = dplan.run(b)
+        # keep every step's decode status on the device; verified after the timed region
+        status_log[step_no[0] % status_log.shape[0]].copy_(r._status_dev)
+        step_no[0] += 1
         if ev:
             ev[2].record(stream)
         return b, r
@@ -251,11 +262,13 @@ def run_ours(args, ws, rank, local):
     for _ in range(max(args.warmup - 1, 0)):
         step()
 
-    # per-kernel launch times (separate, untimed pass)
+    # per-kernel launch times (separate, untimed pass without graphs)
     codec.ctx.profile(True)
     nprof = 3
     for _ in range(nprof):
-        step()
+        pb = codec.compress(ts)
+        exchange(pb)
+        codec.decompress(pb)
     prof = codec.ctx.profile_report()
     codec.ctx.profile(False)
     launches_per_step = sum(c for c, _ in prof.values()) / nprof
@@ -275,6 +288,8 @@ def run_ours(args, ws, rank, local):
     end.record(stream)
     torch.cuda.synchronize()
     clocks = sampler.stop()
+    if int(status_log.abs().sum().item()) != 0:
+        raise SystemExit("a timed step reported a decode error")
     if dist is not None:
         dist.barrier()
     total_ms = start.elapsed_time(end)
@@ -340,31 +355,38 @@ def run_ours(args, ws, rank, local):
 
 
 def measure_e2e(codec, ts, args, ws, dist):
+    """Round trip through the public API with pinned host buffers: H2D of the
+    checkpoint into the registered tensors, CompressPlan.run, D2H of the
+    streams; H2D of the streams, DecompressPlan.run, D2H of the payload."""
     import torch
 
     host = [t.view(torch.uint8).reshape(-1).cpu().pin_memory() for t in ts]
     nbytes = sum(h.numel() for h in host)
     stream = torch.cuda.current_stream()
-    dev_in = [torch.empty_like(h, device="cuda") for h in host]
-    b = codec.compress(ts)
-    cap = b.total_bytes() + (1 << 20)
+    dev_in = [torch.empty_like(t) for t in ts]
+    dev_in_u8 = [d.view(torch.uint8).reshape(-1) for d in dev_in]
+    cplan = codec.compress_plan(dev_in)
+    dplan = cplan.decompress_plan()
+    cap = cplan.bound
     host_streams = torch.empty(cap, dtype=torch.uint8).pin_memory()
+    host_out = torch.empty(dplan.out.numel(), dtype=torch.uint8).pin_memory()
     dev_streams = torch.empty(cap, dtype=torch.uint8, device="cuda")
-    host_out = torch.empty(nbytes + 16 * len(ts), dtype=torch.uint8).pin_memory()
 
     def step():
-        for d, h in zip(dev_in, host):
+        for d, h in zip(dev_in_u8, host):
             d.copy_(h, non_blocking=True)
-        bb = codec.compress([d.view(t.dtype).view(t.shape) for d, t in zip(dev_in, ts)])
-        off, ln = bb.host_layout()  # syncs on the lengths
+        bb = cplan.run()
+        off, ln = bb.host_layout()          # stream sizes (needed to size the D2H copy)
+        bb._host = None
         total = off[-1] + ln[-1]
         host_streams[:total].copy_(bb.data[:total], non_blocking=True)
         # ... and back: streams host -> device, decompress, payload device -> host
         dev_streams[:total].copy_(host_streams[:total], non_blocking=True)
-        r = codec.decompress([dev_streams[o: o + n] for o, n in zip(off, ln)])
-        used = r.offsets[-1] + r.lengths[-1]
-        host_out[:used].copy_(r.data[:used], non_blocking=True)
-        return total
+        from paper_2505_09810_b200.stream import CompressedBatch
+        rb = CompressedBatch(dev_streams, bb.offsets, bb.lengths, bb.hints)
+        r = dplan.run(rb)
+        host_out.copy_(r.data, non_blocking=True)
+        return total, r
 
     for _ in range(2):
         step()
@@ -374,17 +396,19 @@ def measure_e2e(codec, ts, args, ws, dist):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        sb = step()
+        sb, r = step()
     e1.record(stream)
     torch.cuda.synchronize()
+    if any(r.status):
+        raise SystemExit("e2e decode error")
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = ms.item()
     return {"value": round(ws * nbytes * args.steps / (ms / 1e3) / GIB, 3), "unit": "GiB/s",
             "h2d_bytes_per_step": nbytes + sb, "d2h_bytes_per_step": sb + nbytes,
-            "path": "pinned host checkpoint -> H2D -> Codec.compress -> D2H streams -> H2D streams -> "
-                    "Codec.decompress -> D2H payload"}
+            "path": "pinned host checkpoint -> H2D -> CompressPlan.run -> D2H streams -> H2D streams -> "
+                    "DecompressPlan.run -> D2H payload"}
 
 
 def cpu_baseline(ts):
