@@ -101,8 +101,8 @@ void build_crc_tables(CrcTables& t) {
         for (int i = 0; i < 256; i++) t.slice[k][i] = (t.slice[k - 1][i] >> 8) ^ t.slice[0][t.slice[k - 1][i] & 0xFF];
     t.x2n[0] = 1u << 30;  // x^1
     for (int k = 1; k < 64; k++) t.x2n[k] = h_multmodp(t.x2n[k - 1], t.x2n[k - 1]);
-    for (int lvl = 0; lvl < 9; lvl++) {
-        const uint64_t nbytes = 64ull << lvl;
+    for (int lvl = 0; lvl < 11; lvl++) {
+        const uint64_t nbytes = 16ull << lvl;
         // x^(8 nbytes)
         uint32_t p = 1u << 31;
         uint64_t n = nbytes;

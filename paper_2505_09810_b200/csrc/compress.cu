@@ -28,12 +28,14 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
 }
 
 // -------------------------------------------------------------- K1 hist+crc
-// One CTA per block slot.  Each warp owns 2 KiB warp-tiles of source bytes;
-// lane l holds bytes [64 l, 64 l + 64) of its tile, i.e. 64/w consecutive
-// grouped positions of one plane.  Fast tiles (entirely inside one plane,
-// 16-byte aligned) use 4 x 16-byte loads per lane; other tiles gather byte
-// by byte.  Plane-0 tiles also fold their full elements into the CRC.
-__global__ void __launch_bounds__(kThreads) k_hist_crc(
+// One CTA per block slot.  Each warp owns 2 KiB warp-tiles of source bytes,
+// read as four fully coalesced 512-byte rows: lane l holds the 16-byte
+// pieces at 512 q + 16 l (q = 0..3), i.e. 16/w consecutive grouped positions
+// of one plane each.  Fast tiles (entirely inside one plane, 16-byte
+// aligned) use vector loads; other tiles gather byte by byte.  Plane-0
+// tiles also fold their full elements into the CRC (lane tree over 16-byte
+// pieces, then the four rows in order).
+__global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
     const CrcTables* __restrict__ ct, uint32_t* __restrict__ hist_out, uint32_t* __restrict__ crc_out,
     BlockMeta* __restrict__ meta) {
@@ -55,33 +57,38 @@ __global__ void __launch_bounds__(kThreads) k_hist_crc(
     const uint64_t p0 = k * B;
     const uint64_t p1 = min(wd.W, p0 + B);
     const uint32_t w = wd.w;
-    const uint64_t T = kTileBytes / w;         // positions per warp-tile
-    const uint64_t ntiles = (p1 - p0 + T - 1) / T;
+    const uint32_t lw = lg2w(w);
+    const uint64_t T = kTileBytes >> lw;        // positions per warp-tile
+    const uint64_t ntiles = (p1 - p0 + T - 1) >> (11 - lw);
     const uint64_t crc_end = min(p1, wd.n);    // plane-0 positions of this block end here
     uint32_t* hist = sh_hist[warp];
 
     for (uint64_t t = warp; t < ntiles; t += kWarps) {
         const uint64_t tp = p0 + t * T;
         const uint64_t te = min(tp + T, p1);
-        const uint64_t g = (w == 1) ? 0 : tp / wd.n;
+        const uint64_t g = plane_of(tp, wd.n, w);
         const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
         if (fast) {
-            uint32_t v[16], s[16];
-            const uint64_t e0 = tp - g * wd.n;
-            load64(wd.src, wd.prev, e0 * w + (uint64_t)lane * kLaneBytes, v);
-            const int ns = extract_plane(v, w, (uint32_t)g, s);
+            const uint64_t base = ((tp - g * wd.n) << lw) + 16ull * lane;
+            uint4 a[4];
 #pragma unroll
-            for (int q = 0; q < 16; q++) {
+            for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, base + 512ull * q);
 #pragma unroll
-                for (int r = 0; r < 4; r++)
-                    if (4 * q + r < ns) atomicAdd(&hist[(s[q] >> (8 * r)) & 0xFF], 1u);
+            for (int q = 0; q < 4; q++) {
+                uint32_t sy[4];
+                const int ns = piece_symbols(a[q], w, (uint32_t)g, sy);
+#pragma unroll
+                for (int i = 0; i < 16; i++)
+                    if (i < ns) atomicAdd(&hist[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF], 1u);
             }
             if (g == 0) {
-                uint32_t c = 0;
+                // tile CRC = XOR_l shift(v_l, 16 (31 - l)) with v_l = Horner over this
+                // lane's four rows (row stride 512 bytes): one lane tree per tile
+                uint32_t v = crc16(sh_slice, a[0]);
 #pragma unroll
-                for (int q = 0; q < 16; q++) c = crc_word(sh_slice, c, v[q]);
-                c = crc_warp_tree(ct, c, lane);
-                if (lane == 0) { sh_part[t] = c; sh_plen[t] = kTileBytes; }
+                for (int q = 1; q < 4; q++) v = crc_shift_tab(&ct->shift[kShift512][0][0], v) ^ crc16(sh_slice, a[q]);
+                v = crc_warp_tree(ct, v, lane, kShift16);
+                if (lane == 0) { sh_part[t] = v; sh_plen[t] = kTileBytes; }
             }
         } else {
             // slow gather: lane owns positions [tp + lane*T/32, ...)
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(kThreads) k_hist_crc(
                     if (wd.prev) x ^= wd.prev[o];
                     c = crc_byte(sh_slice, c, x);
                 }
-                c = crc_warp_tree(ct, c, lane);
+                c = crc_warp_tree(ct, c, lane, 2);
                 if (lane == 0) { sh_part[t] = c; sh_plen[t] = (uint16_t)L; }
             }
         }
@@ -116,10 +123,10 @@ __global__ void __launch_bounds__(kThreads) k_hist_crc(
     }
     if (tid == 0) {
         if (p0 < crc_end) {
-            const uint64_t nct = (crc_end - p0 + T - 1) / T;
+            const uint64_t nct = (crc_end - p0 + T - 1) >> (11 - lw);
             uint32_t acc = 0;
             for (uint64_t t = 0; t < nct; t++) {
-                if (sh_plen[t] == kTileBytes) acc = crc_shift_tab(&ct->shift[5][0][0], acc);
+                if (sh_plen[t] == kTileBytes) acc = crc_shift_tab(&ct->shift[kShift2K][0][0], acc);
                 else acc = crc_shift_generic(ct->x2n, acc, sh_plen[t]);
                 acc ^= sh_part[t];
             }
@@ -616,11 +623,31 @@ __global__ void __launch_bounds__(kThreads) k_frame(const StreamDesc* __restrict
 }
 
 // --------------------------------------------------------------- K4 encode
+// Symbols of piece (q, lane) of a warp-tile: the 16 source bytes at
+// 512 q + 16 lane, i.e. grouped positions [tp + (512 q + 16 lane)/w, +16/w)
+// clipped to [tp, te); vector loads on fast tiles, byte gathers otherwise.
+__device__ __forceinline__ int tile_piece(const WinDesc& wd, uint64_t tp, uint64_t te, uint64_t g, bool fast, int q,
+                                          int lane, uint32_t sy[4], uint64_t& pos) {
+    const uint32_t w = wd.w, lw = lg2w(w);
+    const uint32_t rel = (512u * q + 16u * lane) >> lw;
+    pos = tp + rel;
+    if (fast) {
+        const uint4 a = ldg16x(wd.src, wd.prev, ((tp - g * wd.n) << lw) + 512u * q + 16u * lane);
+        return piece_symbols(a, w, (uint32_t)g, sy);
+    }
+    sy[0] = sy[1] = sy[2] = sy[3] = 0;
+    const int want = 16 / (int)w;
+    int ns = 0;
+    for (int i = 0; i < want && pos + i < te; i++, ns++) sy[i >> 2] |= gather_byte(wd, pos + i) << (8 * (i & 3));
+    return ns;
+}
+
 // One CTA per block slot.  Canonical codes (huffman.py:213-225) are built in
-// shared memory from the wire codebook; every lane packs the codes of its
-// 64/w consecutive symbols MSB-first into a shared staging area laid out on
-// the 4-byte grid of the destination, so complete words leave with plain
-// 32-bit stores and only the two edge words of a record are written bytewise.
+// shared memory from the wire codebook; each lane packs the codes of its four
+// pieces MSB-first into a shared staging area laid out on the 4-byte grid of
+// the destination, so complete words leave with plain 32-bit stores and only
+// the two edge words of a record are written bytewise.  Stored records copy
+// the symbols straight to the output.
 __global__ void __launch_bounds__(kThreads) k_encode(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
     uint32_t segs, const StreamDesc* __restrict__ streams, const BlockMeta* __restrict__ meta,
@@ -630,7 +657,7 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     __shared__ uint32_t sh_code[256];
     __shared__ uint32_t sh_cnt[kWarps][16];
     __shared__ uint32_t sh_first[16];
-    __shared__ uint32_t sh_wsum[kWarps * 2];
+    __shared__ uint32_t sh_wsum[kWarps];
     const uint64_t slot = blockIdx.x;
     if (slot >= nslots) return;
     const WinDesc wd = wins[slot2win[slot]];
@@ -659,24 +686,54 @@ __global__ void __launch_bounds__(kThreads) k_encode(
         else v = (uint8_t)(m.bits >> (8 * (tid - 133)));
         rp[tid] = v;
     }
+    const uint32_t w = wd.w;
+    const uint64_t T = kTileBytes >> lg2w(w);
+    const uint64_t p0 = k * B, p1 = min(wd.W, p0 + B);
+    if (!huff) {
+        // stored record: the block's bytes verbatim after the 5-byte header
+        uint8_t* base = rp + 5;
+        for (uint64_t t = warp; p0 + t * T < p1; t += kWarps) {
+            const uint64_t tp = p0 + t * T;
+            const uint64_t te = min(tp + T, p1);
+            const uint64_t g = plane_of(tp, wd.n, w);
+            const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                uint32_t sy[5];
+                uint64_t pos;
+                int ns = tile_piece(wd, tp, te, g, fast, q, lane, sy, pos);
+                if (pos >= te) ns = 0;
+                sy[4] = 0;
+                if (ns == 0) continue;
+                uint8_t* d = base + (pos - p0);
+                const uint32_t head = min((uint32_t)ns, (uint32_t)((4 - (reinterpret_cast<uint64_t>(d) & 3)) & 3));
+                for (uint32_t i = 0; i < head; i++) d[i] = (uint8_t)(sy[0] >> (8 * i));
+                const uint32_t nw = ((uint32_t)ns - head) / 4;
+                uint32_t* dw = reinterpret_cast<uint32_t*>(d + head);
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    if ((uint32_t)i < nw) dw[i] = __funnelshift_r(sy[i], sy[i + 1], 8 * head);
+                for (uint32_t i = head + 4 * nw; i < (uint32_t)ns; i++) {
+                    const uint32_t wv = (i >> 2) == 0 ? sy[0] : (i >> 2) == 1 ? sy[1] : (i >> 2) == 2 ? sy[2] : sy[3];
+                    d[i] = (uint8_t)(wv >> (8 * (i & 3)));
+                }
+            }
+        }
+        return;
+    }
     // canonical code table (huffman.py:213-225): thread t handles symbol t
     if (tid < kWarps * 16) (&sh_cnt[0][0])[tid] = 0;
     __syncthreads();
     uint32_t my_len, my_rank_w;
     {
-        if (huff) {
-            const uint8_t wb = wire[b * 128 + (tid >> 1)];
-            my_len = (tid & 1) ? (wb >> 4) : (wb & 15);
-        } else {
-            my_len = 8;
-        }
+        const uint8_t wb = wire[b * 128 + (tid >> 1)];
+        my_len = (tid & 1) ? (wb >> 4) : (wb & 15);
         const uint32_t mm = __match_any_sync(0xFFFFFFFFu, my_len);
         my_rank_w = __popc(mm & ((1u << lane) - 1));
         if (lane == __ffs(mm) - 1) sh_cnt[warp][my_len] = __popc(mm);
     }
     __syncthreads();
     if (tid < 16) {
-        // first left-justified code of each length
         uint32_t tot[16];
         for (int l = 0; l < 16; l++) {
             uint32_t c = 0;
@@ -694,16 +751,13 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     if (my_len) {
         uint32_t r = my_rank_w;
         for (int q = 0; q < warp; q++) r += sh_cnt[q][my_len];
-        const uint32_t code = (sh_first[my_len] >> (kMaxLen - my_len)) + r;
-        sh_code[tid] = (my_len << 16) | code;
+        sh_code[tid] = (my_len << 16) | ((sh_first[my_len] >> (kMaxLen - my_len)) + r);
     } else {
         sh_code[tid] = 0;
     }
     // staging
-    const uint32_t w = wd.w;
-    const uint64_t T = kTileBytes / w;
     const uint64_t iterpos = T * kWarps;
-    const uint32_t stg_words = (uint32_t)((iterpos * (huff ? 15 : 8)) / 32 + 4);
+    const uint32_t stg_words = (uint32_t)((iterpos * 15) / 32 + 4);
     for (uint32_t i = tid; i < stg_words; i += kThreads) stg[i] = 0;
     __syncthreads();
     const uint64_t gaddr = (uint64_t)(rp + hdr);
@@ -711,71 +765,92 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     uint32_t* gw = reinterpret_cast<uint32_t*>(gaddr & ~(uint64_t)3);
     uint64_t bitpos = lead;     // staging coordinate of the next bit (relative to gw)
     uint64_t base_word = 0;     // global word index (relative to gw) of stg[0]
-    const uint64_t p0 = k * B, p1 = min(wd.W, p0 + B);
+    // A unit = up to 8 consecutive symbols of one piece; its code bits (<= 120)
+    // are built left-aligned in four words x[0..3] in a single pass.
+    const int upp = (w == 1) ? 2 : 1;  // units per piece
     for (uint64_t it0 = p0; it0 < p1; it0 += iterpos) {
         const uint64_t tp = it0 + (uint64_t)warp * T;
         const uint64_t te = min(tp + T, p1);
-        uint32_t s[16];
-        int ns = 0;
-        uint64_t g = 0;
-        if (tp < te) {
-            g = (w == 1) ? 0 : tp / wd.n;
-            const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
-            if (fast) {
-                uint32_t v[16];
-                const uint64_t e0 = tp - g * wd.n;
-                load64(wd.src, wd.prev, e0 * w + (uint64_t)lane * kLaneBytes, v);
-                ns = extract_plane(v, w, (uint32_t)g, s);
-            } else {
-                const uint64_t per = T / 32;
-                const uint64_t a = tp + lane * per, bnd = min(a + per, te);
+        const bool live = tp < te;
+        const uint64_t g = live ? plane_of(tp, wd.n, w) : 0;
+        const bool fast = live && wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
+        uint32_t x[4][2][4];
+        uint32_t nbu[4][2];
+        uint32_t off[4];
+        uint32_t wtot = 0;
 #pragma unroll
-                for (int q = 0; q < 16; q++) s[q] = 0;
-                for (uint64_t p = a; p < bnd; p++, ns++) s[ns >> 2] |= gather_byte(wd, p) << (8 * (ns & 3));
+        for (int q = 0; q < 4; q++) {
+            uint32_t sy[4];
+            uint64_t pos;
+            int ns = live ? tile_piece(wd, tp, te, g, fast, q, lane, sy, pos) : 0;
+            if (live && pos >= te) ns = 0;
+            uint32_t lane_bits = 0;
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                uint64_t hi = 0, lo = 0;
+                uint32_t nb = 0;
+                if (u < upp) {
+#pragma unroll
+                    for (int i = 0; i < 8; i++) {
+                        const int si = 8 * u + i;
+                        const uint32_t e = si < ns ? sh_code[(sy[si >> 2] >> (8 * (si & 3))) & 0xFF] : 0u;
+                        const uint32_t l = e >> 16;
+                        // (hi:lo) = (hi:lo) << l | code, as a 128-bit shift
+                        hi = (hi << l) | (l ? (lo >> (64 - l)) : 0);
+                        lo = (lo << l) | (e & 0xFFFF);
+                        nb += l;
+                    }
+                    // left-align the nb bits in 128 bits
+                    const uint32_t sh = 128 - nb;
+                    if (nb == 0) { hi = 0; lo = 0; }
+                    else if (sh >= 64) { hi = lo << (sh - 64); lo = 0; }
+                    else if (sh > 0) { hi = (hi << sh) | (lo >> (64 - sh)); lo <<= sh; }
+                }
+                x[q][u][0] = (uint32_t)(hi >> 32); x[q][u][1] = (uint32_t)hi;
+                x[q][u][2] = (uint32_t)(lo >> 32); x[q][u][3] = (uint32_t)lo;
+                nbu[q][u] = nb;
+                lane_bits += nb;
             }
-        }
-        uint32_t nbits = 0;
+            uint32_t incl = lane_bits;
 #pragma unroll
-        for (int q = 0; q < 16; q++) {
-#pragma unroll
-            for (int r = 0; r < 4; r++)
-                if (4 * q + r < ns) nbits += sh_code[(s[q] >> (8 * r)) & 0xFF] >> 16;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            off[q] = wtot + incl - lane_bits;
+            wtot += __shfl_sync(0xFFFFFFFFu, incl, 31);
         }
-        // CTA exclusive scan of nbits in (warp, lane) order
-        uint32_t incl = nbits;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) sh_wsum[warp] = incl;
+        if (lane == 0) sh_wsum[warp] = wtot;
         __syncthreads();
         uint32_t wpre = 0, tot = 0;
 #pragma unroll
         for (int q = 0; q < kWarps; q++) { if (q < warp) wpre += sh_wsum[q]; tot += sh_wsum[q]; }
-        const uint64_t start = bitpos + wpre + incl - nbits - base_word * 32;
-        if (ns) {
-            uint64_t acc = 0;
-            uint32_t nacc = (uint32_t)(start & 31);
-            uint32_t wi = (uint32_t)(start >> 5);
 #pragma unroll
-            for (int q = 0; q < 16; q++) {
+        for (int q = 0; q < 4; q++) {
+            uint64_t o = bitpos + wpre + off[q] - base_word * 32;
 #pragma unroll
-                for (int r = 0; r < 4; r++) {
-                    if (4 * q + r < ns) {
-                        const uint32_t e = sh_code[(s[q] >> (8 * r)) & 0xFF];
-                        const uint32_t l = e >> 16;
-                        acc = (acc << l) | (e & 0xFFFF);
-                        nacc += l;
-                        if (nacc >= 32) {
-                            atomicOr(&stg[wi], (uint32_t)(acc >> (nacc - 32)));
-                            wi++;
-                            nacc -= 32;
-                        }
-                    }
+            for (int u = 0; u < 2; u++) {
+                const uint32_t nb = nbu[q][u];
+                if (nb) {
+                    // shift the left-aligned unit right by the start's bit phase into <= 5 words;
+                    // the first and last words may be shared with neighbouring units
+                    const uint32_t s0 = (uint32_t)(o & 31);
+                    const uint32_t wi = (uint32_t)(o >> 5);
+                    const uint32_t nw = (s0 + nb + 31) / 32;
+                    const uint32_t* xx = x[q][u];
+                    const uint32_t y0 = xx[0] >> s0;
+                    const uint32_t y1 = __funnelshift_r(xx[1], xx[0], s0);
+                    const uint32_t y2 = __funnelshift_r(xx[2], xx[1], s0);
+                    const uint32_t y3 = __funnelshift_r(xx[3], xx[2], s0);
+                    const uint32_t y4 = s0 ? (xx[3] << (32 - s0)) : 0u;
+                    atomicOr(&stg[wi], y0);
+                    if (nw > 2) stg[wi + 1] = y1; else if (nw == 2) atomicOr(&stg[wi + 1], y1);
+                    if (nw > 3) stg[wi + 2] = y2; else if (nw == 3) atomicOr(&stg[wi + 2], y2);
+                    if (nw > 4) stg[wi + 3] = y3; else if (nw == 4) atomicOr(&stg[wi + 3], y3);
+                    if (nw == 5) atomicOr(&stg[wi + 4], y4);
                 }
+                o += nb;
             }
-            if (nacc) atomicOr(&stg[wi], (uint32_t)(acc << (32 - nacc)));
         }
         __syncthreads();
         const uint64_t end = bitpos + tot;

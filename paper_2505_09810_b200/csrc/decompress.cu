@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
     const uint64_t ob = t0 + lo_b - Z;
     const bool vec = full && ((reinterpret_cast<uint64_t>(o) + ob) % 16 == 0) &&
                      (w == 1 ? ((reinterpret_cast<uint64_t>(g) + ob) % 16 == 0)
-                             : ((ob / w) % 16 == 0 && (wd.n % 16) == 0));
+                             : (((ob >> lg2w(w)) & 15) == 0 && (wd.n & 15) == 0));
     if (vec) {
         uint32_t v[16];
         if (w == 1) {
@@ -1053,18 +1053,18 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
     } else {
         for (uint64_t q = max(lo_b, Z); q < hi_b; q++) {
             const uint64_t ob1 = t0 + q - Z;
-            const uint64_t e = ob1 / w, gg = ob1 - e * w;
+            const uint64_t e = ob1 >> lg2w(w), gg = ob1 - (e << lg2w(w));
             const uint8_t x = g[gg * wd.n + e];
             o[ob1] = x;
             c = crc_byte(sh_slice, c, x);
         }
     }
-    c = crc_warp_tree(ct, c, lane);
+    c = crc_warp_tree(ct, c, lane, 2);
     if (lane == 0) sh_part[warp] = c;
     __syncthreads();
     if (tid == 0) {
         uint32_t acc = 0;
-        for (int q = 0; q < kWarps; q++) acc = crc_shift_tab(&ct->shift[5][0][0], acc) ^ sh_part[q];
+        for (int q = 0; q < kWarps; q++) acc = crc_shift_tab(&ct->shift[kShift2K][0][0], acc) ^ sh_part[q];
         tile_crc[tile] = acc;
     }
 }

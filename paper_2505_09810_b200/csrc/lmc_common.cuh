@@ -68,12 +68,12 @@ struct BlockMeta {
 //
 // Global tables (built once per context, see capi.cu):
 //   crc_slice[4][256]     slice-by-4 tables
-//   crc_shift[k][4][256]  byte-sliced operators "append 64*2^k zero bytes",
-//                         k = 0..8 (64 B .. 16 KiB)
+//   crc_shift[k][4][256]  byte-sliced operators "append 16*2^k zero bytes",
+//                         k = 0..10 (16 B .. 16 KiB)
 //   x2n[64]               x^(2^k) mod P for the generic shift
 struct CrcTables {
     uint32_t slice[4][256];
-    uint32_t shift[9][4][256];
+    uint32_t shift[11][4][256];
     uint32_t x2n[64];
 };
 
@@ -154,16 +154,53 @@ __device__ uint32_t crc_combine_uniform(const CrcTables* __restrict__ ct, uint64
     return r;
 }
 
-// Warp tree over 32 lane parts of kLaneBytes each (lane order = byte order):
-// returns on lane 0 the raw CRC of the 2 KiB warp-tile.
-__device__ __forceinline__ uint32_t crc_warp_tree(const CrcTables* __restrict__ ct, uint32_t c, int lane) {
+constexpr int kShift16 = 0, kShift512 = 5, kShift2K = 7, kShift16K = 10;  // crc_shift levels
+
+// Warp tree over 32 lane parts of (16 << lvl0) bytes each (lane order = byte
+// order): returns on lane 0 the raw CRC of the 32 parts.
+__device__ __forceinline__ uint32_t crc_warp_tree(const CrcTables* __restrict__ ct, uint32_t c, int lane, int lvl0) {
 #pragma unroll
     for (int k = 0; k < 5; k++) {
         uint32_t other = __shfl_down_sync(0xFFFFFFFFu, c, 1 << k);
-        uint32_t shifted = crc_shift_tab(&ct->shift[k][0][0], c);
+        uint32_t shifted = crc_shift_tab(&ct->shift[lvl0 + k][0][0], c);
         if ((lane & ((2 << k) - 1)) == 0) c = shifted ^ other;
     }
     return c;
+}
+
+// raw CRC of 16 bytes held as 4 little-endian words
+__device__ __forceinline__ uint32_t crc16(const uint32_t* __restrict__ sl, uint4 a) {
+    uint32_t c = crc_word(sl, 0, a.x);
+    c = crc_word(sl, c, a.y);
+    c = crc_word(sl, c, a.z);
+    return crc_word(sl, c, a.w);
+}
+
+// Plane-g symbols of the 16/w elements in one 16-byte piece, packed 4 per
+// word in position order; returns the symbol count (16, 8 or 4).
+__device__ __forceinline__ int piece_symbols(uint4 a, uint32_t w, uint32_t g, uint32_t s[4]) {
+    if (w == 1) {
+        s[0] = a.x; s[1] = a.y; s[2] = a.z; s[3] = a.w;
+        return 16;
+    }
+    if (w == 2) {
+        const uint32_t sel = g ? 0x7531 : 0x6420;
+        s[0] = __byte_perm(a.x, a.y, sel);
+        s[1] = __byte_perm(a.z, a.w, sel);
+        return 8;
+    }
+    const uint32_t sel = g | ((4 + g) << 4);
+    s[0] = __byte_perm(__byte_perm(a.x, a.y, sel), __byte_perm(a.z, a.w, sel), 0x5410);
+    return 4;
+}
+
+__device__ __forceinline__ uint4 ldg16x(const uint8_t* src, const uint8_t* prev, uint64_t off) {
+    uint4 a = __ldg(reinterpret_cast<const uint4*>(src + off));
+    if (prev) {
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(prev + off));
+        a.x ^= b.x; a.y ^= b.y; a.z ^= b.z; a.w ^= b.w;
+    }
+    return a;
 }
 
 // ------------------------------------------------------------- gathers
@@ -234,6 +271,15 @@ __device__ __forceinline__ int64_t slot_to_block(const WinDesc& wd, uint64_t loc
     uint64_t sg1 = (g + 1 == wd.w) ? wd.nblocks : ((g + 1) * wd.n + B - 1) / B;
     uint64_t k = sg + j;
     return k < sg1 ? (int64_t)k : -1;
+}
+
+// log2 of an element width (1, 2 or 4)
+__device__ __forceinline__ uint32_t lg2w(uint32_t w) { return w == 1 ? 0u : (w == 2 ? 1u : 2u); }
+// plane of grouped position p (no 64-bit division)
+__device__ __forceinline__ uint64_t plane_of(uint64_t p, uint64_t n, uint32_t w) {
+    uint64_t g = 0;
+    while (g + 1 < w && p >= (g + 1) * n) g++;
+    return g;
 }
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
