@@ -32,7 +32,7 @@ METRIC = "lmc compress+decompress round-trip throughput (uncompressed checkpoint
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg2")
@@ -198,8 +198,12 @@ def _host_checkpoint(specs, seed):
 
 
 # ----------------------------------------------------------------- ours
-ALGO = {  # algorithmic bytes per launch, as multiples of (N_in, N_stream)
-    "k_encode": (1, 1), "k_hist_crc": (1, 0), "k_decode": (1, 1), "k_ungroup": (2, 0), "k_cand": (0, 1),
+# Algorithmic bytes per launch as multiples of (N_in, N_stream); one launch per
+# batch.  k_hist_crc reads the checkpoint; k_encode reads it again and writes
+# the streams; k_scandec reads the streams and writes the grouped planes;
+# k_ungroup reads the planes and writes the payload ("Kernels").
+ALGO = {
+    "k_hist_crc": (1, 0), "k_encode": (1, 1), "k_scandec": (1, 1), "k_ungroup": (2, 0),
 }
 
 
