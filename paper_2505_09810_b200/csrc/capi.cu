@@ -118,6 +118,14 @@ void build_crc_tables(CrcTables& t) {
                 t.shift[lvl][byte][b] = c ? h_multmodp(p, c) : 0;
             }
     }
+    for (int m = 0; m < kPow2Levels; m++) {
+        const uint32_t p = t.x2n[m + 3];  // x^(8 * 2^m)
+        for (int byte = 0; byte < 4; byte++)
+            for (uint32_t b = 0; b < 256; b++) {
+                const uint32_t c = b << (8 * byte);
+                t.pow2[m][byte][b] = c ? h_multmodp(p, c) : 0;
+            }
+    }
 }
 
 int ensure_ctx(lmcg_ctx* ctx) {

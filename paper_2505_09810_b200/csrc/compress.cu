@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
             uint32_t acc = 0;
             for (uint64_t t = 0; t < nct; t++) {
                 if (sh_plen[t] == kTileBytes) acc = crc_shift_tab(&ct->shift[kShift2K][0][0], acc);
-                else acc = crc_shift_generic(ct->x2n, acc, sh_plen[t]);
+                else acc = crc_shift_bytes(ct, acc, sh_plen[t]);
                 acc ^= sh_part[t];
             }
             crc_out[b] = acc;
@@ -571,32 +571,23 @@ __global__ void __launch_bounds__(kThreads) k_frame(const StreamDesc* __restrict
     const int s = blockIdx.x;
     const StreamDesc sd = streams[s];
     const uint64_t base = soff[s];
-    // --- CRC: sum over plane-0 parts of shift(part, bytes after part)
+    // --- CRC: the plane-0 parts of a window are the raw CRCs of consecutive
+    // B*w-byte element ranges (the last one shorter): fold them CTA-wide with
+    // byte-shift tables, then chain the windows.
     uint32_t acc = 0;
-    {
-        uint64_t after_win = sd.nbytes;  // bytes after the current window start... computed per window below
-        uint64_t woff = 0;
-        for (uint32_t wl = 0; wl < sd.nwin; wl++) {
-            const WinDesc wd = wins[sd.win0 + wl];
-            after_win = sd.nbytes - woff - wd.W;  // bytes of later windows
-            const uint64_t nparts = (wd.n + B - 1) / B;  // blocks holding plane-0 positions
-            for (uint64_t k = threadIdx.x; k < nparts; k += blockDim.x) {
-                const uint64_t e1 = min(wd.n, (k + 1) * B);
-                const uint64_t after = (wd.n - e1) * wd.w + after_win;
-                acc ^= crc_shift_generic(ct->x2n, crcpart[wd.blk0 + k], after);
-            }
-            woff += wd.W;
+    for (uint32_t wl = 0; wl < sd.nwin; wl++) {
+        const WinDesc wd = wins[sd.win0 + wl];
+        const uint64_t unit = (uint64_t)B * wd.w;
+        const uint64_t nfull = wd.n / B, rem = (wd.n % B) * wd.w;
+        const uint32_t* cp = crcpart + wd.blk0;
+        uint32_t wc = crc_combine_uniform(ct, nfull, unit, [&](uint64_t i) { return cp[i]; }, sh_red);
+        if (threadIdx.x == 0) {
+            if (rem) wc = crc_shift_bytes(ct, wc, rem) ^ cp[nfull];
+            acc = crc_shift_bytes(ct, acc, wd.W) ^ wc;
         }
     }
-    sh_red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int o = kThreads / 2; o; o >>= 1) {
-        if (threadIdx.x < o) sh_red[threadIdx.x] ^= sh_red[threadIdx.x + o];
-        __syncthreads();
-    }
     if (threadIdx.x == 0) {
-        uint32_t raw = sh_red[0];
-        uint32_t crc = raw ^ crc_shift_generic(ct->x2n, 0xFFFFFFFFu, sd.nbytes) ^ 0xFFFFFFFFu;
+        uint32_t crc = acc ^ crc_shift_bytes(ct, 0xFFFFFFFFu, sd.nbytes) ^ 0xFFFFFFFFu;
         uint8_t* h = out + base;
         h[0] = 'L'; h[1] = 'M'; h[2] = 'C'; h[3] = '1';
         h[4] = 1; h[5] = (uint8_t)sd.flags; h[6] = (uint8_t)sd.et; h[7] = 0;

@@ -1087,12 +1087,12 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const DecStreamOut* __res
         const uint32_t* tc = tile_crc + wd.tile0;
         uint32_t wc = crc_combine_uniform(ct, full, kOutTile, [&](uint64_t i) { return tc[i]; }, red);
         if (threadIdx.x == 0) {
-            if (rem) wc = crc_shift_generic(ct->x2n, wc, rem) ^ tc[full];
-            acc = crc_shift_generic(ct->x2n, acc, wd.W) ^ wc;
+            if (rem) wc = crc_shift_bytes(ct, wc, rem) ^ tc[full];
+            acc = crc_shift_bytes(ct, acc, wd.W) ^ wc;
         }
     }
     if (threadIdx.x == 0) {
-        const uint32_t crc = acc ^ crc_shift_generic(ct->x2n, 0xFFFFFFFFu, h.orig) ^ 0xFFFFFFFFu;
+        const uint32_t crc = acc ^ crc_shift_bytes(ct, 0xFFFFFFFFu, h.orig) ^ 0xFFFFFFFFu;
         if (crc != h.crc) atomicOr(&status[s], ST_INTEGRITY);
     }
 }

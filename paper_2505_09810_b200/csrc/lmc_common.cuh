@@ -71,10 +71,12 @@ struct BlockMeta {
 //   crc_shift[k][4][256]  byte-sliced operators "append 16*2^k zero bytes",
 //                         k = 0..10 (16 B .. 16 KiB)
 //   x2n[64]               x^(2^k) mod P for the generic shift
+constexpr int kPow2Levels = 61;            // shifts by 2^m bytes, m = 0..60
 struct CrcTables {
     uint32_t slice[4][256];
-    uint32_t shift[11][4][256];
+    uint32_t shift[11][4][256];            // shift by (16 << lvl) bytes
     uint32_t x2n[64];
+    uint32_t pow2[kPow2Levels][4][256];    // shift by 2^m bytes
 };
 
 __device__ __forceinline__ uint32_t crc_word(const uint32_t* __restrict__ sl, uint32_t crc, uint32_t word) {
@@ -120,6 +122,15 @@ __device__ __forceinline__ uint32_t crc_shift_generic(const uint32_t* __restrict
     if (c == 0 || nbytes == 0) return c;
     return multmodp(x8nmodp(x2n, nbytes), c);
 }
+// raw CRC shifted by n zero bytes: one table shift per set bit of n
+__device__ __forceinline__ uint32_t crc_shift_bytes(const CrcTables* __restrict__ ct, uint32_t c, uint64_t n) {
+    while (c && n) {
+        const int m = __ffsll((long long)n) - 1;
+        c = crc_shift_tab(&ct->pow2[m][0][0], c);
+        n &= n - 1;
+    }
+    return c;
+}
 
 // Raw CRC of `count` consecutive parts of `unit` bytes each, part(i) given by
 // get(i), combined by the whole CTA (blockDim.x threads, `red` = blockDim.x
@@ -133,20 +144,16 @@ __device__ uint32_t crc_combine_uniform(const CrcTables* __restrict__ ct, uint64
     const uint64_t q = (count + T - 1) / T;
     const int64_t pad = (int64_t)(q * T) - (int64_t)count;
     uint32_t acc = 0;
-    if (count) {
-        const uint32_t K = x8nmodp(ct->x2n, unit);
-        for (uint64_t v = (uint64_t)tid * q; v < (uint64_t)tid * q + q; v++) {
-            const int64_t i = (int64_t)v - pad;
-            acc = multmodp(K, acc);
-            if (i >= 0) acc ^= get((uint64_t)i);
-        }
+    for (uint64_t v = (uint64_t)tid * q; v < (uint64_t)tid * q + q; v++) {
+        const int64_t i = (int64_t)v - pad;
+        acc = crc_shift_bytes(ct, acc, unit);
+        if (i >= 0) acc ^= get((uint64_t)i);
     }
     red[tid] = acc;
     __syncthreads();
-    uint32_t Kk = count ? x8nmodp(ct->x2n, unit * q) : 0;
     for (int k = 1; k < T; k <<= 1) {
-        if ((tid & (2 * k - 1)) == 0 && tid + k < T) red[tid] = multmodp(Kk, red[tid]) ^ red[tid + k];
-        Kk = multmodp(Kk, Kk);
+        if ((tid & (2 * k - 1)) == 0 && tid + k < T)
+            red[tid] = crc_shift_bytes(ct, red[tid], unit * q * (uint64_t)k) ^ red[tid + k];
         __syncthreads();
     }
     const uint32_t r = red[0];
