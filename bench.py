@@ -200,10 +200,10 @@ def _host_checkpoint(specs, seed):
 # ----------------------------------------------------------------- ours
 # Algorithmic bytes per launch as multiples of (N_in, N_stream); one launch per
 # batch.  k_hist_crc reads the checkpoint; k_encode reads it again and writes
-# the streams; k_scandec reads the streams and writes the grouped planes;
+# the streams; k_cand scans the streams; k_decrec reads them again and writes the grouped planes;
 # k_ungroup reads the planes and writes the payload ("Kernels").
 ALGO = {
-    "k_hist_crc": (1, 0), "k_encode": (1, 1), "k_scandec": (1, 1), "k_ungroup": (2, 0),
+    "k_hist_crc": (1, 0), "k_encode": (1, 1), "k_decrec": (1, 1), "k_cand": (0, 1), "k_ungroup": (2, 0),
 }
 
 

@@ -691,7 +691,7 @@ int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
 
 namespace {
 // Workspace layout of one decompress (offsets into the workspace).
-enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CST, D_TK, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_TC, D_SCR, D_NOFF };
+enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CAND, D_CCNT, D_CTOT, D_CPRE, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_TC, D_SCR, D_NOFF };
 size_t dec_layout(const DPlan& P, int n, size_t* o) {
     Arena a;
     o[D_IN] = a.take<DecStreamIn>(n + 1);
@@ -700,8 +700,10 @@ size_t dec_layout(const DPlan& P, int n, size_t* o) {
     o[D_ST] = a.take<uint32_t>(n + 1);
     o[D_WIN] = a.take<DecWin>(P.nwin + 1);
     o[D_SEG] = a.take<DecSeg>(P.nseg + 1);
-    o[D_CST] = a.take<uint64_t>(P.nchunk + 1);
-    o[D_TK] = a.take<uint32_t>(4);
+    o[D_CAND] = a.take<uint32_t>((P.nchunk + 1) * kWarps * kSpanCap);
+    o[D_CCNT] = a.take<uint32_t>((P.nchunk + 1) * kWarps);
+    o[D_CTOT] = a.take<uint32_t>(P.nchunk + 1);
+    o[D_CPRE] = a.take<uint32_t>(P.nchunk + 1);
     o[D_SCNT] = a.take<uint32_t>(P.nseg + 1);
     o[D_SFAIL] = a.take<uint32_t>(P.nseg + 1);
     o[D_RPOS] = a.take<uint64_t>(P.nrec + 1);
@@ -723,8 +725,10 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     auto* d_st = reinterpret_cast<uint32_t*>(ws + o[D_ST]);
     auto* d_win = reinterpret_cast<DecWin*>(ws + o[D_WIN]);
     auto* d_seg = reinterpret_cast<DecSeg*>(ws + o[D_SEG]);
-    auto* d_cst = reinterpret_cast<uint64_t*>(ws + o[D_CST]);
-    auto* d_tk = reinterpret_cast<uint32_t*>(ws + o[D_TK]);
+    auto* d_cand = reinterpret_cast<uint32_t*>(ws + o[D_CAND]);
+    auto* d_ccnt = reinterpret_cast<uint32_t*>(ws + o[D_CCNT]);
+    auto* d_ctot = reinterpret_cast<uint32_t*>(ws + o[D_CTOT]);
+    auto* d_cpre = reinterpret_cast<uint32_t*>(ws + o[D_CPRE]);
     auto* d_scnt = reinterpret_cast<uint32_t*>(ws + o[D_SCNT]);
     auto* d_sfail = reinterpret_cast<uint32_t*>(ws + o[D_SFAIL]);
     auto* d_rpos = reinterpret_cast<uint64_t*>(ws + o[D_RPOS]);
@@ -735,24 +739,29 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     ctx->d_dstatus = d_st;
     ctx->dn = n;
     CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
-    CK(cudaMemsetAsync(d_cst, 0, (nchunk + 1) * sizeof(uint64_t), st));
-    CK(cudaMemsetAsync(d_tk, 0, 16, st));
     CK(cudaMemsetAsync(d_sfail, 0, (nseg + 1) * sizeof(uint32_t), st));
     if (!n) return LMCG_OK;
     const size_t dsm = sizeof(DecSmem);
     if (!ctx->dec_attr) {
-        CK(cudaFuncSetAttribute(k_scandec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        CK(cudaFuncSetAttribute(k_decrec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         CK(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
-        ctx->scandec_occ = occupancy(ctx, (const void*)k_scandec, kThreads, dsm);
         ctx->dec_attr = true;
     }
     { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg); }
-    if (nchunk) {
-        const int grid = (int)std::min<uint64_t>(nchunk, (uint64_t)ctx->scandec_occ);
-        PROF(k_scandec);
-        k_scandec<<<grid, kThreads, dsm, st>>>(d_seg, nseg, nchunk, d_tk, d_cst, d_scnt, d_sfail, d_rpos, d_rnext, d_scr);
+    if (nchunk) { PROF(k_cand); k_cand<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, nseg, nchunk, d_cand, d_ccnt, d_ctot); }
+    if (nseg) {
+        PROF(k_number);
+        k_number<<<(unsigned)std::min<uint64_t>(nseg, 148 * 4), kThreads, 0, st>>>(d_seg, nseg, d_ctot, d_cpre, d_scnt, d_sfail);
     }
-    if (nrec) { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, nseg, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
+    if (nchunk) {
+        PROF(k_assign);
+        k_assign<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, nseg, nchunk, d_cand, d_ccnt, d_cpre, d_sfail, d_rpos, d_rnext);
+    }
+    if (nrec) {
+        { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, nseg, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
+        PROF(k_decrec);
+        k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, nseg, nrec, d_sfail, d_rpos, d_scr);
+    }
     if (nseg) {
         const int grid = (int)std::min<uint64_t>(nseg, 148 * 2);
         PROF(k_fallback);
@@ -913,6 +922,11 @@ int lmcg_decompress_host(lmcg_ctx* ctx, const void* stream, uint64_t len, void* 
 }
 
 #ifdef LMCG_DEBUG
+int lmcg_debug_events(unsigned long long* out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, lmcg::lmcg_dbg_ev, sizeof(unsigned long long) * 4096);
+    return 0;
+}
 int lmcg_debug_counters(unsigned long long* out, int reset) {
     cudaDeviceSynchronize();
     cudaMemcpyFromSymbol(out, lmcg::lmcg_dbg, sizeof(unsigned long long) * 32);

@@ -34,6 +34,7 @@ constexpr int kLut = 11;             // LUT index bits
 
 #ifdef LMCG_DEBUG
 __device__ unsigned long long lmcg_dbg[32];
+__device__ unsigned long long lmcg_dbg_ev[4096];   // 512 events x 8 words
 #define DBG_ADD(i, v) atomicAdd(&lmcg_dbg[i], (unsigned long long)(v))
 #define DBG_T0(var) unsigned long long var = clock64()
 #define DBG_TADD(i, var) do { if (threadIdx.x == 0) atomicAdd(&lmcg_dbg[i], clock64() - var); } while (0)
@@ -214,13 +215,15 @@ __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __res
 // self-synchronise within a few codewords); pass 2 re-decodes every chunk
 // from its exact start and writes the symbols.  The decoder consumes up to
 // three symbols per table lookup.
-constexpr int kStage = 40960;  // bitstream bytes staged in shared memory (longer ones are read from global)
+constexpr int kStage = 40960;
+constexpr int kCheckpoints = 3;  // at 128, 256 and 512 bits into a chunk  // bitstream bytes staged in shared memory (longer ones are read from global)
 
 struct DecSmem {
     uint32_t bits[kStage / 4 + 4];      // staged bitstream, big-endian words
     uint32_t lut3[1 << kLut];           // n(2)|tl(4)|pad(2)|s3(8)|s2(8)|s1(8); n == 0: slow path
     uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0
     uint32_t bm[2][kThreads];           // pass-0 boundary bitmaps (first 64 bits of each chunk)
+    uint32_t cp[kCheckpoints][kThreads];  // pass-0 checkpoints: (offset from p0) << 16 | symbol count
     uint32_t end[kThreads];
     uint8_t lens[256];
     uint8_t csym[256];
@@ -228,12 +231,7 @@ struct DecSmem {
     uint32_t cnt_w[kWarps][16];
     uint32_t wsum[kWarps];
     uint32_t kraft;
-    int minlen, maxlen;
-    // k_scandec bookkeeping
-    uint32_t wcand[kWarps][64];
-    uint32_t wcnt[kWarps];
-    uint32_t base;
-    uint64_t tile;
+    int minlen, maxlen, lgcd;
 };
 
 // Payload bit source: big-endian words, bit i of the payload is bit
@@ -255,11 +253,12 @@ struct Src {
         return v;
     }
     // the 32 payload bits starting at bit pos (zeros past the end)
+    template <bool STAGED = false>
     __device__ __forceinline__ uint32_t peek(uint32_t pos) const {
         const uint32_t a = pos + sh;
         const uint32_t j = a >> 5;
         uint32_t w0, w1;
-        if (sw) {
+        if (STAGED) {
             w0 = sw[j];
             w1 = sw[j + 1];
         } else {
@@ -297,7 +296,7 @@ __device__ __forceinline__ uint32_t step1(const DecSmem& s, uint32_t win, uint32
 // The bulk loop is branch-free apart from codes longer than kLut bits:
 // one 32-bit window (two word reads + funnel shift), one table lookup, up to
 // three symbols.
-template <bool EMIT>
+template <bool EMIT, bool STAGED>
 __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32_t lim, uint32_t p0, int bm,
                                 uint32_t& count, uint8_t* dst, uint32_t* hit) {
     // Lanes decode different chunks with different trip counts: every loop is
@@ -315,7 +314,7 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
         while (__any_sync(mask, act)) {
             if (act) {
                 uint32_t sym;
-                const uint32_t l = step1(s, src.peek(pos), sym);
+                const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
                 if (!l) {
                     bad = true;
                 } else {
@@ -337,6 +336,50 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
             }
         }
         if (bm == 1) { s.bm[0][tid] = m0; s.bm[1][tid] = m1; }
+        // checkpoints: the first codeword boundary at or after p0 + (128 << k)
+        // (pass 0 records it with its symbol count; a fix-up path that lands
+        // on it is synchronised), for paths that do not resynchronise within
+        // the 64-bit bitmap
+#pragma unroll 1
+        for (int k = 0; k < kCheckpoints; k++) {
+            const uint32_t T = p0 + (128u << k);
+            const bool on = bm != 0 && !bad && !done && T < lim;
+            bool a2 = on && pos + kLut <= T;
+            while (__any_sync(mask, a2)) {
+                if (a2) {
+                    const uint32_t win = src.template peek<STAGED>(pos);
+                    const uint32_t e = s.lut3[win >> (32 - kLut)];
+                    uint32_t n = e >> 30, tl = (e >> 26) & 15;
+                    if (n == 0) {
+                        uint32_t sym;
+                        tl = step1(s, win, sym);
+                        n = 1;
+                        bad = tl == 0;
+                    }
+                    pos += tl;
+                    c += n;
+                    a2 = !bad && pos + kLut <= T;
+                }
+            }
+            a2 = on && !bad && pos < T;
+            while (__any_sync(mask, a2)) {
+                if (a2) {
+                    uint32_t sym;
+                    const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
+                    if (!l) bad = true;
+                    else { pos += l; c++; }
+                    a2 = !bad && pos < T;
+                }
+            }
+            if (on && !bad) {
+                if (bm == 1) {
+                    s.cp[k][tid] = ((pos - p0) << 16) | c;
+                } else if (pos - p0 == (s.cp[k][tid] >> 16)) {
+                    *hit = s.cp[k][tid] & 0xFFFF;
+                    done = true;
+                }
+            }
+        }
     }
     uint8_t* d = dst;
     if (EMIT) {
@@ -345,7 +388,7 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
         while (__any_sync(mask, act)) {
             if (act) {
                 uint32_t sym;
-                const uint32_t l = step1(s, src.peek(pos), sym);
+                const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
                 if (!l) {
                     bad = true;
                 } else {
@@ -363,7 +406,7 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
     bool act = !bad && !done && pos + kLut <= lim;
     while (__any_sync(mask, act)) {
         if (act) {
-            const uint32_t win = src.peek(pos);
+            const uint32_t win = src.template peek<STAGED>(pos);
             const uint32_t e = s.lut3[win >> (32 - kLut)];
             uint32_t n = e >> 30, tl = (e >> 26) & 15, packed = e & 0xFFFFFF;
             if (n == 0) {
@@ -391,7 +434,7 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
     while (__any_sync(mask, act)) {
         if (act) {
             uint32_t sym;
-            const uint32_t l = step1(s, src.peek(pos), sym);
+            const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
             if (!l) {
                 bad = true;
             } else {
@@ -421,44 +464,66 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
 }
 
 // All passes over the chunks of one record (see huff_decode).
+template <bool STAGED>
 __device__ bool huff_passes(DecSmem& s, const Src& src, uint32_t bits, uint32_t len, uint8_t* dst) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t S = (bits + kThreads - 1) / kThreads;
     S = max(128u, (S + 31) & ~31u);
     const uint32_t nch = (bits + S - 1) / S;
-    const bool fixed = s.minlen == s.maxlen;
+    // every codeword boundary is a multiple of the gcd of the code lengths:
+    // chunk starts off that grid could never resynchronise
+    const uint32_t gq = s.lgcd;
     const uint32_t c = tid;
     const uint32_t lim = min((c + 1) * S, bits);
     uint32_t p0 = 0, my_start = 0, my_end = 0, my_cnt = 0;
     DBG_T0(t_p0);
+#pragma unroll
+    for (int k = 0; k < kCheckpoints; k++) s.cp[k][tid] = ~0u;
     if (c < nch) {
         p0 = c * S;
-        if (fixed) p0 = ((p0 + s.minlen - 1) / s.minlen) * s.minlen;
+        if (gq > 1) p0 = ((p0 + gq - 1) / gq) * gq;
         my_start = p0;
         if (my_start >= lim) { my_end = my_start; s.bm[0][tid] = 0; s.bm[1][tid] = 0; }
-        else my_end = decode_span<false>(s, src, my_start, lim, p0, 1, my_cnt, nullptr, nullptr);
+        else my_end = decode_span<false, STAGED>(s, src, my_start, lim, p0, 1, my_cnt, nullptr, nullptr);
         s.end[c] = my_end;
     }
     __syncthreads();
     DBG_TADD(18, t_p0);
     DBG_T0(t_fix);
-    // fix-up rounds until every chunk starts where its predecessor ended
+    // fix-up rounds until every chunk starts where its predecessor ended; a
+    // re-decoded path that meets the pass-0 path (bitmap or checkpoint) takes
+    // the rest of its count and its end from pass 0
+    const uint32_t p0_end = my_end, p0_cnt = my_cnt;
     for (;;) {
         uint32_t pe = 0;
         if (c < nch && c > 0) pe = s.end[c - 1];
         __syncthreads();
         int changed = 0;
         if (c < nch && c > 0 && pe != ~0u && pe != my_start) {
-            const bool first_fix = my_start == p0;
             my_start = pe;
             if (my_start >= lim) {
                 my_end = my_start;
                 my_cnt = 0;
             } else {
                 uint32_t h = ~0u, cnt2 = 0;
-                const uint32_t e2 = decode_span<false>(s, src, my_start, lim, p0, first_fix ? 2 : 0, cnt2, nullptr, &h);
-                if (first_fix && e2 != ~0u && h != ~0u) {
-                    my_cnt = cnt2 + (my_cnt - h);  // the rest of the path is the pass-0 path
+                const uint32_t e2 = decode_span<false, STAGED>(s, src, my_start, lim, p0, 2, cnt2, nullptr, &h);
+                DBG_ADD(6, h == ~0u);
+#ifdef LMCG_DEBUG
+                if (h == ~0u) {
+                    const unsigned long long k = atomicAdd(&lmcg_dbg[10], 1ull);
+                    if (k < 512) {
+                        unsigned long long* e = lmcg_dbg_ev + 8 * k;
+                        e[0] = blockIdx.x; e[1] = c; e[2] = p0; e[3] = pe; e[4] = lim; e[5] = bits;
+                        e[6] = (unsigned long long)s.minlen << 32 | s.maxlen; e[7] = (unsigned long long)p0_cnt << 32 | cnt2;
+                    }
+                }
+#endif
+                DBG_ADD(9, h == ~0u && c == nch - 1);
+                DBG_ADD(27, h == ~0u && e2 == ~0u);
+                DBG_ADD(7, cnt2);
+                if (e2 != ~0u && h != ~0u) {
+                    my_cnt = cnt2 + (p0_cnt - h);  // the rest of the path is the pass-0 path
+                    my_end = p0_end;
                 } else {
                     my_end = e2;
                     my_cnt = cnt2;
@@ -489,7 +554,7 @@ __device__ bool huff_passes(DecSmem& s, const Src& src, uint32_t bits, uint32_t 
     DBG_T0(t_emit);
     if (c < nch && my_cnt) {
         uint32_t cc;
-        decode_span<true>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
+        decode_span<true, STAGED>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
     }
     __syncthreads();
     DBG_TADD(20, t_emit);
@@ -520,7 +585,7 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     __syncthreads();
     if (tid == 0) {
         uint32_t left = 0, idx = 0;
-        int mn = 16, mx = 0;
+        int mn = 16, mx = 0, gl = 0;
         for (int q = 1; q <= kMaxLen; q++) {
             uint32_t c = 0;
             for (int w = 0; w < kWarps; w++) c += s.cnt_w[w][q];
@@ -529,10 +594,17 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
             s.first_idx[q] = idx;
             left += c << (kMaxLen - q);
             idx += c;
-            if (c) { mn = min(mn, q); mx = max(mx, q); }
+            if (c) {
+                mn = min(mn, q);
+                mx = max(mx, q);
+                int a = gl, b = q;  // gcd of the code lengths in use
+                while (b) { const int t = a % b; a = b; b = t; }
+                gl = a;
+            }
         }
         s.minlen = mn;
         s.maxlen = mx;
+        s.lgcd = gl ? gl : 1;
     }
     __syncthreads();
     const uint32_t bits = rd32(pl + 128);
@@ -553,8 +625,22 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     G.nwords_full = G.glimit / 4;
     const uint64_t nwords = (G.glimit + 3) / 4;
     const bool staged = nwords + 3 <= kStage / 4 + 4;
-    if (staged)  // stage the payload words (zero past the end) in shared memory
-        for (uint64_t j = tid; j < nwords + 3; j += kThreads) s.bits[j] = G.gword(j);
+    if (staged) {  // stage the payload words (zero past the end) in shared memory, 8 loads in flight
+        const uint64_t nw = nwords + 3;
+        for (uint64_t j0 = tid; j0 < nw; j0 += 8 * kThreads) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint64_t j = j0 + (uint64_t)u * kThreads;
+                v[u] = j < nw ? G.gword(j) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const uint64_t j = j0 + (uint64_t)u * kThreads;
+                if (j < nw) s.bits[j] = v[u];
+            }
+        }
+    }
     __syncthreads();
     // single-symbol LUT over kLut-bit prefixes
     for (int e = tid; e < (1 << kLut); e += kThreads) {
@@ -589,8 +675,11 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     __syncthreads();
     DBG_TADD(16, t_setup);
     DBG_ADD(17, staged ? 1 : 0);
-    if (staged) G.sw = s.bits;
-    return huff_passes(s, G, bits, len, dst);
+    if (staged) {
+        G.sw = s.bits;
+        return huff_passes<true>(s, G, bits, len, dst);
+    }
+    return huff_passes<false>(s, G, bits, len, dst);
 }
 
 __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t n) {
@@ -712,40 +801,73 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* 
     const uint64_t qa = max(pa, (uint64_t)1) + 1 + kb;
     const uint64_t qe = min(pe + 1 + kb, sg.comp);
     if (qa >= qe) return true;
-    const uint64_t A = (reinterpret_cast<uint64_t>(b) + qa) & ~15ull;   // aligned absolute start
+    const uint64_t A = (reinterpret_cast<uint64_t>(b) + qa - 1 - kb) & ~15ull;   // aligned row start (mode bytes)
     const uint64_t Aend = reinterpret_cast<uint64_t>(b) + qe;
     const uint64_t segend = reinterpret_cast<uint64_t>(b) + sg.comp;
     bool ok = true;
-    for (uint64_t g0 = A; g0 < Aend; g0 += 512) {
+    constexpr int kRows = 4;  // 512-byte rows in flight per warp
+    for (uint64_t gb = A; gb < Aend; gb += 512 * kRows) {
+      uint4 rows[kRows];
+#pragma unroll
+      for (int rr = 0; rr < kRows; rr++) {
+        const uint64_t g = gb + 512ull * rr + 16ull * lane;
+        rows[rr] = make_uint4(0, 0, 0, 0);
+        if (g < Aend && g + 16 <= segend) rows[rr] = __ldg(reinterpret_cast<const uint4*>(g));
+      }
+#pragma unroll 1
+      for (int rr = 0; rr < kRows; rr++) {
+        const uint64_t g0 = gb + 512ull * rr;
+        if (g0 >= Aend) break;
         const uint64_t g = g0 + 16ull * lane;
-        uint32_t w4[4] = {0, 0, 0, 0};
-        if (g < Aend) {
-            if (g + 16 <= segend) {
-                const uint4 v = __ldg(reinterpret_cast<const uint4*>(g));
-                w4[0] = v.x; w4[1] = v.y; w4[2] = v.z; w4[3] = v.w;
-            } else {
-                for (int q = 0; q < 16; q++)
-                    if (g + q < segend) w4[q >> 2] |= (uint32_t)(*reinterpret_cast<const uint8_t*>(g + q)) << (8 * (q & 3));
+        uint32_t w4[4] = {rows[rr].x, rows[rr].y, rows[rr].z, rows[rr].w};
+        if (g < Aend && g + 16 > segend) {
+            w4[0] = w4[1] = w4[2] = w4[3] = 0;
+            for (int q = 0; q < 16; q++)
+                if (g + q < segend) w4[q >> 2] |= (uint32_t)(*reinterpret_cast<const uint8_t*>(g + q)) << (8 * (q & 3));
+        }
+        // branch-free header test at all 16 byte positions of the lane:
+        // mode byte <= 2 followed by the 4 little-endian bytes of B
+        uint32_t w5 = __shfl_down_sync(0xFFFFFFFFu, w4[0], 1);
+        if (lane == 31) {
+            w5 = 0;
+            const uint64_t gn = g + 16;
+            if (gn + 4 <= segend) w5 = __ldg(reinterpret_cast<const uint32_t*>(gn));
+            else for (int q = 0; q < 4; q++) if (gn + q < segend) w5 |= (uint32_t)(*reinterpret_cast<const uint8_t*>(gn + q)) << (8 * q);
+        }
+        // the u32 at byte p + 1 for p = 4i + j: funnel shifts of word pairs
+        const uint32_t wv[5] = {w4[0], w4[1], w4[2], w4[3], w5};
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            any |= __funnelshift_r(wv[i], wv[i + 1], 8) == B;
+            any |= __funnelshift_r(wv[i], wv[i + 1], 16) == B;
+            any |= __funnelshift_r(wv[i], wv[i + 1], 24) == B;
+            any |= wv[i + 1] == B;
+        }
+        uint32_t cm = 0;
+        if (any) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const uint32_t x = j == 3 ? wv[i + 1] : __funnelshift_r(wv[i], wv[i + 1], 8 * (j + 1));
+                    const uint32_t mode = (wv[i] >> (8 * j)) & 0xFF;
+                    if (x == B && mode <= 2) cm |= 1u << (4 * i + j);
+                }
             }
         }
         uint32_t found[4];
         uint32_t k = 0;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            uint32_t m = __vcmpeq4(w4[q], pat);
-            while (m) {
-                const int bit = __ffs(m) - 1;
-                m &= ~(0xFFu << (bit & ~7));
-                const uint64_t abs_q = g + 4 * q + (bit >> 3);
-                if (abs_q >= reinterpret_cast<uint64_t>(b) + qa && abs_q < Aend) {
-                    const uint64_t p = abs_q - reinterpret_cast<uint64_t>(b) - 1 - kb;
-                    if (is_cand(b, sg.comp, p, B, Ltail)) {
-                        if (k < 4) found[k] = (uint32_t)p;
-                        k++;
-                    }
-                }
+        while (cm) {
+            const int j = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const uint64_t p = g + j - reinterpret_cast<uint64_t>(b);
+            if (p + 1 + kb >= qa && p + 1 + kb < qe && is_cand(b, sg.comp, p, B, Ltail)) {
+                if (k < 4) found[k] = (uint32_t)p;
+                k++;
             }
         }
+        if (!__any_sync(0xFFFFFFFFu, k != 0)) continue;
         if (k > 4) ok = false;
         const uint32_t kk = min(k, 4u);
         uint32_t incl = kk;
@@ -762,131 +884,178 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* 
         if (lane == 0) *cnt += tot;
         __syncwarp();
         if (*cnt > 64) ok = false;
+      }
     }
     return __all_sync(0xFFFFFFFFu, ok);
 }
 
-__global__ void __launch_bounds__(kThreads) k_scandec(const DecSeg* __restrict__ segs, uint64_t nseg_total,
-                                                    uint64_t nchunk_total, uint32_t* __restrict__ ticket,
-                                                    uint64_t* __restrict__ cstat, uint32_t* __restrict__ seg_cnt,
-                                                    uint32_t* __restrict__ seg_fail, uint64_t* __restrict__ rec_pos,
-                                                    uint64_t* __restrict__ rec_next, uint8_t* __restrict__ scratch) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
+constexpr uint32_t kSpanCap = 64;                  // candidates per 8 KiB span
+constexpr uint32_t kDense = 0xFFFFFFFFu;            // span overflowed its list
+
+// CTA per 64 KiB chunk slot of segment payload, warp per 8 KiB span: the
+// candidate record headers of the span, in increasing order, into
+// cand[span][0..kSpanCap) and their count (kDense on overflow) into ccnt.
+__global__ void __launch_bounds__(kThreads) k_cand(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+                                                 uint64_t nchunk_total, uint32_t* __restrict__ cand,
+                                                 uint32_t* __restrict__ ccnt, uint32_t* __restrict__ ctot) {
+    __shared__ uint32_t wcnt[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) s.tile = atomicAdd(ticket, 1u);
-        __syncthreads();
-        const uint64_t t = s.tile;
-        if (t >= nchunk_total) return;
-        uint64_t lo = 0, hi = nseg_total;
-        while (hi - lo > 1) {
-            const uint64_t mid = (lo + hi) >> 1;
-            if (segs[mid].chunk0 <= t) lo = mid; else hi = mid;
-        }
-        const DecSeg sg = segs[lo];
-        if (t < sg.chunk0 || t >= sg.chunk0 + sg.nchunk) {
-            if (tid == 0) st_rel(&cstat[t], kFlagI);  // unused capacity slot
-            continue;
-        }
-        const uint64_t ci = t - sg.chunk0;
-        const uint64_t c0 = ci * kChunk, c1 = min(c0 + kChunk, sg.comp);
-        DBG_T0(t_scan);
-        DBG_ADD(21, tid == 0);
-        // ---- candidates of this chunk: warp w scans positions [c0 + w*8K, ...)
-        constexpr uint64_t kWarpSpan = kChunk / kWarps;
-        const uint64_t pa = c0 + warp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
-        if (lane == 0) {
-            s.wcnt[warp] = 0;
-            if (pa == 0 && pa < pe) {  // the segment start is always a record start
-                s.wcand[warp][0] = 0;
-                s.wcnt[warp] = 1;
-            }
-        }
-        __syncwarp();
-        bool ok = true;
-        if (pa < pe) ok = warp_scan(sg, pa, pe, s.wcand[warp], &s.wcnt[warp], lane);
-        const bool dense = __syncthreads_or(!ok);
-        uint32_t tot = 0, wpre[kWarps];
-#pragma unroll
-        for (int w = 0; w < kWarps; w++) { wpre[w] = tot; tot += s.wcnt[w]; }
-        DBG_TADD(22, t_scan);
-        DBG_T0(t_lb);
-        // ---- segmented decoupled look-back over the segment's chunks (warp 0,
-        // 32 predecessors per round trip)
-        if (warp == 0) {
-            uint64_t pre = 0;
-            if (ci == 0) {
-                if (lane == 0) st_rel(&cstat[t], kFlagI | tot);
-            } else {
-                if (lane == 0) st_rel(&cstat[t], kFlagA | tot);
-                int64_t j = (int64_t)t - 1;  // next predecessor to look at (lane 0's slot)
-                for (;;) {
-                    const int64_t jj = j - lane;
-                    uint64_t st = jj >= 0 ? ld_acq(&cstat[jj]) : kFlagI;
-                    // wait until the 32 slots are published
-                    while (__any_sync(0xFFFFFFFFu, (st >> 62) == 0)) {
-                        if ((st >> 62) == 0) st = ld_acq(&cstat[jj]);
-                    }
-                    const uint32_t inc = __ballot_sync(0xFFFFFFFFu, (st >> 62) == 2);
-                    const int first = inc ? __ffs(inc) - 1 : 32;  // nearest inclusive predecessor
-                    uint64_t v = (lane <= first && lane < 32) ? (st & kMask) : 0;
-#pragma unroll
-                    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-                    pre += v;
-                    if (inc) break;
-                    j -= 32;
-                }
-                if (lane == 0) st_rel(&cstat[t], kFlagI | (pre + tot));
-            }
-            if (lane == 0) {
-                s.base = (uint32_t)pre;
-                if (c1 == sg.comp) seg_cnt[lo] = (uint32_t)(pre + tot);
-            }
-        }
-        __syncthreads();
-        DBG_TADD(23, t_lb);
-        if (dense) {
-            // e.g. long runs of 6-byte RLE records: the serial path handles the segment
-            DBG_ADD(12, tid == 0);
-            if (tid == 0) atomicOr(&seg_fail[lo], 1u);
-            continue;
-        }
-        const uint32_t base = s.base;
-        const uint32_t R = sg.nrec, B = sg.block;
-        const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(R - 1) * B);
-        int w = 0;
-        for (uint32_t k = 0; k < tot; k++) {
-            while (k >= wpre[w] + s.wcnt[w]) w++;
-            uint64_t pos = s.wcand[w][k - wpre[w]];
-            uint32_t r = base + k;
-            if (r >= R) {
-                DBG_ADD(13, tid == 0);
-                if (tid == 0) atomicOr(&seg_fail[lo], 1u);
-                break;
-            }
-            // the candidate record, then (after record R-2) the tail record, which is
-            // not a candidate because its length differs from the block size
-            for (int part = 0; part < 2; part++) {
-                uint32_t mode = 0, l = 0;
-                uint64_t ps = 0;
-                bool rok = rec_size(sg.base, sg.comp, pos, mode, l, ps) && l == ((r + 1 == R) ? Ltail : B);
-                DBG_T0(t_rec);
-                if (rok) rok = decode_record(s, sg.base + pos, mode, l, scratch + sg.goff + (uint64_t)r * B);
-                DBG_TADD(24 + (mode & 3), t_rec);
-                DBG_ADD(28 + (mode & 3), tid == 0);
-                if (tid == 0) {
-                    rec_pos[sg.rec0 + r] = pos;
-                    rec_next[sg.rec0 + r] = rok ? pos + 5 + ps : ~0ull;
-                    if (!rok) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(14, 1); }
-                }
-                if (!(rok && part == 0 && r + 2 == R && Ltail != B)) break;
-                pos += 5 + ps;
-                r = R - 1;
-            }
+    const uint64_t t = blockIdx.x;
+    if (t >= nchunk_total) return;
+    uint64_t lo = 0, hi = nseg_total;
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (segs[mid].chunk0 <= t) lo = mid; else hi = mid;
+    }
+    const DecSeg sg = segs[lo];
+    const uint64_t span = t * kWarps + warp;
+    if (t < sg.chunk0 || t >= sg.chunk0 + sg.nchunk) {  // unused capacity slot
+        if (lane == 0) ccnt[span] = 0;
+        if (tid == 0) ctot[t] = 0;
+        return;
+    }
+    constexpr uint64_t kWarpSpan = kChunk / kWarps;
+    const uint64_t c0 = (t - sg.chunk0) * kChunk, c1 = min(c0 + kChunk, sg.comp);
+    const uint64_t pa = c0 + warp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
+    uint32_t* list = cand + span * kSpanCap;
+    if (lane == 0) {
+        wcnt[warp] = 0;
+        if (pa == 0 && pa < pe) {  // the segment start is always a record start
+            list[0] = 0;
+            wcnt[warp] = 1;
         }
     }
+    __syncwarp();
+    bool ok = true;
+    if (pa < pe) ok = warp_scan(sg, pa, pe, list, &wcnt[warp], lane);
+    if (lane == 0) {
+        ccnt[span] = ok ? wcnt[warp] : kDense;
+        if (!ok) wcnt[warp] = kDense;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t tot = 0;
+        for (int w = 0; w < kWarps; w++) tot = (tot == kDense || wcnt[w] == kDense) ? kDense : tot + wcnt[w];
+        ctot[t] = tot;
+    }
+}
+
+// CTA per segment: exclusive scan of the chunk candidate totals (record
+// number of each chunk's first candidate), the segment's candidate count,
+// and failure for a segment with an overflowing span.
+__global__ void __launch_bounds__(kThreads) k_number(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+                                                   const uint32_t* __restrict__ ctot, uint32_t* __restrict__ cpre,
+                                                   uint32_t* __restrict__ seg_cnt, uint32_t* __restrict__ seg_fail) {
+    __shared__ uint32_t wsum[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint64_t si = blockIdx.x; si < nseg_total; si += gridDim.x) {
+        const DecSeg sg = segs[si];
+        uint32_t carry = 0;
+        bool bad = false;
+        for (uint64_t c0 = 0; c0 < sg.nchunk; c0 += kThreads) {
+            const uint64_t i = c0 + tid;
+            uint32_t c = i < sg.nchunk ? ctot[sg.chunk0 + i] : 0u;
+            if (c == kDense) { bad = true; c = 0; }
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            uint32_t pre = carry, tot = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; w++) { if (w < warp) pre += wsum[w]; tot += wsum[w]; }
+            if (i < sg.nchunk) cpre[sg.chunk0 + i] = pre + incl - c;
+            carry += tot;
+            __syncthreads();
+        }
+        bad = __syncthreads_or(bad);
+        if (tid == 0) {
+            seg_cnt[si] = carry;
+            if (bad) seg_fail[si] = 1;
+        }
+    }
+}
+
+// CTA per chunk slot: record slot r = (chunk prefix + span prefix + i) gets
+// candidate i's position and the position its header says the next record
+// starts at; after record R-2 the tail record (not a candidate when its
+// length differs from the block size) follows.
+__global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+                                                   uint64_t nchunk_total, const uint32_t* __restrict__ cand,
+                                                   const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cpre,
+                                                   uint32_t* __restrict__ seg_fail, uint64_t* __restrict__ rec_pos,
+                                                   uint64_t* __restrict__ rec_next) {
+    __shared__ uint32_t spre[kWarps + 1];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t t = blockIdx.x;
+    if (t >= nchunk_total) return;
+    uint64_t lo = 0, hi = nseg_total;
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (segs[mid].chunk0 <= t) lo = mid; else hi = mid;
+    }
+    const DecSeg sg = segs[lo];
+    if (t < sg.chunk0 || t >= sg.chunk0 + sg.nchunk) return;
+    if (tid == 0) {
+        uint32_t acc = cpre[t];
+        bool dense = false;
+        for (int w = 0; w < kWarps; w++) {
+            spre[w] = acc;
+            const uint32_t c = ccnt[t * kWarps + w];
+            if (c == kDense) dense = true; else acc += c;
+        }
+        spre[kWarps] = dense ? 1u : 0u;
+    }
+    __syncthreads();
+    if (spre[kWarps]) return;  // k_number failed the segment
+    const uint64_t span = t * kWarps + warp;
+    const uint32_t c = ccnt[span];
+    const uint32_t R = sg.nrec, B = sg.block;
+    const uint32_t Ltail = R ? (uint32_t)(sg.orig - (uint64_t)(R - 1) * B) : 0;
+    for (uint32_t k = lane; k < c; k += 32) {
+        uint64_t pos = cand[span * kSpanCap + k];
+        uint32_t r = spre[warp] + k;
+        if (r >= R) { atomicOr(&seg_fail[lo], 1u); break; }
+        for (int part = 0; part < 2; part++) {
+            uint32_t mode = 0, l = 0;
+            uint64_t ps = 0;
+            const bool rok = rec_size(sg.base, sg.comp, pos, mode, l, ps) && l == ((r + 1 == R) ? Ltail : B);
+            rec_pos[sg.rec0 + r] = pos;
+            rec_next[sg.rec0 + r] = rok ? pos + 5 + ps : ~0ull;
+            if (!rok) atomicOr(&seg_fail[lo], 1u);
+            if (!(rok && part == 0 && r + 2 == R && Ltail != B)) break;
+            pos += 5 + ps;
+            r = R - 1;
+        }
+    }
+}
+
+// CTA per record slot of the segments k_verify accepted: RLE fill, stored
+// copy or CTA-wide Huffman decode into the grouped scratch.  A failure marks
+// the segment for k_fallback, which re-walks it serially and reports the
+// reference's error.
+__global__ void __launch_bounds__(kThreads) k_decrec(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+                                                   uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
+                                                   const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
+    const uint64_t g = blockIdx.x;
+    if (g >= nrec_total) return;
+    uint64_t lo = 0, hi = nseg_total;
+    while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (segs[mid].rec0 <= g) lo = mid; else hi = mid;
+    }
+    const DecSeg sg = segs[lo];
+    if (g < sg.rec0 || g >= sg.rec0 + sg.nrec || seg_fail[lo]) return;
+    const uint32_t r = (uint32_t)(g - sg.rec0);
+    const uint8_t* rec = sg.base + rec_pos[g];
+    const uint32_t mode = rec[0], len = rd32(rec + 1);
+    const bool ok = decode_record(s, rec, mode, len, scratch + sg.goff + (uint64_t)r * sg.block);
+    if (!ok && threadIdx.x == 0) atomicOr(&seg_fail[lo], 1u);
 }
 
 // --------------------------------------------------------------- k_verify

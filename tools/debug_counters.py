@@ -22,9 +22,15 @@ L.lmcg_debug_counters(cnt, 1)
 print("first decompress: fallback segs", cnt[11], "dense", cnt[12], "r>=R", cnt[13], "recfail", cnt[14], "verify", cnt[15])
 r = codec.decompress(b)
 L.lmcg_debug_counters(cnt, 1)
-names = ["count calls", "count syms", "rec-bm calls", "rec-bm syms", "emit calls", "emit syms", "chk-bm calls", "chk-bm syms", "fixup rounds", "-", "-", "fallback segs",
+names = ["count calls", "count syms", "rec-bm calls", "rec-bm syms", "emit calls", "emit syms", "fix nosync", "fix syms", "fixup rounds", "nosync last", "nosync p0bad", "fallback segs",
          "dense", "r>=R", "rec fail", "verify fail", "huff setup cyc", "staged recs", "pass0 cyc", "fixup cyc", "emit cyc", "chunks", "scan cyc",
-         "lookback cyc", "huff rec cyc", "rle rec cyc", "stored rec cyc", "-", "huff recs", "rle recs", "stored recs"]
+         "lookback cyc", "huff rec cyc", "rle rec cyc", "stored rec cyc", "nosync e2bad", "huff recs", "rle recs", "stored recs"]
 for i, n in enumerate(names):
     print(f"{n:14s} {cnt[i]}")
 print("status", set(r.status))
+ev = (ctypes.c_ulonglong * 4096)()
+L.lmcg_debug_events(ev)
+for k in range(min(12, int(cnt[10]) if cnt[10] else 512)):
+    e = ev[8 * k: 8 * k + 8]
+    if e[5] == 0: break
+    print("ev cta", e[0], "c", e[1], "p0", e[2], "pe", e[3], "lim", e[4], "bits", e[5], "min/max", e[6] >> 32, e[6] & 0xFFFFFFFF, "p0cnt/cnt2", e[7] >> 32, e[7] & 0xFFFFFFFF)
