@@ -19,6 +19,8 @@
 
 namespace lmcg {
 
+constexpr int kEncRun = 64;  // k_encode positions per thread per round
+
 // ------------------------------------------------------------------ slotmap
 __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* __restrict__ slot2win) {
     int wi = blockIdx.x;
@@ -633,6 +635,116 @@ __device__ __forceinline__ int tile_piece(const WinDesc& wd, uint64_t tp, uint64
     return ns;
 }
 
+// Huffman packing of positions [p0, p1) of a window plane, in rounds of
+// kEncRun positions per thread: thread t packs the contiguous run
+// [r0 + t kEncRun, +kEncRun) sequentially into a 64-bit accumulator; a first
+// pass sums its code lengths so a CTA scan gives every run its bit offset.
+// Complete words go to the staging area (laid out on the destination's
+// 4-byte grid) with plain stores; a run's first word, which may hold bits of
+// the previous run, and its final partial word are merged with atomicOr.
+// Complete staging words leave with coalesced 32-bit stores each round.
+template <int W>
+__device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const uint8_t* sh_len8, const uint32_t* sh_code,
+                            uint32_t* sh_wsum, uint32_t* sh_first_word, uint32_t* stg, uint32_t* gw, uint32_t lead,
+                            uint32_t& bitpos, uint64_t& base_word) {
+    constexpr uint32_t lw = W == 1 ? 0 : (W == 2 ? 1 : 2);
+    constexpr int per = 16 >> lw;   // symbols per 16-byte piece
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint64_t r0 = p0; r0 < p1; r0 += (uint64_t)kEncRun * kThreads) {
+        const uint64_t q0 = r0 + (uint64_t)tid * kEncRun;
+        const uint64_t q1 = min(q0 + kEncRun, p1);
+        const uint64_t g = q0 < q1 ? plane_of(q0, wd.n, W) : 0;
+        const bool fast = q0 < q1 && wd.vec && ((q1 - q0) % per == 0) && (q1 <= (g + 1) * wd.n);
+        const uint8_t* srcp = wd.src + ((q0 - g * wd.n) << lw);
+        const uint8_t* prvp = wd.prev ? wd.prev + ((q0 - g * wd.n) << lw) : nullptr;
+        auto piece = [&](uint64_t pos, uint32_t sy[4]) -> int {
+            if (fast) {
+                uint4 a = __ldg(reinterpret_cast<const uint4*>(srcp + ((pos - q0) << lw)));
+                if (prvp) {
+                    const uint4 c = __ldg(reinterpret_cast<const uint4*>(prvp + ((pos - q0) << lw)));
+                    a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
+                }
+                return piece_symbols(a, W, (uint32_t)g, sy);
+            }
+            sy[0] = sy[1] = sy[2] = sy[3] = 0;
+            int ns = 0;
+            for (int i = 0; i < per && pos + i < q1; i++, ns++) sy[i >> 2] |= gather_byte(wd, pos + i) << (8 * (i & 3));
+            return ns;
+        };
+        // pass A: bits of the run
+        uint32_t nb = 0;
+        for (uint64_t pos = q0; pos < q1; pos += per) {
+            uint32_t sy[4];
+            const int ns = piece(pos, sy);
+#pragma unroll
+            for (int i = 0; i < per; i++)
+                nb += (i < ns) ? sh_len8[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF] : 0u;
+        }
+        // CTA exclusive scan of nb
+        uint32_t incl = nb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) sh_wsum[warp] = incl;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+#pragma unroll
+        for (int q = 0; q < kWarps; q++) { if (q < warp) pre += sh_wsum[q]; tot += sh_wsum[q]; }
+        const uint32_t start = bitpos + pre + incl - nb;
+        const uint32_t fw = start >> 5, lwi = (start + nb - 1) >> 5;
+        if (nb && lwi != fw) stg[lwi] = 0;   // final partial word (merged); word fw is merged too
+        if (nb && fw) stg[fw] = 0;           // (word 0 holds the carry of the previous round)
+        __syncthreads();
+        // pass B: pack; the first complete word goes to a private slot
+        if (nb) {
+            uint64_t acc = 0;
+            uint32_t n = start & 31, wi = fw;
+            sh_first_word[tid] = 0;
+            for (uint64_t pos = q0; pos < q1; pos += per) {
+                uint32_t sy[4];
+                const int ns = piece(pos, sy);
+#pragma unroll
+                for (int i = 0; i < per; i++) {
+                    if (i < ns) {
+                        const uint32_t e = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
+                        const uint32_t l = e >> 16;
+                        acc = (acc << l) | (e & 0xFFFF);
+                        n += l;
+                        const bool fl = n >= 32;
+                        n -= fl ? 32 : 0;
+                        uint32_t* dst = (wi == fw) ? &sh_first_word[tid] : &stg[wi];
+                        if (fl) *dst = (uint32_t)(acc >> n);
+                        wi += fl ? 1 : 0;
+                    }
+                }
+            }
+            if (wi != fw) atomicOr(&stg[fw], sh_first_word[tid]);
+            if (n) atomicOr(&stg[wi], (uint32_t)(acc << (32 - n)));
+        }
+        __syncthreads();
+        const uint32_t end = bitpos + tot;
+        const uint32_t full = end >> 5;   // complete words in staging
+        for (uint32_t j = tid; j < full; j += kThreads) {
+            const uint64_t gwi = base_word + j;
+            const uint32_t v = bswap32(stg[j]);
+            if (gwi == 0 && lead) {
+                uint8_t* bp = reinterpret_cast<uint8_t*>(gw);
+                for (uint32_t q = lead / 8; q < 4; q++) bp[q] = (uint8_t)(v >> (8 * q));
+            } else {
+                gw[gwi] = v;
+            }
+        }
+        const uint32_t carry = stg[full];
+        __syncthreads();
+        if (tid == 0) stg[0] = (end & 31) ? carry : 0u;
+        base_word += full;
+        bitpos = end & 31;
+        __syncthreads();
+    }
+}
+
 // One CTA per block slot.  Canonical codes (huffman.py:213-225) are built in
 // shared memory from the wire codebook; each lane packs the codes of its four
 // pieces MSB-first into a shared staging area laid out on the 4-byte grid of
@@ -746,132 +858,26 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     } else {
         sh_code[tid] = 0;
     }
-    // staging
-    const uint64_t iterpos = T * kWarps;
-    const uint32_t stg_words = (uint32_t)((iterpos * 15) / 32 + 4);
-    for (uint32_t i = tid; i < stg_words; i += kThreads) stg[i] = 0;
-    __syncthreads();
+    __shared__ uint8_t sh_len8[256];
+    __shared__ uint32_t sh_first_word[kThreads];
+    sh_len8[tid] = (uint8_t)my_len;
     const uint64_t gaddr = (uint64_t)(rp + hdr);
     const uint32_t lead = (uint32_t)(gaddr & 3) * 8;
     uint32_t* gw = reinterpret_cast<uint32_t*>(gaddr & ~(uint64_t)3);
-    uint64_t bitpos = lead;     // staging coordinate of the next bit (relative to gw)
+    uint32_t bitpos = lead;     // staging coordinate of the next bit (< 32 at a round start)
     uint64_t base_word = 0;     // global word index (relative to gw) of stg[0]
-    // A unit = up to 8 consecutive symbols of one piece; its code bits (<= 120)
-    // are built left-aligned in four words x[0..3] in a single pass.
-    const int upp = (w == 1) ? 2 : 1;  // units per piece
-    for (uint64_t it0 = p0; it0 < p1; it0 += iterpos) {
-        const uint64_t tp = it0 + (uint64_t)warp * T;
-        const uint64_t te = min(tp + T, p1);
-        const bool live = tp < te;
-        const uint64_t g = live ? plane_of(tp, wd.n, w) : 0;
-        const bool fast = live && wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
-        uint32_t x[4][2][4];
-        uint32_t nbu[4][2];
-        uint32_t off[4];
-        uint32_t wtot = 0;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            uint32_t sy[4];
-            uint64_t pos;
-            int ns = live ? tile_piece(wd, tp, te, g, fast, q, lane, sy, pos) : 0;
-            if (live && pos >= te) ns = 0;
-            uint32_t lane_bits = 0;
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                uint64_t hi = 0, lo = 0;
-                uint32_t nb = 0;
-                if (u < upp) {
-#pragma unroll
-                    for (int i = 0; i < 8; i++) {
-                        const int si = 8 * u + i;
-                        const uint32_t e = si < ns ? sh_code[(sy[si >> 2] >> (8 * (si & 3))) & 0xFF] : 0u;
-                        const uint32_t l = e >> 16;
-                        // (hi:lo) = (hi:lo) << l | code, as a 128-bit shift
-                        hi = (hi << l) | (l ? (lo >> (64 - l)) : 0);
-                        lo = (lo << l) | (e & 0xFFFF);
-                        nb += l;
-                    }
-                    // left-align the nb bits in 128 bits
-                    const uint32_t sh = 128 - nb;
-                    if (nb == 0) { hi = 0; lo = 0; }
-                    else if (sh >= 64) { hi = lo << (sh - 64); lo = 0; }
-                    else if (sh > 0) { hi = (hi << sh) | (lo >> (64 - sh)); lo <<= sh; }
-                }
-                x[q][u][0] = (uint32_t)(hi >> 32); x[q][u][1] = (uint32_t)hi;
-                x[q][u][2] = (uint32_t)(lo >> 32); x[q][u][3] = (uint32_t)lo;
-                nbu[q][u] = nb;
-                lane_bits += nb;
-            }
-            uint32_t incl = lane_bits;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            off[q] = wtot + incl - lane_bits;
-            wtot += __shfl_sync(0xFFFFFFFFu, incl, 31);
-        }
-        if (lane == 0) sh_wsum[warp] = wtot;
-        __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-#pragma unroll
-        for (int q = 0; q < kWarps; q++) { if (q < warp) wpre += sh_wsum[q]; tot += sh_wsum[q]; }
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-            uint64_t o = bitpos + wpre + off[q] - base_word * 32;
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                const uint32_t nb = nbu[q][u];
-                if (nb) {
-                    // shift the left-aligned unit right by the start's bit phase into <= 5 words;
-                    // the first and last words may be shared with neighbouring units
-                    const uint32_t s0 = (uint32_t)(o & 31);
-                    const uint32_t wi = (uint32_t)(o >> 5);
-                    const uint32_t nw = (s0 + nb + 31) / 32;
-                    const uint32_t* xx = x[q][u];
-                    const uint32_t y0 = xx[0] >> s0;
-                    const uint32_t y1 = __funnelshift_r(xx[1], xx[0], s0);
-                    const uint32_t y2 = __funnelshift_r(xx[2], xx[1], s0);
-                    const uint32_t y3 = __funnelshift_r(xx[3], xx[2], s0);
-                    const uint32_t y4 = s0 ? (xx[3] << (32 - s0)) : 0u;
-                    atomicOr(&stg[wi], y0);
-                    if (nw > 2) stg[wi + 1] = y1; else if (nw == 2) atomicOr(&stg[wi + 1], y1);
-                    if (nw > 3) stg[wi + 2] = y2; else if (nw == 3) atomicOr(&stg[wi + 2], y2);
-                    if (nw > 4) stg[wi + 3] = y3; else if (nw == 4) atomicOr(&stg[wi + 3], y3);
-                    if (nw == 5) atomicOr(&stg[wi + 4], y4);
-                }
-                o += nb;
-            }
-        }
-        __syncthreads();
-        const uint64_t end = bitpos + tot;
-        const uint64_t full = end / 32 - base_word;   // complete words in staging
-        for (uint64_t j = tid; j < full; j += kThreads) {
-            const uint64_t gwi = base_word + j;
-            const uint32_t v = bswap32(stg[j]);
-            if (gwi == 0 && lead) {
-                uint8_t* bp = reinterpret_cast<uint8_t*>(gw);
-                for (uint32_t q = lead / 8; q < 4; q++) bp[q] = (uint8_t)(v >> (8 * q));
-            } else {
-                gw[gwi] = v;
-            }
-        }
-        const uint32_t carry = (tid == 0) ? stg[full] : 0;  // read before anyone clears it
-        __syncthreads();
-        for (uint64_t j = tid; j <= full; j += kThreads) stg[j] = 0;
-        __syncthreads();
-        if (tid == 0) stg[0] = carry;
-        base_word += full;
-        bitpos = end;
-        __syncthreads();
-    }
+    if (tid == 0) stg[0] = 0;
+    __syncthreads();
+    if (w == 1) encode_runs<1>(wd, p0, p1, sh_len8, sh_code, sh_wsum, sh_first_word, stg, gw, lead, bitpos, base_word);
+    else if (w == 2) encode_runs<2>(wd, p0, p1, sh_len8, sh_code, sh_wsum, sh_first_word, stg, gw, lead, bitpos, base_word);
+    else encode_runs<4>(wd, p0, p1, sh_len8, sh_code, sh_wsum, sh_first_word, stg, gw, lead, bitpos, base_word);
     // trailing partial word: bytes up to the record end
-    if (tid == 0 && (bitpos & 31)) {
+    if (tid == 0 && bitpos) {
         const uint32_t v = bswap32(stg[0]);
-        const uint64_t end_byte = (bitpos + 7) / 8;   // relative to gw
         uint8_t* bp = reinterpret_cast<uint8_t*>(gw) + base_word * 4;
-        uint32_t q0 = (base_word == 0) ? lead / 8 : 0;
-        for (uint32_t q = q0; q < 4 && base_word * 4 + q < end_byte; q++) bp[q] = (uint8_t)(v >> (8 * q));
+        const uint32_t q0 = (base_word == 0) ? lead / 8 : 0;
+        const uint32_t q1 = (bitpos + 7) / 8;
+        for (uint32_t q = q0; q < q1; q++) bp[q] = (uint8_t)(v >> (8 * q));
     }
 }
 

@@ -795,8 +795,6 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* 
     const uint32_t B = sg.block;
     const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(sg.nrec - 1) * B);
     const int kb = (__ffs(B) - 1) >> 3;
-    const uint32_t kv = B >> (8 * kb);
-    const uint32_t pat = kv * 0x01010101u;
     const uint8_t* b = sg.base;
     const uint64_t qa = max(pa, (uint64_t)1) + 1 + kb;
     const uint64_t qe = min(pe + 1 + kb, sg.comp);
