@@ -409,7 +409,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
                                          ctx->d_crc, d_soff, static_cast<uint8_t*>(d_out)); }
     }
     if (nslots) {
-        const size_t smem = (size_t)(((uint64_t)kEncRun * kThreads * 15) / 32 + 8) * sizeof(uint32_t);
+        const size_t smem = (size_t)(kStageWords + kThreads * kSlot) * sizeof(uint32_t);
         if (smem > 48 * 1024 && !ctx->enc_attr) {
             CK(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             ctx->enc_attr = true;

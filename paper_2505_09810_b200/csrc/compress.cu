@@ -636,20 +636,24 @@ __device__ __forceinline__ int tile_piece(const WinDesc& wd, uint64_t tp, uint64
 }
 
 // Huffman packing of positions [p0, p1) of a window plane, in rounds of
-// kEncRun positions per thread: thread t packs the contiguous run
-// [r0 + t kEncRun, +kEncRun) sequentially into a 64-bit accumulator; a first
-// pass sums its code lengths so a CTA scan gives every run its bit offset.
-// Complete words go to the staging area (laid out on the destination's
-// 4-byte grid) with plain stores; a run's first word, which may hold bits of
-// the previous run, and its final partial word are merged with atomicOr.
-// Complete staging words leave with coalesced 32-bit stores each round.
+// kEncRun positions per thread.  Thread t packs its contiguous run
+// [r0 + t kEncRun, +kEncRun) MSB-first into a private slot of whole words
+// through a 64-bit accumulator (one pass, no branches); a CTA scan of the
+// run bit counts places every run, whose words are then shifted into the
+// round's staging area on the destination's 4-byte grid (the two edge words
+// of a run, shared with its neighbours, merged with atomicOr) and leave with
+// coalesced 32-bit stores.
+constexpr int kSlot = (kEncRun * kMaxLen + 31) / 32 + 1;   // private words per run
+constexpr int kStageWords = (kEncRun * kThreads * kMaxLen) / 32 + 8;
+
 template <int W>
-__device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const uint8_t* sh_len8, const uint32_t* sh_code,
-                            uint32_t* sh_wsum, uint32_t* sh_first_word, uint32_t* stg, uint32_t* gw, uint32_t lead,
+__device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const uint32_t* sh_code,
+                            uint32_t* sh_wsum, uint32_t* stg, uint32_t* gw, uint32_t lead,
                             uint32_t& bitpos, uint64_t& base_word) {
     constexpr uint32_t lw = W == 1 ? 0 : (W == 2 ? 1 : 2);
     constexpr int per = 16 >> lw;   // symbols per 16-byte piece
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint32_t* priv = stg + kStageWords + tid * kSlot;
     for (uint64_t r0 = p0; r0 < p1; r0 += (uint64_t)kEncRun * kThreads) {
         const uint64_t q0 = r0 + (uint64_t)tid * kEncRun;
         const uint64_t q1 = min(q0 + kEncRun, p1);
@@ -657,29 +661,41 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
         const bool fast = q0 < q1 && wd.vec && ((q1 - q0) % per == 0) && (q1 <= (g + 1) * wd.n);
         const uint8_t* srcp = wd.src + ((q0 - g * wd.n) << lw);
         const uint8_t* prvp = wd.prev ? wd.prev + ((q0 - g * wd.n) << lw) : nullptr;
-        auto piece = [&](uint64_t pos, uint32_t sy[4]) -> int {
+        // pack the run into the private slot
+        uint64_t acc = 0;
+        uint32_t n = 0, wi = 0;
+        for (uint64_t pos = q0; pos < q1; pos += per) {
+            uint32_t sy[4];
+            int ns;
             if (fast) {
                 uint4 a = __ldg(reinterpret_cast<const uint4*>(srcp + ((pos - q0) << lw)));
                 if (prvp) {
                     const uint4 c = __ldg(reinterpret_cast<const uint4*>(prvp + ((pos - q0) << lw)));
                     a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
                 }
-                return piece_symbols(a, W, (uint32_t)g, sy);
+                ns = piece_symbols(a, W, (uint32_t)g, sy);
+            } else {
+                sy[0] = sy[1] = sy[2] = sy[3] = 0;
+                ns = 0;
+                for (int i = 0; i < per && pos + i < q1; i++, ns++) sy[i >> 2] |= gather_byte(wd, pos + i) << (8 * (i & 3));
             }
-            sy[0] = sy[1] = sy[2] = sy[3] = 0;
-            int ns = 0;
-            for (int i = 0; i < per && pos + i < q1; i++, ns++) sy[i >> 2] |= gather_byte(wd, pos + i) << (8 * (i & 3));
-            return ns;
-        };
-        // pass A: bits of the run
-        uint32_t nb = 0;
-        for (uint64_t pos = q0; pos < q1; pos += per) {
-            uint32_t sy[4];
-            const int ns = piece(pos, sy);
 #pragma unroll
-            for (int i = 0; i < per; i++)
-                nb += (i < ns) ? sh_len8[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF] : 0u;
+            for (int i = 0; i < per; i++) {
+                if (i < ns) {
+                    const uint32_t e = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
+                    const uint32_t l = e >> 16;
+                    acc = (acc << l) | (e & 0xFFFF);
+                    n += l;
+                    const bool fl = n >= 32;
+                    n -= fl ? 32 : 0;
+                    if (fl) priv[wi] = (uint32_t)(acc >> n);
+                    wi += fl ? 1 : 0;
+                }
+            }
         }
+        const uint32_t nwp = wi + (n ? 1 : 0);
+        if (n) priv[wi] = (uint32_t)(acc << (32 - n));
+        const uint32_t nb = wi * 32 + n;
         // CTA exclusive scan of nb
         uint32_t incl = nb;
 #pragma unroll
@@ -694,34 +710,18 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
         for (int q = 0; q < kWarps; q++) { if (q < warp) pre += sh_wsum[q]; tot += sh_wsum[q]; }
         const uint32_t start = bitpos + pre + incl - nb;
         const uint32_t fw = start >> 5, lwi = (start + nb - 1) >> 5;
-        if (nb && lwi != fw) stg[lwi] = 0;   // final partial word (merged); word fw is merged too
-        if (nb && fw) stg[fw] = 0;           // (word 0 holds the carry of the previous round)
+        if (nb && fw) stg[fw] = 0;           // word 0 holds the carry of the previous round
+        if (nb && lwi != fw) stg[lwi] = 0;
         __syncthreads();
-        // pass B: pack; the first complete word goes to a private slot
         if (nb) {
-            uint64_t acc = 0;
-            uint32_t n = start & 31, wi = fw;
-            sh_first_word[tid] = 0;
-            for (uint64_t pos = q0; pos < q1; pos += per) {
-                uint32_t sy[4];
-                const int ns = piece(pos, sy);
-#pragma unroll
-                for (int i = 0; i < per; i++) {
-                    if (i < ns) {
-                        const uint32_t e = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
-                        const uint32_t l = e >> 16;
-                        acc = (acc << l) | (e & 0xFFFF);
-                        n += l;
-                        const bool fl = n >= 32;
-                        n -= fl ? 32 : 0;
-                        uint32_t* dst = (wi == fw) ? &sh_first_word[tid] : &stg[wi];
-                        if (fl) *dst = (uint32_t)(acc >> n);
-                        wi += fl ? 1 : 0;
-                    }
-                }
+            const uint32_t s0 = start & 31;
+            const uint32_t nwo = lwi - fw + 1;
+            for (uint32_t k = 0; k < nwo; k++) {
+                const uint32_t cur = k < nwp ? priv[k] : 0u;
+                const uint32_t v = s0 ? ((k ? priv[k - 1] << (32 - s0) : 0u) | (cur >> s0)) : cur;
+                if (k == 0 || k + 1 == nwo) atomicOr(&stg[fw + k], v);
+                else stg[fw + k] = v;
             }
-            if (wi != fw) atomicOr(&stg[fw], sh_first_word[tid]);
-            if (n) atomicOr(&stg[wi], (uint32_t)(acc << (32 - n)));
         }
         __syncthreads();
         const uint32_t end = bitpos + tot;
@@ -742,6 +742,66 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
         base_word += full;
         bitpos = end & 31;
         __syncthreads();
+    }
+}
+
+// Stored record payload: the plane's bytes of [p0, p1), gathered with
+// coalesced 16-byte loads into the staging area on the destination's 4-byte
+// grid, then written with coalesced 32-bit stores (the record's first and
+// last words bytewise: they share bytes with the header / the next record).
+__device__ void store_plane(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_t* stg, uint8_t* d0) {
+    const int tid = threadIdx.x;
+    const uint32_t w = wd.w, lw = lg2w(w);
+    const uint32_t per = 16u >> lw;
+    const uint32_t lb = (uint32_t)(reinterpret_cast<uint64_t>(d0) & 3);
+    uint32_t* gwd = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t>(d0) & ~3ull);
+    uint8_t* sb = reinterpret_cast<uint8_t*>(stg);
+    const uint64_t round = (uint64_t)kThreads * 4 * per;
+    uint64_t wbase = 0;
+    uint32_t rem = lb;  // bytes pending in staging word 0
+    if (tid == 0) stg[0] = 0;
+    __syncthreads();
+    for (uint64_t r0 = p0; r0 < p1; r0 += round) {
+        const uint64_t r1 = min(r0 + round, p1);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint64_t pos = r0 + (uint64_t)(q * kThreads + tid) * per;
+            if (pos >= r1) continue;
+            const uint64_t g = plane_of(pos, wd.n, w);
+            uint8_t* dst = sb + lb + (pos - r0);
+            if (wd.vec && pos + per <= r1 && pos + per <= (g + 1) * wd.n) {
+                const uint4 a = ldg16x(wd.src, wd.prev, (pos - g * wd.n) << lw);
+                uint32_t sy[4];
+                const int ns = piece_symbols(a, w, (uint32_t)g, sy);
+                for (int i = 0; i < ns; i++) dst[i] = (uint8_t)(sy[i >> 2] >> (8 * (i & 3)));
+            } else {
+                for (uint32_t i = 0; i < per && pos + i < r1; i++) dst[i] = (uint8_t)gather_byte(wd, pos + i);
+            }
+        }
+        __syncthreads();
+        const uint32_t nbytes = lb + (uint32_t)(r1 - r0);
+        const uint32_t full = nbytes / 4;
+        for (uint32_t j = tid; j < full; j += kThreads) {
+            const uint64_t gwi = wbase + j;
+            const uint32_t v = stg[j];
+            if (gwi == 0 && lb) {
+                uint8_t* bp = reinterpret_cast<uint8_t*>(gwd);
+                for (uint32_t q = lb; q < 4; q++) bp[q] = (uint8_t)(v >> (8 * q));
+            } else {
+                gwd[gwi] = v;
+            }
+        }
+        const uint32_t carry = stg[full];
+        __syncthreads();
+        if (tid == 0) stg[0] = carry;
+        wbase += full;
+        rem = nbytes & 3;
+        __syncthreads();
+    }
+    if (tid == 0 && rem) {
+        const uint32_t v = stg[0];
+        uint8_t* bp = reinterpret_cast<uint8_t*>(gwd + wbase);
+        for (uint32_t q = (wbase == 0 ? lb : 0); q < rem; q++) bp[q] = (uint8_t)(v >> (8 * q));
     }
 }
 
@@ -790,38 +850,9 @@ __global__ void __launch_bounds__(kThreads) k_encode(
         rp[tid] = v;
     }
     const uint32_t w = wd.w;
-    const uint64_t T = kTileBytes >> lg2w(w);
     const uint64_t p0 = k * B, p1 = min(wd.W, p0 + B);
-    if (!huff) {
-        // stored record: the block's bytes verbatim after the 5-byte header
-        uint8_t* base = rp + 5;
-        for (uint64_t t = warp; p0 + t * T < p1; t += kWarps) {
-            const uint64_t tp = p0 + t * T;
-            const uint64_t te = min(tp + T, p1);
-            const uint64_t g = plane_of(tp, wd.n, w);
-            const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                uint32_t sy[5];
-                uint64_t pos;
-                int ns = tile_piece(wd, tp, te, g, fast, q, lane, sy, pos);
-                if (pos >= te) ns = 0;
-                sy[4] = 0;
-                if (ns == 0) continue;
-                uint8_t* d = base + (pos - p0);
-                const uint32_t head = min((uint32_t)ns, (uint32_t)((4 - (reinterpret_cast<uint64_t>(d) & 3)) & 3));
-                for (uint32_t i = 0; i < head; i++) d[i] = (uint8_t)(sy[0] >> (8 * i));
-                const uint32_t nw = ((uint32_t)ns - head) / 4;
-                uint32_t* dw = reinterpret_cast<uint32_t*>(d + head);
-#pragma unroll
-                for (int i = 0; i < 4; i++)
-                    if ((uint32_t)i < nw) dw[i] = __funnelshift_r(sy[i], sy[i + 1], 8 * head);
-                for (uint32_t i = head + 4 * nw; i < (uint32_t)ns; i++) {
-                    const uint32_t wv = (i >> 2) == 0 ? sy[0] : (i >> 2) == 1 ? sy[1] : (i >> 2) == 2 ? sy[2] : sy[3];
-                    d[i] = (uint8_t)(wv >> (8 * (i & 3)));
-                }
-            }
-        }
+    if (!huff) {  // stored record: the block's bytes verbatim after the 5-byte header
+        store_plane(wd, p0, p1, stg, rp + 5);
         return;
     }
     // canonical code table (huffman.py:213-225): thread t handles symbol t
@@ -858,9 +889,6 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     } else {
         sh_code[tid] = 0;
     }
-    __shared__ uint8_t sh_len8[256];
-    __shared__ uint32_t sh_first_word[kThreads];
-    sh_len8[tid] = (uint8_t)my_len;
     const uint64_t gaddr = (uint64_t)(rp + hdr);
     const uint32_t lead = (uint32_t)(gaddr & 3) * 8;
     uint32_t* gw = reinterpret_cast<uint32_t*>(gaddr & ~(uint64_t)3);
@@ -868,9 +896,9 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     uint64_t base_word = 0;     // global word index (relative to gw) of stg[0]
     if (tid == 0) stg[0] = 0;
     __syncthreads();
-    if (w == 1) encode_runs<1>(wd, p0, p1, sh_len8, sh_code, sh_wsum, sh_first_word, stg, gw, lead, bitpos, base_word);
-    else if (w == 2) encode_runs<2>(wd, p0, p1, sh_len8, sh_code, sh_wsum, sh_first_word, stg, gw, lead, bitpos, base_word);
-    else encode_runs<4>(wd, p0, p1, sh_len8, sh_code, sh_wsum, sh_first_word, stg, gw, lead, bitpos, base_word);
+    if (w == 1) encode_runs<1>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word);
+    else if (w == 2) encode_runs<2>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word);
+    else encode_runs<4>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word);
     // trailing partial word: bytes up to the record end
     if (tid == 0 && bitpos) {
         const uint32_t v = bswap32(stg[0]);
