@@ -47,6 +47,9 @@ struct lmcg_ctx {
     const uint32_t* d_dstatus = nullptr;
     bool dec_attr = false;
     int scandec_occ = 1;
+    bool crc_attr = false;
+    uint32_t* d_sh496 = nullptr;
+    int crc_occ = 1;
     bool enc_attr = false;
     // per-kernel event timing (lmcg_profile)
     bool prof = false;
@@ -89,6 +92,13 @@ uint32_t h_multmodp(uint32_t a, uint32_t b) {
         b = b & 1 ? (b >> 1) ^ 0xEDB88320u : b >> 1;
     }
     return p;
+}
+
+static int occupancy(lmcg_ctx* ctx, const void* fn, int threads, size_t smem) {
+    int per = 0, dev = ctx->device, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return std::max(1, per) * std::max(1, sms);
 }
 
 void build_crc_tables(CrcTables& t) {
@@ -209,7 +219,7 @@ bool host_valid_block(uint64_t b) { return b >= 4096 && b <= (1u << 20) && (b & 
 struct CPlan {
     std::vector<StreamDesc> streams;
     std::vector<WinDesc> wins;
-    uint64_t nb = 0, nslots = 0;
+    uint64_t nb = 0, nslots = 0, ncrc = 0;
     uint32_t min_w = 4;
 };
 
@@ -251,6 +261,10 @@ void make_plan(const lmcg_tensor* t, int n, const lmcg_options* o, CPlan& P) {
             wd.win_local = nw++;
             const bool al = ((uint64_t)wd.src % 16 == 0) && ((uint64_t)wd.prev % 16 == 0);
             wd.vec = al && (w == 1 || wd.W % 16 == 0);
+            wd.al16 = al ? 1u : 0u;
+            wd.pad = 0;
+            wd.crc0 = P.ncrc;
+            P.ncrc += (wd.W + kCrcChunk - 1) / kCrcChunk;
             P.nb += wd.nblocks;
             P.nslots += wd.nslots;
             P.min_w = std::min(P.min_w, w);
@@ -280,6 +294,17 @@ lmcg_ctx* lmcg_create(int device) {
     build_crc_tables(*h);
     if (cudaMalloc(&ctx->d_crc, sizeof(CrcTables)) == cudaSuccess)
         cudaMemcpy(ctx->d_crc, h, sizeof(CrcTables), cudaMemcpyHostToDevice);
+    {
+        // k_crc's 496-byte shift table: [k][b] = (b << 8k) * x^(8 * 496) mod P
+        uint32_t p = 1u << 31;
+        for (uint64_t nn = 496, k = 3; nn; nn >>= 1, k++)
+            if (nn & 1) p = h_multmodp(h->x2n[k & 63], p);
+        std::vector<uint32_t> t(1024);
+        for (int k = 0; k < 4; k++)
+            for (uint32_t b = 0; b < 256; b++) t[k * 256 + b] = b ? h_multmodp(p, b << (8 * k)) : 0;
+        if (ctx->d_crc && cudaMalloc(&ctx->d_sh496, 1024 * sizeof(uint32_t)) == cudaSuccess)
+            cudaMemcpy(ctx->d_sh496, t.data(), 1024 * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    }
     delete h;
     cudaEventCreateWithFlags(&ctx->pin_done, cudaEventDisableTiming);
     return ctx;
@@ -290,6 +315,7 @@ void lmcg_destroy(lmcg_ctx* ctx) {
     if (ctx->d_crc) {
         cudaDeviceSynchronize();
         cudaFree(ctx->d_crc);
+        if (ctx->d_sh496) cudaFree(ctx->d_sh496);
         if (ctx->ws) cudaFree(ctx->ws);
         if (ctx->dws) cudaFree(ctx->dws);
         if (ctx->hws) cudaFree(ctx->hws);
@@ -336,7 +362,7 @@ static size_t compress_layout(const CPlan& P, int n, size_t* offs /* 16 */) {
     offs[1] = a.take<StreamDesc>(n + 1);
     offs[2] = a.take<uint32_t>(P.nslots + 1);
     offs[3] = a.take<uint32_t>(nb * 256 + 1);
-    offs[4] = a.take<uint32_t>(nb + 1);
+    offs[4] = a.take<uint32_t>(P.ncrc + 1);
     offs[5] = a.take<BlockMeta>(nb + 1);
     offs[6] = a.take<uint8_t>(nb * 128 + 1);
     offs[7] = a.take<uint64_t>(nb + 1);
@@ -372,7 +398,7 @@ static int check_compress_args(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const
 // Kernel sequence of one compress over descriptors already resident on the
 // device (workspace laid out by compress_layout).  No host synchronisation:
 // capturable in a CUDA graph.
-static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t nslots, uint32_t min_w,
+static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t nslots, uint64_t ncrc, uint32_t min_w,
                            const lmcg_options* o, uint8_t* ws, const size_t* offs, void* d_out, uint64_t* d_offsets,
                            uint64_t* d_lengths, cudaStream_t st) {
     WinDesc* d_wins = reinterpret_cast<WinDesc*>(ws + offs[0]);
@@ -394,8 +420,18 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
     if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win); }
     if (nslots) {
         PROF(k_hist_crc);
-        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, ctx->d_crc, d_hist,
-                                                          d_crcp, d_meta);
+        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta);
+    }
+    if (ncrc) {
+        if (!ctx->crc_attr) {
+            CK(cudaFuncSetAttribute(k_crc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem));
+            ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kThreads, kCrcSmem);
+            ctx->crc_attr = true;
+        }
+        const uint64_t need = (ncrc + kWarps - 1) / kWarps;
+        PROF(k_crc);
+        k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, st>>>(
+            d_wins, nwin, ncrc, ctx->d_crc, ctx->d_sh496, d_crcp);
     }
     if (nb) {
         { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
@@ -451,7 +487,7 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options
     if (wbytes) CK(cudaMemcpyAsync(ws + offs[0], ctx->pin, wbytes, cudaMemcpyHostToDevice, st));
     if (sbytes) CK(cudaMemcpyAsync(ws + offs[1], ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(ctx->pin_done, st));
-    return compress_launch(ctx, n, (int)P.wins.size(), P.nb, P.nslots, P.min_w, o, ws, offs, d_out, d_offsets, d_lengths, st);
+    return compress_launch(ctx, n, (int)P.wins.size(), P.nb, P.nslots, P.ncrc, P.min_w, o, ws, offs, d_out, d_offsets, d_lengths, st);
 }
 
 // ---------------------------------------------------------------- plans
@@ -463,7 +499,7 @@ struct lmcg_plan {
     // compress
     lmcg_options opts{};
     int nwin = 0;
-    uint64_t nb = 0, nslots = 0, bound = 0;
+    uint64_t nb = 0, nslots = 0, ncrc = 0, bound = 0;
     uint32_t min_w = 4;
     size_t offs[16] = {};
     // decompress
@@ -483,6 +519,7 @@ lmcg_plan* lmcg_compress_plan_create(lmcg_ctx* ctx, const lmcg_tensor* t, int n,
     pl->nwin = (int)P.wins.size();
     pl->nb = P.nb;
     pl->nslots = P.nslots;
+    pl->ncrc = P.ncrc;
     pl->min_w = P.min_w;
     pl->bound = lmcg_compress_bound(t, n, o);
     pl->ws_bytes = compress_layout(P, n, pl->offs);
@@ -512,7 +549,7 @@ int lmcg_compress_plan_run(lmcg_ctx* ctx, lmcg_plan* pl, void* d_out, uint64_t o
     if (!ctx || !pl || pl->kind != 1) return fail(ctx, LMCG_ERR_ARGUMENT, "not a compress plan");
     if (out_capacity < pl->bound) return fail(ctx, LMCG_ERR_CAPACITY, "output capacity below the plan's bound");
     if (int r = ensure_ctx(ctx)) return r;
-    return compress_launch(ctx, pl->n, pl->nwin, pl->nb, pl->nslots, pl->min_w, &pl->opts, pl->ws, pl->offs, d_out,
+    return compress_launch(ctx, pl->n, pl->nwin, pl->nb, pl->nslots, pl->ncrc, pl->min_w, &pl->opts, pl->ws, pl->offs, d_out,
                            d_offsets, d_lengths, static_cast<cudaStream_t>(cuda_stream));
 }
 
@@ -638,13 +675,6 @@ void make_dplan(const uint64_t* lens, int n, const lmcg_stream_hint* hints, cons
         P.nwin += c.nwin; P.nseg += c.nseg; P.nrec += c.nrec; P.nchunk += c.nchunk; P.ntile += c.ntile;
         P.scratch += c.scratch;
     }
-}
-
-int occupancy(lmcg_ctx* ctx, const void* fn, int threads, size_t smem) {
-    int per = 0, dev = ctx->device, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return std::max(1, per) * std::max(1, sms);
 }
 
 }  // namespace

@@ -29,6 +29,90 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
     for (uint32_t i = threadIdx.x; i < wd.nslots; i += blockDim.x) slot2win[wd.slot0 + i] = (uint32_t)wi;
 }
 
+// ------------------------------------------------------------------ CRC
+// Raw CRC-32 of every 8 KiB chunk of every window's element bytes (the
+// payload in original byte order, XOR delta applied), one warp per chunk:
+// lane l folds the contiguous 256 bytes [256 l, 256 (l + 1)) of the chunk
+// byte by byte through a 32-fold replicated table (lane l reads copy l: no
+// bank conflicts), then a 5-level shift tree joins the lanes.  A short last
+// chunk is treated as left-padded with zero bytes, which leave a raw CRC
+// unchanged.  k_frame combines the chunks (stream.py:329).
+constexpr uint32_t kCrcChunk = 8192;
+constexpr size_t kCrcSmem = (size_t)256 * 32 * sizeof(uint32_t);
+
+__device__ __forceinline__ uint32_t crc1_word(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
+    crc ^= w;
+    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+    return (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+}
+
+__global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wins, int nwin, uint64_t nchunk,
+                                                const CrcTables* __restrict__ ct, const uint32_t* __restrict__ unused,
+                                                uint32_t* __restrict__ out) {
+    extern __shared__ uint32_t tab[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 256 * 32; i += kThreads) tab[i] = ct->slice[0][i >> 5];
+    __syncthreads();
+    const uint32_t* tl = tab + lane;
+    constexpr uint32_t kSpan = kCrcChunk / 32;   // 256
+    for (uint64_t c = (uint64_t)blockIdx.x * kWarps + warp; c < nchunk; c += (uint64_t)gridDim.x * kWarps) {
+        int lo = 0, hi = nwin;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (wins[mid].crc0 <= c) lo = mid; else hi = mid;
+        }
+        const WinDesc wd = wins[lo];
+        const uint64_t off = (c - wd.crc0) * kCrcChunk;
+        const uint32_t L = (uint32_t)min((uint64_t)kCrcChunk, wd.W - off);
+        const uint32_t Z = kCrcChunk - L;
+        const uint8_t* src = wd.src + off;
+        const uint8_t* prv = wd.prev ? wd.prev + off : nullptr;
+        const uint32_t qa = max(lane * kSpan, Z), qb = (lane + 1) * kSpan;
+        uint32_t crc = 0;
+        if (qa < qb) {
+            uint32_t d = qa - Z;
+            const uint32_t d1 = qb - Z;
+            auto byte_at = [&](uint32_t i) -> uint32_t {
+                uint32_t x = src[i];
+                if (prv) x ^= prv[i];
+                return x;
+            };
+            if (wd.al16) {
+                for (; d < d1 && (d & 15); d++) crc = (crc >> 8) ^ tl[((crc ^ byte_at(d)) & 0xFF) * 32];
+                for (; d + 64 <= d1; d += 64) {
+                    uint4 a[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) a[q] = __ldg(reinterpret_cast<const uint4*>(src + d) + q);
+                    if (prv) {
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            const uint4 b = __ldg(reinterpret_cast<const uint4*>(prv + d) + q);
+                            a[q].x ^= b.x; a[q].y ^= b.y; a[q].z ^= b.z; a[q].w ^= b.w;
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        crc = crc1_word(tl, crc, a[q].x);
+                        crc = crc1_word(tl, crc, a[q].y);
+                        crc = crc1_word(tl, crc, a[q].z);
+                        crc = crc1_word(tl, crc, a[q].w);
+                    }
+                }
+            }
+            for (; d < d1; d++) crc = (crc >> 8) ^ tl[((crc ^ byte_at(d)) & 0xFF) * 32];
+        }
+#pragma unroll
+        for (int k2 = 0; k2 < 5; k2++) {
+            const uint32_t other = __shfl_down_sync(0xFFFFFFFFu, crc, 1 << k2);
+            const uint32_t shifted = crc_shift_tab(&ct->pow2[8 + k2][0][0], crc);
+            if ((lane & ((2 << k2) - 1)) == 0) crc = shifted ^ other;
+        }
+        if (lane == 0) out[c] = crc;
+    }
+}
+
 // -------------------------------------------------------------- K1 hist+crc
 // One CTA per block slot.  Each warp owns 2 KiB warp-tiles of source bytes,
 // read as four fully coalesced 512-byte rows: lane l holds the 16-byte
@@ -39,12 +123,8 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
 // pieces, then the four rows in order).
 __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
-    const CrcTables* __restrict__ ct, uint32_t* __restrict__ hist_out, uint32_t* __restrict__ crc_out,
-    BlockMeta* __restrict__ meta) {
+    uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta) {
     __shared__ uint32_t sh_hist[kWarps][256];
-    __shared__ uint32_t sh_slice[1024];
-    __shared__ uint32_t sh_part[2048];  // per-tile raw CRCs of plane-0 tiles
-    __shared__ uint16_t sh_plen[2048];  // their byte lengths (<= 2048)
     const uint64_t slot = blockIdx.x;
     if (slot >= nslots) return;
     const WinDesc wd = wins[slot2win[slot]];
@@ -53,7 +133,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
     const uint64_t k = (uint64_t)kk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < kWarps * 256; i += kThreads) (&sh_hist[0][0])[i] = 0;
-    for (int i = tid; i < 1024; i += kThreads) sh_slice[i] = ct->slice[i >> 8][i & 255];
     __syncthreads();
 
     const uint64_t p0 = k * B;
@@ -62,7 +141,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
     const uint32_t lw = lg2w(w);
     const uint64_t T = kTileBytes >> lw;        // positions per warp-tile
     const uint64_t ntiles = (p1 - p0 + T - 1) >> (11 - lw);
-    const uint64_t crc_end = min(p1, wd.n);    // plane-0 positions of this block end here
     uint32_t* hist = sh_hist[warp];
 
     for (uint64_t t = warp; t < ntiles; t += kWarps) {
@@ -83,35 +161,11 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
                 for (int i = 0; i < 16; i++)
                     if (i < ns) atomicAdd(&hist[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF], 1u);
             }
-            if (g == 0) {
-                // tile CRC = XOR_l shift(v_l, 16 (31 - l)) with v_l = Horner over this
-                // lane's four rows (row stride 512 bytes): one lane tree per tile
-                uint32_t v = crc16(sh_slice, a[0]);
-#pragma unroll
-                for (int q = 1; q < 4; q++) v = crc_shift_tab(&ct->shift[kShift512][0][0], v) ^ crc16(sh_slice, a[q]);
-                v = crc_warp_tree(ct, v, lane, kShift16);
-                if (lane == 0) { sh_part[t] = v; sh_plen[t] = kTileBytes; }
-            }
         } else {
             // slow gather: lane owns positions [tp + lane*T/32, ...)
             const uint64_t per = T / 32;
             const uint64_t a = tp + lane * per, bnd = min(a + per, te);
             for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p)], 1u);
-            if (tp < crc_end) {
-                // plane-0 element bytes [tp*w, min(te,n)*w): left-pad to 2 KiB with zeros
-                const uint64_t b0 = tp * w, b1 = min(te, crc_end) * w;
-                const uint64_t L = b1 - b0, Z = kTileBytes - L;
-                uint32_t c = 0;
-                const uint64_t lo = (uint64_t)lane * kLaneBytes, hi = lo + kLaneBytes;
-                for (uint64_t q = max(lo, Z); q < hi; q++) {
-                    uint64_t o = b0 + q - Z;
-                    uint32_t x = wd.src[o];
-                    if (wd.prev) x ^= wd.prev[o];
-                    c = crc_byte(sh_slice, c, x);
-                }
-                c = crc_warp_tree(ct, c, lane, 2);
-                if (lane == 0) { sh_part[t] = c; sh_plen[t] = (uint16_t)L; }
-            }
         }
     }
     __syncthreads();
@@ -124,16 +178,6 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
         hist_out[b * 256 + tid] = sum;
     }
     if (tid == 0) {
-        if (p0 < crc_end) {
-            const uint64_t nct = (crc_end - p0 + T - 1) >> (11 - lw);
-            uint32_t acc = 0;
-            for (uint64_t t = 0; t < nct; t++) {
-                if (sh_plen[t] == kTileBytes) acc = crc_shift_tab(&ct->shift[kShift2K][0][0], acc);
-                else acc = crc_shift_bytes(ct, acc, sh_plen[t]);
-                acc ^= sh_part[t];
-            }
-            crc_out[b] = acc;
-        }
         BlockMeta m;
         m.len = (uint32_t)(p1 - p0);
         m.recsize = 0; m.bits = 0; m.mode = 0; m.sym = 0; m.pm = 0; m.pad = 0;
@@ -579,9 +623,9 @@ __global__ void __launch_bounds__(kThreads) k_frame(const StreamDesc* __restrict
     uint32_t acc = 0;
     for (uint32_t wl = 0; wl < sd.nwin; wl++) {
         const WinDesc wd = wins[sd.win0 + wl];
-        const uint64_t unit = (uint64_t)B * wd.w;
-        const uint64_t nfull = wd.n / B, rem = (wd.n % B) * wd.w;
-        const uint32_t* cp = crcpart + wd.blk0;
+        const uint64_t unit = kCrcChunk;
+        const uint64_t nfull = wd.W / kCrcChunk, rem = wd.W % kCrcChunk;
+        const uint32_t* cp = crcpart + wd.crc0;
         uint32_t wc = crc_combine_uniform(ct, nfull, unit, [&](uint64_t i) { return cp[i]; }, sh_red);
         if (threadIdx.x == 0) {
             if (rem) wc = crc_shift_bytes(ct, wc, rem) ^ cp[nfull];

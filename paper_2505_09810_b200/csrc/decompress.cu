@@ -297,7 +297,7 @@ __device__ __forceinline__ uint32_t step1(const DecSmem& s, uint32_t win, uint32
 // one 32-bit window (two word reads + funnel shift), one table lookup, up to
 // three symbols.
 template <bool EMIT, bool STAGED>
-__device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32_t lim, uint32_t p0, int bm,
+__device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32_t lim, uint32_t p0, int bm,
                                 uint32_t& count, uint8_t* dst, uint32_t* hit) {
     // Lanes decode different chunks with different trip counts: every loop is
     // driven by a warp vote so the warp re-converges each iteration (instead of
@@ -404,29 +404,52 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
     uint64_t acc = 0;
     uint32_t nacc = 0;
     bool act = !bad && !done && pos + kLut <= lim;
+    // bulk: up to three symbols per table lookup, two lookups per vote; the
+    // staged payload is read through a 64-bit register bit buffer
+    uint64_t bbuf = 0;
+    uint32_t bavail = 0, bnj = 0;
+    if (STAGED && act) {
+        const uint32_t a0 = pos + src.sh, j0 = a0 >> 5, r0 = a0 & 31;
+        bbuf = (((uint64_t)src.sw[j0] << 32) | src.sw[j0 + 1]) << r0;
+        bavail = 64 - r0;
+        bnj = j0 + 2;
+    }
+    auto lookup = [&]() {
+        const uint32_t win = STAGED ? (uint32_t)(bbuf >> 32) : src.template peek<STAGED>(pos);
+        const uint32_t e = s.lut3[win >> (32 - kLut)];
+        uint32_t n = e >> 30, tl = (e >> 26) & 15, packed = e & 0xFFFFFF;
+        if (n == 0) {
+            uint32_t sym;
+            tl = step1(s, win, sym);
+            n = 1;
+            packed = sym;
+            bad = tl == 0;
+        }
+        pos += tl;
+        c += n;
+        DBG_ADD(EMIT ? 25 : 26, 1);
+        if (STAGED) {
+            bbuf <<= tl;
+            bavail -= tl;
+            if (bavail < 32) {
+                bbuf |= (uint64_t)src.sw[bnj++] << (32 - bavail);
+                bavail += 32;
+            }
+        }
+        if (EMIT) {
+            acc |= (uint64_t)packed << (8 * nacc);
+            const uint32_t nn = nacc + n;
+            const bool full = nn >= 8;
+            if (full) *w = acc;
+            w += full ? 1 : 0;
+            acc = full ? (nacc ? ((uint64_t)packed >> (8 * (8 - nacc))) : 0ull) : acc;
+            nacc = full ? nn - 8 : nn;
+        }
+    };
     while (__any_sync(mask, act)) {
         if (act) {
-            const uint32_t win = src.template peek<STAGED>(pos);
-            const uint32_t e = s.lut3[win >> (32 - kLut)];
-            uint32_t n = e >> 30, tl = (e >> 26) & 15, packed = e & 0xFFFFFF;
-            if (n == 0) {
-                uint32_t sym;
-                tl = step1(s, win, sym);
-                n = 1;
-                packed = sym;
-                bad = tl == 0;
-            }
-            pos += tl;
-            c += n;
-            if (EMIT) {
-                acc |= (uint64_t)packed << (8 * nacc);
-                const uint32_t nn = nacc + n;
-                const bool full = nn >= 8;
-                if (full) *w = acc;
-                w += full ? 1 : 0;
-                acc = full ? (nacc ? ((uint64_t)packed >> (8 * (8 - nacc))) : 0ull) : acc;
-                nacc = full ? nn - 8 : nn;
-            }
+            lookup();
+            if (!bad && pos + kLut <= lim) lookup();
             act = !bad && pos + kLut <= lim;
         }
     }
@@ -465,7 +488,7 @@ __device__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32
 
 // All passes over the chunks of one record (see huff_decode).
 template <bool STAGED>
-__device__ bool huff_passes(DecSmem& s, const Src& src, uint32_t bits, uint32_t len, uint8_t* dst) {
+__device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t bits, uint32_t len, uint8_t* dst) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t S = (bits + kThreads - 1) / kThreads;
     S = max(128u, (S + 31) & ~31u);

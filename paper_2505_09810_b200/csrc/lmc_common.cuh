@@ -35,6 +35,9 @@ struct WinDesc {
     uint32_t stream;      // owning stream
     uint32_t win_local;   // window index inside the stream
     uint32_t vec;         // 16-byte vector loads allowed (alignment of src/prev/W)
+    uint64_t crc0;        // global index of the window's first CRC chunk (k_crc)
+    uint32_t al16;        // src / prev 16-byte aligned
+    uint32_t pad;
 };
 
 // One stream of the batch.
