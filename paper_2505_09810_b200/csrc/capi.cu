@@ -48,7 +48,7 @@ struct lmcg_ctx {
     bool dec_attr = false;
     int scandec_occ = 1;
     bool crc_attr = false;
-    uint32_t* d_sh496 = nullptr;
+    uint32_t* d_sh992 = nullptr;
     int crc_occ = 1;
     bool enc_attr = false;
     // per-kernel event timing (lmcg_profile)
@@ -295,15 +295,15 @@ lmcg_ctx* lmcg_create(int device) {
     if (cudaMalloc(&ctx->d_crc, sizeof(CrcTables)) == cudaSuccess)
         cudaMemcpy(ctx->d_crc, h, sizeof(CrcTables), cudaMemcpyHostToDevice);
     {
-        // k_crc's 496-byte shift table: [k][b] = (b << 8k) * x^(8 * 496) mod P
+        // k_crc's 992-byte shift table: [k][b] = (b << 8k) * x^(8 * 992) mod P
         uint32_t p = 1u << 31;
-        for (uint64_t nn = 496, k = 3; nn; nn >>= 1, k++)
+        for (uint64_t nn = 992, k = 3; nn; nn >>= 1, k++)
             if (nn & 1) p = h_multmodp(h->x2n[k & 63], p);
         std::vector<uint32_t> t(1024);
         for (int k = 0; k < 4; k++)
             for (uint32_t b = 0; b < 256; b++) t[k * 256 + b] = b ? h_multmodp(p, b << (8 * k)) : 0;
-        if (ctx->d_crc && cudaMalloc(&ctx->d_sh496, 1024 * sizeof(uint32_t)) == cudaSuccess)
-            cudaMemcpy(ctx->d_sh496, t.data(), 1024 * sizeof(uint32_t), cudaMemcpyHostToDevice);
+        if (ctx->d_crc && cudaMalloc(&ctx->d_sh992, 1024 * sizeof(uint32_t)) == cudaSuccess)
+            cudaMemcpy(ctx->d_sh992, t.data(), 1024 * sizeof(uint32_t), cudaMemcpyHostToDevice);
     }
     delete h;
     cudaEventCreateWithFlags(&ctx->pin_done, cudaEventDisableTiming);
@@ -315,7 +315,7 @@ void lmcg_destroy(lmcg_ctx* ctx) {
     if (ctx->d_crc) {
         cudaDeviceSynchronize();
         cudaFree(ctx->d_crc);
-        if (ctx->d_sh496) cudaFree(ctx->d_sh496);
+        if (ctx->d_sh992) cudaFree(ctx->d_sh992);
         if (ctx->ws) cudaFree(ctx->ws);
         if (ctx->dws) cudaFree(ctx->dws);
         if (ctx->hws) cudaFree(ctx->hws);
@@ -431,7 +431,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         const uint64_t need = (ncrc + kWarps - 1) / kWarps;
         PROF(k_crc);
         k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, st>>>(
-            d_wins, nwin, ncrc, ctx->d_crc, ctx->d_sh496, d_crcp);
+            d_wins, nwin, ncrc, ctx->d_crc, ctx->d_sh992, d_crcp);
     }
     if (nb) {
         { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(

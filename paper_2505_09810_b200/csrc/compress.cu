@@ -30,15 +30,18 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
 }
 
 // ------------------------------------------------------------------ CRC
-// Raw CRC-32 of every 8 KiB chunk of every window's element bytes (the
-// payload in original byte order, XOR delta applied), one warp per chunk:
-// lane l folds the contiguous 256 bytes [256 l, 256 (l + 1)) of the chunk
-// byte by byte through a 32-fold replicated table (lane l reads copy l: no
-// bank conflicts), then a 5-level shift tree joins the lanes.  A short last
-// chunk is treated as left-padded with zero bytes, which leave a raw CRC
-// unchanged.  k_frame combines the chunks (stream.py:329).
-constexpr uint32_t kCrcChunk = 8192;
-constexpr size_t kCrcSmem = (size_t)256 * 32 * sizeof(uint32_t);
+// Raw CRC-32 of every 32 KiB chunk of every window's element bytes (the
+// payload in original byte order, XOR delta applied), one warp per chunk.
+// The warp reads 1 KiB rows (lane l: the 32 bytes at 1024 r + 32 l, two
+// 16-byte loads that together cover whole lines) and lane l folds its
+// pieces in order: shift by the 992 bytes of the other lanes' pieces (4
+// lookups), then the piece byte by byte through a 32-fold replicated table
+// (lane l reads copy l: no bank conflicts).  Lane l's value ends 32 (31 - l)
+// bytes before the chunk end: shift and XOR-reduce.  A short last chunk is
+// treated as left-padded with zero bytes, which leave a raw CRC unchanged.
+// k_frame combines the chunks (stream.py:329).
+constexpr uint32_t kCrcChunk = 32768;
+constexpr size_t kCrcSmem = (size_t)(256 * 32 + 1024) * sizeof(uint32_t);
 
 __device__ __forceinline__ uint32_t crc1_word(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
     crc ^= w;
@@ -49,14 +52,16 @@ __device__ __forceinline__ uint32_t crc1_word(const uint32_t* __restrict__ tl, u
 }
 
 __global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wins, int nwin, uint64_t nchunk,
-                                                const CrcTables* __restrict__ ct, const uint32_t* __restrict__ unused,
+                                                const CrcTables* __restrict__ ct, const uint32_t* __restrict__ sh992,
                                                 uint32_t* __restrict__ out) {
     extern __shared__ uint32_t tab[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < 256 * 32; i += kThreads) tab[i] = ct->slice[0][i >> 5];
+    uint32_t* st = tab + 256 * 32;
+    for (int i = tid; i < 1024; i += kThreads) st[i] = sh992[i];
     __syncthreads();
     const uint32_t* tl = tab + lane;
-    constexpr uint32_t kSpan = kCrcChunk / 32;   // 256
+    constexpr uint32_t kRows = kCrcChunk / 1024;
     for (uint64_t c = (uint64_t)blockIdx.x * kWarps + warp; c < nchunk; c += (uint64_t)gridDim.x * kWarps) {
         int lo = 0, hi = nwin;
         while (hi - lo > 1) {
@@ -66,49 +71,63 @@ __global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wi
         const WinDesc wd = wins[lo];
         const uint64_t off = (c - wd.crc0) * kCrcChunk;
         const uint32_t L = (uint32_t)min((uint64_t)kCrcChunk, wd.W - off);
-        const uint32_t Z = kCrcChunk - L;
+        const uint32_t Z = kCrcChunk - L;   // leading zero bytes of the padded chunk
         const uint8_t* src = wd.src + off;
         const uint8_t* prv = wd.prev ? wd.prev + off : nullptr;
-        const uint32_t qa = max(lane * kSpan, Z), qb = (lane + 1) * kSpan;
-        uint32_t crc = 0;
-        if (qa < qb) {
-            uint32_t d = qa - Z;
-            const uint32_t d1 = qb - Z;
-            auto byte_at = [&](uint32_t i) -> uint32_t {
-                uint32_t x = src[i];
-                if (prv) x ^= prv[i];
-                return x;
-            };
-            if (wd.al16) {
-                for (; d < d1 && (d & 15); d++) crc = (crc >> 8) ^ tl[((crc ^ byte_at(d)) & 0xFF) * 32];
-                for (; d + 64 <= d1; d += 64) {
-                    uint4 a[4];
+        const bool vec = wd.al16 && (Z & 15) == 0;
+        // two independent Horner chains per lane (rows [0, 16) and [16, 32))
+        // for instruction-level parallelism
+        auto load_piece = [&](uint32_t r, uint4 a[2]) {
+            const uint32_t pb = 1024 * r + 32 * lane;   // padded offset of this lane's piece
 #pragma unroll
-                    for (int q = 0; q < 4; q++) a[q] = __ldg(reinterpret_cast<const uint4*>(src + d) + q);
+            for (int h = 0; h < 2; h++) {
+                const uint32_t q = pb + 16 * h;
+                a[h] = make_uint4(0, 0, 0, 0);
+                if (q + 16 <= Z) continue;
+                if (vec && q >= Z) {
+                    a[h] = __ldg(reinterpret_cast<const uint4*>(src + (q - Z)));
                     if (prv) {
-#pragma unroll
-                        for (int q = 0; q < 4; q++) {
-                            const uint4 b = __ldg(reinterpret_cast<const uint4*>(prv + d) + q);
-                            a[q].x ^= b.x; a[q].y ^= b.y; a[q].z ^= b.z; a[q].w ^= b.w;
+                        const uint4 b = __ldg(reinterpret_cast<const uint4*>(prv + (q - Z)));
+                        a[h].x ^= b.x; a[h].y ^= b.y; a[h].z ^= b.z; a[h].w ^= b.w;
+                    }
+                } else {
+                    uint32_t v[4] = {0, 0, 0, 0};
+                    for (int i = 0; i < 16; i++) {
+                        if (q + i >= Z) {
+                            uint32_t x = src[q + i - Z];
+                            if (prv) x ^= prv[q + i - Z];
+                            v[i >> 2] |= x << (8 * (i & 3));
                         }
                     }
-#pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        crc = crc1_word(tl, crc, a[q].x);
-                        crc = crc1_word(tl, crc, a[q].y);
-                        crc = crc1_word(tl, crc, a[q].z);
-                        crc = crc1_word(tl, crc, a[q].w);
-                    }
+                    a[h] = make_uint4(v[0], v[1], v[2], v[3]);
                 }
             }
-            for (; d < d1; d++) crc = (crc >> 8) ^ tl[((crc ^ byte_at(d)) & 0xFF) * 32];
+        };
+        auto shift992 = [&](uint32_t x) {
+            return st[x & 0xFF] ^ st[256 + ((x >> 8) & 0xFF)] ^ st[512 + ((x >> 16) & 0xFF)] ^ st[768 + (x >> 24)];
+        };
+        uint32_t ca = 0, cb = 0;
+        constexpr uint32_t kHalf = kRows / 2;
+        for (uint32_t i = 0; i < kHalf; i++) {
+            uint4 a[2], b[2];
+            load_piece(i, a);
+            load_piece(i + kHalf, b);
+            ca = shift992(ca);
+            cb = shift992(cb);
+            ca = crc1_word(tl, ca, a[0].x); cb = crc1_word(tl, cb, b[0].x);
+            ca = crc1_word(tl, ca, a[0].y); cb = crc1_word(tl, cb, b[0].y);
+            ca = crc1_word(tl, ca, a[0].z); cb = crc1_word(tl, cb, b[0].z);
+            ca = crc1_word(tl, ca, a[0].w); cb = crc1_word(tl, cb, b[0].w);
+            ca = crc1_word(tl, ca, a[1].x); cb = crc1_word(tl, cb, b[1].x);
+            ca = crc1_word(tl, ca, a[1].y); cb = crc1_word(tl, cb, b[1].y);
+            ca = crc1_word(tl, ca, a[1].z); cb = crc1_word(tl, cb, b[1].z);
+            ca = crc1_word(tl, ca, a[1].w); cb = crc1_word(tl, cb, b[1].w);
         }
+        // chain a ends 16 rows (16 KiB) before chain b
+        uint32_t crc = crc_shift_tab(&ct->pow2[14][0][0], ca) ^ cb;
+        crc = crc_shift_bytes(ct, crc, 32u * (31 - lane));
 #pragma unroll
-        for (int k2 = 0; k2 < 5; k2++) {
-            const uint32_t other = __shfl_down_sync(0xFFFFFFFFu, crc, 1 << k2);
-            const uint32_t shifted = crc_shift_tab(&ct->pow2[8 + k2][0][0], crc);
-            if ((lane & ((2 << k2) - 1)) == 0) crc = shifted ^ other;
-        }
+        for (int o = 16; o; o >>= 1) crc ^= __shfl_xor_sync(0xFFFFFFFFu, crc, o);
         if (lane == 0) out[c] = crc;
     }
 }
