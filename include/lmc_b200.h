@@ -150,6 +150,13 @@ int lmcg_compress_plan_run(lmcg_ctx* ctx, lmcg_plan* plan, void* d_out, uint64_t
 lmcg_plan* lmcg_decompress_plan_create(lmcg_ctx* ctx, int n, const lmcg_stream_hint* hints, const uint64_t* len_bounds);
 int lmcg_decompress_plan_run(lmcg_ctx* ctx, lmcg_plan* plan, const void* d_base, const uint64_t* d_offsets,
                              const uint64_t* d_lengths, void* d_out, int32_t* d_status, void* cuda_stream);
+/* SM-driven copy of a few bytes (e.g. a plan's stream offsets / lengths) into
+ * page-locked host memory, ordered on cuda_stream: unlike cudaMemcpyAsync it
+ * is not queued behind bulk transfers on the copy engines, so the host can
+ * learn the stream sizes while large copies are in flight.  h_dst must be
+ * pinned (cudaHostAlloc / torch pin_memory). */
+int lmcg_copy_to_host(void* h_dst, const void* d_src, uint64_t bytes, void* cuda_stream);
+
 /* Output bytes a run needs: compress bound / decompressed payload bytes. */
 uint64_t lmcg_plan_output_bytes(const lmcg_plan* plan);
 void lmcg_plan_destroy(lmcg_plan* plan);

@@ -539,6 +539,16 @@ lmcg_plan* lmcg_compress_plan_create(lmcg_ctx* ctx, const lmcg_tensor* t, int n,
     return pl;
 }
 
+int lmcg_copy_to_host(void* h_dst, const void* d_src, uint64_t bytes, void* cuda_stream) {
+    if ((bytes && (!h_dst || !d_src)) || bytes > (1u << 20)) return LMCG_ERR_ARGUMENT;
+    if (!bytes) return LMCG_OK;
+    void* dptr = nullptr;
+    if (cudaHostGetDevicePointer(&dptr, h_dst, 0) != cudaSuccess) return LMCG_ERR_ARGUMENT;
+    k_small_copy<<<1, 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(static_cast<uint8_t*>(dptr),
+                                                                        static_cast<const uint8_t*>(d_src), bytes);
+    return cudaGetLastError() == cudaSuccess ? LMCG_OK : LMCG_ERR_CUDA;
+}
+
 uint64_t lmcg_plan_output_bytes(const lmcg_plan* pl) {
     if (!pl) return 0;
     return pl->kind == 1 ? pl->bound : pl->out_bytes;

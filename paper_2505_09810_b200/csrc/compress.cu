@@ -21,6 +21,12 @@ namespace lmcg {
 
 constexpr int kEncRun = 64;  // k_encode positions per thread per round
 
+// Bytes from device memory into mapped page-locked host memory (by the SMs).
+__global__ void k_small_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, uint64_t n) {
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+}
+
 // ------------------------------------------------------------------ slotmap
 __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* __restrict__ slot2win) {
     int wi = blockIdx.x;

@@ -456,6 +456,20 @@ class CompressPlan:
         n = self.n
         return CompressedBatch(self.out, self.meta[:n], self.meta[max(n, 1): max(n, 1) + n], self.hints)
 
+    def layout_to_host(self, host_meta, stream=None) -> None:
+        """Copy the last run's stream offsets and lengths (2n int64) into the
+        pinned host tensor ``host_meta``, ordered on ``stream`` but written by
+        the SMs (lmcg_copy_to_host), so it does not queue behind bulk copies."""
+        import torch
+
+        st = stream if stream is not None else torch.cuda.current_stream(self.codec.device)
+        n = max(self.n, 1)
+        if host_meta.device.type != "cpu" or not host_meta.is_pinned() or host_meta.numel() * host_meta.element_size() < 16 * n:
+            raise ValueError("host_meta must be a pinned host tensor of at least 2n int64")
+        rc = self.codec.ctx.lib.lmcg_copy_to_host(ctypes.c_void_p(host_meta.data_ptr()), ctypes.c_void_p(self.meta.data_ptr()),
+                                                  16 * n, ctypes.c_void_p(st.cuda_stream))
+        self.codec.ctx.check(rc)
+
     def decompress_plan(self, graph=False) -> "DecompressPlan":
         """A plan decoding this plan's output (exact structure hints)."""
         return DecompressPlan(self.codec, self.hints, self.stream_bounds, graph=graph, source=self)
