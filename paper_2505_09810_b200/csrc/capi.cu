@@ -28,6 +28,8 @@ struct lmcg_ctx {
     uint8_t* pin = nullptr;
     size_t pin_cap = 0;
     cudaEvent_t pin_done = nullptr;
+    cudaStream_t side = nullptr;          // second stream for kernels that overlap the main chain
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     // last compress (block_info)
     uint64_t last_nb = 0;
     const BlockMeta* last_meta = nullptr;
@@ -307,6 +309,9 @@ lmcg_ctx* lmcg_create(int device) {
     }
     delete h;
     cudaEventCreateWithFlags(&ctx->pin_done, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     return ctx;
 }
 
@@ -323,6 +328,9 @@ void lmcg_destroy(lmcg_ctx* ctx) {
         if (ctx->d_out) cudaFree(ctx->d_out);
         if (ctx->pin) cudaFreeHost(ctx->pin);
         if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
+        if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+        if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+        if (ctx->side) cudaStreamDestroy(ctx->side);
     }
     delete ctx;
 }
@@ -418,20 +426,28 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
     CK(cudaMemsetAsync(d_status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     CK(cudaMemsetAsync(d_ctr, 0, 4 * sizeof(uint32_t), st));
     if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win); }
-    if (nslots) {
-        PROF(k_hist_crc);
-        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta);
-    }
-    if (ncrc) {
+    // k_crc only reads the tensors: it runs on the side stream, overlapping
+    // the histogram / codebook / encode chain, and joins before k_frame
+    const bool fork = ncrc && n;
+    if (fork) {
         if (!ctx->crc_attr) {
             CK(cudaFuncSetAttribute(k_crc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem));
             ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kThreads, kCrcSmem);
             ctx->crc_attr = true;
         }
+        CK(cudaEventRecord(ctx->fork_ev, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
         const uint64_t need = (ncrc + kWarps - 1) / kWarps;
-        PROF(k_crc);
-        k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, st>>>(
+        cudaStream_t sst = ctx->side;
+        ProfScope prof_scope_k_crc(ctx, "k_crc", sst);
+        k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, sst>>>(
             d_wins, nwin, ncrc, ctx->d_crc, ctx->d_sh992, d_crcp);
+        CK(cudaEventRecord(ctx->join_ev, sst));
+    }
+
+    if (nslots) {
+        PROF(k_hist_crc);
+        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta);
     }
     if (nb) {
         { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
@@ -441,8 +457,6 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
     { PROF(k_scan); k_scan<<<(unsigned)std::max<uint64_t>(ntiles, 1), kScanThreads, 0, st>>>(d_meta, nb, d_scan, d_status, d_ctr); }
     if (n) {
         { PROF(k_layout); k_layout<<<1, 1024, 0, st>>>(d_streams, n, o->segment_count, d_scan, d_soff, d_slen); }
-        { PROF(k_frame); k_frame<<<n, kThreads, 0, st>>>(d_streams, d_wins, o->block_size, o->segment_count, d_scan, d_crcp,
-                                         ctx->d_crc, d_soff, static_cast<uint8_t*>(d_out)); }
     }
     if (nslots) {
         const size_t smem = (size_t)(kStageWords + kThreads * kSlot) * sizeof(uint32_t);
@@ -454,6 +468,12 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         k_encode<<<(unsigned)nslots, kThreads, smem, st>>>(d_wins, d_slot2win, nslots, o->block_size, o->segment_count,
                                                          d_streams, d_meta, d_wire, d_scan, d_soff,
                                                          static_cast<uint8_t*>(d_out));
+    }
+    if (n) {
+        if (fork) CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
+        PROF(k_frame);
+        k_frame<<<n, kThreads, 0, st>>>(d_streams, d_wins, o->block_size, o->segment_count, d_scan, d_crcp, ctx->d_crc, d_soff,
+                                        static_cast<uint8_t*>(d_out));
     }
     CK(cudaGetLastError());
     ctx->last_nb = nb;
