@@ -133,11 +133,12 @@ def run_reference(args, ws, rank):
 
     cores = os.cpu_count() or 1
     specs = synth.CONFIGS[args.config]()
-    raws = _host_checkpoint(specs, seed=1000)
+    delta = args.config in DELTA
+    raws = _host_checkpoint(specs, seed=1000, delta=delta)
     nbytes = sum(len(r) for r in raws)
     # bounded sample: whole checkpoint when it fits ~60 s of total work
     t0 = time.perf_counter()
-    s = [O.compress(r, 1, threads=cores) for r in raws[:8]]
+    s = [O.compress(r, 1, delta=delta, threads=cores) for r in raws[:8]]
     [O.decompress(x, threads=cores) for x in s]
     probe = time.perf_counter() - t0
     probe_bytes = sum(len(r) for r in raws[:8])
@@ -156,7 +157,7 @@ def run_reference(args, ws, rank):
               f"{sample_bytes / 2**20:.1f} MiB per step (compress + decompress, oracle C port, {cores} threads)")
 
     def step():
-        st = [O.compress(r, 1, threads=cores) for r in raws]
+        st = [O.compress(r, 1, delta=delta, threads=cores) for r in raws]
         for x in st:
             O.decompress(x, threads=cores)
         return st
@@ -173,9 +174,7 @@ def run_reference(args, ws, rank):
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GiB/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.config}: GPT-2-small bf16 checkpoint (148 tensors), every tensor its own "
-                               "LMC1 stream, byte_group=True, block_size=65536, segment_count=1, buffer_size=128MiB",
-                   "sample_tensors": len(raws)},
+        "config": {"workload": workload(args.config), "sample_tensors": len(raws)},
         "compression_ratio": round(ratio, 6),
         "cpu_baseline": {"value": round(value, 4), "unit": "GiB/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": round(value, 4), "unit": "GiB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,8 +182,9 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def _host_checkpoint(specs, seed):
-    """Host bytes of the synthetic checkpoint (generated with torch, CPU or GPU)."""
+def _host_checkpoint(specs, seed, delta=False):
+    """Host bytes of the synthetic checkpoint (generated with torch, CPU or GPU);
+    with delta, the XOR of step t+1 and step t (what a DeltaBuffer holds)."""
     import torch
 
     from paper_2505_09810_b200 import synth
@@ -193,9 +193,31 @@ def _host_checkpoint(specs, seed):
     out = []
     for i, s in enumerate(specs):
         t = synth.make_tensor(s, seed, i, device=dev)
-        out.append(t.view(torch.uint8).reshape(-1).cpu().numpy().tobytes())
-        del t
+        x = t.view(torch.uint8).reshape(-1)
+        if delta:
+            x = x ^ synth.next_step(t, seed, i).view(torch.uint8).reshape(-1)
+        out.append(x.cpu().numpy().tobytes())
+        del t, x
     return out
+
+
+# Workload names of BASELINE.json's configs (bench default: cfg2, the one the
+# metric is quoted on; the others are parity cases and optional bench runs).
+WORKLOAD = {
+    "cfg1": "single bf16 tensor 4096x4096 ~ N(0, 0.02) (32 MiB)",
+    "cfg2": "GPT-2-small bf16 checkpoint (148 tensors, 237.4 MiB)",
+    "cfg3": "RLE-heavy: 8192x8192 bf16 with 50% exact zeros + 1M-element all-zero tensor",
+    "cfg4": "GPT-style 1.3B, two consecutive bf16 steps, XOR delta fused into the compress (2.45 GiB per step; "
+            "the previous step stays resident on the GPU)",
+    "cfg5": "Llama-7B bf16 checkpoint (291 tensors, 12.55 GiB)",
+}
+DELTA = {"cfg4"}
+L2_FLUSH_BELOW = 126_000_000   # bytes: the L2 size (inputs must be larger, or flushed)
+
+
+def workload(cfg: str, nbytes: float | None = None) -> str:
+    return (f"{cfg}: {WORKLOAD[cfg]}, every tensor its own LMC1 stream, byte_group=True, block_size=65536, "
+            "segment_count=1, buffer_size=128MiB")
 
 
 # ----------------------------------------------------------------- ours
@@ -221,12 +243,16 @@ def run_ours(args, ws, rank, local):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     specs, ts = synth.make_checkpoint(args.config, seed=1000 + rank, device="cuda")
+    prev = None
+    if args.config in DELTA:   # compress step t+1 against step t (fused XOR)
+        prev = ts
+        ts = [synth.next_step(w, 1000 + rank, i) for i, w in enumerate(prev)]
     nbytes = sum(t.numel() * t.element_size() for t in ts)
     codec = lmcb.Codec(local)
     stream = torch.cuda.current_stream()
     # The checkpoint's tensors are registered once (CompressPlan): every step
     # re-compresses their current contents.  Runs replay captured CUDA graphs.
-    cplan = codec.compress_plan(ts, graph=not args.no_graph)
+    cplan = codec.compress_plan(ts, prev=prev, graph=not args.no_graph)
     dplan = cplan.decompress_plan(graph=not args.no_graph)
     status_log = torch.zeros((args.steps + args.warmup + 8, len(ts)), dtype=torch.int32, device="cuda")
 
@@ -260,7 +286,10 @@ def run_ours(args, ws, rank, local):
     b, r = step()
     r.raise_for_status()
     for i, t in enumerate(ts):
-        if not torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1)):
+        want = t.view(torch.uint8).reshape(-1)
+        if prev is not None:
+            want = want ^ prev[i].view(torch.uint8).reshape(-1)
+        if not torch.equal(r.payload(i), want):
             raise SystemExit(f"round trip mismatch on {specs[i].name}")
     stream_bytes = b.total_bytes()
     ratio = stream_bytes / nbytes
@@ -271,7 +300,7 @@ def run_ours(args, ws, rank, local):
     codec.ctx.profile(True)
     nprof = 3
     for _ in range(nprof):
-        pb = codec.compress(ts)
+        pb = codec.compress(ts, prev=prev)
         exchange(pb)
         codec.decompress(pb)
     prof = codec.ctx.profile_report()
@@ -287,8 +316,13 @@ def run_ours(args, ws, rank, local):
     sampler.start()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
+    # inputs smaller than the 126 MB L2: flush it between timed steps
+    # (a 512 MB write outside the per-step events) and time the steps alone
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if nbytes < L2_FLUSH_BELOW else None
     start.record(stream)
     for k in range(args.steps):
+        if flush is not None:
+            flush.fill_(k & 0xFF)
         step(evs[k])
     end.record(stream)
     torch.cuda.synchronize()
@@ -300,6 +334,8 @@ def run_ours(args, ws, rank, local):
     total_ms = start.elapsed_time(end)
     comp_ms = sum(e[0].elapsed_time(e[1]) for e in evs)
     dec_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
+    if flush is not None:
+        total_ms = sum(e[0].elapsed_time(e[2]) for e in evs)
     t = torch.tensor([total_ms, comp_ms, dec_ms], dtype=torch.float64, device="cuda")
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -309,7 +345,12 @@ def run_ours(args, ws, rank, local):
     # end-to-end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = measure_e2e(codec, ts, args, ws, dist)
+        # the device-resident plans are done: free them for the e2e buffer sets
+        del cplan, dplan, b, r, pb
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        e2e = measure_e2e(codec, ts, args, ws, dist, prev=prev)
 
     # roofline of the dominant kernel
     peak, peak_src = measured_peaks()
@@ -334,16 +375,15 @@ def run_ours(args, ws, rank, local):
     }
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(ts)
+        cpu = cpu_baseline(ts, prev)
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": "GiB/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.config}: GPT-2-small bf16 checkpoint (148 tensors, "
-                                   f"{nbytes / 2**20:.1f} MiB per rank), every tensor its own LMC1 stream, "
-                                   "byte_group=True, block_size=65536, segment_count=1, buffer_size=128MiB",
-                       "l2": "inputs 249 MB > 126 MB L2 per step; no flush needed",
+            "config": {"workload": workload(args.config),
+                       "l2": (f"inputs {nbytes / 1e6:.0f} MB > 126 MB L2 per step; no flush needed" if flush is None
+                              else f"inputs {nbytes / 1e6:.0f} MB: 512 MB L2 flush between timed steps, steps timed alone"),
                        "parallelism": f"dp{ws} (independent checkpoints per rank + all-gather of stream sizes)"},
             "compression_ratio": round(ratio, 6),
             "pipeline": pipeline,
@@ -359,7 +399,7 @@ def run_ours(args, ws, rank, local):
         dist.destroy_process_group()
 
 
-def measure_e2e(codec, ts, args, ws, dist):
+def measure_e2e(codec, ts, args, ws, dist, prev=None):
     """Round trip through the public plan API with pinned host buffers, every
     step: H2D of the checkpoint into the registered tensors, CompressPlan.run,
     D2H of the streams; H2D of the streams, DecompressPlan.run, D2H of the
@@ -389,10 +429,15 @@ def measure_e2e(codec, ts, args, ws, dist):
     for _ in range(2):
         dev_all = torch.empty(pos, dtype=torch.uint8, device="cuda")
         dev_in = [dev_all[o:o + t.numel() * t.element_size()].view(t.dtype).view(t.shape) for t, o in zip(ts, offs)]
-        cp = codec.compress_plan(dev_in, graph=True)
+        cp = codec.compress_plan(dev_in, prev=prev, graph=True)
         # the streams come back from the host into `ret`; the decompress plan's
         # graph decodes ret with the layout in `ret_meta`
         ret = types.SimpleNamespace(out=torch.empty_like(cp.out), meta=torch.empty_like(cp.meta))
+        for t, o in zip(ts, offs):   # valid streams in ret before the plan's warm-up run
+            dev_all[o:o + t.numel() * t.element_size()].copy_(t.view(torch.uint8).reshape(-1))
+        cp.run()
+        ret.out.copy_(cp.out)
+        ret.meta.copy_(cp.meta)
         dp = lmcb.DecompressPlan(codec, cp.hints, cp.stream_bounds, graph=True, source=ret)
         sets.append({
             "dev_all": dev_all, "cp": cp, "dp": dp, "ret": ret,
@@ -496,7 +541,8 @@ def measure_e2e(codec, ts, args, ws, dist):
     S = sets[(args.steps - 1) % 2]
     for i, h in enumerate(host):
         o = S["dp"].offsets[i]
-        if not torch.equal(S["host_out"][o:o + h.numel()], h):
+        want = h if prev is None else h ^ prev[i].view(torch.uint8).reshape(-1).cpu()
+        if not torch.equal(S["host_out"][o:o + h.numel()], want):
             raise SystemExit("e2e round trip mismatch")
     if trace:
         for b, S in enumerate(sets):
@@ -513,19 +559,28 @@ def measure_e2e(codec, ts, args, ws, dist):
                     "D2H streams"}
 
 
-def cpu_baseline(ts):
+def cpu_baseline(ts, prev=None):
     """Oracle (C port of the reference algorithm) on the host cores, bounded sample."""
     import torch
 
     from oracle import oracle as O
 
     cores = os.cpu_count() or 1
-    raws = [t.view(torch.uint8).reshape(-1).cpu().numpy().tobytes() for t in ts[2:26]]  # layers 0-1
-    nb = sum(len(r) for r in raws)
+    raws, nb = [], 0
+    order = list(range(2, len(ts))) + [0, 1] if len(ts) > 8 else list(range(len(ts)))  # skip embeddings first
+    for i in order:
+        x = ts[i].view(torch.uint8).reshape(-1)
+        if prev is not None:
+            x = x ^ prev[i].view(torch.uint8).reshape(-1)
+        raws.append(x.cpu().numpy().tobytes())
+        nb += len(raws[-1])
+        if nb >= 24 << 20:
+            break
+    delta = prev is not None
     t0 = time.perf_counter()
     reps = 0
     while True:
-        st = [O.compress(r, 1, threads=cores) for r in raws]
+        st = [O.compress(r, 1, delta=delta, threads=cores) for r in raws]
         for x in st:
             O.decompress(x, threads=cores)
         reps += 1
@@ -533,7 +588,7 @@ def cpu_baseline(ts):
             break
     dt = time.perf_counter() - t0
     return {"value": round(nb * reps / dt / GIB, 4), "unit": "GiB/s", "cores": cores, "kind": "port",
-            "sample": f"GPT-2 layers 0-1 (24 tensors, {nb / 2**20:.1f} MiB) compress+decompress x{reps} "
+            "sample": f"{len(raws)} tensors of the checkpoint ({nb / 2**20:.1f} MiB) compress+decompress x{reps} "
                       f"with the C oracle port, {cores} threads"}
 
 

@@ -818,6 +818,8 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     }
     if (nrec) {
         { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, nseg, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
+        { PROF(k_resolve); k_resolve<<<(unsigned)std::min<uint64_t>(nseg, 148 * 2), kThreads, 0, st>>>(
+            d_seg, nseg, d_cand, d_ccnt, d_cpre, d_scnt, d_sfail, d_rpos, d_rnext); }
         PROF(k_decrec);
         k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, nseg, nrec, d_sfail, d_rpos, d_scr);
     }

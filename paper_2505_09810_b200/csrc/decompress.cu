@@ -802,6 +802,20 @@ __device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint6
     uint32_t mode, l;
     uint64_t ps;
     if (!rec_size_dev(seg, comp, pos, mode, l, ps)) return false;
+    if (mode == MODE_HUFFMAN) {
+        // what an encoder writes: a non-empty bit stream smaller than the
+        // stored record (stream.py:173) and a codebook within the Kraft bound
+        // (huffman.py:191-210); byte runs inside payloads rarely pass both
+        const uint32_t bits = rd32(seg + pos + 5 + 128);
+        if (bits == 0 || kHuffOverhead + ((uint64_t)bits + 7) / 8 > B) return false;
+        uint32_t kraft = 0;
+        const uint8_t* cb = seg + pos + 5;
+        for (int i = 0; i < 128; i++) {
+            const uint32_t v = cb[i], a = v & 15, b2 = v >> 4;
+            kraft += (a ? 1u << (kMaxLen - a) : 0u) + (b2 ? 1u << (kMaxLen - b2) : 0u);
+        }
+        if (kraft == 0 || kraft > (1u << kMaxLen)) return false;
+    }
     const uint64_t q = pos + 5 + ps;
     if (q == comp) return true;
     if (q + 5 > comp || seg[q] > 2) return false;
@@ -813,8 +827,10 @@ __device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint6
 // coalesced 16-byte loads: the little-endian block size has exactly one
 // non-zero byte (at offset 1 + kb of a record header), so anchors are the
 // bytes equal to it, compared 4 at a time with __vcmpeq4.  Appends the
-// candidates in increasing order to list[0..*cnt); returns false on overflow.
-__device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* list, uint32_t* cnt, int lane) {
+// candidates in increasing order: emit(position, rank) with ranks counted
+// from cnt (warp-uniform, updated); false if a lane overflowed its buffer.
+template <class Emit>
+__device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t& cnt, int lane, Emit emit) {
     const uint32_t B = sg.block;
     const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(sg.nrec - 1) * B);
     const int kb = (__ffs(B) - 1) >> 3;
@@ -897,21 +913,16 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t* 
             uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
             if (lane >= o) incl += y;
         }
-        const uint32_t base = *cnt + incl - kk;
-        for (uint32_t i = 0; i < kk; i++)
-            if (base + i < 64) list[base + i] = found[i];
-        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        __syncwarp();
-        if (lane == 0) *cnt += tot;
-        __syncwarp();
-        if (*cnt > 64) ok = false;
+        const uint32_t base = cnt + incl - kk;
+        for (uint32_t i = 0; i < kk; i++) emit(found[i], base + i);
+        cnt += __shfl_sync(0xFFFFFFFFu, incl, 31);
       }
     }
     return __all_sync(0xFFFFFFFFu, ok);
 }
 
-constexpr uint32_t kSpanCap = 64;                  // candidates per 8 KiB span
-constexpr uint32_t kDense = 0xFFFFFFFFu;            // span overflowed its list
+constexpr uint32_t kSpanCap = 64;                  // candidates listed per 8 KiB span (more: k_assign rescans)
+constexpr uint32_t kDense = 0xFFFFFFFFu;            // a lane overflowed: the serial path takes the segment
 
 // CTA per 64 KiB chunk slot of segment payload, warp per 8 KiB span: the
 // candidate record headers of the span, in increasing order, into
@@ -939,19 +950,16 @@ __global__ void __launch_bounds__(kThreads) k_cand(const DecSeg* __restrict__ se
     const uint64_t c0 = (t - sg.chunk0) * kChunk, c1 = min(c0 + kChunk, sg.comp);
     const uint64_t pa = c0 + warp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
     uint32_t* list = cand + span * kSpanCap;
-    if (lane == 0) {
-        wcnt[warp] = 0;
-        if (pa == 0 && pa < pe) {  // the segment start is always a record start
-            list[0] = 0;
-            wcnt[warp] = 1;
-        }
+    uint32_t n = 0;
+    if (pa == 0 && pa < pe) {  // the segment start is always a record start
+        if (lane == 0) list[0] = 0;
+        n = 1;
     }
-    __syncwarp();
     bool ok = true;
-    if (pa < pe) ok = warp_scan(sg, pa, pe, list, &wcnt[warp], lane);
+    if (pa < pe) ok = warp_scan(sg, pa, pe, n, lane, [&](uint64_t p, uint32_t r) { if (r < kSpanCap) list[r] = (uint32_t)p; });
     if (lane == 0) {
-        ccnt[span] = ok ? wcnt[warp] : kDense;
-        if (!ok) wcnt[warp] = kDense;
+        ccnt[span] = ok ? n : kDense;
+        wcnt[warp] = ok ? n : kDense;
     }
     __syncthreads();
     if (tid == 0) {
@@ -1036,10 +1044,9 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
     const uint32_t c = ccnt[span];
     const uint32_t R = sg.nrec, B = sg.block;
     const uint32_t Ltail = R ? (uint32_t)(sg.orig - (uint64_t)(R - 1) * B) : 0;
-    for (uint32_t k = lane; k < c; k += 32) {
-        uint64_t pos = cand[span * kSpanCap + k];
+    auto assign = [&](uint64_t pos, uint32_t k) {
         uint32_t r = spre[warp] + k;
-        if (r >= R) { atomicOr(&seg_fail[lo], 1u); break; }
+        if (r >= R) { atomicOr(&seg_fail[lo], 1u); return; }
         for (int part = 0; part < 2; part++) {
             uint32_t mode = 0, l = 0;
             uint64_t ps = 0;
@@ -1051,6 +1058,20 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
             pos += 5 + ps;
             r = R - 1;
         }
+    };
+    if (c <= kSpanCap) {
+        for (uint32_t k = lane; k < c; k += 32) assign(cand[span * kSpanCap + k], k);
+    } else {
+        // dense span (e.g. runs of 6-byte RLE records): enumerate it again
+        constexpr uint64_t kWarpSpan = kChunk / kWarps;
+        const uint64_t c0 = (t - sg.chunk0) * kChunk, c1 = min(c0 + kChunk, sg.comp);
+        const uint64_t pa = c0 + warp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
+        uint32_t n = 0;
+        if (pa == 0 && pa < pe) {
+            if (lane == 0) assign(0, 0);
+            n = 1;
+        }
+        if (pa < pe) warp_scan(sg, pa, pe, n, lane, assign);
     }
 }
 
@@ -1109,6 +1130,154 @@ __global__ void k_verify(const DecSeg* __restrict__ segs, uint64_t nseg_total, u
         else ok = nx == sg.comp;
     }
     if (!ok) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(15, 1); }
+}
+
+// ------------------------------------------------------------- k_resolve
+// CTA per segment that failed verification (false candidates: header-like
+// bytes inside payloads whose successor test also passed).  The true records
+// are exactly the path that starts at candidate 0 (the segment start) and
+// follows each record's size: gather the segment's candidates in position
+// order, link each to the candidate (or tail record, or segment end) its
+// header points to, mark the path from 0 by pointer doubling (log2 m rounds),
+// and rank the marked ones.  A consistent path (R records ending at the
+// segment end) clears the failure; anything else stays with k_fallback.
+constexpr int kResMax = 4096;   // candidates per segment resolvable in shared memory
+
+__global__ void __launch_bounds__(kThreads) k_resolve(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+                                                    const uint32_t* __restrict__ cand, const uint32_t* __restrict__ ccnt,
+                                                    const uint32_t* __restrict__ cpre, const uint32_t* __restrict__ seg_cnt,
+                                                    uint32_t* __restrict__ seg_fail, uint64_t* __restrict__ rec_pos,
+                                                    uint64_t* __restrict__ rec_next) {
+    __shared__ uint32_t ps[kResMax];          // candidate positions
+    __shared__ int16_t nx[2][kResMax];        // successor index (kEnd / kTail / -1)
+    __shared__ uint8_t mark[kResMax + 1];
+    __shared__ uint32_t wsum[kWarps];
+    __shared__ int sh_ok;
+    constexpr int16_t kEnd = 0x7FFF, kTail = 0x7FFE, kBad = -1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (uint64_t si = blockIdx.x; si < nseg_total; si += gridDim.x) {
+        if (!seg_fail[si]) continue;
+        const DecSeg sg = segs[si];
+        const uint32_t m = seg_cnt[si];
+        const uint32_t R = sg.nrec, B = sg.block;
+        if (m == 0 || m > kResMax || R == 0) continue;
+        const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(R - 1) * B);
+        if (tid == 0) sh_ok = 1;
+        __syncthreads();
+        // gather (warp per chunk, spans in order)
+        for (uint32_t cj = warp; cj < sg.nchunk; cj += kWarps) {
+            const uint64_t t = sg.chunk0 + cj;
+            uint32_t base = cpre[t];
+            for (int w = 0; w < kWarps; w++) {
+                const uint64_t span = t * kWarps + w;
+                const uint32_t c = ccnt[span];
+                if (c == kDense) { if (lane == 0) sh_ok = 0; break; }
+                if (c <= kSpanCap) {
+                    for (uint32_t k = lane; k < c; k += 32) ps[base + k] = cand[span * kSpanCap + k];
+                } else {
+                    constexpr uint64_t kWarpSpan = kChunk / kWarps;
+                    const uint64_t c0 = cj * (uint64_t)kChunk, c1 = min(c0 + kChunk, sg.comp);
+                    const uint64_t pa = c0 + w * kWarpSpan, pe = min(pa + kWarpSpan, c1);
+                    uint32_t n = 0;
+                    if (pa == 0 && pa < pe) { if (lane == 0) ps[base] = 0; n = 1; }
+                    if (pa < pe) warp_scan(sg, pa, pe, n, lane, [&](uint64_t p, uint32_t r) { ps[base + r] = (uint32_t)p; });
+                }
+                base += c;
+            }
+        }
+        __syncthreads();
+        if (!sh_ok || ps[0] != 0) { __syncthreads(); continue; }
+        // links
+        for (uint32_t i = tid; i < m; i += kThreads) {
+            int16_t v = kBad;
+            uint32_t mode, l;
+            uint64_t psz;
+            if (rec_size(sg.base, sg.comp, ps[i], mode, l, psz) && (l == B || l == Ltail)) {
+                const uint64_t q = ps[i] + 5 + psz;
+                if (q == sg.comp) v = kEnd;
+                else {
+                    uint32_t lo = 0, hi = m;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (ps[mid] < q) lo = mid + 1; else hi = mid;
+                    }
+                    if (lo < m && ps[lo] == q) v = (int16_t)lo;
+                    else if (Ltail != B) {   // the tail record is not a candidate
+                        uint32_t m2, l2;
+                        uint64_t p2;
+                        if (rec_size(sg.base, sg.comp, q, m2, l2, p2) && l2 == Ltail && q + 5 + p2 == sg.comp) v = kTail;
+                    }
+                }
+            }
+            nx[0][i] = v;
+            mark[i] = i == 0;
+        }
+        if (tid == 0) mark[kResMax] = 0;
+        __syncthreads();
+        int cur = 0;
+        for (uint32_t span = 1; span <= m + 1; span <<= 1) {
+            for (uint32_t i = tid; i < m; i += kThreads) {
+                const int16_t j = nx[cur][i];
+                if (mark[i] && j >= 0 && j < (int16_t)m) mark[j] = 1;
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < m; i += kThreads) {
+                const int16_t j = nx[cur][i];
+                nx[cur ^ 1][i] = (j >= 0 && j < (int16_t)m) ? nx[cur][j] : j;
+            }
+            cur ^= 1;
+            __syncthreads();
+        }
+        // rank the marked candidates; rebuild their links from the headers
+        uint32_t cnt = 0;
+        const uint32_t per = (m + kThreads - 1) / kThreads;
+        const uint32_t i0 = tid * per, i1 = min(m, i0 + per);
+        for (uint32_t i = i0; i < i1; i++) cnt += mark[i];
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        uint32_t pre = 0, tot = 0;
+        for (int w = 0; w < kWarps; w++) { if (w < warp) pre += wsum[w]; tot += wsum[w]; }
+        pre += incl - cnt;
+        const bool has_tail = Ltail != B;
+        if (tot + (has_tail ? 1u : 0u) != R) { __syncthreads(); continue; }
+        bool bad = false;
+        const uint32_t nlast = tot - 1;   // rank of the last candidate record on the path
+        for (uint32_t i = i0; i < i1; i++) {
+            if (!mark[i]) continue;
+            uint32_t mode, l;
+            uint64_t psz;
+            const uint64_t p = ps[i];
+            rec_size(sg.base, sg.comp, p, mode, l, psz);
+            const uint32_t r = pre++;
+            const uint64_t q = p + 5 + psz;
+            rec_pos[sg.rec0 + r] = p;
+            rec_next[sg.rec0 + r] = q;
+            if (l != ((r + 1 == R) ? Ltail : B)) bad = true;
+            if (r == nlast) {
+                if (!has_tail) {
+                    if (q != sg.comp) bad = true;
+                } else {
+                    uint32_t m2, l2;
+                    uint64_t p2;
+                    if (rec_size(sg.base, sg.comp, q, m2, l2, p2) && l2 == Ltail && q + 5 + p2 == sg.comp) {
+                        rec_pos[sg.rec0 + R - 1] = q;
+                        rec_next[sg.rec0 + R - 1] = q + 5 + p2;
+                    } else {
+                        bad = true;
+                    }
+                }
+            }
+        }
+        bad = __syncthreads_or(bad);
+        if (tid == 0 && !bad) seg_fail[si] = 0;
+        __syncthreads();
+    }
 }
 
 // ------------------------------------------------------------- k_fallback
