@@ -157,6 +157,12 @@ int lmcg_decompress_plan_run(lmcg_ctx* ctx, lmcg_plan* plan, const void* d_base,
  * pinned (cudaHostAlloc / torch pin_memory). */
 int lmcg_copy_to_host(void* h_dst, const void* d_src, uint64_t bytes, void* cuda_stream);
 
+/* Diagnostics: segments decoded by the serial fallback walk (stream.py:234-268
+ * restated on the device) since the last reset, across all contexts of the
+ * process (synchronises the device).  Well-formed streams stay on the
+ * parallel path; corrupt ones end there to report the reference's error. */
+uint64_t lmcg_fallback_segments(int reset);
+
 /* Output bytes a run needs: compress bound / decompressed payload bytes. */
 uint64_t lmcg_plan_output_bytes(const lmcg_plan* plan);
 void lmcg_plan_destroy(lmcg_plan* plan);

@@ -50,6 +50,7 @@ struct lmcg_ctx {
     bool dec_attr = false;
     int scandec_occ = 1;
     bool crc_attr = false;
+    bool res_attr = false;
     uint32_t* d_sh992 = nullptr;
     int crc_occ = 1;
     bool enc_attr = false;
@@ -569,6 +570,17 @@ int lmcg_copy_to_host(void* h_dst, const void* d_src, uint64_t bytes, void* cuda
     return cudaGetLastError() == cudaSuccess ? LMCG_OK : LMCG_ERR_CUDA;
 }
 
+uint64_t lmcg_fallback_segments(int reset) {
+    unsigned long long v = 0;
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(&v, lmcg::lmcg_fallback_segs, sizeof(v));
+    if (reset) {
+        const unsigned long long z = 0;
+        cudaMemcpyToSymbol(lmcg::lmcg_fallback_segs, &z, sizeof(z));
+    }
+    return v;
+}
+
 uint64_t lmcg_plan_output_bytes(const lmcg_plan* pl) {
     if (!pl) return 0;
     return pl->kind == 1 ? pl->bound : pl->out_bytes;
@@ -818,7 +830,11 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     }
     if (nrec) {
         { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, nseg, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
-        { PROF(k_resolve); k_resolve<<<(unsigned)std::min<uint64_t>(nseg, 148 * 2), kThreads, 0, st>>>(
+        if (!ctx->res_attr) {
+            CK(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResSmem));
+            ctx->res_attr = true;
+        }
+        { PROF(k_resolve); k_resolve<<<(unsigned)std::min<uint64_t>(nseg, 148 * 2), kThreads, kResSmem, st>>>(
             d_seg, nseg, d_cand, d_ccnt, d_cpre, d_scnt, d_sfail, d_rpos, d_rnext); }
         PROF(k_decrec);
         k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, nseg, nrec, d_sfail, d_rpos, d_scr);

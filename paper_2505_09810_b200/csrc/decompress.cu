@@ -44,6 +44,11 @@ __device__ unsigned long long lmcg_dbg_ev[4096];   // 512 events x 8 words
 #define DBG_TADD(i, var) ((void)0)
 #endif
 
+// segments the serial path (k_fallback) walked since the last reset
+// (lmcg_fallback_segments): streams this library or the reference wrote
+// decode on the parallel path; tests assert that it stays there.
+__device__ unsigned long long lmcg_fallback_segs;
+
 enum : uint32_t { ST_CORRUPT = 1, ST_INTEGRITY = 2, ST_UNSUPPORTED = 4, ST_RETRY = 8, ST_CAPACITY = 16 };
 
 struct DecStreamIn {
@@ -829,6 +834,8 @@ __device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint6
 // bytes equal to it, compared 4 at a time with __vcmpeq4.  Appends the
 // candidates in increasing order: emit(position, rank) with ranks counted
 // from cnt (warp-uniform, updated); false if a lane overflowed its buffer.
+constexpr int kLaneCand = 8;   // candidates per lane per 16 bytes (6-byte RLE records: true + offset-3 echoes)
+
 template <class Emit>
 __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t& cnt, int lane, Emit emit) {
     const uint32_t B = sg.block;
@@ -893,20 +900,20 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t& 
                 }
             }
         }
-        uint32_t found[4];
+        uint32_t found[kLaneCand];
         uint32_t k = 0;
         while (cm) {
             const int j = __ffs(cm) - 1;
             cm &= cm - 1;
             const uint64_t p = g + j - reinterpret_cast<uint64_t>(b);
             if (p + 1 + kb >= qa && p + 1 + kb < qe && is_cand(b, sg.comp, p, B, Ltail)) {
-                if (k < 4) found[k] = (uint32_t)p;
+                if (k < kLaneCand) found[k] = (uint32_t)p;
                 k++;
             }
         }
         if (!__any_sync(0xFFFFFFFFu, k != 0)) continue;
-        if (k > 4) ok = false;
-        const uint32_t kk = min(k, 4u);
+        if (k > kLaneCand) ok = false;
+        const uint32_t kk = min(k, (uint32_t)kLaneCand);
         uint32_t incl = kk;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -1003,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads) k_number(const DecSeg* __restrict__ 
         bad = __syncthreads_or(bad);
         if (tid == 0) {
             seg_cnt[si] = carry;
-            if (bad) seg_fail[si] = 1;
+            if (bad) { seg_fail[si] = 1; DBG_ADD(12, 1); }
         }
     }
 }
@@ -1046,14 +1053,14 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
     const uint32_t Ltail = R ? (uint32_t)(sg.orig - (uint64_t)(R - 1) * B) : 0;
     auto assign = [&](uint64_t pos, uint32_t k) {
         uint32_t r = spre[warp] + k;
-        if (r >= R) { atomicOr(&seg_fail[lo], 1u); return; }
+        if (r >= R) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(13, 1); return; }
         for (int part = 0; part < 2; part++) {
             uint32_t mode = 0, l = 0;
             uint64_t ps = 0;
             const bool rok = rec_size(sg.base, sg.comp, pos, mode, l, ps) && l == ((r + 1 == R) ? Ltail : B);
             rec_pos[sg.rec0 + r] = pos;
             rec_next[sg.rec0 + r] = rok ? pos + 5 + ps : ~0ull;
-            if (!rok) atomicOr(&seg_fail[lo], 1u);
+            if (!rok) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(14, 1); }
             if (!(rok && part == 0 && r + 2 == R && Ltail != B)) break;
             pos += 5 + ps;
             r = R - 1;
@@ -1097,7 +1104,7 @@ __global__ void __launch_bounds__(kThreads) k_decrec(const DecSeg* __restrict__ 
     const uint8_t* rec = sg.base + rec_pos[g];
     const uint32_t mode = rec[0], len = rd32(rec + 1);
     const bool ok = decode_record(s, rec, mode, len, scratch + sg.goff + (uint64_t)r * sg.block);
-    if (!ok && threadIdx.x == 0) atomicOr(&seg_fail[lo], 1u);
+    if (!ok && threadIdx.x == 0) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(16, 1); }
 }
 
 // --------------------------------------------------------------- k_verify
@@ -1141,16 +1148,18 @@ __global__ void k_verify(const DecSeg* __restrict__ segs, uint64_t nseg_total, u
 // header points to, mark the path from 0 by pointer doubling (log2 m rounds),
 // and rank the marked ones.  A consistent path (R records ending at the
 // segment end) clears the failure; anything else stays with k_fallback.
-constexpr int kResMax = 4096;   // candidates per segment resolvable in shared memory
+constexpr int kResMax = 8192;   // candidates per segment resolvable in shared memory
+constexpr size_t kResSmem = (size_t)kResMax * (4 + 2 + 2 + 1) + 16;
 
 __global__ void __launch_bounds__(kThreads) k_resolve(const DecSeg* __restrict__ segs, uint64_t nseg_total,
                                                     const uint32_t* __restrict__ cand, const uint32_t* __restrict__ ccnt,
                                                     const uint32_t* __restrict__ cpre, const uint32_t* __restrict__ seg_cnt,
                                                     uint32_t* __restrict__ seg_fail, uint64_t* __restrict__ rec_pos,
                                                     uint64_t* __restrict__ rec_next) {
-    __shared__ uint32_t ps[kResMax];          // candidate positions
-    __shared__ int16_t nx[2][kResMax];        // successor index (kEnd / kTail / -1)
-    __shared__ uint8_t mark[kResMax + 1];
+    extern __shared__ __align__(16) uint8_t res_smem[];
+    uint32_t* ps = reinterpret_cast<uint32_t*>(res_smem);                         // candidate positions
+    int16_t (*nx)[kResMax] = reinterpret_cast<int16_t (*)[kResMax]>(ps + kResMax);  // successor index (kEnd / kTail / -1)
+    uint8_t* mark = reinterpret_cast<uint8_t*>(nx[2]);
     __shared__ uint32_t wsum[kWarps];
     __shared__ int sh_ok;
     constexpr int16_t kEnd = 0x7FFF, kTail = 0x7FFE, kBad = -1;
@@ -1276,6 +1285,7 @@ __global__ void __launch_bounds__(kThreads) k_resolve(const DecSeg* __restrict__
         }
         bad = __syncthreads_or(bad);
         if (tid == 0 && !bad) seg_fail[si] = 0;
+        if (tid == 0) DBG_ADD(bad ? 10 : 9, 1);
         __syncthreads();
     }
 }
@@ -1293,6 +1303,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
     for (uint64_t si = blockIdx.x; si < nseg_total; si += gridDim.x) {
         if (!seg_fail[si]) continue;
         DBG_ADD(11, threadIdx.x == 0);
+        if (threadIdx.x == 0) atomicAdd(&lmcg_fallback_segs, 1ull);
         const DecSeg sg = segs[si];
         if (threadIdx.x == 0) { sh_pos = 0; sh_got = 0; }
         __syncthreads();

@@ -22,6 +22,11 @@ def codec():
     return lmcb.Codec()
 
 
+def fallback_segments(codec) -> int:
+    """Segments the serial fallback walked since the last call (resets)."""
+    return int(codec.ctx.lib.lmcg_fallback_segments(1))
+
+
 def dev_bytes(b: bytes):
     if not b:
         return torch.empty(0, dtype=torch.uint8, device="cuda")
@@ -45,8 +50,10 @@ def test_golden_stream_bytes(codec, case):
 @pytest.mark.parametrize("case", load_golden_streams(), ids=lambda c: c[0]["name"])
 def test_golden_stream_decode(codec, case):
     m, data, stream = case
+    fallback_segments(codec)
     r = codec.decompress([dev_bytes(stream)])
     assert r.status == [0]
+    assert fallback_segments(codec) == 0   # reference streams decode on the parallel path
     assert r.lengths[0] == len(data)
     assert host_bytes(r.payload(0)) == data
     assert r.element_types[0] == m["element_type"]
@@ -100,8 +107,10 @@ def test_cfg1_full_parity(codec):
     assert (info["bits"][huff] == bits[huff]).all()
     assert (info["lengths"][huff] == lengths[huff]).all()
     assert pm.sum() > 0  # package-merge blocks are part of this config
+    fallback_segments(codec)
     r = codec.decompress(b)
     assert r.status == [0]
+    assert fallback_segments(codec) == 0
     assert torch.equal(r.payload(0), ts[0].view(torch.uint8).reshape(-1))
 
 
@@ -113,8 +122,10 @@ def test_cfg2_gpt2_small_parity(codec):
     want = _oracle_streams(ts, [1] * len(ts))
     assert [len(x) for x in got] == [len(x) for x in want]
     assert got == want
+    fallback_segments(codec)
     r = codec.decompress(b)
     assert r.status == [0] * len(ts)
+    assert fallback_segments(codec) == 0
     for i, t in enumerate(ts):
         assert torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1)), specs[i].name
 
@@ -126,8 +137,10 @@ def test_cfg3_rle_heavy_parity(codec):
     want = _oracle_streams(ts, [1, 1])
     assert got == want
     assert len(got[1]) == 236  # 28 + 16 + 32 x 6-byte RLE records
+    fallback_segments(codec)
     r = codec.decompress(b)
     assert r.status == [0, 0]
+    assert fallback_segments(codec) == 0
     for i, t in enumerate(ts):
         assert torch.equal(r.payload(i), t.view(torch.uint8).reshape(-1))
 
@@ -141,8 +154,10 @@ def test_cfg4_delta_fused_xor_parity(codec):
     xors = [(p.view(torch.uint8) ^ q.view(torch.uint8)).reshape(-1) for p, q in zip(prev, nxt)]
     want = [O.compress(host_bytes(x), 1, delta=True, threads=8) for x in xors]
     assert got == want
+    fallback_segments(codec)
     r = codec.decompress(b)
     assert r.status == [0] * len(nxt)
+    assert fallback_segments(codec) == 0   # false candidates in delta payloads are resolved
     for i, x in enumerate(xors):
         assert torch.equal(r.payload(i), x)
 
