@@ -108,6 +108,21 @@ typedef struct {
     uint64_t windows;
 } lmcg_stream_hint;
 
+/* One part of a stream compressed on several GPUs (a tensor
+ * larger than a rank's fair share is split by block range).  The records of
+ * blocks [blk_begin, blk_end) of the tensor's stream (global record order:
+ * windows in turn, each window's blocks in grouped order) are written back to
+ * back into d_out and their sizes into d_rec_sizes (u32 each); the raw CRC-32
+ * (no pre/post inversion) of the element bytes [crc_begin, crc_end) of the
+ * payload (XOR delta applied) goes to *d_crc.  With every rank's sizes and
+ * CRCs all-gathered, paper_2505_09810_b200.shard assembles the 28-byte header
+ * (CRC combined), the segment tables (stream.py:271-284, 344-355) and the
+ * records into the stream lmcg_compress writes, byte for byte.  Same
+ * compression path as lmcg_compress (stream.py:161-187, huffman.py:79-255). */
+int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* tensor, const lmcg_options* opts, uint64_t blk_begin,
+                       uint64_t blk_end, void* d_out, uint64_t out_capacity, uint32_t* d_rec_sizes, uint64_t crc_begin,
+                       uint64_t crc_end, uint32_t* d_crc, void* cuda_stream);
+
 /* Exact hints for n device streams: validates headers and segment tables on
  * the device (nothing is decoded) and reports their structure (synchronises).
  * Streams the walk rejects get all-zero hints; lmcg_decompress then reports

@@ -52,7 +52,7 @@ EXPORTS = [
     "lmcg_compress_bound", "lmcg_compress_workspace", "lmcg_compress", "lmcg_read_hints",
     "lmcg_decompress", "lmcg_decompress_result", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
     "lmcg_block_info", "lmcg_profile", "lmcg_profile_report", "lmcg_compress_plan_create", "lmcg_compress_plan_run",
-    "lmcg_decompress_plan_create", "lmcg_decompress_plan_run", "lmcg_plan_output_bytes", "lmcg_plan_destroy", "lmcg_copy_to_host", "lmcg_fallback_segments",
+    "lmcg_decompress_plan_create", "lmcg_decompress_plan_run", "lmcg_plan_output_bytes", "lmcg_plan_destroy", "lmcg_copy_to_host", "lmcg_fallback_segments", "lmcg_compress_part",
 ]
 
 _lib = None
@@ -111,6 +111,8 @@ def load(path: str = SO_PATH):
         L.lmcg_decompress_plan_create.argtypes = [vp, ctypes.c_int, P(lmcg_stream_hint), P(u64)]
         L.lmcg_decompress_plan_run.restype = ctypes.c_int
         L.lmcg_decompress_plan_run.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp]
+        L.lmcg_compress_part.restype = ctypes.c_int
+        L.lmcg_compress_part.argtypes = [vp, P(lmcg_tensor), P(lmcg_options), u64, u64, vp, u64, vp, u64, u64, vp, vp]
         L.lmcg_fallback_segments.restype = u64
         L.lmcg_fallback_segments.argtypes = [ctypes.c_int]
         L.lmcg_copy_to_host.restype = ctypes.c_int

@@ -50,6 +50,8 @@ struct lmcg_ctx {
     bool dec_attr = false;
     int scandec_occ = 1;
     bool crc_attr = false;
+    uint8_t* part_ws = nullptr;
+    size_t part_ws_cap = 0;
     bool res_attr = false;
     uint32_t* d_sh992 = nullptr;
     int crc_occ = 1;
@@ -322,6 +324,7 @@ void lmcg_destroy(lmcg_ctx* ctx) {
         cudaDeviceSynchronize();
         cudaFree(ctx->d_crc);
         if (ctx->d_sh992) cudaFree(ctx->d_sh992);
+        if (ctx->part_ws) cudaFree(ctx->part_ws);
         if (ctx->ws) cudaFree(ctx->ws);
         if (ctx->dws) cudaFree(ctx->dws);
         if (ctx->hws) cudaFree(ctx->hws);
@@ -407,9 +410,14 @@ static int check_compress_args(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const
 // Kernel sequence of one compress over descriptors already resident on the
 // device (workspace laid out by compress_layout).  No host synchronisation:
 // capturable in a CUDA graph.
+// Part mode (part_out != null, lmcg_compress_part): only blocks [part_lo,
+// part_hi) are compressed, their records land back to back in part_out and
+// their sizes in d_rec_sizes; no header, segment tables or CRC.
 static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t nslots, uint64_t ncrc, uint32_t min_w,
                            const lmcg_options* o, uint8_t* ws, const size_t* offs, void* d_out, uint64_t* d_offsets,
-                           uint64_t* d_lengths, cudaStream_t st) {
+                           uint64_t* d_lengths, cudaStream_t st, uint64_t part_lo = 0, uint64_t part_hi = ~0ull,
+                           uint8_t* part_out = nullptr, uint32_t* d_rec_sizes = nullptr) {
+    const bool part = part_out != nullptr;
     WinDesc* d_wins = reinterpret_cast<WinDesc*>(ws + offs[0]);
     StreamDesc* d_streams = reinterpret_cast<StreamDesc*>(ws + offs[1]);
     uint32_t* d_slot2win = reinterpret_cast<uint32_t*>(ws + offs[2]);
@@ -429,7 +437,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
     if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win); }
     // k_crc only reads the tensors: it runs on the side stream, overlapping
     // the histogram / codebook / encode chain, and joins before k_frame
-    const bool fork = ncrc && n;
+    const bool fork = ncrc && n && !part;
     if (fork) {
         if (!ctx->crc_attr) {
             CK(cudaFuncSetAttribute(k_crc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem));
@@ -448,15 +456,16 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
 
     if (nslots) {
         PROF(k_hist_crc);
-        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta);
+        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta,
+                                                          part ? part_lo : 0, part ? part_hi : ~0ull);
     }
     if (nb) {
         { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
-            d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist); }
+            d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist, part ? part_lo : 0, part ? part_hi : ~0ull); }
         { PROF(k_pkgmerge); k_pkgmerge<<<296, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr); }
     }
     { PROF(k_scan); k_scan<<<(unsigned)std::max<uint64_t>(ntiles, 1), kScanThreads, 0, st>>>(d_meta, nb, d_scan, d_status, d_ctr); }
-    if (n) {
+    if (n && !part) {
         { PROF(k_layout); k_layout<<<1, 1024, 0, st>>>(d_streams, n, o->segment_count, d_scan, d_soff, d_slen); }
     }
     if (nslots) {
@@ -468,9 +477,13 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         PROF(k_encode);
         k_encode<<<(unsigned)nslots, kThreads, smem, st>>>(d_wins, d_slot2win, nslots, o->block_size, o->segment_count,
                                                          d_streams, d_meta, d_wire, d_scan, d_soff,
-                                                         static_cast<uint8_t*>(d_out));
+                                                         part ? part_out : static_cast<uint8_t*>(d_out),
+                                                         part ? part_lo : 0, part ? part_hi : ~0ull);
     }
-    if (n) {
+    if (part) {
+        if (part_hi > part_lo)
+            k_recsizes<<<(unsigned)((part_hi - part_lo + 255) / 256), 256, 0, st>>>(d_meta, part_lo, part_hi, d_rec_sizes);
+    } else if (n) {
         if (fork) CK(cudaStreamWaitEvent(st, ctx->join_ev, 0));
         PROF(k_frame);
         k_frame<<<n, kThreads, 0, st>>>(d_streams, d_wins, o->block_size, o->segment_count, d_scan, d_crcp, ctx->d_crc, d_soff,
@@ -509,6 +522,73 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options
     if (sbytes) CK(cudaMemcpyAsync(ws + offs[1], ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(ctx->pin_done, st));
     return compress_launch(ctx, n, (int)P.wins.size(), P.nb, P.nslots, P.ncrc, P.min_w, o, ws, offs, d_out, d_offsets, d_lengths, st);
+}
+
+int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* o, uint64_t blk_begin,
+                       uint64_t blk_end, void* d_out, uint64_t out_capacity, uint32_t* d_rec_sizes, uint64_t crc_begin,
+                       uint64_t crc_end, uint32_t* d_crc, void* cuda_stream) {
+    if (int r = check_compress_args(ctx, t, 1, o)) return r;
+    cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+    CPlan P;
+    make_plan(t, 1, o, P);
+    if (blk_begin > blk_end || blk_end > P.nb || crc_begin > crc_end || crc_end > t->nbytes ||
+        (blk_end > blk_begin && (!d_out || !d_rec_sizes)))
+        return fail(ctx, LMCG_ERR_ARGUMENT, "bad part ranges");
+    // capacity: the stored-record bound of the blocks in range
+    uint64_t need_out = 0;
+    for (const WinDesc& wd : P.wins)
+        for (uint64_t k = 0; k < wd.nblocks; k++) {
+            const uint64_t b = wd.blk0 + k;
+            if (b >= blk_begin && b < blk_end) need_out += std::min<uint64_t>(o->block_size, wd.W - k * o->block_size) + 5;
+        }
+    if (need_out > out_capacity) return fail(ctx, LMCG_ERR_CAPACITY, "part output capacity below %llu", (unsigned long long)need_out);
+    size_t offs[16];
+    const size_t need = compress_layout(P, 1, offs);
+    if (int r = grow(ctx, &ctx->ws, &ctx->ws_cap, need)) return r;
+    uint8_t* ws = ctx->ws;
+    const size_t wbytes = P.wins.size() * sizeof(WinDesc), sbytes = P.streams.size() * sizeof(StreamDesc);
+    if (int r = grow_pinned(ctx, wbytes + sbytes + 64)) return r;
+    if (wbytes) memcpy(ctx->pin, P.wins.data(), wbytes);
+    if (sbytes) memcpy(ctx->pin + wbytes, P.streams.data(), sbytes);
+    if (wbytes) CK(cudaMemcpyAsync(ws + offs[0], ctx->pin, wbytes, cudaMemcpyHostToDevice, st));
+    if (sbytes) CK(cudaMemcpyAsync(ws + offs[1], ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(ctx->pin_done, st));
+    if (blk_end > blk_begin) {
+        if (int r = compress_launch(ctx, 1, (int)P.wins.size(), P.nb, P.nslots, P.ncrc, P.min_w, o, ws, offs, nullptr,
+                                    nullptr, nullptr, st, blk_begin, blk_end, static_cast<uint8_t*>(d_out), d_rec_sizes))
+            return r;
+    }
+    if (!d_crc) return LMCG_OK;
+    const uint64_t L = crc_end - crc_begin;
+    if (!L) {
+        CK(cudaMemsetAsync(d_crc, 0, sizeof(uint32_t), st));
+        return LMCG_OK;
+    }
+    // raw CRC of the element bytes [crc_begin, crc_end): k_crc over one
+    // pseudo-window, then one combine
+    const uint64_t nchunk = (L + kCrcChunk - 1) / kCrcChunk;
+    if (int r = grow(ctx, &ctx->part_ws, &ctx->part_ws_cap, 256 + 4 * (nchunk + 1))) return r;
+    WinDesc cw{};
+    cw.src = static_cast<const uint8_t*>(t->data) + crc_begin;
+    cw.prev = t->prev ? static_cast<const uint8_t*>(t->prev) + crc_begin : nullptr;
+    cw.W = L;
+    cw.n = L;
+    cw.w = 1;
+    cw.crc0 = 0;
+    cw.al16 = ((uint64_t)cw.src % 16 == 0) && ((uint64_t)cw.prev % 16 == 0);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(ctx->part_ws, &cw, sizeof(WinDesc), cudaMemcpyHostToDevice));
+    if (!ctx->crc_attr) {
+        CK(cudaFuncSetAttribute(k_crc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem));
+        ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kThreads, kCrcSmem);
+        ctx->crc_attr = true;
+    }
+    uint32_t* parts = reinterpret_cast<uint32_t*>(ctx->part_ws + 256);
+    k_crc<<<(unsigned)std::min<uint64_t>((nchunk + kWarps - 1) / kWarps, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, st>>>(
+        reinterpret_cast<const WinDesc*>(ctx->part_ws), 1, nchunk, ctx->d_crc, ctx->d_sh992, parts);
+    k_crc_join<<<1, kThreads, 0, st>>>(parts, L, ctx->d_crc, d_crc);
+    CK(cudaGetLastError());
+    return LMCG_OK;
 }
 
 // ---------------------------------------------------------------- plans

@@ -21,6 +21,12 @@ namespace lmcg {
 
 constexpr int kEncRun = 64;  // k_encode positions per thread per round
 
+// Record sizes of blocks [lo, hi) (lmcg_compress_part).
+__global__ void k_recsizes(const BlockMeta* __restrict__ meta, uint64_t lo, uint64_t hi, uint32_t* __restrict__ out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (lo + i < hi) out[i] = meta[lo + i].recsize;
+}
+
 // Bytes from device memory into mapped page-locked host memory (by the SMs).
 __global__ void k_small_copy(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, uint64_t n) {
     for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wi
 // pieces, then the four rows in order).
 __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
-    uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta) {
+    uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta, uint64_t part_lo, uint64_t part_hi) {
     __shared__ uint32_t sh_hist[kWarps][256];
     const uint64_t slot = blockIdx.x;
     if (slot >= nslots) return;
@@ -156,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
     const int64_t kk = slot_to_block(wd, slot - wd.slot0, B);
     if (kk < 0) return;
     const uint64_t k = (uint64_t)kk;
+    if (wd.blk0 + k < part_lo || wd.blk0 + k >= part_hi) return;   // outside the part (lmcg_compress_part)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < kWarps * 256; i += kThreads) (&sh_hist[0][0])[i] = 0;
     __syncthreads();
@@ -353,11 +360,19 @@ constexpr int kCbWarps = 4;
 __global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __restrict__ hist, uint64_t nb,
                                                           BlockMeta* __restrict__ meta, uint8_t* __restrict__ wire,
                                                           uint8_t* __restrict__ lens_out, uint32_t* __restrict__ pm_flag,
-                                                          uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list) {
+                                                          uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list,
+                                                          uint64_t part_lo = 0, uint64_t part_hi = ~0ull) {
     __shared__ CbSmem sm[kCbWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t b = (uint64_t)blockIdx.x * kCbWarps + warp;
     if (b >= nb) return;
+    if (b < part_lo || b >= part_hi) {   // outside the part: no record
+        if (lane == 0) {
+            BlockMeta m{};
+            meta[b] = m;
+        }
+        return;
+    }
     CbSmem& s = sm[warp];
     uint32_t cnt[8];
     {
@@ -684,6 +699,18 @@ __global__ void __launch_bounds__(kThreads) k_frame(const StreamDesc* __restrict
     }
 }
 
+// Raw CRC-32 of one byte range from its k_crc chunk CRCs (lmcg_compress_part).
+__global__ void __launch_bounds__(kThreads) k_crc_join(const uint32_t* __restrict__ parts, uint64_t L,
+                                                     const CrcTables* __restrict__ ct, uint32_t* __restrict__ out) {
+    __shared__ uint32_t red[kThreads];
+    const uint64_t nfull = L / kCrcChunk, rem = L % kCrcChunk;
+    uint32_t c = crc_combine_uniform(ct, nfull, kCrcChunk, [&](uint64_t i) { return parts[i]; }, red);
+    if (threadIdx.x == 0) {
+        if (rem) c = crc_shift_bytes(ct, c, rem) ^ parts[nfull];
+        *out = c;
+    }
+}
+
 // --------------------------------------------------------------- K4 encode
 // Symbols of piece (q, lane) of a warp-tile: the 16 source bytes at
 // 512 q + 16 lane, i.e. grouped positions [tp + (512 q + 16 lane)/w, +16/w)
@@ -884,7 +911,7 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
     uint32_t segs, const StreamDesc* __restrict__ streams, const BlockMeta* __restrict__ meta,
     const uint8_t* __restrict__ wire, const uint64_t* __restrict__ scan, const uint64_t* __restrict__ soff,
-    uint8_t* __restrict__ out) {
+    uint8_t* __restrict__ out, uint64_t part_lo, uint64_t part_hi) {
     extern __shared__ uint32_t stg[];
     __shared__ uint32_t sh_code[256];
     __shared__ uint32_t sh_cnt[kWarps][16];
@@ -897,10 +924,13 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     if (kk < 0) return;
     const uint64_t k = (uint64_t)kk;
     const uint64_t b = wd.blk0 + k;
+    if (b < part_lo || b >= part_hi) return;
     const BlockMeta m = meta[b];
     const StreamDesc sd = streams[wd.stream];
-    const uint64_t rec = soff[wd.stream] + kHeader + (uint64_t)(wd.win_local + 1) * kSegEntry * segs +
-                         (scan[b] - scan[sd.blk0]);
+    // a part (lmcg_compress_part) holds its records only, back to back
+    const uint64_t rec = part_hi != ~0ull ? scan[b] - scan[part_lo]
+                                          : soff[wd.stream] + kHeader + (uint64_t)(wd.win_local + 1) * kSegEntry * segs +
+                                                (scan[b] - scan[sd.blk0]);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint8_t* rp = out + rec;
     if (m.mode == MODE_RLE) {

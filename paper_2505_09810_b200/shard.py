@@ -139,6 +139,150 @@ def decompress_sharded(packed, lengths: Sequence[int], owner: Sequence[int], *, 
     return dict(zip(mine, decompress_fn(streams))) if mine else {}
 
 
+# ------------------------------------------------- splitting one tensor
+# A tensor larger than a rank's fair share is split by block range (SURVEY
+# §8(e)): rank r compresses blocks [b_r, b_{r+1}) of the stream's record list
+# and the raw CRC-32 of payload bytes [c_r, c_{r+1}) (Codec.compress_part /
+# lmcg_compress_part); one all-gather of record sizes and CRCs lets every
+# rank place its records, and the header (CRC combined) and segment tables
+# are written from the gathered sizes (stream.py:100-111, 271-284, 344-355).
+
+_P = 0xEDB88320
+
+
+def _multmodp(a: int, b: int) -> int:
+    m, p = 1 << 31, 0
+    while m:
+        if a & m:
+            p ^= b
+            if (a & (m - 1)) == 0:
+                break
+        m >>= 1
+        b = (b >> 1) ^ _P if b & 1 else b >> 1
+    return p
+
+
+def crc_shift(c: int, nbytes: int) -> int:
+    """Raw CRC-32 c followed by nbytes zero bytes (GF(2) x^(8n) mod P)."""
+    x2n = 1 << 30   # x^1
+    p = 1 << 31     # x^0
+    n, k = nbytes, 0
+    xk = x2n
+    # x^(2^k) for k = 3.. (8 n = n << 3)
+    for _ in range(3):
+        xk = _multmodp(xk, xk)
+    while n:
+        if n & 1:
+            p = _multmodp(xk, p)
+        n >>= 1
+        xk = _multmodp(xk, xk)
+    return _multmodp(p, c) if c else 0
+
+
+def crc_combine(parts: Sequence[tuple[int, int]]) -> int:
+    """zlib.crc32 of the concatenation of byte ranges given as (raw CRC, length)."""
+    raw, total = 0, 0
+    for c, n in parts:
+        raw = crc_shift(raw, n) ^ c
+        total += n
+    return raw ^ crc_shift(0xFFFFFFFF, total) ^ 0xFFFFFFFF
+
+
+def stream_layout(nbytes: int, width: int, byte_group: bool, block_size: int, segment_count: int,
+                  buffer_size: int) -> list[dict]:
+    """Windows of a stream: bytes, first block, block count and, per segment,
+    (original bytes, first block, end block) -- the record order of the stream."""
+    from .stream import segment_bounds
+
+    out, blk = [], 0
+    for woff in range(0, nbytes, buffer_size):
+        W = min(buffer_size, nbytes - woff)
+        nb = (W + block_size - 1) // block_size
+        segs = []
+        for ea, eb in segment_bounds(W, block_size, segment_count):
+            ba = ea // block_size
+            bb = ba if eb == ea else (eb + block_size - 1) // block_size
+            segs.append((eb - ea, blk + ba, blk + bb))
+        out.append({"W": W, "blk0": blk, "nblocks": nb, "segments": segs})
+        blk += nb
+    return out
+
+
+def split_ranges(nblocks: int, nbytes: int, world: int) -> list[tuple[int, int, int, int]]:
+    """Balanced (block range, CRC byte range) of every rank."""
+    return [(nblocks * r // world, nblocks * (r + 1) // world, nbytes * r // world, nbytes * (r + 1) // world)
+            for r in range(world)]
+
+
+def assemble_stream(nbytes: int, element_type: int, flags: int, block_size: int, segment_count: int,
+                    buffer_size: int, rec_sizes: Sequence[int], records: bytes,
+                    crc_parts: Sequence[tuple[int, int]]) -> bytes:
+    """The LMC1 stream from all records (in record order, back to back), their
+    sizes and the (raw CRC, length) of consecutive payload byte ranges."""
+    import struct
+
+    from .stream import _WIDTH
+
+    lay = stream_layout(nbytes, _WIDTH[element_type], bool(flags & 1), block_size, segment_count, buffer_size)
+    offs = [0]
+    for n in rec_sizes:
+        offs.append(offs[-1] + int(n))
+    crc = crc_combine(crc_parts) if nbytes else 0
+    out = [struct.pack("<4sBBBBQIII", b"LMC1", 1, flags, element_type, 0, nbytes, block_size, segment_count, crc)]
+    for w in lay:
+        tab = b"".join(struct.pack("<QQ", orig, offs[bb] - offs[ba]) for orig, ba, bb in w["segments"])
+        out.append(tab)
+        out.append(records[offs[w["blk0"]]:offs[w["blk0"] + w["nblocks"]]])
+    return b"".join(out)
+
+
+def compress_split(tensor, *, group=None, element_type: int | None = None, prev=None, byte_group: bool = True,
+                   block_size: int = 65536, segment_count: int = 1, buffer_size: int = 128 << 20,
+                   codec=None, part_fn: Callable | None = None):
+    """Compress ONE tensor with all ranks of ``group`` (each holds the whole
+    tensor, e.g. replicated parameters): rank r compresses its block range,
+    one all-gather exchanges record sizes / CRCs / parts, and every rank
+    returns the full stream (byte-identical to a one-GPU lmc_compress).
+
+    ``part_fn(blk_a, blk_b, crc_a, crc_b) -> (records: bytes, sizes: list,
+    raw_crc: int)`` replaces the GPU part compression (tests drive the
+    exchange logic on CPU with it)."""
+    import torch.distributed as dist
+
+    from .stream import _WIDTH, _bytes_view, _torch_et
+
+    if dist.is_initialized():
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    else:
+        rank, world = 0, 1
+    et = int(element_type if element_type is not None else _torch_et(tensor.dtype))
+    nbytes = int(_bytes_view(tensor).numel()) if hasattr(tensor, "data_ptr") else len(tensor)
+    lay = stream_layout(nbytes, _WIDTH[et], byte_group, block_size, segment_count, buffer_size)
+    nblk = sum(w["nblocks"] for w in lay)
+    ranges = split_ranges(nblk, nbytes, world)
+    ba, bb, ca, cb = ranges[rank]
+    if part_fn is None:
+        codec = codec or __import__("paper_2505_09810_b200").stream.default_codec()
+        rec, sizes, crc = codec.compress_part(tensor, ba, bb, ca, cb, element_type=et, prev=prev, byte_group=byte_group,
+                                              block_size=block_size, segment_count=segment_count,
+                                              buffer_size=buffer_size)
+        sizes = [int(x) for x in sizes.tolist()]
+        records = rec[:sum(sizes)].cpu().numpy().tobytes()
+        raw = int(crc.item()) & 0xFFFFFFFF
+    else:
+        records, sizes, raw = part_fn(ba, bb, ca, cb)
+    flags = (1 if byte_group else 0) | (2 if prev is not None else 0)
+    if world > 1:
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (sizes, raw, records), group=group)
+    else:
+        gathered = [(sizes, raw, records)]
+    all_sizes = [x for g in gathered for x in g[0]]
+    crc_parts = [(g[1], ranges[r][3] - ranges[r][2]) for r, g in enumerate(gathered)]
+    return assemble_stream(nbytes, et, flags, block_size, segment_count, buffer_size, all_sizes,
+                           b"".join(g[2] for g in gathered), crc_parts)
+
+
 def _nbytes(t) -> int:
     if t is None:
         raise ValueError("tensor sizes are needed for unowned entries: pass nbytes=")

@@ -298,6 +298,46 @@ class Codec:
         batch._keep = (views, pviews)
         return batch
 
+    def compress_part(self, tensor, blk_begin: int, blk_end: int, crc_begin: int, crc_end: int, *,
+                      element_type: int | None = None, prev=None, delta: bool = False, byte_group: bool = True,
+                      block_size: int = DEFAULT_BLOCK_SIZE, segment_count: int = 1,
+                      buffer_size: int = DEFAULT_BUFFER_SIZE, stream=None):
+        """One part of ``tensor``'s stream for multi-GPU assembly
+        (lmcg_compress_part): the records of blocks [blk_begin, blk_end) back
+        to back, their sizes, and the raw CRC-32 of payload bytes
+        [crc_begin, crc_end).  Returns device tensors (records, sizes, crc);
+        ``shard.assemble_stream`` joins the parts of all ranks."""
+        import torch
+
+        et = int(element_type if element_type is not None else _torch_et(tensor.dtype))
+        v = _bytes_view(tensor)
+        pv = _bytes_view(prev) if prev is not None else None
+        if pv is not None and pv.numel() != v.numel():
+            from .errors import ShapeMismatchError
+            raise ShapeMismatchError(f"length mismatch: {pv.numel()} vs {v.numel()}")
+        _validate_options(_WIDTH[et], block_size, segment_count, buffer_size)
+        if v.numel() % _WIDTH[et]:
+            raise AlignmentError(f"buffer of {v.numel()} bytes is not a multiple of width {_WIDTH[et]}")
+        t = _lib.lmcg_tensor()
+        t.data = v.data_ptr() if v.numel() else 0
+        t.prev = pv.data_ptr() if pv is not None and pv.numel() else 0
+        t.nbytes = v.numel()
+        t.element_type = et
+        t.delta = int(bool(delta) or pv is not None)
+        opts = _lib.lmcg_options(int(bool(byte_group)), block_size, segment_count, 0, buffer_size)
+        nblk = blk_end - blk_begin
+        cap = 5 * max(nblk, 0) + min(v.numel(), max(nblk, 0) * block_size) + 16
+        out = torch.empty(max(cap, 16), dtype=torch.uint8, device=self.device)
+        sizes = torch.empty(max(nblk, 1), dtype=torch.int32, device=self.device)
+        crc = torch.zeros(1, dtype=torch.int64, device=self.device)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.ctx.lib.lmcg_compress_part(self.ctx.ptr, ctypes.byref(t), ctypes.byref(opts), blk_begin, blk_end,
+                                             out.data_ptr(), out.numel(), sizes.data_ptr(), crc_begin, crc_end,
+                                             crc.data_ptr(), ctypes.c_void_p(s.cuda_stream))
+        self.ctx.check(rc)
+        out._keep = (v, pv)
+        return out, sizes[:max(nblk, 0)], crc
+
     def compress_plan(self, tensors, **kw) -> CompressPlan:
         """A CompressPlan over these tensors (see CompressPlan)."""
         return CompressPlan(self, tensors, **kw)

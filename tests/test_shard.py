@@ -136,3 +136,106 @@ def test_single_rank_gpu_codec_matches_oracle():
     packed = b"".join(streams)
     dec = shard.decompress_sharded(packed, res.lengths, res.owner, rank=0)
     assert all(dec[i].data == ts[i] for i in range(len(ts)))
+
+
+# ------------------------------------------------ one tensor, several ranks
+def _records(stream):
+    """(sizes, concatenated records) of an LMC1 stream, in record order."""
+    import struct
+    hdr = struct.unpack_from("<4sBBBBQIII", stream, 0)
+    orig, B, S = hdr[5], hdr[6], hdr[7]
+    pos, sizes, recs = 28, [], []
+    left = orig
+    while left > 0:
+        tab = [struct.unpack_from("<QQ", stream, pos + 16 * i) for i in range(S)]
+        pos += 16 * S
+        for o, c in tab:
+            end = pos + c
+            while pos < end:
+                mode, L = stream[pos], struct.unpack_from("<I", stream, pos + 1)[0]
+                n = 5 + (1 if mode == 1 else L if mode == 2 else 132 + (struct.unpack_from("<I", stream, pos + 133)[0] + 7) // 8)
+                sizes.append(n)
+                recs.append(stream[pos:pos + n])
+                pos += n
+            left -= o
+    return sizes, b"".join(recs)
+
+
+def _raw_crc(b):
+    import zlib
+    return zlib.crc32(b) ^ 0xFFFFFFFF ^ shard.crc_shift(0xFFFFFFFF, len(b))
+
+
+def _oracle_part_fn(data, **opts):
+    full = O.compress(data, BF16, threads=1, **opts)
+    sizes, recs = _records(full)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+    def part(ba, bb, ca, cb):
+        return recs[offs[ba]:offs[bb]], sizes[ba:bb], _raw_crc(data[ca:cb])
+    return full, part
+
+
+def test_split_single_process_matches_oracle():
+    for opts in ({"block_size": 4096, "segment_count": 3, "buffer_size": 40000}, {"block_size": 65536}):
+        data = _tensors()[6]
+        full, part = _oracle_part_fn(data, **opts)
+        got = shard.compress_split(data, element_type=BF16, part_fn=part, **opts)
+        assert got == full
+
+
+def _split_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        data = _tensors()[6]
+        opts = {"block_size": 4096, "segment_count": 3, "buffer_size": 40000}
+        full, part = _oracle_part_fn(data, **opts)
+        got = shard.compress_split(data, element_type=BF16, part_fn=part, **opts)
+        q.put((rank, got == full))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_split_one_tensor():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert got == [(0, True), (1, True)]
+
+
+@pytest.mark.gpu
+def test_gpu_parts_assemble_to_the_one_call_stream():
+    import torch
+    from paper_2505_09810_b200 import synth
+    import paper_2505_09810_b200 as lmcb
+
+    codec = lmcb.Codec()
+    t = synth.make_tensor(synth.TensorSpec("w", (4096, 4096), "weight"), 7, 0)
+    p = synth.make_tensor(synth.TensorSpec("w", (4096, 4096), "weight"), 8, 0)
+    for opts, prev in (({}, None), ({"block_size": 16384, "segment_count": 4, "buffer_size": 12 << 20}, None),
+                       ({}, p)):
+        b = codec.compress([t], prev=None if prev is None else [prev], **opts)
+        want = b.to_bytes()[0]
+        for world in (2, 3, 5):
+            lay = shard.stream_layout(t.numel() * 2, 2, True, opts.get("block_size", 65536),
+                                      opts.get("segment_count", 1), opts.get("buffer_size", 128 << 20))
+            nblk = sum(w["nblocks"] for w in lay)
+            sizes, recs, crcs = [], [], []
+            for ba, bb, ca, cb in shard.split_ranges(nblk, t.numel() * 2, world):
+                r, s, c = codec.compress_part(t, ba, bb, ca, cb, prev=prev, **opts)
+                s = [int(x) for x in s.tolist()]
+                sizes += s
+                recs.append(r[:sum(s)].cpu().numpy().tobytes())
+                crcs.append((int(c.item()) & 0xFFFFFFFF, cb - ca))
+            got = shard.assemble_stream(t.numel() * 2, 1, 1 | (2 if prev is not None else 0),
+                                        opts.get("block_size", 65536), opts.get("segment_count", 1),
+                                        opts.get("buffer_size", 128 << 20), sizes, b"".join(recs), crcs)
+            assert got == want, (opts.keys(), world)
