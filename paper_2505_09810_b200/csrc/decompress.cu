@@ -311,6 +311,29 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     const int tid = threadIdx.x;
     uint32_t c = 0;
     bool bad = false, done = false;
+    // staged payload: read through a 64-bit register bit buffer, refilled
+    // branch-free (the next word is always inside the staging area)
+    uint64_t bbuf = 0;
+    uint32_t bavail = 0, bnj = 0;
+    if (STAGED) {
+        const uint32_t a0 = pos + src.sh, j0 = a0 >> 5, r0 = a0 & 31;
+        bbuf = (((uint64_t)src.sw[j0] << 32) | src.sw[j0 + 1]) << r0;
+        bavail = 64 - r0;
+        bnj = j0 + 2;
+    }
+    auto win = [&]() -> uint32_t { return STAGED ? (uint32_t)(bbuf >> 32) : src.template peek<STAGED>(pos); };
+    auto adv = [&](uint32_t l) {
+        pos += l;
+        if (STAGED) {
+            bbuf <<= l;
+            bavail -= l;
+            const bool rf = bavail < 32;
+            const uint32_t nw = src.sw[bnj];
+            bbuf |= rf ? ((uint64_t)nw << (32 - bavail)) : 0ull;
+            bnj += rf ? 1u : 0u;
+            bavail += rf ? 32u : 0u;
+        }
+    };
     if (!EMIT) {
         // (every lane of the mask runs this loop's votes, also those with bm == 0)
         uint32_t m0 = 0, m1 = 0;
@@ -319,11 +342,11 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         while (__any_sync(mask, act)) {
             if (act) {
                 uint32_t sym;
-                const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
+                const uint32_t l = step1(s, win(), sym);
                 if (!l) {
                     bad = true;
                 } else {
-                    pos += l;
+                    adv(l);
                     c++;
                     const uint32_t rel = pos - p0;
                     if (rel < 64) {
@@ -352,16 +375,16 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
             bool a2 = on && pos + kLut <= T;
             while (__any_sync(mask, a2)) {
                 if (a2) {
-                    const uint32_t win = src.template peek<STAGED>(pos);
-                    const uint32_t e = s.lut3[win >> (32 - kLut)];
+                    const uint32_t wv = win();
+                    const uint32_t e = s.lut3[wv >> (32 - kLut)];
                     uint32_t n = e >> 30, tl = (e >> 26) & 15;
                     if (n == 0) {
                         uint32_t sym;
-                        tl = step1(s, win, sym);
+                        tl = step1(s, wv, sym);
                         n = 1;
                         bad = tl == 0;
                     }
-                    pos += tl;
+                    adv(tl);
                     c += n;
                     a2 = !bad && pos + kLut <= T;
                 }
@@ -370,9 +393,9 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
             while (__any_sync(mask, a2)) {
                 if (a2) {
                     uint32_t sym;
-                    const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
+                    const uint32_t l = step1(s, win(), sym);
                     if (!l) bad = true;
-                    else { pos += l; c++; }
+                    else { adv(l); c++; }
                     a2 = !bad && pos < T;
                 }
             }
@@ -393,11 +416,11 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         while (__any_sync(mask, act)) {
             if (act) {
                 uint32_t sym;
-                const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
+                const uint32_t l = step1(s, win(), sym);
                 if (!l) {
                     bad = true;
                 } else {
-                    pos += l;
+                    adv(l);
                     c++;
                     *d++ = (uint8_t)sym;
                 }
@@ -409,45 +432,29 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     uint64_t acc = 0;
     uint32_t nacc = 0;
     bool act = !bad && !done && pos + kLut <= lim;
-    // bulk: up to three symbols per table lookup, two lookups per vote; the
-    // staged payload is read through a 64-bit register bit buffer
-    uint64_t bbuf = 0;
-    uint32_t bavail = 0, bnj = 0;
-    if (STAGED && act) {
-        const uint32_t a0 = pos + src.sh, j0 = a0 >> 5, r0 = a0 & 31;
-        bbuf = (((uint64_t)src.sw[j0] << 32) | src.sw[j0 + 1]) << r0;
-        bavail = 64 - r0;
-        bnj = j0 + 2;
-    }
+    // bulk: up to three symbols per table lookup, two lookups per vote
     auto lookup = [&]() {
-        const uint32_t win = STAGED ? (uint32_t)(bbuf >> 32) : src.template peek<STAGED>(pos);
-        const uint32_t e = s.lut3[win >> (32 - kLut)];
+        const uint32_t wv = win();
+        const uint32_t e = s.lut3[wv >> (32 - kLut)];
         uint32_t n = e >> 30, tl = (e >> 26) & 15, packed = e & 0xFFFFFF;
         if (n == 0) {
             uint32_t sym;
-            tl = step1(s, win, sym);
+            tl = step1(s, wv, sym);
             n = 1;
             packed = sym;
             bad = tl == 0;
         }
-        pos += tl;
+        adv(tl);
         c += n;
         DBG_ADD(EMIT ? 25 : 26, 1);
-        if (STAGED) {
-            bbuf <<= tl;
-            bavail -= tl;
-            if (bavail < 32) {
-                bbuf |= (uint64_t)src.sw[bnj++] << (32 - bavail);
-                bavail += 32;
-            }
-        }
-        if (EMIT) {
+        if (EMIT) {   // branch-free packing: predicated 8-byte store
             acc |= (uint64_t)packed << (8 * nacc);
             const uint32_t nn = nacc + n;
-            const bool full = nn >= 8;
-            if (full) *w = acc;
+            const bool full = nn >= 8;   // (implies nacc >= 5)
+            asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.u64 [%0], %1; }"
+                         :: "l"(w), "l"(acc), "r"((uint32_t)full) : "memory");
             w += full ? 1 : 0;
-            acc = full ? (nacc ? ((uint64_t)packed >> (8 * (8 - nacc))) : 0ull) : acc;
+            acc = full ? ((uint64_t)packed >> (8 * (8 - nacc))) : acc;
             nacc = full ? nn - 8 : nn;
         }
     };
@@ -462,11 +469,11 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     while (__any_sync(mask, act)) {
         if (act) {
             uint32_t sym;
-            const uint32_t l = step1(s, src.template peek<STAGED>(pos), sym);
+            const uint32_t l = step1(s, win(), sym);
             if (!l) {
                 bad = true;
             } else {
-                pos += l;
+                adv(l);
                 c++;
                 if (EMIT) {
                     acc |= (uint64_t)sym << (8 * nacc);
@@ -1086,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
 // copy or CTA-wide Huffman decode into the grouped scratch.  A failure marks
 // the segment for k_fallback, which re-walks it serially and reports the
 // reference's error.
-__global__ void __launch_bounds__(kThreads) k_decrec(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+__global__ void __launch_bounds__(kThreads, 3) k_decrec(const DecSeg* __restrict__ segs, uint64_t nseg_total,
                                                    uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
                                                    const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
