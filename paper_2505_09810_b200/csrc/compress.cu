@@ -775,13 +775,17 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
                 ns = 0;
                 for (int i = 0; i < per && pos + i < q1; i++, ns++) sy[i >> 2] |= gather_byte(wd, pos + i) << (8 * (i & 3));
             }
+            // symbol pairs: two codes (<= 30 bits) joined in 32 bits, one
+            // accumulator update and at most one word flush per pair
 #pragma unroll
-            for (int i = 0; i < per; i++) {
+            for (int i = 0; i < per; i += 2) {
                 if (i < ns) {
-                    const uint32_t e = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
-                    const uint32_t l = e >> 16;
-                    acc = (acc << l) | (e & 0xFFFF);
-                    n += l;
+                    const uint32_t e1 = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
+                    const uint32_t e2 = (i + 1 < ns) ? sh_code[(sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF] : 0u;
+                    const uint32_t l2 = e2 >> 16;
+                    const uint32_t pl = (e1 >> 16) + l2;
+                    acc = (acc << pl) | (((e1 & 0xFFFF) << l2) | (e2 & 0xFFFF));
+                    n += pl;
                     const bool fl = n >= 32;
                     n -= fl ? 32 : 0;
                     if (fl) priv[wi] = (uint32_t)(acc >> n);
