@@ -850,58 +850,54 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
 // grid, then written with coalesced 32-bit stores (the record's first and
 // last words bytewise: they share bytes with the header / the next record).
 __device__ void store_plane(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_t* stg, uint8_t* d0) {
+    // The staging area holds each round's payload bytes at aligned offsets
+    // (a piece of 16/w symbols is 1, 2 or 4 whole words).  Destination words
+    // that lie entirely inside the round leave as 32-bit stores, shifted onto
+    // the destination's 4-byte grid; the at most 3 + 3 bytes at the round's
+    // edges go out bytewise (the record's first / last word shares bytes with
+    // the header / the next record, and rounds meet inside words).
     const int tid = threadIdx.x;
     const uint32_t w = wd.w, lw = lg2w(w);
     const uint32_t per = 16u >> lw;
     const uint32_t lb = (uint32_t)(reinterpret_cast<uint64_t>(d0) & 3);
     uint32_t* gwd = reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t>(d0) & ~3ull);
-    uint8_t* sb = reinterpret_cast<uint8_t*>(stg);
-    const uint64_t round = (uint64_t)kThreads * 4 * per;
-    uint64_t wbase = 0;
-    uint32_t rem = lb;  // bytes pending in staging word 0
-    if (tid == 0) stg[0] = 0;
-    __syncthreads();
+    const uint8_t* sb = reinterpret_cast<const uint8_t*>(stg);
+    const uint64_t round = (uint64_t)kThreads * 4 * per;   // positions (= payload bytes) per round
     for (uint64_t r0 = p0; r0 < p1; r0 += round) {
         const uint64_t r1 = min(r0 + round, p1);
+        const uint64_t g0 = plane_of(r0, wd.n, w), gend = (g0 + 1) * wd.n;
 #pragma unroll
         for (int q = 0; q < 4; q++) {
             const uint64_t pos = r0 + (uint64_t)(q * kThreads + tid) * per;
             if (pos >= r1) continue;
-            const uint64_t g = plane_of(pos, wd.n, w);
-            uint8_t* dst = sb + lb + (pos - r0);
+            const uint64_t g = pos >= gend ? g0 + 1 : g0;
+            uint32_t* dw = stg + ((pos - r0) >> 2);
             if (wd.vec && pos + per <= r1 && pos + per <= (g + 1) * wd.n) {
                 const uint4 a = ldg16x(wd.src, wd.prev, (pos - g * wd.n) << lw);
                 uint32_t sy[4];
-                const int ns = piece_symbols(a, w, (uint32_t)g, sy);
-                for (int i = 0; i < ns; i++) dst[i] = (uint8_t)(sy[i >> 2] >> (8 * (i & 3)));
+                piece_symbols(a, w, (uint32_t)g, sy);
+                if (per == 16) *reinterpret_cast<uint4*>(dw) = make_uint4(sy[0], sy[1], sy[2], sy[3]);
+                else if (per == 8) *reinterpret_cast<uint2*>(dw) = make_uint2(sy[0], sy[1]);
+                else *dw = sy[0];
             } else {
+                uint8_t* dst = reinterpret_cast<uint8_t*>(dw);
                 for (uint32_t i = 0; i < per && pos + i < r1; i++) dst[i] = (uint8_t)gather_byte(wd, pos + i);
             }
         }
         __syncthreads();
-        const uint32_t nbytes = lb + (uint32_t)(r1 - r0);
-        const uint32_t full = nbytes / 4;
-        for (uint32_t j = tid; j < full; j += kThreads) {
-            const uint64_t gwi = wbase + j;
-            const uint32_t v = stg[j];
-            if (gwi == 0 && lb) {
-                uint8_t* bp = reinterpret_cast<uint8_t*>(gwd);
-                for (uint32_t q = lb; q < 4; q++) bp[q] = (uint8_t)(v >> (8 * q));
-            } else {
-                gwd[gwi] = v;
-            }
+        // destination word j holds payload bytes [4j - lb, 4j - lb + 4)
+        const uint64_t R0 = r0 - p0, R1 = r1 - p0;
+        const uint64_t ja = (R0 + lb + 3) / 4, je = (R1 + lb) / 4;   // words inside [R0, R1)
+        const uint32_t sh = 8 * ((4 - lb) & 3);                       // staging byte phase
+        for (uint64_t j = ja + tid; j < je; j += kThreads) {
+            const uint32_t i0 = (uint32_t)((4 * j - lb - R0) >> 2);
+            gwd[j] = sh ? __funnelshift_r(stg[i0], stg[i0 + 1], sh) : stg[i0];
         }
-        const uint32_t carry = stg[full];
+        if (tid == 0)
+            for (uint64_t pb = R0; pb < min(R1, 4 * ja - lb); pb++) d0[pb] = sb[pb - R0];
+        if (tid == 32)
+            for (uint64_t pb = max(R0, 4 * je - lb); pb < R1; pb++) d0[pb] = sb[pb - R0];
         __syncthreads();
-        if (tid == 0) stg[0] = carry;
-        wbase += full;
-        rem = nbytes & 3;
-        __syncthreads();
-    }
-    if (tid == 0 && rem) {
-        const uint32_t v = stg[0];
-        uint8_t* bp = reinterpret_cast<uint8_t*>(gwd + wbase);
-        for (uint32_t q = (wbase == 0 ? lb : 0); q < rem; q++) bp[q] = (uint8_t)(v >> (8 * q));
     }
 }
 
