@@ -411,6 +411,27 @@ __global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __re
         if (lane == 0 && pm_flag) atomicOr(pm_flag, 2u);
         return;
     }
+    if (lens_out == nullptr) {
+        // entropy bound: every prefix code costs at least n H bits; when even
+        // that cannot beat the stored record (stream.py:173) the block is
+        // stored and its code is never built (incompressible planes)
+        double ent = 0.0;   // sum c log2 c
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+            if (cnt[r]) ent += (double)cnt[r] * log2((double)cnt[r]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) ent += __shfl_xor_sync(0xFFFFFFFFu, ent, o);
+        const double nH = (double)total * log2((double)total) - ent;
+        const uint32_t len = meta[b].len;
+        if (8.0 * kHuffOverhead + nH - 64.0 > 8.0 * len) {   // (64-bit margin for rounding)
+            if (lane == 0) {
+                BlockMeta m = meta[b];
+                m.mode = MODE_STORED; m.bits = 0; m.recsize = 5 + len; m.pm = 0;
+                meta[b] = m;
+            }
+            return;
+        }
+    }
     const int n = sorted_leaves(cnt, lane, s.wt, s.sym);
     if (n == 1) {
         if (lane == 0) s.lens[s.sym[0]] = 1;  // huffman.py:89-91
