@@ -31,6 +31,7 @@ namespace lmcg {
 constexpr int kChunk = 65536;        // segment payload bytes per k_scandec chunk
 constexpr int kOutTile = 16384;      // output bytes per k_ungroup CTA
 constexpr int kLut = 11;             // LUT index bits
+constexpr int kCntLut = 12;          // count-LUT index bits (no symbols: more codewords per lookup)
 
 #ifdef LMCG_DEBUG
 __device__ unsigned long long lmcg_dbg[32];
@@ -227,6 +228,7 @@ struct DecSmem {
     uint32_t bits[kStage / 4 + 4];      // staged bitstream, big-endian words
     uint32_t lut3[1 << kLut];           // n(2)|tl(4)|pad(2)|s3(8)|s2(8)|s1(8); n == 0: slow path
     uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0
+    uint8_t lutc[1 << kCntLut];         // count passes: n(4) | tl(4) of the whole codewords in a 12-bit window
     uint32_t bm[2][kThreads];           // pass-0 boundary bitmaps (first 64 bits of each chunk)
     uint32_t cp[kCheckpoints][kThreads];  // pass-0 checkpoints: (offset from p0) << 16 | symbol count
     uint32_t end[kThreads];
@@ -372,12 +374,12 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         for (int k = 0; k < kCheckpoints; k++) {
             const uint32_t T = p0 + (128u << k);
             const bool on = bm != 0 && !bad && !done && T < lim;
-            bool a2 = on && pos + kLut <= T;
+            bool a2 = on && pos + kCntLut <= T;
             while (__any_sync(mask, a2)) {
                 if (a2) {
                     const uint32_t wv = win();
-                    const uint32_t e = s.lut3[wv >> (32 - kLut)];
-                    uint32_t n = e >> 30, tl = (e >> 26) & 15;
+                    const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
+                    uint32_t n = e >> 4, tl = e & 15;
                     if (n == 0) {
                         uint32_t sym;
                         tl = step1(s, wv, sym);
@@ -386,7 +388,7 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
                     }
                     adv(tl);
                     c += n;
-                    a2 = !bad && pos + kLut <= T;
+                    a2 = !bad && pos + kCntLut <= T;
                 }
             }
             a2 = on && !bad && pos < T;
@@ -431,12 +433,19 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     uint64_t* w = reinterpret_cast<uint64_t*>(d);
     uint64_t acc = 0;
     uint32_t nacc = 0;
-    bool act = !bad && !done && pos + kLut <= lim;
-    // bulk: up to three symbols per table lookup, two lookups per vote
+    constexpr int kW = EMIT ? kLut : kCntLut;   // window bits of the bulk lookups
+    bool act = !bad && !done && pos + kW <= lim;
+    // bulk: up to three symbols (count passes: twelve) per table lookup, two lookups per vote
     auto lookup = [&]() {
         const uint32_t wv = win();
-        const uint32_t e = s.lut3[wv >> (32 - kLut)];
-        uint32_t n = e >> 30, tl = (e >> 26) & 15, packed = e & 0xFFFFFF;
+        uint32_t n, tl, packed = 0;
+        if (EMIT) {
+            const uint32_t e = s.lut3[wv >> (32 - kLut)];
+            n = e >> 30; tl = (e >> 26) & 15; packed = e & 0xFFFFFF;
+        } else {
+            const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
+            n = e >> 4; tl = e & 15;
+        }
         if (n == 0) {
             uint32_t sym;
             tl = step1(s, wv, sym);
@@ -461,8 +470,8 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     while (__any_sync(mask, act)) {
         if (act) {
             lookup();
-            if (!bad && pos + kLut <= lim) lookup();
-            act = !bad && pos + kLut <= lim;
+            if (!bad && pos + kW <= lim) lookup();
+            act = !bad && pos + kW <= lim;
         }
     }
     act = !bad && !done && pos < lim;
@@ -706,6 +715,19 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
         }
         if (n) ent = (n << 30) | (tl << 26) | syms;
         s.lut3[e] = ent;
+    }
+    // count LUT: every whole codeword of a 12-bit window (greedy)
+    for (int e = tid; e < (1 << kCntLut); e += kThreads) {
+        uint32_t n = 0, tl = 0;
+        for (;;) {
+            const uint32_t rest = ((uint32_t)e << tl) & ((1u << kCntLut) - 1);
+            const uint32_t a = s.lut1[rest >> (kCntLut - kLut)];
+            const uint32_t la = a >> 8;
+            if (!a || tl + la > kCntLut) break;
+            n++;
+            tl += la;
+        }
+        s.lutc[e] = (uint8_t)((n << 4) | tl);
     }
     __syncthreads();
     DBG_TADD(16, t_setup);
