@@ -225,7 +225,7 @@ constexpr int kStage = 40960;
 constexpr int kCheckpoints = 3;  // at 128, 256 and 512 bits into a chunk  // bitstream bytes staged in shared memory (longer ones are read from global)
 
 struct DecSmem {
-    uint32_t bits[kStage / 4 + 4];      // staged bitstream, big-endian words
+    uint32_t bits[kStage / 4 + 4];      // staged bitstream (TMA of the 16-byte aligned cover), big-endian words
     uint32_t lut3[1 << kLut];           // n(2)|tl(4)|pad(2)|s3(8)|s2(8)|s1(8); n == 0: slow path
     uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0
     uint8_t lutc[1 << kCntLut];         // count passes: n(4) | tl(4) of the whole codewords in a 12-bit window
@@ -239,6 +239,7 @@ struct DecSmem {
     uint32_t wsum[kWarps];
     uint32_t kraft;
     int minlen, maxlen, lgcd;
+    uint64_t mbar;                      // TMA staging of the payload
 };
 
 // Payload bit source: big-endian words, bit i of the payload is bit
@@ -605,6 +606,22 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
     return true;
 }
 
+// TMA 1-D bulk copy global -> shared with an mbarrier (SASS UBLKCP).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
+    asm volatile("{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n @!P bra WAIT_%=;\n}\n"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+
 // CTA-wide decode of one Huffman record payload `pl` (codebook | bits u32 |
 // bits) into dst[0, len).  Returns false on any corruption the reference
 // would report (malformed codebook, zero bit count, invalid prefix, wrong end
@@ -613,6 +630,17 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     DBG_T0(t_setup);
     __syncthreads();
+    // stage the payload in shared memory with one TMA bulk copy of its
+    // 16-byte aligned cover, issued first so it lands while the tables are built
+    const uint32_t bits0 = rd32(pl + 128);
+    const uint8_t* data0 = pl + kHuffOverhead;
+    const uint64_t a16 = reinterpret_cast<uint64_t>(data0) & ~15ull;
+    const uint64_t e16 = (reinterpret_cast<uint64_t>(data0) + ((uint64_t)bits0 + 7) / 8 + 15) & ~15ull;
+    const bool staged = bits0 != 0 && e16 - a16 <= (uint64_t)kStage;
+    if (staged && tid == 0) {
+        mbar_init1(&s.mbar);
+        tma_load_1d(s.bits, reinterpret_cast<const void*>(a16), (uint32_t)(e16 - a16), &s.mbar);
+    }
     const uint8_t wb = pl[tid >> 1];
     const uint32_t l = (tid & 1) ? (wb >> 4) : (wb & 15);
     s.lens[tid] = (uint8_t)l;
@@ -653,7 +681,10 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     __syncthreads();
     const uint32_t bits = rd32(pl + 128);
     // _validate_codebook (huffman.py:191-210) and decode_block's bit-length check (:275)
-    if (s.maxlen == 0 || s.kraft > (1u << kMaxLen) || bits == 0) return false;
+    if (s.maxlen == 0 || s.kraft > (1u << kMaxLen) || bits == 0) {
+        if (staged) mbar_wait0(&s.mbar);   // no bulk copy left in flight
+        return false;
+    }
     if (l) {
         uint32_t rk = rank_w;
         for (int w = 0; w < warp; w++) rk += s.cnt_w[w][l];
@@ -667,24 +698,6 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     G.sh = (uint32_t)(reinterpret_cast<uint64_t>(data) & 3) * 8;
     G.glimit = (uint64_t)(data - G.gbase) + nbytes;
     G.nwords_full = G.glimit / 4;
-    const uint64_t nwords = (G.glimit + 3) / 4;
-    const bool staged = nwords + 3 <= kStage / 4 + 4;
-    if (staged) {  // stage the payload words (zero past the end) in shared memory, 8 loads in flight
-        const uint64_t nw = nwords + 3;
-        for (uint64_t j0 = tid; j0 < nw; j0 += 8 * kThreads) {
-            uint32_t v[8];
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const uint64_t j = j0 + (uint64_t)u * kThreads;
-                v[u] = j < nw ? G.gword(j) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; u++) {
-                const uint64_t j = j0 + (uint64_t)u * kThreads;
-                if (j < nw) s.bits[j] = v[u];
-            }
-        }
-    }
     __syncthreads();
     // single-symbol LUT over kLut-bit prefixes
     for (int e = tid; e < (1 << kLut); e += kThreads) {
@@ -733,8 +746,19 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     DBG_TADD(16, t_setup);
     DBG_ADD(17, staged ? 1 : 0);
     if (staged) {
-        G.sw = s.bits;
-        return huff_passes<true>(s, G, bits, len, dst);
+        // the staged words in memory order -> big-endian words (bit i of the
+        // payload is bit 31 - ((i + sh) & 31) of word (i + sh) >> 5)
+        mbar_wait0(&s.mbar);
+        const uint32_t nw = (uint32_t)((e16 - a16) / 4);
+        for (uint32_t j = tid; j < nw; j += kThreads) s.bits[j] = bswap32(s.bits[j]);
+        __syncthreads();
+        Src St;
+        St.sw = s.bits;
+        St.gbase = reinterpret_cast<const uint8_t*>(a16);
+        St.sh = (uint32_t)(reinterpret_cast<uint64_t>(data) - a16) * 8;
+        St.glimit = (uint64_t)(data - St.gbase) + nbytes;
+        St.nwords_full = St.glimit / 4;
+        return huff_passes<true>(s, St, bits, len, dst);
     }
     return huff_passes<false>(s, G, bits, len, dst);
 }
@@ -745,25 +769,38 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t n) {
     const uint32_t nv = n / 16;
     const uint32_t sh = (uint32_t)(reinterpret_cast<uint64_t>(src) & 3) * 8;
     const uint32_t* w = reinterpret_cast<const uint32_t*>(reinterpret_cast<uint64_t>(src) & ~3ull);
-    for (uint32_t i = tid; i < nv; i += kThreads) {
-        uint4 v;
-        const uint32_t* wi = w + 4 * i;
-        const uint32_t a0 = __ldg(wi), a1 = __ldg(wi + 1), a2 = __ldg(wi + 2), a3 = __ldg(wi + 3);
-        if (sh == 0) {
-            v = make_uint4(a0, a1, a2, a3);
-        } else {
-            uint32_t a4;
-            if (16 * i + 20 <= n) a4 = __ldg(wi + 4);
-            else {
-                a4 = 0;
-                const uint8_t* b4 = reinterpret_cast<const uint8_t*>(wi + 4);
-                const int64_t lim = (int64_t)((uint64_t)(src + n) - reinterpret_cast<uint64_t>(b4));
-                for (int q = 0; q < 4 && q < lim; q++) a4 |= (uint32_t)b4[q] << (8 * q);
+    // four 16-byte pieces per thread in flight (loads first)
+    for (uint32_t i0 = tid; i0 < nv; i0 += 4 * kThreads) {
+        uint32_t a[4][5];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t i = i0 + u * kThreads;
+            if (i < nv) {
+                const uint32_t* wi = w + 4 * i;
+#pragma unroll
+                for (int q = 0; q < 4; q++) a[u][q] = __ldg(wi + q);
+                a[u][4] = (sh && 16 * i + 20 <= n) ? __ldg(wi + 4) : 0u;
             }
-            v = make_uint4(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh), __funnelshift_r(a2, a3, sh),
-                           __funnelshift_r(a3, a4, sh));
         }
-        reinterpret_cast<uint4*>(dst)[i] = v;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const uint32_t i = i0 + u * kThreads;
+            if (i >= nv) break;
+            uint4 v;
+            if (sh == 0) {
+                v = make_uint4(a[u][0], a[u][1], a[u][2], a[u][3]);
+            } else {
+                uint32_t a4 = a[u][4];
+                if (16 * i + 20 > n) {
+                    const uint8_t* b4 = reinterpret_cast<const uint8_t*>(w + 4 * i + 4);
+                    const int64_t lim = (int64_t)((uint64_t)(src + n) - reinterpret_cast<uint64_t>(b4));
+                    for (int q = 0; q < 4 && q < lim; q++) a4 |= (uint32_t)b4[q] << (8 * q);
+                }
+                v = make_uint4(__funnelshift_r(a[u][0], a[u][1], sh), __funnelshift_r(a[u][1], a[u][2], sh),
+                               __funnelshift_r(a[u][2], a[u][3], sh), __funnelshift_r(a[u][3], a4, sh));
+            }
+            reinterpret_cast<uint4*>(dst)[i] = v;
+        }
     }
     for (uint32_t i = nv * 16 + tid; i < n; i += kThreads) dst[i] = src[i];
 }
