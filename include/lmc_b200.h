@@ -11,6 +11,10 @@
  *   lmcg_decompress (+ lmcg_read_hints, lmcg_decompress_result) / lmcg_decompress_host
  *       <- lmc.stream.lmc_decompress        (pkg/src/lmc/stream.py:406-423)
  *       <- lmc.parallel.plmc_decompress     (pkg/src/lmc/parallel.py:106-128)
+ *   lmcg_decompress_apply
+ *       <- lmc.delta.xor_apply(prev, lmc_decompress(delta stream))
+ *          (pkg/src/lmc/delta.py:50-52, as lmc.chain.restore_step uses it,
+ *          pkg/src/lmc/chain.py:293-300), fused into the decode
  *   lmcg_validate_options
  *       <- lmc.stream._validate_options     (pkg/src/lmc/stream.py:287-301)
  *   lmcg_build_codebooks
@@ -49,6 +53,7 @@ extern "C" {
 #define LMCG_ERR_CAPACITY 8           /* caller buffer too small                      */
 #define LMCG_ERR_ARGUMENT 9           /* bad argument (NULL pointer, n < 0, ...)      */
 #define LMCG_ERR_RETRY 10             /* decompress hints too small: call again        */
+#define LMCG_ERR_SHAPE 11             /* ShapeMismatchError (xor_apply length mismatch) */
 
 /* ElementType wire codes (types.py:24-27) */
 #define LMCG_RAW8 0
@@ -139,8 +144,22 @@ int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
                     const lmcg_stream_hint* hints, void* d_out, uint64_t out_capacity,
                     const uint64_t* h_out_offsets, void* cuda_stream);
 
+/* lmcg_decompress followed by xor_apply (delta.py:50-52): stream i's payload
+ * is XORed with the prev_lengths[i] bytes at d_prev[i] on its way out, so
+ * d_out + offset receives prev ^ payload (the next checkpoint step when the
+ * stream holds the XOR delta against prev).  d_prev[i] may be the output
+ * location itself (in-place restore of a resident step) and may be NULL (plain
+ * decode of that stream).  The CRC check is on the payload, as in the
+ * reference; a payload whose length differs from prev_lengths[i] is reported
+ * as LMCG_ERR_SHAPE (xor_bytes, delta.py:20-21) after the decode's own
+ * errors, and nothing is XORed.  On any error the output bytes of that stream
+ * are unspecified (with d_prev[i] == output, the prev bytes are lost). */
+int lmcg_decompress_apply(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* stream_lengths, int n,
+                          const lmcg_stream_hint* hints, const void* const* d_prev, const uint64_t* prev_lengths,
+                          void* d_out, uint64_t out_capacity, const uint64_t* h_out_offsets, void* cuda_stream);
+
 /* Synchronise and report the last lmcg_decompress per stream: status
- * (LMCG_OK / UNSUPPORTED / CORRUPT / INTEGRITY, or LMCG_ERR_RETRY /
+ * (LMCG_OK / UNSUPPORTED / CORRUPT / INTEGRITY / SHAPE, or LMCG_ERR_RETRY /
  * LMCG_ERR_CAPACITY when the hints were too small), original length, element
  * type, flags and window count.  Any pointer may be NULL. */
 int lmcg_decompress_result(lmcg_ctx* ctx, int n, int32_t* h_status, uint64_t* h_orig_lengths,

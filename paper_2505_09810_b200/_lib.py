@@ -50,7 +50,7 @@ class lmcg_stream_hint(ctypes.Structure):
 EXPORTS = [
     "lmcg_create", "lmcg_destroy", "lmcg_last_error", "lmcg_version", "lmcg_validate_options",
     "lmcg_compress_bound", "lmcg_compress_workspace", "lmcg_compress", "lmcg_read_hints",
-    "lmcg_decompress", "lmcg_decompress_result", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
+    "lmcg_decompress", "lmcg_decompress_apply", "lmcg_decompress_result", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
     "lmcg_block_info", "lmcg_profile", "lmcg_profile_report", "lmcg_compress_plan_create", "lmcg_compress_plan_run",
     "lmcg_decompress_plan_create", "lmcg_decompress_plan_run", "lmcg_plan_output_bytes", "lmcg_plan_destroy", "lmcg_copy_to_host", "lmcg_fallback_segments", "lmcg_compress_part",
 ]
@@ -89,6 +89,9 @@ def load(path: str = SO_PATH):
         L.lmcg_read_hints.argtypes = [vp, P(vp), P(u64), ctypes.c_int, P(lmcg_stream_hint), vp]
         L.lmcg_decompress.restype = ctypes.c_int
         L.lmcg_decompress.argtypes = [vp, P(vp), P(u64), ctypes.c_int, P(lmcg_stream_hint), vp, u64, P(u64), vp]
+        L.lmcg_decompress_apply.restype = ctypes.c_int
+        L.lmcg_decompress_apply.argtypes = [vp, P(vp), P(u64), ctypes.c_int, P(lmcg_stream_hint), P(vp), P(u64), vp, u64,
+                                            P(u64), vp]
         L.lmcg_decompress_result.restype = ctypes.c_int
         L.lmcg_decompress_result.argtypes = [vp, ctypes.c_int, P(i32), P(u64), P(i32), P(i32), P(u64)]
         L.lmcg_compress_host.restype = ctypes.c_int

@@ -50,6 +50,7 @@ struct lmcg_ctx {
     bool dec_attr = false;
     int scandec_occ = 1;
     bool crc_attr = false;
+    bool serial = false;                  // LMCG_SERIAL=1: no side stream (per-kernel timing experiments)
     uint8_t* part_ws = nullptr;
     size_t part_ws_cap = 0;
     bool res_attr = false;
@@ -315,6 +316,7 @@ lmcg_ctx* lmcg_create(int device) {
     cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
+    if (const char* e = getenv("LMCG_SERIAL")) ctx->serial = e[0] == '1';
     return ctx;
 }
 
@@ -444,10 +446,12 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
             ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kThreads, kCrcSmem);
             ctx->crc_attr = true;
         }
-        CK(cudaEventRecord(ctx->fork_ev, st));
-        CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+        if (!ctx->serial) {
+            CK(cudaEventRecord(ctx->fork_ev, st));
+            CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
+        }
         const uint64_t need = (ncrc + kWarps - 1) / kWarps;
-        cudaStream_t sst = ctx->side;
+        cudaStream_t sst = ctx->serial ? st : ctx->side;
         ProfScope prof_scope_k_crc(ctx, "k_crc", sst);
         k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, sst>>>(
             d_wins, nwin, ncrc, ctx->d_crc, ctx->d_sh992, d_crcp);
@@ -819,7 +823,7 @@ int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
     auto* d_caps = reinterpret_cast<DecCaps*>(ctx->hws + o_caps);
     auto* d_sout = reinterpret_cast<DecStreamOut*>(ctx->hws + o_out);
     std::vector<DecStreamIn> in(n);
-    for (int i = 0; i < n; i++) in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i]};
+    for (int i = 0; i < n; i++) in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i], nullptr, 0};
     CK(cudaMemcpyAsync(d_in, in.data(), n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_caps, 0, n * sizeof(DecCaps), st));
     k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, nullptr, nullptr);
@@ -925,16 +929,17 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         k_fallback<<<grid, kThreads, dsm, st>>>(d_seg, nseg, d_sfail, d_st, d_scr);
     }
     if (ntile) { PROF(k_ungroup); k_ungroup<<<(unsigned)ntile, kThreads, 0, st>>>(d_win, nwin, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_st); }
-    { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st); }
+    { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st, d_in); }
     if (d_codes) k_status<<<(n + 255) / 256, 256, 0, st>>>(d_sout, d_st, n, d_codes);
     CK(cudaGetLastError());
     return LMCG_OK;
 }
 
-int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
-                    const lmcg_stream_hint* hints, void* d_out, uint64_t out_capacity, const uint64_t* h_out_offsets,
-                    void* cuda_stream) {
+static int decompress_impl(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
+                           const lmcg_stream_hint* hints, const void* const* d_prev, const uint64_t* prev_lens,
+                           void* d_out, uint64_t out_capacity, const uint64_t* h_out_offsets, void* cuda_stream) {
     if (!ctx || n < 0 || (n && (!d_streams || !lens || !hints))) return fail(ctx, LMCG_ERR_ARGUMENT, "bad arguments");
+    if (d_prev && !prev_lens) return fail(ctx, LMCG_ERR_ARGUMENT, "d_prev without prev_lengths");
     if (!ctx->d_crc) return fail(ctx, LMCG_ERR_CUDA, "no CUDA device: the LMC B200 path has no CPU fallback");
     if (int r = ensure_ctx(ctx)) return r;
     cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
@@ -948,7 +953,10 @@ int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
     if (int r = grow_pinned(ctx, hb)) return r;
     if (n) {
         DecStreamIn* pin_in = reinterpret_cast<DecStreamIn*>(ctx->pin);
-        for (int i = 0; i < n; i++) pin_in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i]};
+        for (int i = 0; i < n; i++) {
+            const uint8_t* pv = d_prev ? static_cast<const uint8_t*>(d_prev[i]) : nullptr;
+            pin_in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i], pv, pv ? prev_lens[i] : 0};
+        }
         memcpy(ctx->pin + (size_t)n * sizeof(DecStreamIn), P.caps.data(), (size_t)n * sizeof(DecCaps));
         CK(cudaMemcpyAsync(ws + o[D_IN], ctx->pin, (size_t)n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(ws + o[D_CAPS], ctx->pin + (size_t)n * sizeof(DecStreamIn), (size_t)n * sizeof(DecCaps),
@@ -956,6 +964,21 @@ int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
         CK(cudaEventRecord(ctx->pin_done, st));
     }
     return decompress_launch(ctx, n, P.nwin, P.nseg, P.nrec, P.nchunk, P.ntile, ws, o, d_out, nullptr, st);
+}
+
+int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
+                    const lmcg_stream_hint* hints, void* d_out, uint64_t out_capacity, const uint64_t* h_out_offsets,
+                    void* cuda_stream) {
+    return decompress_impl(ctx, d_streams, lens, n, hints, nullptr, nullptr, d_out, out_capacity, h_out_offsets,
+                           cuda_stream);
+}
+
+int lmcg_decompress_apply(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
+                          const lmcg_stream_hint* hints, const void* const* d_prev, const uint64_t* prev_lengths,
+                          void* d_out, uint64_t out_capacity, const uint64_t* h_out_offsets, void* cuda_stream) {
+    if (n && (!d_prev || !prev_lengths)) return fail(ctx, LMCG_ERR_ARGUMENT, "lmcg_decompress_apply needs d_prev and prev_lengths");
+    return decompress_impl(ctx, d_streams, lens, n, hints, d_prev, prev_lengths, d_out, out_capacity, h_out_offsets,
+                           cuda_stream);
 }
 
 lmcg_plan* lmcg_decompress_plan_create(lmcg_ctx* ctx, int n, const lmcg_stream_hint* hints, const uint64_t* len_bounds) {
@@ -1011,6 +1034,7 @@ int lmcg_decompress_result(lmcg_ctx* ctx, int n, int32_t* h_status, uint64_t* h_
         else if (s & ST_RETRY) code = LMCG_ERR_RETRY;
         else if (s & ST_CAPACITY) code = LMCG_ERR_CAPACITY;
         else if (s & ST_INTEGRITY) code = LMCG_ERR_INTEGRITY;
+        else if (s & ST_SHAPE) code = LMCG_ERR_SHAPE;
         if (h_status) h_status[i] = code;
         if (h_orig) h_orig[i] = so[i].orig;
         if (h_et) h_et[i] = (int32_t)so[i].et;

@@ -50,11 +50,13 @@ __device__ unsigned long long lmcg_dbg_ev[4096];   // 512 events x 8 words
 // decode on the parallel path; tests assert that it stays there.
 __device__ unsigned long long lmcg_fallback_segs;
 
-enum : uint32_t { ST_CORRUPT = 1, ST_INTEGRITY = 2, ST_UNSUPPORTED = 4, ST_RETRY = 8, ST_CAPACITY = 16 };
+enum : uint32_t { ST_CORRUPT = 1, ST_INTEGRITY = 2, ST_UNSUPPORTED = 4, ST_RETRY = 8, ST_CAPACITY = 16, ST_SHAPE = 32 };
 
 struct DecStreamIn {
     const uint8_t* p;
     uint64_t len;
+    const uint8_t* prev;      // lmcg_decompress_apply: XOR the payload with prev (nullptr: plain decode)
+    uint64_t prev_len;
 };
 
 // Per-stream capacity regions (host-computed from hints).
@@ -85,6 +87,7 @@ struct DecWin {
     uint64_t soff;            // window start within the stream payload
     uint64_t tile0;           // global first tile
     uint32_t ntile, w, stream, pad;
+    const uint8_t* prev;      // xor_apply source of this window's output (nullptr: none)
 };
 
 struct DecSeg {
@@ -152,6 +155,8 @@ __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __res
                     d.W = W; d.n = W / wdt; d.w = wdt; d.stream = (uint32_t)s; d.pad = 0;
                     d.goff = cp.scratch0 + scr; d.ooff = cp.out0 + opos; d.soff = opos;
                     d.tile0 = cp.tile0 + ntile; d.ntile = (uint32_t)wtiles;
+                    // xor_apply only with a prev of the payload's length (else k_finalize reports the mismatch)
+                    d.prev = (in[s].prev && in[s].prev_len == h.orig) ? in[s].prev + opos : nullptr;
                     wins[cp.win0 + nwin] = d;
                 }
                 uint64_t gpos = 0;
@@ -1411,7 +1416,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
 // each thread produces 64 contiguous output bytes and their raw CRC.
 __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__ wins, uint64_t nwin_total,
                                                     uint64_t ntile_total, const uint8_t* __restrict__ scratch,
-                                                    uint8_t* __restrict__ out, const CrcTables* __restrict__ ct,
+                                                    uint8_t* out /* may alias a window's prev */, const CrcTables* __restrict__ ct,
                                                     uint32_t* __restrict__ tile_crc, const uint32_t* __restrict__ status) {
     __shared__ uint32_t sh_slice[1024];
     __shared__ uint32_t sh_part[kWarps];
@@ -1440,7 +1445,9 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
     uint32_t c = 0;
     const bool full = lo_b >= Z;
     const uint64_t ob = t0 + lo_b - Z;
+    const uint8_t* pv = wd.prev;   // xor_apply (delta.py:50-52): out = payload ^ prev; the CRC is the payload's
     const bool vec = full && ((reinterpret_cast<uint64_t>(o) + ob) % 16 == 0) &&
+                     (!pv || (reinterpret_cast<uint64_t>(pv) + ob) % 16 == 0) &&
                      (w == 1 ? ((reinterpret_cast<uint64_t>(g) + ob) % 16 == 0)
                              : (((ob >> lg2w(w)) & 15) == 0 && (wd.n & 15) == 0));
     if (vec) {
@@ -1481,9 +1488,19 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
                 v[4 * q + 3] = __byte_perm(x01hi, x23hi, 0x7632);
             }
         }
+        if (pv) {
+            uint4 pq[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-            *reinterpret_cast<uint4*>(o + ob + 16 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            for (int q = 0; q < 4; q++) pq[q] = *reinterpret_cast<const uint4*>(pv + ob + 16 * q);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                *reinterpret_cast<uint4*>(o + ob + 16 * q) = make_uint4(v[4 * q] ^ pq[q].x, v[4 * q + 1] ^ pq[q].y,
+                                                                       v[4 * q + 2] ^ pq[q].z, v[4 * q + 3] ^ pq[q].w);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                *reinterpret_cast<uint4*>(o + ob + 16 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
 #pragma unroll
         for (int q = 0; q < 16; q++) c = crc_word(sh_slice, c, v[q]);
     } else {
@@ -1491,7 +1508,7 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
             const uint64_t ob1 = t0 + q - Z;
             const uint64_t e = ob1 >> lg2w(w), gg = ob1 - (e << lg2w(w));
             const uint8_t x = g[gg * wd.n + e];
-            o[ob1] = x;
+            o[ob1] = pv ? (uint8_t)(x ^ pv[ob1]) : x;
             c = crc_byte(sh_slice, c, x);
         }
     }
@@ -1509,7 +1526,7 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
 __global__ void __launch_bounds__(kThreads) k_finalize(const DecStreamOut* __restrict__ sout, const DecCaps* __restrict__ caps,
                                                      const DecWin* __restrict__ wins, int ns,
                                                      const uint32_t* __restrict__ tile_crc, const CrcTables* __restrict__ ct,
-                                                     uint32_t* __restrict__ status) {
+                                                     uint32_t* __restrict__ status, const DecStreamIn* __restrict__ in) {
     __shared__ uint32_t red[kThreads];
     const int s = blockIdx.x;
     if (s >= ns) return;
@@ -1530,6 +1547,9 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const DecStreamOut* __res
     if (threadIdx.x == 0) {
         const uint32_t crc = acc ^ crc_shift_bytes(ct, 0xFFFFFFFFu, h.orig) ^ 0xFFFFFFFFu;
         if (crc != h.crc) atomicOr(&status[s], ST_INTEGRITY);
+        // lmcg_decompress_apply: xor_bytes' length check comes after the decode
+        // and its CRC check (chain.py:296-300 -> delta.py:20-21)
+        else if (in[s].prev && in[s].prev_len != h.orig) atomicOr(&status[s], ST_SHAPE);
     }
 }
 
@@ -1538,7 +1558,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const DecStreamOut* __res
 __global__ void k_mkin(const uint8_t* __restrict__ base, const uint64_t* __restrict__ offsets,
                        const uint64_t* __restrict__ lengths, int n, DecStreamIn* __restrict__ in) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) in[i] = DecStreamIn{base + offsets[i], lengths[i]};
+    if (i < n) in[i] = DecStreamIn{base + offsets[i], lengths[i], nullptr, 0};
 }
 
 // Final per-stream status as C-ABI codes (LMCG_*), written to device memory.
@@ -1553,6 +1573,7 @@ __global__ void k_status(const DecStreamOut* __restrict__ sout, const uint32_t* 
     else if (s & ST_RETRY) code = 10;
     else if (s & ST_CAPACITY) code = 8;
     else if (s & ST_INTEGRITY) code = 3;
+    else if (s & ST_SHAPE) code = 11;
     out[i] = code;
 }
 

@@ -220,7 +220,8 @@ class DecompressedBatch:
         for i, s in enumerate(self.status):
             if s:
                 raise_status(s, f"stream {i}: " + {1: "unsupported format", 2: "corrupt stream",
-                                                   3: "payload CRC mismatch"}.get(s, f"status {s}"))
+                                                   3: "payload CRC mismatch",
+                                                   11: "payload length differs from prev"}.get(s, f"status {s}"))
 
 
 class Codec:
@@ -372,13 +373,19 @@ class Codec:
         self.ctx.check(self.ctx.lib.lmcg_read_hints(self.ctx.ptr, ptrs, lens, n, hs, ctypes.c_void_p(s.cuda_stream)))
         return [(hs[i].orig, hs[i].segments, hs[i].block, hs[i].windows) for i in range(n)]
 
-    def decompress(self, streams, *, hints=None, out=None, stream=None) -> DecompressedBatch:
+    def decompress(self, streams, *, hints=None, out=None, out_offsets=None, prev=None,
+                   stream=None) -> DecompressedBatch:
         """Decode device streams (a CompressedBatch or a list of CUDA byte tensors).
 
         ``hints`` (per stream: original length, segment count, block size,
         window count) size the device work areas; a CompressedBatch carries
         exact ones, otherwise they are read from the stream headers.  Wrong
-        hints only cost a retry.
+        hints only cost a retry.  ``out`` + ``out_offsets`` place stream i's
+        payload at ``out[out_offsets[i]:]`` (default: packed at 16-byte
+        aligned offsets in a fresh buffer).  ``prev`` (per stream a device
+        tensor or None) fuses ``xor_apply`` (delta.py:50-52) into the decode:
+        the output is ``prev ^ payload``; ``prev`` may be the output location
+        itself (in-place restore, lmcg_decompress_apply).
         """
         import torch
 
@@ -399,6 +406,21 @@ class Codec:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         ptrs = (ctypes.c_void_p * max(n, 1))(*[v.data_ptr() if v.numel() else 0 for v in views])
         lens = (ctypes.c_uint64 * max(n, 1))(*[v.numel() for v in views])
+        pptr = plen = None
+        if prev is not None:
+            if len(prev) != n:
+                raise ValueError("prev needs one entry (tensor or None) per stream")
+            pviews = [None if p is None else _bytes_view(p) for p in prev]
+            pptr = (ctypes.c_void_p * max(n, 1))(*[0 if p is None else (p.data_ptr() or 0) for p in pviews])
+            plen = (ctypes.c_uint64 * max(n, 1))(*[0 if p is None else p.numel() for p in pviews])
+            # an empty prev is still a prev (length 0): point it somewhere non-NULL
+            for i, p in enumerate(pviews):
+                if p is not None and not pptr[i]:
+                    pptr[i] = views[i].data_ptr() or 16
+        if out_offsets is not None:
+            if out is None or len(out_offsets) != n:
+                raise ValueError("out_offsets needs out and one offset per stream")
+            out = _bytes_view(out)
         for _ in range(3):
             hs = (_lib.lmcg_stream_hint * max(n, 1))()
             offs, pos = [], 0
@@ -406,11 +428,18 @@ class Codec:
                 hs[i].orig, hs[i].segments, hs[i].block, hs[i].windows = (int(x) for x in h)
                 offs.append(pos)
                 pos += (int(h[0]) + 15) & ~15
-            if out is None or out.numel() < pos:
+            if out_offsets is not None:
+                offs = [int(x) for x in out_offsets]
+            elif out is None or out.numel() < pos:
                 out = torch.empty(max(pos, 16), dtype=torch.uint8, device=self.device)
             hoff = (ctypes.c_uint64 * max(n, 1))(*offs)
-            self.ctx.check(self.ctx.lib.lmcg_decompress(self.ctx.ptr, ptrs, lens, n, hs, out.data_ptr(), out.numel(),
-                                                        hoff, ctypes.c_void_p(s.cuda_stream)))
+            if pptr is None:
+                rc = self.ctx.lib.lmcg_decompress(self.ctx.ptr, ptrs, lens, n, hs, out.data_ptr(), out.numel(), hoff,
+                                                  ctypes.c_void_p(s.cuda_stream))
+            else:
+                rc = self.ctx.lib.lmcg_decompress_apply(self.ctx.ptr, ptrs, lens, n, hs, pptr, plen, out.data_ptr(),
+                                                        out.numel(), hoff, ctypes.c_void_p(s.cuda_stream))
+            self.ctx.check(rc)
             st = (ctypes.c_int32 * max(n, 1))()
             orig = (ctypes.c_uint64 * max(n, 1))()
             ets = (ctypes.c_int32 * max(n, 1))()
@@ -418,7 +447,7 @@ class Codec:
             nw = (ctypes.c_uint64 * max(n, 1))()
             self.ctx.check(self.ctx.lib.lmcg_decompress_result(self.ctx.ptr, n, st, orig, ets, fl, nw))
             status = list(st)[:n]
-            retry = [i for i in range(n) if status[i] in (8, 10)]
+            retry = [i for i in range(n) if status[i] == 10 or (status[i] == 8 and out_offsets is None)]
             if not retry:
                 return DecompressedBatch(out, offs, list(orig)[:n], list(ets)[:n], list(fl)[:n], status)
             hints = [((int(orig[i]), int(hints[i][1]), int(hints[i][2]), int(nw[i])) if i in retry else hints[i])
