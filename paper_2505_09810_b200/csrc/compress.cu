@@ -763,10 +763,15 @@ __device__ __forceinline__ int tile_piece(const WinDesc& wd, uint64_t tp, uint64
 constexpr int kSlot = (kEncRun * kMaxLen + 31) / 32 + 1;   // private words per run
 constexpr int kStageWords = (kEncRun * kThreads * kMaxLen) / 32 + 8;
 
-template <int W>
+// RUN: the block's code has a 1-bit codeword, which canonical assignment
+// makes '0' (huffman.py:213-225), for symbol `runsym`.  Each thread then only
+// looks up the other symbols of a piece (XOR deltas: a few percent of the
+// bytes) and appends the run symbols between them as zero bits, instead of a
+// table lookup per symbol.
+template <int W, bool RUN>
 __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const uint32_t* sh_code,
                             uint32_t* sh_wsum, uint32_t* stg, uint32_t* gw, uint32_t lead,
-                            uint32_t& bitpos, uint64_t& base_word) {
+                            uint32_t& bitpos, uint64_t& base_word, uint32_t runsym) {
     constexpr uint32_t lw = W == 1 ? 0 : (W == 2 ? 1 : 2);
     constexpr int per = 16 >> lw;   // symbols per 16-byte piece
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -781,14 +786,46 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
         // pack the run into the private slot
         uint64_t acc = 0;
         uint32_t n = 0, wi = 0;
+        uint32_t pend = 0;   // RUN: run symbols not yet appended (<= kEncRun)
+        const uint32_t rep4 = runsym * 0x01010101u;
+        auto put = [&](uint32_t l, uint32_t code) {
+            acc = (acc << l) | code;
+            n += l;
+            const bool fl = n >= 32;
+            n -= fl ? 32 : 0;
+            if (fl) priv[wi] = (uint32_t)(acc >> n);
+            wi += fl ? 1 : 0;
+        };
+        auto zeros = [&](uint32_t z) {   // z <= 64 zero bits, in two steps of <= 32
+            const uint32_t t1 = min(z, 32u);
+            put(t1, 0u);
+            put(z - t1, 0u);
+        };
+        // fast runs: the loads run kAhead pieces ahead of the packing (the
+        // kernel is otherwise bound by load latency at its occupancy)
+        constexpr int kAhead = 2;
+        uint4 la[kAhead], lc[kAhead];
+#pragma unroll
+        for (int u = 0; u < kAhead; u++) {
+            la[u] = lc[u] = make_uint4(0, 0, 0, 0);
+            if (fast && q0 + (uint64_t)u * per < q1) {
+                la[u] = __ldg(reinterpret_cast<const uint4*>(srcp + ((uint64_t)u * per << lw)));
+                if (prvp) lc[u] = __ldg(reinterpret_cast<const uint4*>(prvp + ((uint64_t)u * per << lw)));
+            }
+        }
         for (uint64_t pos = q0; pos < q1; pos += per) {
             uint32_t sy[4];
             int ns;
             if (fast) {
-                uint4 a = __ldg(reinterpret_cast<const uint4*>(srcp + ((pos - q0) << lw)));
-                if (prvp) {
-                    const uint4 c = __ldg(reinterpret_cast<const uint4*>(prvp + ((pos - q0) << lw)));
-                    a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
+                uint4 a = la[0];
+                const uint4 c = lc[0];
+                a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
+#pragma unroll
+                for (int u = 0; u + 1 < kAhead; u++) { la[u] = la[u + 1]; lc[u] = lc[u + 1]; }
+                const uint64_t nx = pos + (uint64_t)kAhead * per;
+                if (nx < q1) {
+                    la[kAhead - 1] = __ldg(reinterpret_cast<const uint4*>(srcp + ((nx - q0) << lw)));
+                    if (prvp) lc[kAhead - 1] = __ldg(reinterpret_cast<const uint4*>(prvp + ((nx - q0) << lw)));
                 }
                 ns = piece_symbols(a, W, (uint32_t)g, sy);
             } else {
@@ -796,11 +833,35 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
                 ns = 0;
                 for (int i = 0; i < per && pos + i < q1; i++, ns++) sy[i >> 2] |= gather_byte(wd, pos + i) << (8 * (i & 3));
             }
+            if (RUN) {
+                // bit i of the piece's group: symbol i is not the run symbol
+                uint32_t m = 0;
+#pragma unroll
+                for (int k = 0; k < (per + 3) / 4; k++) {
+                    const uint32_t r = __vcmpne4(sy[k], rep4) & 0x80808080u;
+                    m |= ((r * 0x00204081u) >> 28) << (4 * k);
+                }
+                m &= (1u << ns) - 1;   // ns <= 16
+                uint32_t last = 0;
+                while (m) {
+                    const uint32_t i = __ffs(m) - 1;
+                    m &= m - 1;
+                    zeros(pend + i - last);
+                    pend = 0;
+                    last = i + 1;
+                    uint32_t word = sy[0];
+                    if (per > 4) word = (i >> 2) == 1 ? sy[1] : word;
+                    if (per > 8) { word = (i >> 2) == 2 ? sy[2] : word; word = (i >> 2) == 3 ? sy[3] : word; }
+                    const uint32_t e = sh_code[(word >> (8 * (i & 3))) & 0xFF];
+                    put(e >> 16, e & 0xFFFF);
+                }
+                pend += ns - last;
+            }
             // symbol pairs: two codes (<= 30 bits) joined in 32 bits, one
             // accumulator update and at most one word flush per pair
 #pragma unroll
             for (int i = 0; i < per; i += 2) {
-                if (i < ns) {
+                if (!RUN && i < ns) {
                     const uint32_t e1 = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
                     const uint32_t e2 = (i + 1 < ns) ? sh_code[(sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF] : 0u;
                     const uint32_t l2 = e2 >> 16;
@@ -814,6 +875,7 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
                 }
             }
         }
+        if (RUN) zeros(pend);
         const uint32_t nwp = wi + (n ? 1 : 0);
         if (n) priv[wi] = (uint32_t)(acc << (32 - n));
         const uint32_t nb = wi * 32 + n;
@@ -938,6 +1000,7 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     __shared__ uint32_t sh_cnt[kWarps][16];
     __shared__ uint32_t sh_first[16];
     __shared__ uint32_t sh_wsum[kWarps];
+    __shared__ uint32_t sh_run;   // symbol with the 1-bit code '0', or 256
     const uint64_t slot = blockIdx.x;
     if (slot >= nslots) return;
     const WinDesc wd = wins[slot2win[slot]];
@@ -1015,10 +1078,22 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     uint32_t bitpos = lead;     // staging coordinate of the next bit (< 32 at a round start)
     uint64_t base_word = 0;     // global word index (relative to gw) of stg[0]
     if (tid == 0) stg[0] = 0;
+    if (tid == 0) sh_run = 256;
     __syncthreads();
-    if (w == 1) encode_runs<1>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word);
-    else if (w == 2) encode_runs<2>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word);
-    else encode_runs<4>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word);
+    if (sh_code[tid] == (1u << 16)) sh_run = tid;
+    __syncthreads();
+    // the run path pays off only when most symbols are the run symbol
+    // (<= 1.5 code bits per symbol on average: XOR deltas, sparse tensors)
+    const uint32_t rs = ((uint64_t)m.bits * 2 <= (uint64_t)(p1 - p0) * 3) ? sh_run : 256u;
+    if (rs < 256) {
+        if (w == 1) encode_runs<1, true>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
+        else if (w == 2) encode_runs<2, true>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
+        else encode_runs<4, true>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
+    } else {
+        if (w == 1) encode_runs<1, false>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
+        else if (w == 2) encode_runs<2, false>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
+        else encode_runs<4, false>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
+    }
     // trailing partial word: bytes up to the record end
     if (tid == 0 && bitpos) {
         const uint32_t v = bswap32(stg[0]);

@@ -24,6 +24,8 @@
 //   k_ungroup   inverse byte-grouping per window (bytegroup.py:53-62) + raw
 //               CRC-32 of each 16 KiB output tile
 //   k_finalize  per-stream CRC combine and status (stream.py:416-423)
+#include <type_traits>
+
 #include "lmc_common.cuh"
 
 namespace lmcg {
@@ -309,7 +311,7 @@ __device__ __forceinline__ uint32_t step1(const DecSmem& s, uint32_t win, uint32
 // The bulk loop is branch-free apart from codes longer than kLut bits:
 // one 32-bit window (two word reads + funnel shift), one table lookup, up to
 // three symbols.
-template <bool EMIT, bool STAGED>
+template <bool EMIT, bool STAGED, bool RUN>
 __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32_t lim, uint32_t p0, int bm,
                                 uint32_t& count, uint8_t* dst, uint32_t* hit) {
     // Lanes decode different chunks with different trip counts: every loop is
@@ -330,6 +332,11 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         bnj = j0 + 2;
     }
     auto win = [&]() -> uint32_t { return STAGED ? (uint32_t)(bbuf >> 32) : src.template peek<STAGED>(pos); };
+    // a 1-bit codeword is '0' (canonical codes start at zero): every leading
+    // zero bit of the window is one more of that symbol, so runs of it (XOR
+    // deltas are mostly zero bytes) go many symbols per lookup
+    constexpr bool run1 = RUN;   // (the record has a 1-bit codeword)
+    const uint64_t rep8 = RUN ? s.csym[s.first_idx[1]] * 0x0101010101010101ull : 0ull;
     auto adv = [&](uint32_t l) {
         pos += l;
         if (STAGED) {
@@ -350,7 +357,31 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         while (__any_sync(mask, act)) {
             if (act) {
                 uint32_t sym;
-                const uint32_t l = step1(s, win(), sym);
+                const uint32_t wv = win();
+                // a run of the 1-bit symbol: its z boundaries pos+1 .. pos+z at once
+                const uint32_t z = RUN ? min((uint32_t)__clz(wv), min(lim - pos, p0 + 64 - pos)) : 0u;
+                if (RUN && z) {
+                    const int r0 = (int)(pos - p0);          // may be negative (fix-up before p0)
+                    const int lo = max(r0 + 1, 0), hi = min(r0 + (int)z, 63);
+                    const uint64_t mk = lo <= hi ? ((~0ull >> (63 - hi + lo)) << lo) : 0ull;
+                    uint32_t take = z;
+                    if (bm == 1) {
+                        m0 |= (uint32_t)mk;
+                        m1 |= (uint32_t)(mk >> 32);
+                    } else {
+                        const uint64_t m = ((uint64_t)m1 << 32) | m0;
+                        const uint64_t h = m & mk;
+                        if (h) {   // synchronised at the first old boundary on the run
+                            const int b = __ffsll((long long)h) - 1;
+                            take = (uint32_t)(b - r0);
+                            *hit = __popcll(m & (~0ull >> (63 - b)));
+                            done = true;
+                        }
+                    }
+                    adv(take);
+                    c += take;
+                } else {
+                const uint32_t l = step1(s, wv, sym);
                 if (!l) {
                     bad = true;
                 } else {
@@ -368,6 +399,7 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
                         }
                     }
                 }
+                }
                 act = !bad && !done && pos < lim && pos < p0 + 64;
             }
         }
@@ -380,12 +412,23 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         for (int k = 0; k < kCheckpoints; k++) {
             const uint32_t T = p0 + (128u << k);
             const bool on = bm != 0 && !bad && !done && T < lim;
-            bool a2 = on && pos + kCntLut <= T;
+            constexpr int kCW = RUN ? kLut : kCntLut;
+            bool a2 = on && pos + kCW <= T;
             while (__any_sync(mask, a2)) {
                 if (a2) {
                     const uint32_t wv = win();
-                    const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
-                    uint32_t n = e >> 4, tl = e & 15;
+                    uint32_t n, tl;
+                    if (RUN) {
+                        const uint32_t e = s.lut3[wv >> (32 - kLut)];
+                        n = e >> 30; tl = (e >> 26) & 15;
+                    } else {
+                        const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
+                        n = e >> 4; tl = e & 15;
+                    }
+                    if (run1) {
+                        const uint32_t z = min((uint32_t)__clz(wv), T - pos);
+                        if (z > n) { n = z; tl = z; }
+                    }
                     if (n == 0) {
                         uint32_t sym;
                         tl = step1(s, wv, sym);
@@ -394,7 +437,7 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
                     }
                     adv(tl);
                     c += n;
-                    a2 = !bad && pos + kCntLut <= T;
+                    a2 = !bad && pos + kCW <= T;
                 }
             }
             a2 = on && !bad && pos < T;
@@ -439,18 +482,33 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     uint64_t* w = reinterpret_cast<uint64_t*>(d);
     uint64_t acc = 0;
     uint32_t nacc = 0;
-    constexpr int kW = EMIT ? kLut : kCntLut;   // window bits of the bulk lookups
+    constexpr int kW = (EMIT || RUN) ? kLut : kCntLut;   // window bits of the bulk lookups
     bool act = !bad && !done && pos + kW <= lim;
     // bulk: up to three symbols (count passes: twelve) per table lookup, two lookups per vote
     auto lookup = [&]() {
         const uint32_t wv = win();
-        uint32_t n, tl, packed = 0;
+        uint32_t n, tl;
+        using PackT = typename std::conditional<RUN, uint64_t, uint32_t>::type;
+        PackT packed = 0;
         if (EMIT) {
             const uint32_t e = s.lut3[wv >> (32 - kLut)];
             n = e >> 30; tl = (e >> 26) & 15; packed = e & 0xFFFFFF;
+            if (run1) {   // up to 8 run symbols: one 8-byte store at most
+                const uint32_t z = min((uint32_t)__clz(wv), 8u);
+                if (z > n) { n = z; tl = z; packed = rep8 >> (64 - 8 * z); }
+            }
         } else {
-            const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
-            n = e >> 4; tl = e & 15;
+            if (RUN) {   // counting with the 3-symbol table (run records build no count LUT)
+                const uint32_t e = s.lut3[wv >> (32 - kLut)];
+                n = e >> 30; tl = (e >> 26) & 15;
+            } else {
+                const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
+                n = e >> 4; tl = e & 15;
+            }
+            if (run1) {
+                const uint32_t z = min((uint32_t)__clz(wv), lim - pos);
+                if (z > n) { n = z; tl = z; }
+            }
         }
         if (n == 0) {
             uint32_t sym;
@@ -465,11 +523,12 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         if (EMIT) {   // branch-free packing: predicated 8-byte store
             acc |= (uint64_t)packed << (8 * nacc);
             const uint32_t nn = nacc + n;
-            const bool full = nn >= 8;   // (implies nacc >= 5)
+            const bool full = nn >= 8;   // (without runs: implies nacc >= 5)
             asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.u64 [%0], %1; }"
                          :: "l"(w), "l"(acc), "r"((uint32_t)full) : "memory");
             w += full ? 1 : 0;
-            acc = full ? ((uint64_t)packed >> (8 * (8 - nacc))) : acc;
+            if (RUN) acc = full ? (nacc ? (uint64_t)packed >> (8 * (8 - nacc)) : 0ull) : acc;
+            else acc = full ? ((uint64_t)packed >> (8 * (8 - nacc))) : acc;
             nacc = full ? nn - 8 : nn;
         }
     };
@@ -514,7 +573,7 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
 }
 
 // All passes over the chunks of one record (see huff_decode).
-template <bool STAGED>
+template <bool STAGED, bool RUN>
 __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t bits, uint32_t len, uint8_t* dst) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint32_t S = (bits + kThreads - 1) / kThreads;
@@ -534,7 +593,7 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
         if (gq > 1) p0 = ((p0 + gq - 1) / gq) * gq;
         my_start = p0;
         if (my_start >= lim) { my_end = my_start; s.bm[0][tid] = 0; s.bm[1][tid] = 0; }
-        else my_end = decode_span<false, STAGED>(s, src, my_start, lim, p0, 1, my_cnt, nullptr, nullptr);
+        else my_end = decode_span<false, STAGED, RUN>(s, src, my_start, lim, p0, 1, my_cnt, nullptr, nullptr);
         s.end[c] = my_end;
     }
     __syncthreads();
@@ -556,7 +615,7 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
                 my_cnt = 0;
             } else {
                 uint32_t h = ~0u, cnt2 = 0;
-                const uint32_t e2 = decode_span<false, STAGED>(s, src, my_start, lim, p0, 2, cnt2, nullptr, &h);
+                const uint32_t e2 = decode_span<false, STAGED, RUN>(s, src, my_start, lim, p0, 2, cnt2, nullptr, &h);
                 DBG_ADD(6, h == ~0u);
 #ifdef LMCG_DEBUG
                 if (h == ~0u) {
@@ -604,7 +663,7 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
     DBG_T0(t_emit);
     if (c < nch && my_cnt) {
         uint32_t cc;
-        decode_span<true, STAGED>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
+        decode_span<true, STAGED, RUN>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
     }
     __syncthreads();
     DBG_TADD(20, t_emit);
@@ -734,7 +793,9 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
         if (n) ent = (n << 30) | (tl << 26) | syms;
         s.lut3[e] = ent;
     }
-    // count LUT: every whole codeword of a 12-bit window (greedy)
+    // count LUT: every whole codeword of a 12-bit window (greedy); records
+    // with a 1-bit code count with the 3-symbol LUT plus runs instead
+    if (!s.bl_count[1])
     for (int e = tid; e < (1 << kCntLut); e += kThreads) {
         uint32_t n = 0, tl = 0;
         for (;;) {
@@ -763,9 +824,9 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
         St.sh = (uint32_t)(reinterpret_cast<uint64_t>(data) - a16) * 8;
         St.glimit = (uint64_t)(data - St.gbase) + nbytes;
         St.nwords_full = St.glimit / 4;
-        return huff_passes<true>(s, St, bits, len, dst);
+        return s.bl_count[1] ? huff_passes<true, true>(s, St, bits, len, dst) : huff_passes<true, false>(s, St, bits, len, dst);
     }
-    return huff_passes<false>(s, G, bits, len, dst);
+    return s.bl_count[1] ? huff_passes<false, true>(s, G, bits, len, dst) : huff_passes<false, false>(s, G, bits, len, dst);
 }
 
 __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t n) {

@@ -299,3 +299,39 @@ def test_false_candidates_inside_payload(codec):
     assert b.to_bytes()[0] == O.compress(data, 0, byte_group=False, block_size=B)
     r = codec.decompress(b)
     assert r.status == [0] and host_bytes(r.payload(0)) == data
+
+
+@pytest.mark.parametrize("et", [ET.RAW8, ET.BF16, ET.FP32])
+@pytest.mark.parametrize("density", [0.002, 0.03, 0.2])
+def test_run_symbol_paths(codec, et, density):
+    """Blocks with a 1-bit code (the encoder's and decoder's run paths):
+    sparse byte streams of every width, aligned and unaligned device views,
+    plain and as fused XOR deltas, against the oracle byte for byte."""
+    g = np.random.default_rng(int(density * 1e4) + et.code)
+    n = 3 * 65536 + 4 * 4099
+    base = np.zeros(n + 64, np.uint8)
+    hits = g.random(n + 64) < density
+    base[hits] = g.integers(1, 256, int(hits.sum()), dtype=np.uint8)
+    prev = g.integers(0, 256, n + 64, dtype=np.uint8)
+    dev = torch.from_numpy(base).cuda()
+    fallback_segments(codec)
+    for off in (0, et.width * 3):   # 16-byte aligned view, and one that is not
+        size = (n // et.width) * et.width
+        x = base[off: off + size]
+        t = dev[off: off + size]
+        for block in (4096, 65536):
+            b = codec.compress([t], element_types=[et.code], block_size=block)
+            s = b.to_bytes()[0]
+            assert s == O.compress(x.tobytes(), et.code, block_size=block), (off, block)
+            r = codec.decompress(b)
+            r.raise_for_status()
+            assert torch.equal(r.payload(0), t)
+        # delta: cur = prev ^ sparse, so the delta stream encodes the sparse bytes
+        p = torch.from_numpy(prev[:size].copy()).cuda()
+        cur = p ^ t
+        b = codec.compress([cur], element_types=[et.code], prev=[p])
+        assert b.to_bytes()[0] == O.compress(x.tobytes(), et.code, delta=True)
+        r = codec.decompress(b, prev=[p])
+        r.raise_for_status()
+        assert torch.equal(r.payload(0), cur)
+    assert fallback_segments(codec) == 0

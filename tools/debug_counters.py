@@ -13,8 +13,11 @@ import paper_2505_09810_b200 as lmcb
 from paper_2505_09810_b200 import synth
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 specs, ts = synth.make_checkpoint(cfg, seed=int(sys.argv[2]) if len(sys.argv) > 2 else 5)
+prev = None
+if len(sys.argv) > 3 and sys.argv[3] == "delta":
+    prev, ts = ts, [synth.next_step(w, 5, i) for i, w in enumerate(ts)]
 codec = lmcb.Codec()
-b = codec.compress(ts)
+b = codec.compress(ts, prev=prev)
 cnt = (ctypes.c_ulonglong * 32)()
 L.lmcg_debug_counters(cnt, 1)
 r = codec.decompress(b)
