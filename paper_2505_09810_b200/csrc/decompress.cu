@@ -939,12 +939,22 @@ __device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint6
     uint32_t mode, l;
     uint64_t ps;
     if (!rec_size_dev(seg, comp, pos, mode, l, ps)) return false;
+    // what an encoder writes: a Huffman record has a non-empty bit stream
+    // smaller than the stored record (stream.py:173) ...
     if (mode == MODE_HUFFMAN) {
-        // what an encoder writes: a non-empty bit stream smaller than the
-        // stored record (stream.py:173) and a codebook within the Kraft bound
-        // (huffman.py:191-210); byte runs inside payloads rarely pass both
         const uint32_t bits = rd32(seg + pos + 5 + 128);
         if (bits == 0 || kHuffOverhead + ((uint64_t)bits + 7) / 8 > B) return false;
+    }
+    // ... and is followed by the segment end or another record header (the
+    // cheap test that rejects most byte patterns inside payloads) ...
+    const uint64_t q = pos + 5 + ps;
+    if (q != comp) {
+        if (q + 5 > comp || seg[q] > 2) return false;
+        const uint32_t l2 = rd32(seg + q + 1);
+        if (l2 != B && l2 != Ltail) return false;
+    }
+    // ... and a codebook within the Kraft bound (huffman.py:191-210)
+    if (mode == MODE_HUFFMAN) {
         uint32_t kraft = 0;
         const uint8_t* cb = seg + pos + 5;
         for (int i = 0; i < 128; i++) {
@@ -953,11 +963,7 @@ __device__ __forceinline__ bool is_cand(const uint8_t* seg, uint64_t comp, uint6
         }
         if (kraft == 0 || kraft > (1u << kMaxLen)) return false;
     }
-    const uint64_t q = pos + 5 + ps;
-    if (q == comp) return true;
-    if (q + 5 > comp || seg[q] > 2) return false;
-    const uint32_t l2 = rd32(seg + q + 1);
-    return l2 == B || l2 == Ltail;
+    return true;
 }
 
 // Candidates of positions [pa, pe) of a segment, found by one warp with
