@@ -147,6 +147,7 @@ def _bytes_view(t):
 
     if not t.is_cuda:
         raise DeviceError("Codec inputs must be CUDA tensors")
+    t = t.detach()   # parameters: bytes only, no autograd
     if not t.is_contiguous():
         t = t.contiguous()
     return t.view(torch.uint8).reshape(-1) if t.numel() else torch.empty(0, dtype=torch.uint8, device=t.device)
