@@ -385,6 +385,7 @@ static size_t compress_layout(const CPlan& P, int n, size_t* offs /* 16 */) {
     offs[10] = a.take<uint32_t>(nb + 1);
     offs[11] = a.take<uint64_t>(n + 1);
     offs[12] = a.take<uint64_t>(n + 1);
+    offs[13] = a.take<uint32_t>(P.ncrc + 1);   // CRC chunk -> window
     return a.off + 256;
 }
 
@@ -436,7 +437,8 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
     const uint64_t ntiles = (nb + kScanTile - 1) / kScanTile;
     CK(cudaMemsetAsync(d_status, 0, (ntiles + 1) * sizeof(uint64_t), st));
     CK(cudaMemsetAsync(d_ctr, 0, 4 * sizeof(uint32_t), st));
-    if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win); }
+    uint32_t* d_crc2win = reinterpret_cast<uint32_t*>(ws + offs[13]);
+    if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win, ncrc ? d_crc2win : nullptr); }
     // k_crc only reads the tensors: it runs on the side stream, overlapping
     // the histogram / codebook / encode chain, and joins before k_frame
     const bool fork = ncrc && n && !part;
@@ -454,7 +456,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         cudaStream_t sst = ctx->serial ? st : ctx->side;
         ProfScope prof_scope_k_crc(ctx, "k_crc", sst);
         k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, sst>>>(
-            d_wins, nwin, ncrc, ctx->d_crc, ctx->d_sh992, d_crcp);
+            d_wins, d_crc2win, ncrc, ctx->d_crc, ctx->d_sh992, d_crcp);
         CK(cudaEventRecord(ctx->join_ev, sst));
     }
 
@@ -571,7 +573,7 @@ int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* 
     // raw CRC of the element bytes [crc_begin, crc_end): k_crc over one
     // pseudo-window, then one combine
     const uint64_t nchunk = (L + kCrcChunk - 1) / kCrcChunk;
-    if (int r = grow(ctx, &ctx->part_ws, &ctx->part_ws_cap, 256 + 4 * (nchunk + 1))) return r;
+    if (int r = grow(ctx, &ctx->part_ws, &ctx->part_ws_cap, 256 + 8 * (nchunk + 1))) return r;
     WinDesc cw{};
     cw.src = static_cast<const uint8_t*>(t->data) + crc_begin;
     cw.prev = t->prev ? static_cast<const uint8_t*>(t->prev) + crc_begin : nullptr;
@@ -588,8 +590,10 @@ int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* 
         ctx->crc_attr = true;
     }
     uint32_t* parts = reinterpret_cast<uint32_t*>(ctx->part_ws + 256);
+    uint32_t* one_win = parts + nchunk + 1;   // every chunk -> window 0
+    CK(cudaMemsetAsync(one_win, 0, 4 * (nchunk + 1), st));
     k_crc<<<(unsigned)std::min<uint64_t>((nchunk + kWarps - 1) / kWarps, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, st>>>(
-        reinterpret_cast<const WinDesc*>(ctx->part_ws), 1, nchunk, ctx->d_crc, ctx->d_sh992, parts);
+        reinterpret_cast<const WinDesc*>(ctx->part_ws), one_win, nchunk, ctx->d_crc, ctx->d_sh992, parts);
     k_crc_join<<<1, kThreads, 0, st>>>(parts, L, ctx->d_crc, d_crc);
     CK(cudaGetLastError());
     return LMCG_OK;
@@ -846,7 +850,7 @@ int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
 
 namespace {
 // Workspace layout of one decompress (offsets into the workspace).
-enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CAND, D_CCNT, D_CTOT, D_CPRE, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_TC, D_SCR, D_NOFF };
+enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CAND, D_CCNT, D_CTOT, D_CPRE, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_TC, D_MAPS, D_SCR, D_NOFF };
 size_t dec_layout(const DPlan& P, int n, size_t* o) {
     Arena a;
     o[D_IN] = a.take<DecStreamIn>(n + 1);
@@ -864,6 +868,7 @@ size_t dec_layout(const DPlan& P, int n, size_t* o) {
     o[D_RPOS] = a.take<uint64_t>(P.nrec + 1);
     o[D_RNEXT] = a.take<uint64_t>(P.nrec + 1);
     o[D_TC] = a.take<uint32_t>(P.ntile + 1);
+    o[D_MAPS] = a.take<uint32_t>(P.nchunk + P.nrec + P.ntile + 3);   // chunk2seg | rec2seg | tile2win
     o[D_SCR] = a.take<uint8_t>(P.scratch + 64);
     return a.off + 256;
 }
@@ -889,6 +894,9 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     auto* d_rpos = reinterpret_cast<uint64_t*>(ws + o[D_RPOS]);
     auto* d_rnext = reinterpret_cast<uint64_t*>(ws + o[D_RNEXT]);
     auto* d_tc = reinterpret_cast<uint32_t*>(ws + o[D_TC]);
+    auto* d_c2s = reinterpret_cast<uint32_t*>(ws + o[D_MAPS]);
+    uint32_t* d_r2s = d_c2s + nchunk + 1;
+    uint32_t* d_t2w = d_r2s + nrec + 1;
     uint8_t* d_scr = ws + o[D_SCR];
     ctx->d_sout = d_sout;
     ctx->d_dstatus = d_st;
@@ -903,17 +911,19 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         ctx->dec_attr = true;
     }
     { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg); }
-    if (nchunk) { PROF(k_cand); k_cand<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, nseg, nchunk, d_cand, d_ccnt, d_ctot); }
+    CK(cudaMemsetAsync(d_c2s, 0xFF, (nchunk + nrec + ntile + 3) * sizeof(uint32_t), st));
+    if (nseg + nwin) { PROF(k_maps); k_maps<<<(unsigned)(nseg + nwin), 256, 0, st>>>(d_seg, nseg, d_win, nwin, d_c2s, d_r2s, d_t2w); }
+    if (nchunk) { PROF(k_cand); k_cand<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, d_c2s, nchunk, d_cand, d_ccnt, d_ctot); }
     if (nseg) {
         PROF(k_number);
         k_number<<<(unsigned)std::min<uint64_t>(nseg, 148 * 4), kThreads, 0, st>>>(d_seg, nseg, d_ctot, d_cpre, d_scnt, d_sfail);
     }
     if (nchunk) {
         PROF(k_assign);
-        k_assign<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, nseg, nchunk, d_cand, d_ccnt, d_cpre, d_sfail, d_rpos, d_rnext);
+        k_assign<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, d_c2s, nchunk, d_cand, d_ccnt, d_cpre, d_sfail, d_rpos, d_rnext);
     }
     if (nrec) {
-        { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, nseg, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
+        { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }
         if (!ctx->res_attr) {
             CK(cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kResSmem));
             ctx->res_attr = true;
@@ -921,14 +931,14 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         { PROF(k_resolve); k_resolve<<<(unsigned)std::min<uint64_t>(nseg, 148 * 2), kThreads, kResSmem, st>>>(
             d_seg, nseg, d_cand, d_ccnt, d_cpre, d_scnt, d_sfail, d_rpos, d_rnext); }
         PROF(k_decrec);
-        k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, nseg, nrec, d_sfail, d_rpos, d_scr);
+        k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr);
     }
     if (nseg) {
         const int grid = (int)std::min<uint64_t>(nseg, 148 * 2);
         PROF(k_fallback);
         k_fallback<<<grid, kThreads, dsm, st>>>(d_seg, nseg, d_sfail, d_st, d_scr);
     }
-    if (ntile) { PROF(k_ungroup); k_ungroup<<<(unsigned)ntile, kThreads, 0, st>>>(d_win, nwin, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_st); }
+    if (ntile) { PROF(k_ungroup); k_ungroup<<<(unsigned)ntile, kThreads, 0, st>>>(d_win, d_t2w, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_st); }
     { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st, d_in); }
     if (d_codes) k_status<<<(n + 255) / 256, 256, 0, st>>>(d_sout, d_st, n, d_codes);
     CK(cudaGetLastError());

@@ -33,12 +33,21 @@ __global__ void k_small_copy(uint8_t* __restrict__ dst, const uint8_t* __restric
     __threadfence_system();
 }
 
+constexpr uint32_t kCrcChunk = 32768;   // k_crc's unit
+
 // ------------------------------------------------------------------ slotmap
-__global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* __restrict__ slot2win) {
+// Owner maps: block slot -> window (k_hist_crc, k_encode) and CRC chunk ->
+// window (k_crc); one load per unit instead of a search.
+__global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* __restrict__ slot2win,
+                          uint32_t* __restrict__ crc2win) {
     int wi = blockIdx.x;
     if (wi >= nwin) return;
     const WinDesc wd = wins[wi];
     for (uint32_t i = threadIdx.x; i < wd.nslots; i += blockDim.x) slot2win[wd.slot0 + i] = (uint32_t)wi;
+    if (crc2win) {
+        const uint64_t nc = (wd.W + kCrcChunk - 1) / kCrcChunk;
+        for (uint64_t i = threadIdx.x; i < nc; i += blockDim.x) crc2win[wd.crc0 + i] = (uint32_t)wi;
+    }
 }
 
 // ------------------------------------------------------------------ CRC
@@ -52,7 +61,6 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
 // bytes before the chunk end: shift and XOR-reduce.  A short last chunk is
 // treated as left-padded with zero bytes, which leave a raw CRC unchanged.
 // k_frame combines the chunks (stream.py:329).
-constexpr uint32_t kCrcChunk = 32768;
 constexpr size_t kCrcSmem = (size_t)(256 * 32 + 1024) * sizeof(uint32_t);
 
 __device__ __forceinline__ uint32_t crc1_word(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
@@ -63,7 +71,7 @@ __device__ __forceinline__ uint32_t crc1_word(const uint32_t* __restrict__ tl, u
     return (crc >> 8) ^ tl[(crc & 0xFF) * 32];
 }
 
-__global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wins, int nwin, uint64_t nchunk,
+__global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wins, const uint32_t* __restrict__ crc2win, uint64_t nchunk,
                                                 const CrcTables* __restrict__ ct, const uint32_t* __restrict__ sh992,
                                                 uint32_t* __restrict__ out) {
     extern __shared__ uint32_t tab[];
@@ -75,12 +83,7 @@ __global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wi
     const uint32_t* tl = tab + lane;
     constexpr uint32_t kRows = kCrcChunk / 1024;
     for (uint64_t c = (uint64_t)blockIdx.x * kWarps + warp; c < nchunk; c += (uint64_t)gridDim.x * kWarps) {
-        int lo = 0, hi = nwin;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (wins[mid].crc0 <= c) lo = mid; else hi = mid;
-        }
-        const WinDesc wd = wins[lo];
+        const WinDesc wd = wins[crc2win[c]];
         const uint64_t off = (c - wd.crc0) * kCrcChunk;
         const uint32_t L = (uint32_t)min((uint64_t)kCrcChunk, wd.W - off);
         const uint32_t Z = kCrcChunk - L;   // leading zero bytes of the padded chunk

@@ -1066,31 +1066,45 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t& 
     return __all_sync(0xFFFFFFFFu, ok);
 }
 
+// Owner maps (chunk -> segment, record slot -> segment, output tile ->
+// window): one load per CTA in the kernels below instead of a binary search
+// of dependent loads.  Unowned capacity slots keep the ~0u of the memset.
+__global__ void k_maps(const DecSeg* __restrict__ segs, uint64_t nseg_total, const DecWin* __restrict__ wins,
+                       uint64_t nwin_total, uint32_t* __restrict__ chunk2seg, uint32_t* __restrict__ rec2seg,
+                       uint32_t* __restrict__ tile2win) {
+    const uint64_t b = blockIdx.x;
+    if (b < nseg_total) {
+        const DecSeg sg = segs[b];
+        for (uint32_t i = threadIdx.x; i < sg.nchunk; i += blockDim.x) chunk2seg[sg.chunk0 + i] = (uint32_t)b;
+        for (uint32_t i = threadIdx.x; i < sg.nrec; i += blockDim.x) rec2seg[sg.rec0 + i] = (uint32_t)b;
+    } else if (b - nseg_total < nwin_total) {
+        const uint64_t w = b - nseg_total;
+        const DecWin wd = wins[w];
+        for (uint32_t i = threadIdx.x; i < wd.ntile; i += blockDim.x) tile2win[wd.tile0 + i] = (uint32_t)w;
+    }
+}
+
 constexpr uint32_t kSpanCap = 64;                  // candidates listed per 8 KiB span (more: k_assign rescans)
 constexpr uint32_t kDense = 0xFFFFFFFFu;            // a lane overflowed: the serial path takes the segment
 
 // CTA per 64 KiB chunk slot of segment payload, warp per 8 KiB span: the
 // candidate record headers of the span, in increasing order, into
 // cand[span][0..kSpanCap) and their count (kDense on overflow) into ccnt.
-__global__ void __launch_bounds__(kThreads) k_cand(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+__global__ void __launch_bounds__(kThreads) k_cand(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ chunk2seg,
                                                  uint64_t nchunk_total, uint32_t* __restrict__ cand,
                                                  uint32_t* __restrict__ ccnt, uint32_t* __restrict__ ctot) {
     __shared__ uint32_t wcnt[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t t = blockIdx.x;
     if (t >= nchunk_total) return;
-    uint64_t lo = 0, hi = nseg_total;
-    while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (segs[mid].chunk0 <= t) lo = mid; else hi = mid;
-    }
-    const DecSeg sg = segs[lo];
     const uint64_t span = t * kWarps + warp;
-    if (t < sg.chunk0 || t >= sg.chunk0 + sg.nchunk) {  // unused capacity slot
+    const uint32_t owner = chunk2seg[t];
+    if (owner == ~0u) {  // unused capacity slot
         if (lane == 0) ccnt[span] = 0;
         if (tid == 0) ctot[t] = 0;
         return;
     }
+    const DecSeg sg = segs[owner];
     constexpr uint64_t kWarpSpan = kChunk / kWarps;
     const uint64_t c0 = (t - sg.chunk0) * kChunk, c1 = min(c0 + kChunk, sg.comp);
     const uint64_t pa = c0 + warp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
@@ -1157,7 +1171,7 @@ __global__ void __launch_bounds__(kThreads) k_number(const DecSeg* __restrict__ 
 // candidate i's position and the position its header says the next record
 // starts at; after record R-2 the tail record (not a candidate when its
 // length differs from the block size) follows.
-__global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+__global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ chunk2seg,
                                                    uint64_t nchunk_total, const uint32_t* __restrict__ cand,
                                                    const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cpre,
                                                    uint32_t* __restrict__ seg_fail, uint64_t* __restrict__ rec_pos,
@@ -1166,13 +1180,9 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t t = blockIdx.x;
     if (t >= nchunk_total) return;
-    uint64_t lo = 0, hi = nseg_total;
-    while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (segs[mid].chunk0 <= t) lo = mid; else hi = mid;
-    }
+    const uint32_t lo = chunk2seg[t];
+    if (lo == ~0u) return;
     const DecSeg sg = segs[lo];
-    if (t < sg.chunk0 || t >= sg.chunk0 + sg.nchunk) return;
     if (tid == 0) {
         uint32_t acc = cpre[t];
         bool dense = false;
@@ -1224,20 +1234,16 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
 // copy or CTA-wide Huffman decode into the grouped scratch.  A failure marks
 // the segment for k_fallback, which re-walks it serially and reports the
 // reference's error.
-__global__ void __launch_bounds__(kThreads, 3) k_decrec(const DecSeg* __restrict__ segs, uint64_t nseg_total,
+__global__ void __launch_bounds__(kThreads, 3) k_decrec(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
                                                    uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
                                                    const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
     const uint64_t g = blockIdx.x;
     if (g >= nrec_total) return;
-    uint64_t lo = 0, hi = nseg_total;
-    while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (segs[mid].rec0 <= g) lo = mid; else hi = mid;
-    }
+    const uint32_t lo = rec2seg[g];
+    if (lo == ~0u || seg_fail[lo]) return;
     const DecSeg sg = segs[lo];
-    if (g < sg.rec0 || g >= sg.rec0 + sg.nrec || seg_fail[lo]) return;
     const uint32_t r = (uint32_t)(g - sg.rec0);
     const uint8_t* rec = sg.base + rec_pos[g];
     const uint32_t mode = rec[0], len = rd32(rec + 1);
@@ -1247,19 +1253,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_decrec(const DecSeg* __restrict
 
 // --------------------------------------------------------------- k_verify
 // One thread per record slot: the candidates must chain exactly.
-__global__ void k_verify(const DecSeg* __restrict__ segs, uint64_t nseg_total, uint64_t nrec_total,
+__global__ void k_verify(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg, uint64_t nrec_total,
                          const uint32_t* __restrict__ seg_cnt, uint32_t* __restrict__ seg_fail,
                          const uint64_t* __restrict__ rec_pos, const uint64_t* __restrict__ rec_next) {
     const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= nrec_total) return;
-    uint64_t lo = 0, hi = nseg_total;
-    while (hi - lo > 1) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (segs[mid].rec0 <= g) lo = mid; else hi = mid;
-    }
-    // several empty segments may share rec0: move to the one that owns g
+    const uint32_t lo = rec2seg[g];
+    if (lo == ~0u) return;
     const DecSeg sg = segs[lo];
-    if (g < sg.rec0 || g >= sg.rec0 + sg.nrec) return;
     const uint32_t r = (uint32_t)(g - sg.rec0);
     const uint32_t R = sg.nrec, B = sg.block;
     const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(R - 1) * B);
@@ -1481,7 +1482,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
 // -------------------------------------------------------------- k_ungroup
 // CTA per 16 KiB output tile of a window: out[e*w + g] = grouped[g*n + e];
 // each thread produces 64 contiguous output bytes and their raw CRC.
-__global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__ wins, uint64_t nwin_total,
+__global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__ wins, const uint32_t* __restrict__ tile2win,
                                                     uint64_t ntile_total, const uint8_t* __restrict__ scratch,
                                                     uint8_t* out /* may alias a window's prev */, const CrcTables* __restrict__ ct,
                                                     uint32_t* __restrict__ tile_crc, const uint32_t* __restrict__ status) {
@@ -1489,14 +1490,14 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
     __shared__ uint32_t sh_part[kWarps];
     const uint64_t tile = blockIdx.x;
     if (tile >= ntile_total) return;
-    uint64_t lo = 0, hi = nwin_total;
-    while (hi - lo > 1) {
-        uint64_t mid = (lo + hi) >> 1;
-        if (wins[mid].tile0 <= tile) lo = mid; else hi = mid;
-    }
-    const DecWin wd = wins[lo];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tile < wd.tile0 || tile >= wd.tile0 + wd.ntile || status[wd.stream]) {
+    const uint32_t wi = tile2win[tile];
+    if (wi == ~0u) {   // unused capacity slot
+        if (tid == 0) tile_crc[tile] = 0;
+        return;
+    }
+    const DecWin wd = wins[wi];
+    if (status[wd.stream]) {
         if (tid == 0) tile_crc[tile] = 0;
         return;
     }
