@@ -50,6 +50,7 @@ struct lmcg_ctx {
     bool dec_attr = false;
     int scandec_occ = 1;
     bool crc_attr = false;
+    int ung_occ = 0;                      // resident k_ungroup CTAs (persistent grid)
     bool serial = false;                  // LMCG_SERIAL=1: no side stream (per-kernel timing experiments)
     uint8_t* part_ws = nullptr;
     size_t part_ws_cap = 0;
@@ -938,7 +939,12 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         PROF(k_fallback);
         k_fallback<<<grid, kThreads, dsm, st>>>(d_seg, nseg, d_sfail, d_st, d_scr);
     }
-    if (ntile) { PROF(k_ungroup); k_ungroup<<<(unsigned)ntile, kThreads, 0, st>>>(d_win, d_t2w, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, d_tc, d_st); }
+    if (ntile) {
+        if (!ctx->ung_occ) ctx->ung_occ = occupancy(ctx, (const void*)k_ungroup, kThreads, kUngSmem);
+        PROF(k_ungroup);
+        k_ungroup<<<(unsigned)std::min<uint64_t>((ntile + kWarps - 1) / kWarps, (uint64_t)ctx->ung_occ), kThreads, kUngSmem, st>>>(
+            d_win, d_t2w, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, ctx->d_sh992, d_tc, d_st);
+    }
     { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st, d_in); }
     if (d_codes) k_status<<<(n + 255) / 256, 256, 0, st>>>(d_sout, d_st, n, d_codes);
     CK(cudaGetLastError());

@@ -31,7 +31,7 @@
 namespace lmcg {
 
 constexpr int kChunk = 65536;        // segment payload bytes per k_scandec chunk
-constexpr int kOutTile = 16384;      // output bytes per k_ungroup CTA
+constexpr int kOutTile = 32768;      // output bytes per k_ungroup warp
 constexpr int kLut = 11;             // LUT index bits
 constexpr int kCntLut = 12;          // count-LUT index bits (no symbols: more codewords per lookup)
 
@@ -1482,111 +1482,144 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
 // -------------------------------------------------------------- k_ungroup
 // CTA per 16 KiB output tile of a window: out[e*w + g] = grouped[g*n + e];
 // each thread produces 64 contiguous output bytes and their raw CRC.
+// Persistent warps over 32 KiB output tiles of the windows (the k_crc
+// layout): out[e*w + g] = grouped[g*n + e].  The warp writes the tile as 32
+// rows of 1 KiB, lane l producing the 32 output bytes at 1024 r + 32 l of
+// each row (coalesced plane loads and 16-byte stores), and folds them into a
+// raw CRC: two Horner chains per lane (rows 0-15, 16-31), a 992-byte shift
+// (4 lookups) per row and the piece through a 32-fold replicated byte table
+// (lane l reads copy l: no bank conflicts); lane values are then shifted to
+// the tile end and XOR-reduced.  A short last tile is treated as left-padded
+// with zero bytes, which leave a raw CRC unchanged.  lmcg_decompress_apply
+// XORs the previous step into the stores (the CRC stays the payload's).
+constexpr size_t kUngSmem = (size_t)(256 * 32 + 1024) * sizeof(uint32_t);
+
+__device__ __forceinline__ uint32_t crc1_rep(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
+    crc ^= w;
+    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+    return (crc >> 8) ^ tl[(crc & 0xFF) * 32];
+}
+
 __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__ wins, const uint32_t* __restrict__ tile2win,
                                                     uint64_t ntile_total, const uint8_t* __restrict__ scratch,
                                                     uint8_t* out /* may alias a window's prev */, const CrcTables* __restrict__ ct,
-                                                    uint32_t* __restrict__ tile_crc, const uint32_t* __restrict__ status) {
-    __shared__ uint32_t sh_slice[1024];
-    __shared__ uint32_t sh_part[kWarps];
-    const uint64_t tile = blockIdx.x;
-    if (tile >= ntile_total) return;
+                                                    const uint32_t* __restrict__ sh992, uint32_t* __restrict__ tile_crc,
+                                                    const uint32_t* __restrict__ status) {
+    extern __shared__ uint32_t ung_tab[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t wi = tile2win[tile];
-    if (wi == ~0u) {   // unused capacity slot
-        if (tid == 0) tile_crc[tile] = 0;
-        return;
-    }
-    const DecWin wd = wins[wi];
-    if (status[wd.stream]) {
-        if (tid == 0) tile_crc[tile] = 0;
-        return;
-    }
-    const uint64_t t0 = (tile - wd.tile0) * kOutTile;
-    for (int i = tid; i < 1024; i += kThreads) sh_slice[i] = ct->slice[i >> 8][i & 255];
+    for (int i = tid; i < 256 * 32; i += kThreads) ung_tab[i] = ct->slice[0][i >> 5];
+    uint32_t* st = ung_tab + 256 * 32;
+    for (int i = tid; i < 1024; i += kThreads) st[i] = sh992[i];
     __syncthreads();
-    const uint64_t L = min((uint64_t)kOutTile, wd.W - t0);
-    const uint64_t Z = kOutTile - L;  // leading zero padding of a short tile
-    const uint32_t w = wd.w;
-    const uint8_t* g = scratch + wd.goff;
-    uint8_t* o = out + wd.ooff;
-    const uint64_t lo_b = (uint64_t)tid * kLaneBytes, hi_b = lo_b + kLaneBytes;
-    uint32_t c = 0;
-    const bool full = lo_b >= Z;
-    const uint64_t ob = t0 + lo_b - Z;
-    const uint8_t* pv = wd.prev;   // xor_apply (delta.py:50-52): out = payload ^ prev; the CRC is the payload's
-    const bool vec = full && ((reinterpret_cast<uint64_t>(o) + ob) % 16 == 0) &&
-                     (!pv || (reinterpret_cast<uint64_t>(pv) + ob) % 16 == 0) &&
-                     (w == 1 ? ((reinterpret_cast<uint64_t>(g) + ob) % 16 == 0)
-                             : (((ob >> lg2w(w)) & 15) == 0 && (wd.n & 15) == 0));
-    if (vec) {
-        uint32_t v[16];
-        if (w == 1) {
+    const uint32_t* tl = ung_tab + lane;
+    auto shift992 = [&](uint32_t x) {
+        return st[x & 0xFF] ^ st[256 + ((x >> 8) & 0xFF)] ^ st[512 + ((x >> 16) & 0xFF)] ^ st[768 + (x >> 24)];
+    };
+    static_assert(kOutTile == 32768, "k_ungroup rows");
+    for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + warp; tile < ntile_total; tile += (uint64_t)gridDim.x * kWarps) {
+        const uint32_t wi = tile2win[tile];
+        if (wi == ~0u) {   // unused capacity slot
+            if (lane == 0) tile_crc[tile] = 0;
+            continue;
+        }
+        const DecWin wd = wins[wi];
+        if (status[wd.stream]) {
+            if (lane == 0) tile_crc[tile] = 0;
+            continue;
+        }
+        const uint64_t t0 = (tile - wd.tile0) * kOutTile;
+        const uint32_t L = (uint32_t)min((uint64_t)kOutTile, wd.W - t0);
+        const uint32_t Z = kOutTile - L;   // leading zero padding of a short tile
+        const uint32_t w = wd.w, lw = lg2w(w);
+        const uint8_t* g = scratch + wd.goff;
+        uint8_t* o = out + wd.ooff;
+        const uint8_t* pv = wd.prev;
+        // vector path for a whole piece: 16-byte aligned output (and prev),
+        // plane loads of 32 >> lw bytes at an aligned element offset
+        const bool avec = ((reinterpret_cast<uint64_t>(o) + t0) % 16 == 0) && (Z % 32 == 0) &&
+                          (!pv || (reinterpret_cast<uint64_t>(pv) + t0) % 16 == 0) &&
+                          (w == 1 ? ((reinterpret_cast<uint64_t>(g) + t0) % 16 == 0) : ((wd.n & 15) == 0));
+        // the 32 output bytes at padded offset pb: written, and returned as 8 words
+        auto piece = [&](uint32_t pb, uint32_t v[8]) {
+            if (pb + 32 <= Z) {
 #pragma unroll
-            for (int q = 0; q < 4; q++) {
-                uint4 a = *reinterpret_cast<const uint4*>(g + ob + 16 * q);
-                v[4 * q] = a.x; v[4 * q + 1] = a.y; v[4 * q + 2] = a.z; v[4 * q + 3] = a.w;
+                for (int q = 0; q < 8; q++) v[q] = 0;
+                return;
             }
-        } else if (w == 2) {
-            const uint64_t e = ob / 2;
-            const uint4 a0 = *reinterpret_cast<const uint4*>(g + e), a1 = *reinterpret_cast<const uint4*>(g + e + 16);
-            const uint4 b0 = *reinterpret_cast<const uint4*>(g + wd.n + e), b1 = *reinterpret_cast<const uint4*>(g + wd.n + e + 16);
-            const uint32_t lw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            const uint32_t hw[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+            const uint64_t ob = t0 + pb - Z;
+            if (avec && pb >= Z) {
+                if (w == 1) {
+                    const uint4 a0 = *reinterpret_cast<const uint4*>(g + ob), a1 = *reinterpret_cast<const uint4*>(g + ob + 16);
+                    v[0] = a0.x; v[1] = a0.y; v[2] = a0.z; v[3] = a0.w; v[4] = a1.x; v[5] = a1.y; v[6] = a1.z; v[7] = a1.w;
+                } else if (w == 2) {
+                    const uint64_t e = ob >> 1;
+                    const uint4 a = *reinterpret_cast<const uint4*>(g + e), b = *reinterpret_cast<const uint4*>(g + wd.n + e);
+                    const uint32_t lo4[4] = {a.x, a.y, a.z, a.w}, hi4[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        v[2 * q] = __byte_perm(lo4[q], hi4[q], 0x5140);
+                        v[2 * q + 1] = __byte_perm(lo4[q], hi4[q], 0x7362);
+                    }
+                } else {
+                    const uint64_t e = ob >> 2;
+                    uint2 pl[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) pl[q] = *reinterpret_cast<const uint2*>(g + q * wd.n + e);
+#pragma unroll
+                    for (int q = 0; q < 2; q++) {
+                        const uint32_t p0 = q ? pl[0].y : pl[0].x, p1 = q ? pl[1].y : pl[1].x;
+                        const uint32_t p2 = q ? pl[2].y : pl[2].x, p3 = q ? pl[3].y : pl[3].x;
+                        const uint32_t x01lo = __byte_perm(p0, p1, 0x5140), x01hi = __byte_perm(p0, p1, 0x7362);
+                        const uint32_t x23lo = __byte_perm(p2, p3, 0x5140), x23hi = __byte_perm(p2, p3, 0x7362);
+                        v[4 * q + 0] = __byte_perm(x01lo, x23lo, 0x5410);
+                        v[4 * q + 1] = __byte_perm(x01lo, x23lo, 0x7632);
+                        v[4 * q + 2] = __byte_perm(x01hi, x23hi, 0x5410);
+                        v[4 * q + 3] = __byte_perm(x01hi, x23hi, 0x7632);
+                    }
+                }
+                uint4 s0 = make_uint4(v[0], v[1], v[2], v[3]), s1 = make_uint4(v[4], v[5], v[6], v[7]);
+                if (pv) {
+                    const uint4 p0 = *reinterpret_cast<const uint4*>(pv + ob), p1 = *reinterpret_cast<const uint4*>(pv + ob + 16);
+                    s0.x ^= p0.x; s0.y ^= p0.y; s0.z ^= p0.z; s0.w ^= p0.w;
+                    s1.x ^= p1.x; s1.y ^= p1.y; s1.z ^= p1.z; s1.w ^= p1.w;
+                }
+                *reinterpret_cast<uint4*>(o + ob) = s0;
+                *reinterpret_cast<uint4*>(o + ob + 16) = s1;
+                return;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; q++) v[q] = 0;
+            for (uint32_t i = 0; i < 32; i++) {
+                if (pb + i < Z) continue;
+                const uint64_t ob1 = t0 + pb + i - Z;
+                const uint64_t e = ob1 >> lw, gg = ob1 - (e << lw);
+                const uint32_t x = g[gg * wd.n + e];
+                o[ob1] = pv ? (uint8_t)(x ^ pv[ob1]) : (uint8_t)x;
+                v[i >> 2] |= x << (8 * (i & 3));
+            }
+        };
+        uint32_t ca = 0, cb = 0;
+        for (uint32_t r = 0; r < 16; r++) {
+            uint32_t va[8], vb[8];
+            piece(1024 * r + 32 * lane, va);
+            piece(1024 * (r + 16) + 32 * lane, vb);
+            ca = shift992(ca);
+            cb = shift992(cb);
 #pragma unroll
             for (int q = 0; q < 8; q++) {
-                v[2 * q] = __byte_perm(lw[q], hw[q], 0x5140);
-                v[2 * q + 1] = __byte_perm(lw[q], hw[q], 0x7362);
-            }
-        } else {
-            const uint64_t e = ob / 4;
-            uint4 pl[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) pl[q] = *reinterpret_cast<const uint4*>(g + q * wd.n + e);
-            const uint32_t* p0 = reinterpret_cast<const uint32_t*>(&pl[0]);
-            const uint32_t* p1 = reinterpret_cast<const uint32_t*>(&pl[1]);
-            const uint32_t* p2 = reinterpret_cast<const uint32_t*>(&pl[2]);
-            const uint32_t* p3 = reinterpret_cast<const uint32_t*>(&pl[3]);
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                const uint32_t x01lo = __byte_perm(p0[q], p1[q], 0x5140), x01hi = __byte_perm(p0[q], p1[q], 0x7362);
-                const uint32_t x23lo = __byte_perm(p2[q], p3[q], 0x5140), x23hi = __byte_perm(p2[q], p3[q], 0x7362);
-                v[4 * q + 0] = __byte_perm(x01lo, x23lo, 0x5410);
-                v[4 * q + 1] = __byte_perm(x01lo, x23lo, 0x7632);
-                v[4 * q + 2] = __byte_perm(x01hi, x23hi, 0x5410);
-                v[4 * q + 3] = __byte_perm(x01hi, x23hi, 0x7632);
+                ca = crc1_rep(tl, ca, va[q]);
+                cb = crc1_rep(tl, cb, vb[q]);
             }
         }
-        if (pv) {
-            uint4 pq[4];
+        // chain a ends 16 rows (16 KiB) before chain b; lane l's value ends
+        // 32 (31 - l) bytes before the tile end
+        uint32_t crc = crc_shift_tab(&ct->pow2[14][0][0], ca) ^ cb;
+        crc = crc_shift_bytes(ct, crc, 32u * (31 - lane));
 #pragma unroll
-            for (int q = 0; q < 4; q++) pq[q] = *reinterpret_cast<const uint4*>(pv + ob + 16 * q);
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                *reinterpret_cast<uint4*>(o + ob + 16 * q) = make_uint4(v[4 * q] ^ pq[q].x, v[4 * q + 1] ^ pq[q].y,
-                                                                       v[4 * q + 2] ^ pq[q].z, v[4 * q + 3] ^ pq[q].w);
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                *reinterpret_cast<uint4*>(o + ob + 16 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
-#pragma unroll
-        for (int q = 0; q < 16; q++) c = crc_word(sh_slice, c, v[q]);
-    } else {
-        for (uint64_t q = max(lo_b, Z); q < hi_b; q++) {
-            const uint64_t ob1 = t0 + q - Z;
-            const uint64_t e = ob1 >> lg2w(w), gg = ob1 - (e << lg2w(w));
-            const uint8_t x = g[gg * wd.n + e];
-            o[ob1] = pv ? (uint8_t)(x ^ pv[ob1]) : x;
-            c = crc_byte(sh_slice, c, x);
-        }
-    }
-    c = crc_warp_tree(ct, c, lane, 2);
-    if (lane == 0) sh_part[warp] = c;
-    __syncthreads();
-    if (tid == 0) {
-        uint32_t acc = 0;
-        for (int q = 0; q < kWarps; q++) acc = crc_shift_tab(&ct->shift[kShift2K][0][0], acc) ^ sh_part[q];
-        tile_crc[tile] = acc;
+        for (int q = 16; q; q >>= 1) crc ^= __shfl_xor_sync(0xFFFFFFFFu, crc, q);
+        if (lane == 0) tile_crc[tile] = crc;
     }
 }
 
