@@ -321,32 +321,33 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     const int tid = threadIdx.x;
     uint32_t c = 0;
     bool bad = false, done = false;
-    // staged payload: read through a 64-bit register bit buffer, refilled
-    // branch-free (the next word is always inside the staging area)
-    uint64_t bbuf = 0;
-    uint32_t bavail = 0, bnj = 0;
+    // staged payload: read through a two-word register bit buffer (hi:lo,
+    // window = funnel shift by boff < 32), refilled branch-free (the next
+    // word is always inside the staging area)
+    uint32_t bhi = 0, blo = 0, boff = 0, bnj = 0;
     if (STAGED) {
-        const uint32_t a0 = pos + src.sh, j0 = a0 >> 5, r0 = a0 & 31;
-        bbuf = (((uint64_t)src.sw[j0] << 32) | src.sw[j0 + 1]) << r0;
-        bavail = 64 - r0;
+        const uint32_t a0 = pos + src.sh, j0 = a0 >> 5;
+        boff = a0 & 31;
+        bhi = src.sw[j0];
+        blo = src.sw[j0 + 1];
         bnj = j0 + 2;
     }
-    auto win = [&]() -> uint32_t { return STAGED ? (uint32_t)(bbuf >> 32) : src.template peek<STAGED>(pos); };
+    auto win = [&]() -> uint32_t { return STAGED ? __funnelshift_l(blo, bhi, boff) : src.template peek<STAGED>(pos); };
     // a 1-bit codeword is '0' (canonical codes start at zero): every leading
     // zero bit of the window is one more of that symbol, so runs of it (XOR
     // deltas are mostly zero bytes) go many symbols per lookup
     constexpr bool run1 = RUN;   // (the record has a 1-bit codeword)
     const uint64_t rep8 = RUN ? s.csym[s.first_idx[1]] * 0x0101010101010101ull : 0ull;
-    auto adv = [&](uint32_t l) {
+    auto adv = [&](uint32_t l) {   // l <= 32
         pos += l;
         if (STAGED) {
-            bbuf <<= l;
-            bavail -= l;
-            const bool rf = bavail < 32;
+            boff += l;
+            const bool rf = boff >= 32;
             const uint32_t nw = src.sw[bnj];
-            bbuf |= rf ? ((uint64_t)nw << (32 - bavail)) : 0ull;
+            bhi = rf ? blo : bhi;
+            blo = rf ? nw : blo;
             bnj += rf ? 1u : 0u;
-            bavail += rf ? 32u : 0u;
+            boff -= rf ? 32u : 0u;
         }
     };
     if (!EMIT) {
