@@ -32,6 +32,7 @@ from filelock import FileLock
 
 from .errors import (CorruptStreamError, DtypeMismatchError, IntegrityError, LmcError, MissingStreamError,
                      ShapeMismatchError, raise_status)
+from .pipeline import StreamItem, StreamWriter
 from .stream import DEFAULT_BLOCK_SIZE, _bytes_view, _torch_et, default_codec, parse_header
 from .types import ElementType, TensorBuffer
 
@@ -91,10 +92,11 @@ class DeltaManifest:
         return ("\n".join(rows) + "\n").encode()
 
 
-def _replace_file(path: Path, data: bytes) -> None:
+def _replace_file(path: Path, data) -> None:
     """Write-then-rename, so readers never see a partial file (chain.py:94-97)."""
     tmp = path.with_name(path.name + ".tmp")
-    tmp.write_bytes(data)
+    with open(tmp, "wb") as f:
+        f.write(data)
     os.replace(tmp, path)
 
 
@@ -198,19 +200,24 @@ class DeviceChain:
             if len(set(files)) != len(files):
                 raise LmcError(f"shard names {names} collide after filename sanitization")
             prev = [self._view(name) for name in names] if nxt > 0 else None
-            batch = self.codec.compress([cur[name][0] for name in names],
-                                        element_types=[cur[name][1].code for name in names], prev=prev,
-                                        byte_group=self.byte_group, block_size=self.block_size,
-                                        segment_count=self.segment_count)
-            streams = batch.to_bytes()
+            # compress overlapped with the D2H copies and the file writes
+            # (pipeline.StreamWriter); the streams land in their files in order
             role = ROLE_BASE if nxt == 0 else ROLE_DELTA
-            entries = []
-            for name, fname, s in zip(names, files, streams):
-                _replace_file(self.dir / fname, s)
-                # the header CRC is zlib.crc32 of the (delta) payload, which is what
-                # the reference records (chain.py:201)
-                entries.append(ChainEntry(step=nxt, role=role, shard=name, dtype=cur[name][1].name.lower(),
-                                          length=cur[name][0].numel(), file=fname, crc32=parse_header(s).crc32))
+            crcs = [0] * len(names)
+
+            def sink(i: int, view: memoryview) -> None:
+                _replace_file(self.dir / files[i], view)
+                # the header CRC is zlib.crc32 of the (delta) payload, which is
+                # what the reference records (chain.py:201)
+                crcs[i] = int.from_bytes(view[24:28], "little")
+
+            items = [StreamItem(cur[name][0], cur[name][1].code, None if prev is None else prev[j])
+                     for j, name in enumerate(names)]
+            StreamWriter(self.codec, byte_group=self.byte_group, block_size=self.block_size,
+                         segment_count=self.segment_count).run(items, sink)
+            entries = [ChainEntry(step=nxt, role=role, shard=name, dtype=cur[name][1].name.lower(),
+                                  length=cur[name][0].numel(), file=fname, crc32=crcs[j])
+                       for j, (name, fname) in enumerate(zip(names, files))]
             manifest.entries.extend(entries)
             save_manifest(self.dir, manifest)
             # the new step becomes the resident one (device-to-device copies)
@@ -322,3 +329,31 @@ class DeviceChain:
             if e.shard not in self._layout or self._layout[e.shard][1] != n:
                 self._step = -1
                 raise ShapeMismatchError(f"length mismatch: {self._layout.get(e.shard, (0, 0))[1]} vs {n}")
+
+
+# ------------------------------------------------- reference-shaped module API
+_chains: dict[tuple, DeviceChain] = {}
+
+
+def _chain_for(chain_dir, block_size: int, byte_group: bool, segment_count: int) -> DeviceChain:
+    codec = default_codec()
+    key = (os.path.realpath(os.fspath(chain_dir)), codec.ctx.device, block_size, bool(byte_group), segment_count)
+    ch = _chains.get(key)
+    if ch is None:
+        ch = _chains[key] = DeviceChain(chain_dir, codec=codec, block_size=block_size, byte_group=byte_group,
+                                        segment_count=segment_count)
+    return ch
+
+
+def add_step(chain_dir, shards: dict, *, step: int | None = None, block_size: int = DEFAULT_BLOCK_SIZE,
+             byte_group: bool = True, segment_count: int = 1) -> int:
+    """chain.py:133-208 (same arguments, same files): the chain's latest step
+    stays resident on the GPU between calls in this process."""
+    return _chain_for(chain_dir, block_size, byte_group, segment_count).add_step(shards, step=step)
+
+
+def restore_step(chain_dir, step: int) -> dict[str, TensorBuffer]:
+    """chain.py:260-278: every shard of one step as host TensorBuffers, decoded
+    from the files on disk like the reference (never from a resident step)."""
+    load_manifest(chain_dir)   # (MissingStreamError before any device work)
+    return DeviceChain(chain_dir, codec=default_codec()).restore_buffers(step)
