@@ -52,6 +52,8 @@ struct lmcg_ctx {
     bool crc_attr = false;
     int ung_occ = 0;                      // resident k_ungroup CTAs (persistent grid)
     bool serial = false;                  // LMCG_SERIAL=1: no side stream (per-kernel timing experiments)
+    bool cb_attr = false;
+    int crc_fork = 0;                     // LMCG_CRC_FORK: k_crc forks before (0) or after (1) the histogram
     uint8_t* part_ws = nullptr;
     size_t part_ws_cap = 0;
     bool res_attr = false;
@@ -318,6 +320,7 @@ lmcg_ctx* lmcg_create(int device) {
     cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (const char* e = getenv("LMCG_SERIAL")) ctx->serial = e[0] == '1';
+    if (const char* e = getenv("LMCG_CRC_FORK")) ctx->crc_fork = atoi(e);
     return ctx;
 }
 
@@ -443,31 +446,40 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
     // k_crc only reads the tensors: it runs on the side stream, overlapping
     // the histogram / codebook / encode chain, and joins before k_frame
     const bool fork = ncrc && n && !part;
-    if (fork) {
+    auto launch_crc = [&]() -> int {
         if (!ctx->crc_attr) {
             CK(cudaFuncSetAttribute(k_crc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem));
-            ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kThreads, kCrcSmem);
+            ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kCrcThreads, kCrcSmem);
             ctx->crc_attr = true;
         }
         if (!ctx->serial) {
             CK(cudaEventRecord(ctx->fork_ev, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
         }
-        const uint64_t need = (ncrc + kWarps - 1) / kWarps;
+        const uint64_t need = (ncrc + kCrcWarps - 1) / kCrcWarps;
         cudaStream_t sst = ctx->serial ? st : ctx->side;
         ProfScope prof_scope_k_crc(ctx, "k_crc", sst);
-        k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, sst>>>(
+        k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kCrcThreads, kCrcSmem, sst>>>(
             d_wins, d_crc2win, ncrc, ctx->d_crc, ctx->d_sh992, d_crcp);
         CK(cudaEventRecord(ctx->join_ev, sst));
-    }
+        return LMCG_OK;
+    };
+    if (fork && ctx->crc_fork == 0)
+        if (int r = launch_crc()) return r;
 
     if (nslots) {
         PROF(k_hist_crc);
         k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta,
                                                           part ? part_lo : 0, part ? part_hi : ~0ull);
     }
+    if (fork && ctx->crc_fork == 1)
+        if (int r = launch_crc()) return r;
     if (nb) {
-        { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbWarps - 1) / kCbWarps), kCbWarps * 32, 0, st>>>(
+        if (!ctx->cb_attr) {
+            CK(cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCbColBytes));
+            ctx->cb_attr = true;
+        }
+        { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbBlocks - 1) / kCbBlocks), kCbWarps * 32, kCbColBytes, st>>>(
             d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist, part ? part_lo : 0, part ? part_hi : ~0ull); }
         { PROF(k_pkgmerge); k_pkgmerge<<<296, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr); }
     }
@@ -587,13 +599,13 @@ int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* 
     CK(cudaMemcpy(ctx->part_ws, &cw, sizeof(WinDesc), cudaMemcpyHostToDevice));
     if (!ctx->crc_attr) {
         CK(cudaFuncSetAttribute(k_crc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem));
-        ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kThreads, kCrcSmem);
+        ctx->crc_occ = occupancy(ctx, (const void*)k_crc, kCrcThreads, kCrcSmem);
         ctx->crc_attr = true;
     }
     uint32_t* parts = reinterpret_cast<uint32_t*>(ctx->part_ws + 256);
     uint32_t* one_win = parts + nchunk + 1;   // every chunk -> window 0
     CK(cudaMemsetAsync(one_win, 0, 4 * (nchunk + 1), st));
-    k_crc<<<(unsigned)std::min<uint64_t>((nchunk + kWarps - 1) / kWarps, (uint64_t)ctx->crc_occ), kThreads, kCrcSmem, st>>>(
+    k_crc<<<(unsigned)std::min<uint64_t>((nchunk + kCrcWarps - 1) / kCrcWarps, (uint64_t)ctx->crc_occ), kCrcThreads, kCrcSmem, st>>>(
         reinterpret_cast<const WinDesc*>(ctx->part_ws), one_win, nchunk, ctx->d_crc, ctx->d_sh992, parts);
     k_crc_join<<<1, kThreads, 0, st>>>(parts, L, ctx->d_crc, d_crc);
     CK(cudaGetLastError());
@@ -758,7 +770,7 @@ int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint
     uint32_t* d_ctr = reinterpret_cast<uint32_t*>(ctx->ws);
     uint32_t* d_list = reinterpret_cast<uint32_t*>(ctx->ws + 256);
     CK(cudaMemsetAsync(d_ctr, 0, 16, st));
-    { PROF(k_codebook); k_codebook<<<(nhist + kCbWarps - 1) / kCbWarps, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
+    { PROF(k_codebook); k_codebook<<<(nhist + kCbBlocks - 1) / kCbBlocks, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
                                                                              d_lengths, d_ctr, d_ctr + 1, d_list); }
     { PROF(k_pkgmerge); k_pkgmerge<<<296, 32, 0, st>>>(d_hists, d_ctr + 1, d_list, nullptr, nullptr, d_lengths); }
     CK(cudaGetLastError());
@@ -940,9 +952,12 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         k_fallback<<<grid, kThreads, dsm, st>>>(d_seg, nseg, d_sfail, d_st, d_scr);
     }
     if (ntile) {
-        if (!ctx->ung_occ) ctx->ung_occ = occupancy(ctx, (const void*)k_ungroup, kThreads, kUngSmem);
+        if (!ctx->ung_occ) {
+            CK(cudaFuncSetAttribute(k_ungroup, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kUngSmem));
+            ctx->ung_occ = occupancy(ctx, (const void*)k_ungroup, kUngThreads, kUngSmem);
+        }
         PROF(k_ungroup);
-        k_ungroup<<<(unsigned)std::min<uint64_t>((ntile + kWarps - 1) / kWarps, (uint64_t)ctx->ung_occ), kThreads, kUngSmem, st>>>(
+        k_ungroup<<<(unsigned)std::min<uint64_t>((ntile + kUngWarps - 1) / kUngWarps, (uint64_t)ctx->ung_occ), kUngThreads, kUngSmem, st>>>(
             d_win, d_t2w, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, ctx->d_sh992, d_tc, d_st);
     }
     { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st, d_in); }

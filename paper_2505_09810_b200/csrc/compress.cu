@@ -56,33 +56,28 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
 // The warp reads 1 KiB rows (lane l: the 32 bytes at 1024 r + 32 l, two
 // 16-byte loads that together cover whole lines) and lane l folds its
 // pieces in order: shift by the 992 bytes of the other lanes' pieces (4
-// lookups), then the piece byte by byte through a 32-fold replicated table
-// (lane l reads copy l: no bank conflicts).  Lane l's value ends 32 (31 - l)
+// lookups), then the piece by slicing-by-4 through 32-fold replicated
+// tables (crc4_rep: lane l reads copy l, no bank conflicts).  Lane l's value ends 32 (31 - l)
 // bytes before the chunk end: shift and XOR-reduce.  A short last chunk is
 // treated as left-padded with zero bytes, which leave a raw CRC unchanged.
 // k_frame combines the chunks (stream.py:329).
-constexpr size_t kCrcSmem = (size_t)(256 * 32 + 1024) * sizeof(uint32_t);
+constexpr int kCrcThreads = 512;   // one CTA per SM (128 KiB of replicated slicing tables), leaving
+                                   // registers and threads for the histogram / encode CTAs it overlaps
+constexpr int kCrcWarps = kCrcThreads / 32;
+constexpr size_t kCrcSmem = (kRep4Words + 1024) * sizeof(uint32_t);
 
-__device__ __forceinline__ uint32_t crc1_word(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
-    crc ^= w;
-    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-    return (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-}
-
-__global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wins, const uint32_t* __restrict__ crc2win, uint64_t nchunk,
+__global__ void __launch_bounds__(kCrcThreads, 1) k_crc(const WinDesc* __restrict__ wins, const uint32_t* __restrict__ crc2win, uint64_t nchunk,
                                                 const CrcTables* __restrict__ ct, const uint32_t* __restrict__ sh992,
                                                 uint32_t* __restrict__ out) {
     extern __shared__ uint32_t tab[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < 256 * 32; i += kThreads) tab[i] = ct->slice[0][i >> 5];
-    uint32_t* st = tab + 256 * 32;
-    for (int i = tid; i < 1024; i += kThreads) st[i] = sh992[i];
+    load_rep4(tab, ct);
+    uint32_t* st = tab + kRep4Words;
+    for (int i = tid; i < 1024; i += kCrcThreads) st[i] = sh992[i];
     __syncthreads();
     const uint32_t* tl = tab + lane;
     constexpr uint32_t kRows = kCrcChunk / 1024;
-    for (uint64_t c = (uint64_t)blockIdx.x * kWarps + warp; c < nchunk; c += (uint64_t)gridDim.x * kWarps) {
+    for (uint64_t c = (uint64_t)blockIdx.x * kCrcWarps + warp; c < nchunk; c += (uint64_t)gridDim.x * kCrcWarps) {
         const WinDesc wd = wins[crc2win[c]];
         const uint64_t off = (c - wd.crc0) * kCrcChunk;
         const uint32_t L = (uint32_t)min((uint64_t)kCrcChunk, wd.W - off);
@@ -129,14 +124,14 @@ __global__ void __launch_bounds__(kThreads) k_crc(const WinDesc* __restrict__ wi
             load_piece(i + kHalf, b);
             ca = shift992(ca);
             cb = shift992(cb);
-            ca = crc1_word(tl, ca, a[0].x); cb = crc1_word(tl, cb, b[0].x);
-            ca = crc1_word(tl, ca, a[0].y); cb = crc1_word(tl, cb, b[0].y);
-            ca = crc1_word(tl, ca, a[0].z); cb = crc1_word(tl, cb, b[0].z);
-            ca = crc1_word(tl, ca, a[0].w); cb = crc1_word(tl, cb, b[0].w);
-            ca = crc1_word(tl, ca, a[1].x); cb = crc1_word(tl, cb, b[1].x);
-            ca = crc1_word(tl, ca, a[1].y); cb = crc1_word(tl, cb, b[1].y);
-            ca = crc1_word(tl, ca, a[1].z); cb = crc1_word(tl, cb, b[1].z);
-            ca = crc1_word(tl, ca, a[1].w); cb = crc1_word(tl, cb, b[1].w);
+            ca = crc4_rep(tl, ca, a[0].x); cb = crc4_rep(tl, cb, b[0].x);
+            ca = crc4_rep(tl, ca, a[0].y); cb = crc4_rep(tl, cb, b[0].y);
+            ca = crc4_rep(tl, ca, a[0].z); cb = crc4_rep(tl, cb, b[0].z);
+            ca = crc4_rep(tl, ca, a[0].w); cb = crc4_rep(tl, cb, b[0].w);
+            ca = crc4_rep(tl, ca, a[1].x); cb = crc4_rep(tl, cb, b[1].x);
+            ca = crc4_rep(tl, ca, a[1].y); cb = crc4_rep(tl, cb, b[1].y);
+            ca = crc4_rep(tl, ca, a[1].z); cb = crc4_rep(tl, cb, b[1].z);
+            ca = crc4_rep(tl, ca, a[1].w); cb = crc4_rep(tl, cb, b[1].w);
         }
         // chain a ends 16 rows (16 KiB) before chain b
         uint32_t crc = crc_shift_tab(&ct->pow2[14][0][0], ca) ^ cb;
@@ -221,32 +216,34 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
 }
 
 // ------------------------------------------------------------ K2 codebook
-// Warp-level bitonic sort of 256 keys (8 per lane, lane-major), ascending.
-__device__ __forceinline__ void warp_bitonic_sort256(uint64_t key[8], int lane) {
+// Warp-level bitonic sort of 32 K keys (K per lane, lane-major: element
+// i = lane K + r), ascending.
+template <int K, class T>
+__device__ __forceinline__ void warp_bitonic_sort(T key[K], int lane) {
 #pragma unroll
-    for (int kk = 2; kk <= 256; kk <<= 1) {
+    for (int kk = 2; kk <= 32 * K; kk <<= 1) {
 #pragma unroll
         for (int j = kk >> 1; j > 0; j >>= 1) {
-            if (j >= 8) {
-                const int lj = j >> 3;
+            if (j >= K) {
+                const int lj = j / K;
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const int i = lane * 8 + r;
-                    uint64_t other = __shfl_xor_sync(0xFFFFFFFFu, key[r], lj);
+                for (int r = 0; r < K; r++) {
+                    const int i = lane * K + r;
+                    const T other = __shfl_xor_sync(0xFFFFFFFFu, key[r], lj);
                     const bool up = (i & kk) == 0;
                     const bool lower = (i & j) == 0;
                     // lower element keeps min when ascending
-                    uint64_t mn = min(key[r], other), mx = max(key[r], other);
+                    const T mn = min(key[r], other), mx = max(key[r], other);
                     key[r] = (lower == up) ? mn : mx;
                 }
             } else {
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
+                for (int r = 0; r < K; r++) {
                     const int partner = r ^ j;
                     if (partner > r) {
-                        const int i = lane * 8 + r;
+                        const int i = lane * K + r;
                         const bool up = (i & kk) == 0;
-                        uint64_t a = key[r], c = key[partner];
+                        const T a = key[r], c = key[partner];
                         if ((a > c) == up) { key[r] = c; key[partner] = a; }
                     }
                 }
@@ -255,7 +252,7 @@ __device__ __forceinline__ void warp_bitonic_sort256(uint64_t key[8], int lane) 
     }
 }
 
-struct CbSmem {
+struct alignas(16) CbSmem {
     uint32_t wt[512];     // node weights (leaves sorted, then internal nodes)
     uint16_t par[512];    // parent / ancestor
     uint8_t dep[512];     // depth accumulator
@@ -337,46 +334,67 @@ __device__ void finish_block(CbSmem& s, const uint32_t cnt[8], int lane, BlockMe
     }
 }
 
-// Sorted (count, symbol) leaves of one histogram; returns n present.
-__device__ __forceinline__ int sorted_leaves(const uint32_t cnt[8], int lane, uint32_t* wt, uint8_t* sym) {
-    uint64_t key[8];
+// Sorted (count, symbol) leaves of one histogram; returns n present.  Keys
+// are (count << 8) | symbol: 32-bit while counts < 2^24 (every record block:
+// at most 1 MiB), 64-bit otherwise (stage-level histograms).  Only the
+// present symbols are sorted: they are compacted (in symbol order) into
+// `keys` (>= 2 KiB of scratch), then sorted as 64 or 256 keys.
+template <int K, class T>
+__device__ __forceinline__ void sort_compact(const T* keys, int np, int lane, uint32_t* wt, uint8_t* sym) {
+    T key[K];
 #pragma unroll
-    for (int r = 0; r < 8; r++) key[r] = cnt[r] ? (((uint64_t)cnt[r] << 8) | (uint64_t)(lane * 8 + r)) : ~0ull;
-    warp_bitonic_sort256(key, lane);
-    int np = 0;
+    for (int r = 0; r < K; r++) key[r] = lane * K + r < np ? keys[lane * K + r] : ~(T)0;
+    warp_bitonic_sort<K, T>(key, lane);
+    __syncwarp();
 #pragma unroll
-    for (int r = 0; r < 8; r++) np += cnt[r] ? 1 : 0;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) np += __shfl_xor_sync(0xFFFFFFFFu, np, o);
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-        const int i = lane * 8 + r;
+    for (int r = 0; r < K; r++) {
+        const int i = lane * K + r;
         if (i < np) { wt[i] = (uint32_t)(key[r] >> 8); sym[i] = (uint8_t)(key[r] & 0xFF); }
     }
+}
+
+template <class T>
+__device__ __forceinline__ void compact_sort(const uint32_t cnt[8], int lane, int pre, int np, uint32_t* wt, uint8_t* sym,
+                                             T* keys) {
+#pragma unroll
+    for (int r = 0; r < 8; r++)
+        if (cnt[r]) keys[pre++] = ((T)cnt[r] << 8) | (T)(lane * 8 + r);
+    __syncwarp();
+    if (np <= 64) sort_compact<2, T>(keys, np, lane, wt, sym);
+    else sort_compact<8, T>(keys, np, lane, wt, sym);
+}
+
+__device__ __noinline__ int sorted_leaves(const uint32_t cnt[8], int lane, uint32_t* wt, uint8_t* sym, void* keys) {
+    int c = 0;
+    uint32_t mx = 0;
+#pragma unroll
+    for (int r = 0; r < 8; r++) { c += cnt[r] ? 1 : 0; mx = max(mx, cnt[r]); }
+    int pre = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, pre, o);
+        if (lane >= o) pre += y;
+    }
+    const int np = __shfl_sync(0xFFFFFFFFu, pre, 31);
+    pre -= c;
+    if (__any_sync(0xFFFFFFFFu, mx >= (1u << 24))) compact_sort<uint64_t>(cnt, lane, pre, np, wt, sym, static_cast<uint64_t*>(keys));
+    else compact_sort<uint32_t>(cnt, lane, pre, np, wt, sym, static_cast<uint32_t*>(keys));
     __syncwarp();
     return np;
 }
 
 constexpr int kCbWarps = 4;
-// mode_only: block-level path (stream records).  For the stage-level API
-// (lmcg_build_codebooks) lens_out != null and RLE is not special-cased.
-__global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __restrict__ hist, uint64_t nb,
-                                                          BlockMeta* __restrict__ meta, uint8_t* __restrict__ wire,
-                                                          uint8_t* __restrict__ lens_out, uint32_t* __restrict__ pm_flag,
-                                                          uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list,
-                                                          uint64_t part_lo = 0, uint64_t part_hi = ~0ull) {
-    __shared__ CbSmem sm[kCbWarps];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t b = (uint64_t)blockIdx.x * kCbWarps + warp;
-    if (b >= nb) return;
-    if (b < part_lo || b >= part_hi) {   // outside the part: no record
-        if (lane == 0) {
-            BlockMeta m{};
-            meta[b] = m;
-        }
-        return;
-    }
-    CbSmem& s = sm[warp];
+constexpr int kCbBlocks = 16;   // blocks per CTA: one lane of the deferred cost pass each
+constexpr int kDeferMin = 96;   // blocks with this many symbols defer their mode decision
+constexpr size_t kCbColBytes = 512 * kCbBlocks * sizeof(uint16_t);
+
+// Mode, code lengths and wire codebook of block b (stream.py:161-177,
+// huffman.py:79-137), warp-wide.  With `col` (record path only), a block of
+// >= kDeferMin symbols stops after sorting: its sorted weights go to column
+// `col` (u16, stride kCbBlocks) and the symbol count is returned, for the cost pass.
+__device__ int cb_block(CbSmem& s, uint64_t b, int lane, const uint32_t* __restrict__ hist, BlockMeta* __restrict__ meta,
+                        uint8_t* __restrict__ wire, uint8_t* __restrict__ lens_out, uint32_t* __restrict__ pm_flag,
+                        uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list, uint16_t* col) {
     uint32_t cnt[8];
     {
         const uint4* h4 = reinterpret_cast<const uint4*>(hist + b * 256 + lane * 8);
@@ -405,37 +423,47 @@ __global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __re
             m.mode = MODE_RLE; m.sym = (uint8_t)arg; m.recsize = 6; m.bits = 0; m.pm = 0;
             meta[b] = m;
         }
-        return;
+        return 0;
     }
     for (int i = lane; i < 256; i += 32) s.lens[i] = 0;
     if (total == 0) {  // empty histogram (stage-level API only)
         __syncwarp();
         if (lens_out) reinterpret_cast<uint2*>(lens_out + b * 256)[lane] = make_uint2(0, 0);
         if (lane == 0 && pm_flag) atomicOr(pm_flag, 2u);
-        return;
+        return 0;
     }
     if (lens_out == nullptr) {
         // entropy bound: every prefix code costs at least n H bits; when even
         // that cannot beat the stored record (stream.py:173) the block is
         // stored and its code is never built (incompressible planes)
-        double ent = 0.0;   // sum c log2 c
+        // (single precision, MUFU log2: <= 2 ulp per log2, so each c log2 c
+        // term is off by < 0.3 bits and the 256-term sum by < 100 bits; the
+        // 256-bit margin keeps the bound conservative)
+        float ent = 0.f;   // sum c log2 c
 #pragma unroll
         for (int r = 0; r < 8; r++)
-            if (cnt[r]) ent += (double)cnt[r] * log2((double)cnt[r]);
+            if (cnt[r] > 1) ent += (float)cnt[r] * __log2f((float)cnt[r]);
 #pragma unroll
         for (int o = 16; o; o >>= 1) ent += __shfl_xor_sync(0xFFFFFFFFu, ent, o);
-        const double nH = (double)total * log2((double)total) - ent;
+        const float nH = (float)total * __log2f((float)total) - ent;
         const uint32_t len = meta[b].len;
-        if (8.0 * kHuffOverhead + nH - 64.0 > 8.0 * len) {   // (64-bit margin for rounding)
+        if (8.f * kHuffOverhead + nH - 256.f > 8.f * len) {
             if (lane == 0) {
                 BlockMeta m = meta[b];
                 m.mode = MODE_STORED; m.bits = 0; m.recsize = 5 + len; m.pm = 0;
                 meta[b] = m;
             }
-            return;
+            return 0;
         }
     }
-    const int n = sorted_leaves(cnt, lane, s.wt, s.sym);
+    const int n = sorted_leaves(cnt, lane, s.wt, s.sym, s.wt);   // (keys alias wt)
+    if (col && n >= kDeferMin && total <= 65536) {   // (column entries are u16)
+        // many symbols (near-uniform planes, usually stored): hand the sorted
+        // weights to the CTA's lane-per-block cost pass instead of building
+        // the code on one lane here
+        for (int i = lane; i < n; i += 32) col[i * kCbBlocks] = (uint16_t)s.wt[i];
+        return n;
+    }
     if (n == 1) {
         if (lane == 0) s.lens[s.sym[0]] = 1;  // huffman.py:89-91
     } else {
@@ -447,16 +475,108 @@ __global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __re
                 else { BlockMeta m = meta[b]; m.pm = 1; meta[b] = m; }
                 pm_list[atomicAdd(pm_count, 1u)] = (uint32_t)b;
             }
-            return;
+            return 0;
         }
         for (int i = lane; i < n; i += 32) s.lens[s.sym[i]] = s.dep[i];
     }
     __syncwarp();
     if (lens_out) {
         reinterpret_cast<uint2*>(lens_out + b * 256)[lane] = reinterpret_cast<const uint2*>(s.lens)[lane];
-        return;
+        return 0;
     }
     finish_block(s, cnt, lane, meta, wire, b);
+    return 0;
+}
+
+// Cost of the unlimited Huffman code of one sorted column of n >= 2 weights
+// (= the sum of the internal node weights; the two-queue merge with leaf-first
+// ties, huffman.py:106-137), one lane per column, no parent pointers.  The
+// queue heads and next entries live in registers; each pick loads the entry
+// after the next (branch-free).  Internal weights other than the root are
+// < 2^16 (all n >= 2 leaves are non-zero), so the u16 column holds them.
+__device__ __forceinline__ uint32_t huff_cost_lane(uint16_t* col, int n) {
+    constexpr uint32_t kInf = 0xFFFFFFFFu;
+    uint32_t cost = 0;
+    int leaf = 0, node = n;
+    uint32_t L0 = col[0], L1 = n > 1 ? col[kCbBlocks] : kInf, N0 = kInf, N1 = kInf;
+    for (int nxt = n; nxt < 2 * n - 1; nxt++) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            const bool tl = leaf < n && (node >= nxt || L0 <= N0);
+            w += tl ? L0 : N0;
+            const int idx = tl ? leaf + 2 : node + 2;
+            const bool ok = tl ? idx < n : idx < nxt;
+            const uint32_t v = ok ? (uint32_t)col[idx * kCbBlocks] : kInf;
+            leaf += tl ? 1 : 0;
+            node += tl ? 0 : 1;
+            L0 = tl ? L1 : L0;
+            L1 = tl ? v : L1;
+            N0 = tl ? N0 : N1;
+            N1 = tl ? N1 : v;
+        }
+        cost += w;
+        col[nxt * kCbBlocks] = (uint16_t)w;
+        if (node == nxt) N0 = w;
+        else if (node + 1 == nxt) N1 = w;
+    }
+    return cost;
+}
+
+// mode_only: block-level path (stream records).  For the stage-level API
+// (lmcg_build_codebooks) lens_out != null and RLE is not special-cased.
+// CTA of kCbWarps warps per kCbBlocks blocks: the warps prepare the blocks;
+// blocks with many symbols are decided by one lane each (Huffman cost vs the
+// stored record: stored needs no code); the rest build their code warp-wide.
+__global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __restrict__ hist, uint64_t nb,
+                                                          BlockMeta* __restrict__ meta, uint8_t* __restrict__ wire,
+                                                          uint8_t* __restrict__ lens_out, uint32_t* __restrict__ pm_flag,
+                                                          uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list,
+                                                          uint64_t part_lo = 0, uint64_t part_hi = ~0ull) {
+    __shared__ CbSmem sm[kCbWarps];
+    extern __shared__ uint16_t cols[];   // kCbColBytes (record path only): 512 rows x kCbBlocks columns
+    __shared__ int dn[kCbBlocks];
+    __shared__ uint32_t dcost[kCbBlocks];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t b0 = (uint64_t)blockIdx.x * kCbBlocks;
+    for (int j = warp; j < kCbBlocks; j += kCbWarps) {
+        const uint64_t b = b0 + j;
+        int n = 0;
+        if (b < nb) {
+            if (b < part_lo || b >= part_hi) {   // outside the part: no record
+                if (lane == 0) {
+                    BlockMeta m{};
+                    meta[b] = m;
+                }
+            } else {
+                n = cb_block(sm[warp], b, lane, hist, meta, wire, lens_out, pm_flag, pm_count, pm_list,
+                             lens_out ? nullptr : cols + j);
+            }
+        }
+        if (lane == 0) dn[j] = n;
+    }
+    __syncthreads();
+    if (warp == 0 && lane < kCbBlocks) {
+        const int n = dn[lane];
+        dcost[lane] = n ? huff_cost_lane(cols + lane, n) : 0u;
+    }
+    __syncthreads();
+    for (int j = warp; j < kCbBlocks; j += kCbWarps) {
+        if (!dn[j]) continue;
+        const uint64_t b = b0 + j;
+        const uint32_t len = meta[b].len, cost = dcost[j];
+        // a length-limited (package-merge) code costs at least the Huffman
+        // code, so a Huffman cost that loses to the stored record settles it
+        if (kHuffOverhead + (cost + 7) / 8 > len) {
+            if (lane == 0) {
+                BlockMeta m = meta[b];
+                m.mode = MODE_STORED; m.bits = cost; m.recsize = 5 + len; m.pm = 0;
+                meta[b] = m;
+            }
+        } else {
+            cb_block(sm[warp], b, lane, hist, meta, wire, lens_out, pm_flag, pm_count, pm_list, nullptr);
+        }
+    }
 }
 
 // ------------------------------------------------------ K2b package-merge
@@ -490,7 +610,7 @@ __global__ void __launch_bounds__(32) k_pkgmerge(const uint32_t* __restrict__ hi
     uint32_t cnt[8];
 #pragma unroll
     for (int r = 0; r < 8; r++) cnt[r] = hist[b * 256 + lane * 8 + r];
-    const int n = sorted_leaves(cnt, lane, s.lw32, s.sym);
+    const int n = sorted_leaves(cnt, lane, s.lw32, s.sym, s.cur);
     for (int i = lane; i < n; i += 32) { s.lw[i] = s.lw32[i]; s.prev[i] = s.lw32[i]; s.lpos[0][i] = (uint16_t)i; }
     __syncwarp();
     int m = n;

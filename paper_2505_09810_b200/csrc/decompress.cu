@@ -1481,45 +1481,37 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
 }
 
 // -------------------------------------------------------------- k_ungroup
-// CTA per 16 KiB output tile of a window: out[e*w + g] = grouped[g*n + e];
-// each thread produces 64 contiguous output bytes and their raw CRC.
 // Persistent warps over 32 KiB output tiles of the windows (the k_crc
 // layout): out[e*w + g] = grouped[g*n + e].  The warp writes the tile as 32
 // rows of 1 KiB, lane l producing the 32 output bytes at 1024 r + 32 l of
 // each row (coalesced plane loads and 16-byte stores), and folds them into a
 // raw CRC: two Horner chains per lane (rows 0-15, 16-31), a 992-byte shift
-// (4 lookups) per row and the piece through a 32-fold replicated byte table
-// (lane l reads copy l: no bank conflicts); lane values are then shifted to
+// (4 lookups) per row and the piece by slicing-by-4 through 32-fold
+// replicated tables (crc4_rep: lane l reads copy l, no bank conflicts); lane values are then shifted to
 // the tile end and XOR-reduced.  A short last tile is treated as left-padded
 // with zero bytes, which leave a raw CRC unchanged.  lmcg_decompress_apply
 // XORs the previous step into the stores (the CRC stays the payload's).
-constexpr size_t kUngSmem = (size_t)(256 * 32 + 1024) * sizeof(uint32_t);
+constexpr int kUngThreads = 1024;   // one CTA per SM shares the 128 KiB of replicated slicing tables
+constexpr int kUngWarps = kUngThreads / 32;
+constexpr size_t kUngSmem = (kRep4Words + 1024) * sizeof(uint32_t);
 
-__device__ __forceinline__ uint32_t crc1_rep(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
-    crc ^= w;
-    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-    crc = (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-    return (crc >> 8) ^ tl[(crc & 0xFF) * 32];
-}
-
-__global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__ wins, const uint32_t* __restrict__ tile2win,
+__global__ void __launch_bounds__(kUngThreads, 1) k_ungroup(const DecWin* __restrict__ wins, const uint32_t* __restrict__ tile2win,
                                                     uint64_t ntile_total, const uint8_t* __restrict__ scratch,
                                                     uint8_t* out /* may alias a window's prev */, const CrcTables* __restrict__ ct,
                                                     const uint32_t* __restrict__ sh992, uint32_t* __restrict__ tile_crc,
                                                     const uint32_t* __restrict__ status) {
     extern __shared__ uint32_t ung_tab[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < 256 * 32; i += kThreads) ung_tab[i] = ct->slice[0][i >> 5];
-    uint32_t* st = ung_tab + 256 * 32;
-    for (int i = tid; i < 1024; i += kThreads) st[i] = sh992[i];
+    load_rep4(ung_tab, ct);
+    uint32_t* st = ung_tab + kRep4Words;
+    for (int i = tid; i < 1024; i += kUngThreads) st[i] = sh992[i];
     __syncthreads();
     const uint32_t* tl = ung_tab + lane;
     auto shift992 = [&](uint32_t x) {
         return st[x & 0xFF] ^ st[256 + ((x >> 8) & 0xFF)] ^ st[512 + ((x >> 16) & 0xFF)] ^ st[768 + (x >> 24)];
     };
     static_assert(kOutTile == 32768, "k_ungroup rows");
-    for (uint64_t tile = (uint64_t)blockIdx.x * kWarps + warp; tile < ntile_total; tile += (uint64_t)gridDim.x * kWarps) {
+    for (uint64_t tile = (uint64_t)blockIdx.x * kUngWarps + warp; tile < ntile_total; tile += (uint64_t)gridDim.x * kUngWarps) {
         const uint32_t wi = tile2win[tile];
         if (wi == ~0u) {   // unused capacity slot
             if (lane == 0) tile_crc[tile] = 0;
@@ -1610,8 +1602,8 @@ __global__ void __launch_bounds__(kThreads) k_ungroup(const DecWin* __restrict__
             cb = shift992(cb);
 #pragma unroll
             for (int q = 0; q < 8; q++) {
-                ca = crc1_rep(tl, ca, va[q]);
-                cb = crc1_rep(tl, cb, vb[q]);
+                ca = crc4_rep(tl, ca, va[q]);
+                cb = crc4_rep(tl, cb, vb[q]);
             }
         }
         // chain a ends 16 rows (16 KiB) before chain b; lane l's value ends

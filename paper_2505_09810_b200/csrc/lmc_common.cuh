@@ -87,6 +87,20 @@ __device__ __forceinline__ uint32_t crc_word(const uint32_t* __restrict__ sl, ui
     return sl[768 + (crc & 0xFF)] ^ sl[512 + ((crc >> 8) & 0xFF)] ^ sl[256 + ((crc >> 16) & 0xFF)] ^
            sl[crc >> 24];
 }
+// Slicing-by-4 through 32-fold replicated tables: tl = table base + lane,
+// entry (k, i) of slice k at tl[(256 k + i) * 32], so every lane reads its own
+// bank (no conflicts) and one 32-bit word costs four lookups and no shifts of
+// the running CRC between them.
+constexpr size_t kRep4Words = 4 * 256 * 32;
+__device__ __forceinline__ void load_rep4(uint32_t* tab, const CrcTables* __restrict__ ct) {
+    const uint32_t* flat = &ct->slice[0][0];
+    for (int i = threadIdx.x; i < (int)kRep4Words; i += blockDim.x) tab[i] = __ldg(flat + (i >> 5));
+}
+__device__ __forceinline__ uint32_t crc4_rep(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
+    const uint32_t x = crc ^ w;
+    return tl[(768 + (x & 0xFF)) * 32] ^ tl[(512 + ((x >> 8) & 0xFF)) * 32] ^ tl[(256 + ((x >> 16) & 0xFF)) * 32] ^
+           tl[(x >> 24) * 32];
+}
 __device__ __forceinline__ uint32_t crc_byte(const uint32_t* __restrict__ sl, uint32_t crc, uint32_t b) {
     return (crc >> 8) ^ sl[(crc ^ b) & 0xFF];
 }
