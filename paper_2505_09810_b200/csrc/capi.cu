@@ -481,7 +481,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         }
         { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbBlocks - 1) / kCbBlocks), kCbWarps * 32, kCbColBytes, st>>>(
             d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist, part ? part_lo : 0, part ? part_hi : ~0ull); }
-        { PROF(k_pkgmerge); k_pkgmerge<<<296, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr); }
+        { PROF(k_pkgmerge); k_pkgmerge<<<kPmGrid, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr); }
     }
     { PROF(k_scan); k_scan<<<(unsigned)std::max<uint64_t>(ntiles, 1), kScanThreads, 0, st>>>(d_meta, nb, d_scan, d_status, d_ctr); }
     if (n && !part) {
@@ -772,7 +772,7 @@ int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint
     CK(cudaMemsetAsync(d_ctr, 0, 16, st));
     { PROF(k_codebook); k_codebook<<<(nhist + kCbBlocks - 1) / kCbBlocks, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
                                                                              d_lengths, d_ctr, d_ctr + 1, d_list); }
-    { PROF(k_pkgmerge); k_pkgmerge<<<296, 32, 0, st>>>(d_hists, d_ctr + 1, d_list, nullptr, nullptr, d_lengths); }
+    { PROF(k_pkgmerge); k_pkgmerge<<<kPmGrid, 32, 0, st>>>(d_hists, d_ctr + 1, d_list, nullptr, nullptr, d_lengths); }
     CK(cudaGetLastError());
     uint32_t flag = 0;
     CK(cudaMemcpyAsync(&flag, d_ctr, 4, cudaMemcpyDeviceToHost, st));

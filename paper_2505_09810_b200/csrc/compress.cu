@@ -383,7 +383,7 @@ __device__ __noinline__ int sorted_leaves(const uint32_t cnt[8], int lane, uint3
     return np;
 }
 
-constexpr int kCbWarps = 4;
+constexpr int kCbWarps = 8;
 constexpr int kCbBlocks = 16;   // blocks per CTA: one lane of the deferred cost pass each
 constexpr int kDeferMin = 96;   // blocks with this many symbols defer their mode decision
 constexpr size_t kCbColBytes = 512 * kCbBlocks * sizeof(uint16_t);
@@ -598,6 +598,7 @@ struct PmSmem {
     uint8_t lens[256];
 };
 
+constexpr int kPmGrid = 148 * 8;   // persistent single-warp CTAs (8 per SM by shared memory)
 __global__ void __launch_bounds__(32) k_pkgmerge(const uint32_t* __restrict__ hist, const uint32_t* __restrict__ pm_count,
                                                  const uint32_t* __restrict__ pm_list, BlockMeta* __restrict__ meta,
                                                  uint8_t* __restrict__ wire, uint8_t* __restrict__ lens_out) {
