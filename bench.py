@@ -114,13 +114,15 @@ def measured_peaks() -> tuple[float, str]:
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel: str):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu summary, or None."""
+def ncu_traffic(kernel: str, config: str):
+    """Per-launch DRAM bytes of `kernel` on `config` from the committed ncu
+    capture (profiles/ncu_traffic.json: config -> kernel -> bytes), or None
+    when that config was not captured."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get(kernel)
+        return d.get(config, {}).get(kernel)
     except Exception:
         return None
 
@@ -373,7 +375,7 @@ def run_ours(args, ws, rank, local):
     algo_bytes = a_in * nbytes + a_st * stream_bytes   # per launch (one launch per batch)
     achieved = algo_bytes / (avg_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname), "peak_source": peak_src,
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, args.config), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": round(avg_ms, 4),
                 "share_of_step": round(dms / sum(v[1] for v in prof.values()), 4)}
     # pipeline-level fractions (compress: in + stream, decompress: stream + out)

@@ -58,6 +58,14 @@ if __name__ == '__main__':
         traffic = {k: to_bytes(d['dram__bytes_read.sum']) + to_bytes(d['dram__bytes_write.sum'])
                    for k, d in res['full'].items()}
         res['traffic_bytes_per_launch'] = traffic
-        json.dump(traffic, open('profiles/ncu_traffic.json', 'w'), indent=1)
+        cfg = os.environ.get('CONFIG', 'cfg2')
+        try:
+            allt = json.load(open('profiles/ncu_traffic.json'))
+            if not all(isinstance(v, dict) for v in allt.values()):
+                allt = {}
+        except Exception:
+            allt = {}
+        allt[cfg] = traffic
+        json.dump(allt, open('profiles/ncu_traffic.json', 'w'), indent=1)
     json.dump(res, open(f'profiles/{tag}_ncu.json', 'w'), indent=1)
     print(json.dumps(res.get('launch_list', {}), indent=1))

@@ -2,7 +2,7 @@
 # Run on the GPU box (under gpurun): plain bench, launch list, one full capture per hot kernel.
 set -u
 OUT=${1:-gpurun_out}
-ARGS="--steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
+ARGS="--steps 2 --warmup 1 --no-e2e --no-cpu-baseline --config ${CONFIG:-cfg2}"
 mkdir -p $OUT
 timeout 300 python bench.py $ARGS > $OUT/prof_plain.log 2>&1 || { echo "plain run failed"; tail -20 $OUT/prof_plain.log; exit 1; }
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python bench.py $ARGS > $OUT/ncu_launch.log 2>&1
