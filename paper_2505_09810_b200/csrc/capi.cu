@@ -456,7 +456,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
             CK(cudaEventRecord(ctx->fork_ev, st));
             CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev, 0));
         }
-        const uint64_t need = (ncrc + kCrcWarps - 1) / kCrcWarps;
+        const uint64_t need = ncrc;   // (chunks are dealt CTA-major)
         cudaStream_t sst = ctx->serial ? st : ctx->side;
         ProfScope prof_scope_k_crc(ctx, "k_crc", sst);
         k_crc<<<(unsigned)std::min<uint64_t>(need, (uint64_t)ctx->crc_occ), kCrcThreads, kCrcSmem, sst>>>(
@@ -476,11 +476,19 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         if (int r = launch_crc()) return r;
     if (nb) {
         if (!ctx->cb_attr) {
-            CK(cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCbColBytes));
+            CK(cudaFuncSetAttribute(k_codebook<kCbBlocksLarge>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCbColBytes));
             ctx->cb_attr = true;
         }
-        { PROF(k_codebook); k_codebook<<<(unsigned)((nb + kCbBlocks - 1) / kCbBlocks), kCbWarps * 32, kCbColBytes, st>>>(
-            d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist, part ? part_lo : 0, part ? part_hi : ~0ull); }
+        if (nb >= kCbLargeFrom) {
+            PROF(k_codebook);
+            k_codebook<kCbBlocksLarge><<<(unsigned)((nb + kCbBlocksLarge - 1) / kCbBlocksLarge), kCbWarps * 32, kCbColBytes, st>>>(
+                d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist, part ? part_lo : 0, part ? part_hi : ~0ull);
+        } else {
+            PROF(k_codebook);
+            k_codebook<kCbBlocksSmall><<<(unsigned)((nb + kCbBlocksSmall - 1) / kCbBlocksSmall), kCbWarps * 32,
+                                         512 * kCbBlocksSmall * sizeof(uint16_t), st>>>(
+                d_hist, nb, d_meta, d_wire, nullptr, nullptr, d_ctr + 1, d_pmlist, part ? part_lo : 0, part ? part_hi : ~0ull);
+        }
         { PROF(k_pkgmerge); k_pkgmerge<<<kPmGrid, 32, 0, st>>>(d_hist, d_ctr + 1, d_pmlist, d_meta, d_wire, nullptr); }
     }
     { PROF(k_scan); k_scan<<<(unsigned)std::max<uint64_t>(ntiles, 1), kScanThreads, 0, st>>>(d_meta, nb, d_scan, d_status, d_ctr); }
@@ -605,7 +613,7 @@ int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* 
     uint32_t* parts = reinterpret_cast<uint32_t*>(ctx->part_ws + 256);
     uint32_t* one_win = parts + nchunk + 1;   // every chunk -> window 0
     CK(cudaMemsetAsync(one_win, 0, 4 * (nchunk + 1), st));
-    k_crc<<<(unsigned)std::min<uint64_t>((nchunk + kCrcWarps - 1) / kCrcWarps, (uint64_t)ctx->crc_occ), kCrcThreads, kCrcSmem, st>>>(
+    k_crc<<<(unsigned)std::min<uint64_t>(nchunk, (uint64_t)ctx->crc_occ), kCrcThreads, kCrcSmem, st>>>(
         reinterpret_cast<const WinDesc*>(ctx->part_ws), one_win, nchunk, ctx->d_crc, ctx->d_sh992, parts);
     k_crc_join<<<1, kThreads, 0, st>>>(parts, L, ctx->d_crc, d_crc);
     CK(cudaGetLastError());
@@ -770,7 +778,7 @@ int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint
     uint32_t* d_ctr = reinterpret_cast<uint32_t*>(ctx->ws);
     uint32_t* d_list = reinterpret_cast<uint32_t*>(ctx->ws + 256);
     CK(cudaMemsetAsync(d_ctr, 0, 16, st));
-    { PROF(k_codebook); k_codebook<<<(nhist + kCbBlocks - 1) / kCbBlocks, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
+    { PROF(k_codebook); k_codebook<kCbBlocksSmall><<<(nhist + kCbBlocksSmall - 1) / kCbBlocksSmall, kCbWarps * 32, 0, st>>>(d_hists, (uint64_t)nhist, nullptr, nullptr,
                                                                              d_lengths, d_ctr, d_ctr + 1, d_list); }
     { PROF(k_pkgmerge); k_pkgmerge<<<kPmGrid, 32, 0, st>>>(d_hists, d_ctr + 1, d_list, nullptr, nullptr, d_lengths); }
     CK(cudaGetLastError());
@@ -957,7 +965,7 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
             ctx->ung_occ = occupancy(ctx, (const void*)k_ungroup, kUngThreads, kUngSmem);
         }
         PROF(k_ungroup);
-        k_ungroup<<<(unsigned)std::min<uint64_t>((ntile + kUngWarps - 1) / kUngWarps, (uint64_t)ctx->ung_occ), kUngThreads, kUngSmem, st>>>(
+        k_ungroup<<<(unsigned)std::min<uint64_t>(ntile, (uint64_t)ctx->ung_occ), kUngThreads, kUngSmem, st>>>(
             d_win, d_t2w, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, ctx->d_sh992, d_tc, d_st);
     }
     { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st, d_in); }

@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(kCrcThreads, 1) k_crc(const WinDesc* __restric
     __syncthreads();
     const uint32_t* tl = tab + lane;
     constexpr uint32_t kRows = kCrcChunk / 1024;
-    for (uint64_t c = (uint64_t)blockIdx.x * kCrcWarps + warp; c < nchunk; c += (uint64_t)gridDim.x * kCrcWarps) {
+    // chunks dealt CTA-major (c = blockIdx.x + gridDim.x * j): small inputs still use every SM
+    for (uint64_t j = warp, c = blockIdx.x + (uint64_t)warp * gridDim.x; c < nchunk;
+         j += kCrcWarps, c = blockIdx.x + j * gridDim.x) {
         const WinDesc wd = wins[crc2win[c]];
         const uint64_t off = (c - wd.crc0) * kCrcChunk;
         const uint32_t L = (uint32_t)min((uint64_t)kCrcChunk, wd.W - off);
@@ -384,14 +386,18 @@ __device__ __noinline__ int sorted_leaves(const uint32_t cnt[8], int lane, uint3
 }
 
 constexpr int kCbWarps = 8;
-constexpr int kCbBlocks = 16;   // blocks per CTA: one lane of the deferred cost pass each
+// Blocks per CTA: 8 (one per warp: the most blocks in flight, for small
+// inputs) or 16 (large inputs: the deferred cost pass keeps 16 lanes busy)
+constexpr int kCbBlocksSmall = 8, kCbBlocksLarge = 16;
+constexpr uint64_t kCbLargeFrom = 65536;   // blocks
 constexpr int kDeferMin = 96;   // blocks with this many symbols defer their mode decision
-constexpr size_t kCbColBytes = 512 * kCbBlocks * sizeof(uint16_t);
+constexpr size_t kCbColBytes = 512 * kCbBlocksLarge * sizeof(uint16_t);
 
 // Mode, code lengths and wire codebook of block b (stream.py:161-177,
 // huffman.py:79-137), warp-wide.  With `col` (record path only), a block of
 // >= kDeferMin symbols stops after sorting: its sorted weights go to column
-// `col` (u16, stride kCbBlocks) and the symbol count is returned, for the cost pass.
+// `col` (u16, stride NB) and the symbol count is returned, for the cost pass.
+template <int NB>
 __device__ int cb_block(CbSmem& s, uint64_t b, int lane, const uint32_t* __restrict__ hist, BlockMeta* __restrict__ meta,
                         uint8_t* __restrict__ wire, uint8_t* __restrict__ lens_out, uint32_t* __restrict__ pm_flag,
                         uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list, uint16_t* col) {
@@ -432,6 +438,7 @@ __device__ int cb_block(CbSmem& s, uint64_t b, int lane, const uint32_t* __restr
         if (lane == 0 && pm_flag) atomicOr(pm_flag, 2u);
         return 0;
     }
+    bool near_stored = false;
     if (lens_out == nullptr) {
         // entropy bound: every prefix code costs at least n H bits; when even
         // that cannot beat the stored record (stream.py:173) the block is
@@ -447,6 +454,8 @@ __device__ int cb_block(CbSmem& s, uint64_t b, int lane, const uint32_t* __restr
         for (int o = 16; o; o >>= 1) ent += __shfl_xor_sync(0xFFFFFFFFu, ent, o);
         const float nH = (float)total * __log2f((float)total) - ent;
         const uint32_t len = meta[b].len;
+        // within 3% of incompressible: most likely stored (the deferred cost pass)
+        near_stored = 8.f * kHuffOverhead + nH > 0.97f * 8.f * len;
         if (8.f * kHuffOverhead + nH - 256.f > 8.f * len) {
             if (lane == 0) {
                 BlockMeta m = meta[b];
@@ -457,11 +466,11 @@ __device__ int cb_block(CbSmem& s, uint64_t b, int lane, const uint32_t* __restr
         }
     }
     const int n = sorted_leaves(cnt, lane, s.wt, s.sym, s.wt);   // (keys alias wt)
-    if (col && n >= kDeferMin && total <= 65536) {   // (column entries are u16)
+    if (col && n >= kDeferMin && near_stored && total <= 65536) {   // (column entries are u16)
         // many symbols (near-uniform planes, usually stored): hand the sorted
         // weights to the CTA's lane-per-block cost pass instead of building
         // the code on one lane here
-        for (int i = lane; i < n; i += 32) col[i * kCbBlocks] = (uint16_t)s.wt[i];
+        for (int i = lane; i < n; i += 32) col[i * NB] = (uint16_t)s.wt[i];
         return n;
     }
     if (n == 1) {
@@ -494,11 +503,12 @@ __device__ int cb_block(CbSmem& s, uint64_t b, int lane, const uint32_t* __restr
 // queue heads and next entries live in registers; each pick loads the entry
 // after the next (branch-free).  Internal weights other than the root are
 // < 2^16 (all n >= 2 leaves are non-zero), so the u16 column holds them.
+template <int NB>
 __device__ __forceinline__ uint32_t huff_cost_lane(uint16_t* col, int n) {
     constexpr uint32_t kInf = 0xFFFFFFFFu;
     uint32_t cost = 0;
     int leaf = 0, node = n;
-    uint32_t L0 = col[0], L1 = n > 1 ? col[kCbBlocks] : kInf, N0 = kInf, N1 = kInf;
+    uint32_t L0 = col[0], L1 = n > 1 ? col[NB] : kInf, N0 = kInf, N1 = kInf;
     for (int nxt = n; nxt < 2 * n - 1; nxt++) {
         uint32_t w = 0;
 #pragma unroll
@@ -507,7 +517,7 @@ __device__ __forceinline__ uint32_t huff_cost_lane(uint16_t* col, int n) {
             w += tl ? L0 : N0;
             const int idx = tl ? leaf + 2 : node + 2;
             const bool ok = tl ? idx < n : idx < nxt;
-            const uint32_t v = ok ? (uint32_t)col[idx * kCbBlocks] : kInf;
+            const uint32_t v = ok ? (uint32_t)col[idx * NB] : kInf;
             leaf += tl ? 1 : 0;
             node += tl ? 0 : 1;
             L0 = tl ? L1 : L0;
@@ -516,7 +526,7 @@ __device__ __forceinline__ uint32_t huff_cost_lane(uint16_t* col, int n) {
             N1 = tl ? N1 : v;
         }
         cost += w;
-        col[nxt * kCbBlocks] = (uint16_t)w;
+        col[nxt * NB] = (uint16_t)w;
         if (node == nxt) N0 = w;
         else if (node + 1 == nxt) N1 = w;
     }
@@ -525,21 +535,22 @@ __device__ __forceinline__ uint32_t huff_cost_lane(uint16_t* col, int n) {
 
 // mode_only: block-level path (stream records).  For the stage-level API
 // (lmcg_build_codebooks) lens_out != null and RLE is not special-cased.
-// CTA of kCbWarps warps per kCbBlocks blocks: the warps prepare the blocks;
+// CTA of kCbWarps warps per NB blocks: the warps prepare the blocks;
 // blocks with many symbols are decided by one lane each (Huffman cost vs the
 // stored record: stored needs no code); the rest build their code warp-wide.
+template <int NB>
 __global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __restrict__ hist, uint64_t nb,
                                                           BlockMeta* __restrict__ meta, uint8_t* __restrict__ wire,
                                                           uint8_t* __restrict__ lens_out, uint32_t* __restrict__ pm_flag,
                                                           uint32_t* __restrict__ pm_count, uint32_t* __restrict__ pm_list,
                                                           uint64_t part_lo = 0, uint64_t part_hi = ~0ull) {
     __shared__ CbSmem sm[kCbWarps];
-    extern __shared__ uint16_t cols[];   // kCbColBytes (record path only): 512 rows x kCbBlocks columns
-    __shared__ int dn[kCbBlocks];
-    __shared__ uint32_t dcost[kCbBlocks];
+    extern __shared__ uint16_t cols[];   // (record path only) 512 rows x NB columns
+    __shared__ int dn[NB];
+    __shared__ uint32_t dcost[NB];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t b0 = (uint64_t)blockIdx.x * kCbBlocks;
-    for (int j = warp; j < kCbBlocks; j += kCbWarps) {
+    const uint64_t b0 = (uint64_t)blockIdx.x * NB;
+    for (int j = warp; j < NB; j += kCbWarps) {
         const uint64_t b = b0 + j;
         int n = 0;
         if (b < nb) {
@@ -549,19 +560,19 @@ __global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __re
                     meta[b] = m;
                 }
             } else {
-                n = cb_block(sm[warp], b, lane, hist, meta, wire, lens_out, pm_flag, pm_count, pm_list,
+                n = cb_block<NB>(sm[warp], b, lane, hist, meta, wire, lens_out, pm_flag, pm_count, pm_list,
                              lens_out ? nullptr : cols + j);
             }
         }
         if (lane == 0) dn[j] = n;
     }
     __syncthreads();
-    if (warp == 0 && lane < kCbBlocks) {
+    if (warp == 0 && lane < NB) {
         const int n = dn[lane];
-        dcost[lane] = n ? huff_cost_lane(cols + lane, n) : 0u;
+        dcost[lane] = n ? huff_cost_lane<NB>(cols + lane, n) : 0u;
     }
     __syncthreads();
-    for (int j = warp; j < kCbBlocks; j += kCbWarps) {
+    for (int j = warp; j < NB; j += kCbWarps) {
         if (!dn[j]) continue;
         const uint64_t b = b0 + j;
         const uint32_t len = meta[b].len, cost = dcost[j];
@@ -574,7 +585,7 @@ __global__ void __launch_bounds__(kCbWarps * 32) k_codebook(const uint32_t* __re
                 meta[b] = m;
             }
         } else {
-            cb_block(sm[warp], b, lane, hist, meta, wire, lens_out, pm_flag, pm_count, pm_list, nullptr);
+            cb_block<NB>(sm[warp], b, lane, hist, meta, wire, lens_out, pm_flag, pm_count, pm_list, nullptr);
         }
     }
 }

@@ -1511,7 +1511,10 @@ __global__ void __launch_bounds__(kUngThreads, 1) k_ungroup(const DecWin* __rest
         return st[x & 0xFF] ^ st[256 + ((x >> 8) & 0xFF)] ^ st[512 + ((x >> 16) & 0xFF)] ^ st[768 + (x >> 24)];
     };
     static_assert(kOutTile == 32768, "k_ungroup rows");
-    for (uint64_t tile = (uint64_t)blockIdx.x * kUngWarps + warp; tile < ntile_total; tile += (uint64_t)gridDim.x * kUngWarps) {
+    // tiles are dealt CTA-major (tile = blockIdx.x + gridDim.x * j, warp w
+    // takes j = w, w + 32, ...), so a small window still spreads over every SM
+    for (uint64_t j = warp, tile = blockIdx.x + (uint64_t)warp * gridDim.x; tile < ntile_total;
+         j += kUngWarps, tile = blockIdx.x + j * gridDim.x) {
         const uint32_t wi = tile2win[tile];
         if (wi == ~0u) {   // unused capacity slot
             if (lane == 0) tile_crc[tile] = 0;
