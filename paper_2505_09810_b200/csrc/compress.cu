@@ -1119,6 +1119,78 @@ __device__ void store_plane(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_
     }
 }
 
+// Stored record payload, fast path: [p0, p1) inside one plane, a multiple of
+// 16 bytes, 16-byte source loads allowed.  Thread t owns payload piece k (16
+// bytes gathered from 16 W source bytes) and writes the 16-byte aligned
+// destination chunk k, which holds the end of piece k-1 (from the lane below
+// by shuffle; lane 0 gathers it again) and the start of piece k: aligned
+// 16-byte stores, no staging.  The record's first and last chunks share bytes
+// with the header / the next record and are written bytewise.
+template <int W>
+__device__ __forceinline__ uint4 stored_piece(const WinDesc& wd, uint64_t sb, uint32_t g, uint32_t k) {
+    constexpr uint32_t lw = W == 1 ? 0 : (W == 2 ? 1 : 2);
+    const uint64_t s = sb + ((uint64_t)k << (4 + lw));
+    if constexpr (W == 1) {
+        return ldg16x(wd.src, wd.prev, s);
+    } else {
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < W; q++) {
+            uint32_t sy[4];
+            piece_symbols(ldg16x(wd.src, wd.prev, s + 16 * q), W, g, sy);
+#pragma unroll
+            for (int i = 0; i < 4 / W; i++) o[q * (4 / W) + i] = sy[i];
+        }
+        return make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+__device__ __forceinline__ uint4 chunk_of(uint4 Q, uint4 P, uint32_t lb) {
+    // bytes [16 - lb, 32 - lb) of Q ++ P (1 <= lb <= 15)
+    const uint32_t s = 16 - lb, r = 8 * (s & 3);
+    switch (s >> 2) {
+    case 0: return make_uint4(__funnelshift_r(Q.x, Q.y, r), __funnelshift_r(Q.y, Q.z, r), __funnelshift_r(Q.z, Q.w, r), __funnelshift_r(Q.w, P.x, r));
+    case 1: return make_uint4(__funnelshift_r(Q.y, Q.z, r), __funnelshift_r(Q.z, Q.w, r), __funnelshift_r(Q.w, P.x, r), __funnelshift_r(P.x, P.y, r));
+    case 2: return make_uint4(__funnelshift_r(Q.z, Q.w, r), __funnelshift_r(Q.w, P.x, r), __funnelshift_r(P.x, P.y, r), __funnelshift_r(P.y, P.z, r));
+    default: return make_uint4(__funnelshift_r(Q.w, P.x, r), __funnelshift_r(P.x, P.y, r), __funnelshift_r(P.y, P.z, r), __funnelshift_r(P.z, P.w, r));
+    }
+}
+
+template <int W>
+__device__ void store_plane_fast(const WinDesc& wd, uint64_t p0, uint64_t p1, uint8_t* d0) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint32_t g = (uint32_t)plane_of(p0, wd.n, W);
+    const uint64_t sb = (p0 - (uint64_t)g * wd.n) * W;   // source byte of payload byte 0
+    const uint32_t K = (uint32_t)((p1 - p0) / 16);
+    const uint32_t lb = (uint32_t)(reinterpret_cast<uint64_t>(d0) & 15);
+    uint4* A = reinterpret_cast<uint4*>(reinterpret_cast<uint64_t>(d0) & ~15ull);
+    for (uint32_t k0 = 0; k0 < K; k0 += kThreads) {
+        const uint32_t k = k0 + tid;
+        const bool have = k < K;
+        const uint4 P = have ? stored_piece<W>(wd, sb, g, k) : make_uint4(0, 0, 0, 0);
+        if (lb == 0) {
+            if (have) A[k] = P;
+            continue;
+        }
+        uint4 Q;
+        Q.x = __shfl_up_sync(0xFFFFFFFFu, P.x, 1);
+        Q.y = __shfl_up_sync(0xFFFFFFFFu, P.y, 1);
+        Q.z = __shfl_up_sync(0xFFFFFFFFu, P.z, 1);
+        Q.w = __shfl_up_sync(0xFFFFFFFFu, P.w, 1);
+        if (!have) continue;
+        if (lane == 0 && k > 0) Q = stored_piece<W>(wd, sb, g, k - 1);
+        if (k > 0) A[k] = chunk_of(Q, P, lb);
+        if (k == 0 || k + 1 == K) {   // the partial chunks: bytewise
+            const uint64_t lo = (uint64_t)P.x | ((uint64_t)P.y << 32), hi = (uint64_t)P.z | ((uint64_t)P.w << 32);
+            auto byte = [&](uint32_t i) { return (uint8_t)((i < 8 ? lo >> (8 * i) : hi >> (8 * (i - 8))) & 0xFF); };
+            if (k == 0)
+                for (uint32_t i = 0; i < 16 - lb; i++) d0[i] = byte(i);
+            if (k + 1 == K)
+                for (uint32_t i = 16 - lb; i < 16; i++) d0[16 * (uint64_t)k + i] = byte(i);
+        }
+    }
+}
+
 // One CTA per block slot.  Canonical codes (huffman.py:213-225) are built in
 // shared memory from the wire codebook; each lane packs the codes of its four
 // pieces MSB-first into a shared staging area laid out on the 4-byte grid of
@@ -1170,6 +1242,13 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     const uint32_t w = wd.w;
     const uint64_t p0 = k * B, p1 = min(wd.W, p0 + B);
     if (!huff) {  // stored record: the block's bytes verbatim after the 5-byte header
+        const uint64_t g0 = plane_of(p0, wd.n, w);
+        if (wd.vec && ((p1 - p0) & 15) == 0 && p1 <= (g0 + 1) * wd.n) {
+            if (w == 1) store_plane_fast<1>(wd, p0, p1, rp + 5);
+            else if (w == 2) store_plane_fast<2>(wd, p0, p1, rp + 5);
+            else store_plane_fast<4>(wd, p0, p1, rp + 5);
+            return;
+        }
         store_plane(wd, p0, p1, stg, rp + 5);
         return;
     }
