@@ -152,6 +152,40 @@ __global__ void __launch_bounds__(kCrcThreads, 1) k_crc(const WinDesc* __restric
 // aligned) use vector loads; other tiles gather byte by byte.  Plane-0
 // tiles also fold their full elements into the CRC (lane tree over 16-byte
 // pieces, then the four rows in order).
+// The warp-tiles of one block for element width W (compile-time: the plane
+// gather and the per-piece symbol count are then static).
+template <int W>
+__device__ __forceinline__ void hist_tiles(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_t* hist, int lane, int warp) {
+    constexpr uint32_t lw = W == 1 ? 0 : (W == 2 ? 1 : 2);
+    constexpr uint64_t T = kTileBytes >> lw;    // positions per warp-tile
+    constexpr int per = 16 / W;                 // symbols per 16-byte piece
+    const uint64_t ntiles = (p1 - p0 + T - 1) / T;
+    for (uint64_t t = warp; t < ntiles; t += kWarps) {
+        const uint64_t tp = p0 + t * T;
+        const uint64_t te = min(tp + T, p1);
+        const uint64_t g = plane_of(tp, wd.n, W);
+        const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
+        if (fast) {
+            const uint64_t base = ((tp - g * wd.n) << lw) + 16ull * lane;
+            uint4 a[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, base + 512ull * q);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                uint32_t sy[4];
+                piece_symbols(a[q], W, (uint32_t)g, sy);
+#pragma unroll
+                for (int i = 0; i < per; i++) atomicAdd(&hist[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF], 1u);
+            }
+        } else {
+            // slow gather: lane owns positions [tp + lane*T/32, ...)
+            constexpr uint64_t pl = T / 32;
+            const uint64_t a = tp + lane * pl, bnd = min(a + pl, te);
+            for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p)], 1u);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
     uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta, uint64_t part_lo, uint64_t part_hi) {
@@ -169,37 +203,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
 
     const uint64_t p0 = k * B;
     const uint64_t p1 = min(wd.W, p0 + B);
-    const uint32_t w = wd.w;
-    const uint32_t lw = lg2w(w);
-    const uint64_t T = kTileBytes >> lw;        // positions per warp-tile
-    const uint64_t ntiles = (p1 - p0 + T - 1) >> (11 - lw);
-    uint32_t* hist = sh_hist[warp];
-
-    for (uint64_t t = warp; t < ntiles; t += kWarps) {
-        const uint64_t tp = p0 + t * T;
-        const uint64_t te = min(tp + T, p1);
-        const uint64_t g = plane_of(tp, wd.n, w);
-        const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
-        if (fast) {
-            const uint64_t base = ((tp - g * wd.n) << lw) + 16ull * lane;
-            uint4 a[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, base + 512ull * q);
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-                uint32_t sy[4];
-                const int ns = piece_symbols(a[q], w, (uint32_t)g, sy);
-#pragma unroll
-                for (int i = 0; i < 16; i++)
-                    if (i < ns) atomicAdd(&hist[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF], 1u);
-            }
-        } else {
-            // slow gather: lane owns positions [tp + lane*T/32, ...)
-            const uint64_t per = T / 32;
-            const uint64_t a = tp + lane * per, bnd = min(a + per, te);
-            for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p)], 1u);
-        }
-    }
+    if (wd.w == 1) hist_tiles<1>(wd, p0, p1, sh_hist[warp], lane, warp);
+    else if (wd.w == 2) hist_tiles<2>(wd, p0, p1, sh_hist[warp], lane, warp);
+    else hist_tiles<4>(wd, p0, p1, sh_hist[warp], lane, warp);
     __syncthreads();
     // block histogram
     const uint64_t b = wd.blk0 + k;
