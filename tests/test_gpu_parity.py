@@ -335,3 +335,40 @@ def test_run_symbol_paths(codec, et, density):
         r.raise_for_status()
         assert torch.equal(r.payload(0), cur)
     assert fallback_segments(codec) == 0
+
+
+def _near_threshold_bytes(rng, n_blocks: int, block: int) -> bytes:
+    """raw8 blocks whose Huffman cost straddles the stored record: a skewed
+    byte distribution (p ~ exp(-a i / 256)) with a swept over [0, 3) from
+    near-uniform (stored) through the decision boundary (a ~ 2.2 for 4 KiB
+    blocks, ~ 1 for 64 KiB: the 132-byte codebook overhead) to clearly
+    compressible, plus fully uniform and 100-symbol blocks."""
+    out = []
+    for j in range(n_blocks):
+        a = 3.0 * j / n_blocks
+        if j % 7 == 3:
+            x = rng.integers(0, 256, block, dtype=np.uint8)
+        elif j % 7 == 5:
+            x = rng.integers(0, 100, block, dtype=np.uint8)
+        else:
+            p = np.exp(-a * np.arange(256) / 256.0)
+            x = rng.choice(256, size=block, p=p / p.sum()).astype(np.uint8)
+        out.append(x.tobytes())
+    return b"".join(out)
+
+
+@pytest.mark.parametrize("block", [4096, 65536, 262144, 1 << 20])
+def test_mode_decision_boundary(codec, rng, block):
+    """Stored / Huffman decisions near the boundary (k_codebook's deferred
+    lane-per-block cost pass, its u16 columns only for blocks <= 64 KiB, the
+    float entropy bound): streams and per-block modes equal the oracle's."""
+    nb = {4096: 96, 65536: 48, 262144: 12, 1 << 20: 4}[block]
+    data = _near_threshold_bytes(rng, nb, block)
+    b = codec.compress([dev_bytes(data)], element_types=[0], block_size=block)
+    assert b.to_bytes()[0] == O.compress(data, 0, block_size=block, threads=8)
+    info = codec.block_info()
+    modes, bits, sizes, lengths, pm = O.analyze_blocks(data, block)
+    assert (info["modes"] == modes).all() and (info["sizes"] == sizes).all()
+    assert len(set(modes.tolist())) >= 2   # both sides of the boundary are present
+    r = codec.decompress(b)
+    assert r.status == [0] and host_bytes(r.payload(0)) == data
