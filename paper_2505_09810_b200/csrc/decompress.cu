@@ -794,11 +794,14 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
         if (n) ent = (n << 30) | (tl << 26) | syms;
         s.lut3[e] = ent;
     }
-    // count LUT: every whole codeword of a 12-bit window (greedy); records
-    // with a 1-bit code count with the 3-symbol LUT plus runs instead
+    // count LUT: every whole codeword of a 12-bit window (greedy, continued
+    // from the 3-symbol LUT's codewords of its first 11 bits); records with a
+    // 1-bit code count with the 3-symbol LUT plus runs instead
+    __syncthreads();
     if (!s.bl_count[1])
     for (int e = tid; e < (1 << kCntLut); e += kThreads) {
-        uint32_t n = 0, tl = 0;
+        const uint32_t e3 = s.lut3[e >> (kCntLut - kLut)];
+        uint32_t n = e3 >> 30, tl = (e3 >> 26) & 15;
         for (;;) {
             const uint32_t rest = ((uint32_t)e << tl) & ((1u << kCntLut) - 1);
             const uint32_t a = s.lut1[rest >> (kCntLut - kLut)];
