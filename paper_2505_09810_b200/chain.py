@@ -32,7 +32,7 @@ from filelock import FileLock
 
 from .errors import (CorruptStreamError, DtypeMismatchError, IntegrityError, LmcError, MissingStreamError,
                      ShapeMismatchError, raise_status)
-from .pipeline import StreamItem, StreamWriter
+from .pipeline import StreamItem, StreamWriter, read_files_to_device
 from .stream import DEFAULT_BLOCK_SIZE, _bytes_view, _torch_et, default_codec, parse_header
 from .types import ElementType, TensorBuffer
 
@@ -273,15 +273,20 @@ class DeviceChain:
         import torch
 
         pre: list[Exception | None] = []
-        streams, headers = [], []
-        for e in entries:
-            err, s, h = None, b"", None
+        headers = []
+        # every stream file of the step read by a thread pool through two
+        # reused pinned slots, overlapped with their host-to-device copies
+        dev_all, hoffs, hlens, heads, herrs = read_files_to_device([self.dir / e.file for e in entries],
+                                                                   self.codec.device)
+        for i, e in enumerate(entries):
+            err, h = None, None
             path = self.dir / e.file
             try:
-                if not path.exists():
-                    raise MissingStreamError(f"stream file {path} is missing")
-                s = path.read_bytes()
-                h = parse_header(s)
+                if herrs[i] is not None:
+                    if not path.exists():
+                        raise MissingStreamError(f"stream file {path} is missing")
+                    raise herrs[i]
+                h = parse_header(heads[i])
                 if h.crc32 != e.crc32:
                     raise IntegrityError(f"stream {e.file} CRC does not match the manifest")
                 if h.delta_applied != (e.role == ROLE_DELTA):
@@ -289,7 +294,6 @@ class DeviceChain:
             except LmcError as exc:
                 err = exc
             pre.append(err)
-            streams.append(s)
             headers.append(h)
         # streams that passed the host checks and decode to their region's size
         # go through one batched decode straight into the resident buffer;
@@ -302,15 +306,14 @@ class DeviceChain:
                  and self._layout[e.shard][1] == e.length else alone).append(i)
         status = {}
         if go:
-            dev = [torch.frombuffer(bytearray(streams[i]), dtype=torch.uint8).to(self.codec.device) for i in go]
+            dev = [dev_all[hoffs[i]: hoffs[i] + hlens[i]] for i in go]
             offs = [self._layout[entries[i].shard][0] for i in go]
             prev = [self._view(entries[i].shard) for i in go] if delta else None
             res = self.codec.decompress(dev, out=self._buf, out_offsets=offs, prev=prev)
             for j, i in enumerate(go):
                 status[i] = (res.status[j], res.element_types[j], res.lengths[j])
         for i in alone:
-            dev = torch.frombuffer(bytearray(streams[i]), dtype=torch.uint8).to(self.codec.device)
-            res = self.codec.decompress([dev])
+            res = self.codec.decompress([dev_all[hoffs[i]: hoffs[i] + hlens[i]]])
             status[i] = (res.status[0], res.element_types[0], res.lengths[0])
         for i, e in enumerate(entries):
             if pre[i] is not None:

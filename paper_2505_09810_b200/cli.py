@@ -325,20 +325,24 @@ def batch_decompress(streams_manifest, out_dir, prev_dir):
     from .errors import raise_status
     from .stream import default_codec, parse_header
 
+    from .pipeline import read_files_to_device
+
     rows = [json.loads(r) for r in Path(streams_manifest).read_text().splitlines() if r.strip()]
     base = Path(streams_manifest).parent
-    streams = []
-    for r in rows:
+    codec = default_codec()
+    # the streams read by a thread pool through reused pinned slots,
+    # overlapped with their host-to-device copies
+    dev_all, offs, lens, heads, errs = read_files_to_device([base / r["file"] for r in rows], codec.device)
+    for i, r in enumerate(rows):
         p = base / r["file"]
-        if not p.exists():
-            raise MissingStreamError(f"stream file {p} is missing")
-        s = p.read_bytes()
-        h = parse_header(s)
+        if errs[i] is not None:
+            if not p.exists():
+                raise MissingStreamError(f"stream file {p} is missing")
+            raise errs[i]
+        h = parse_header(heads[i])
         if h.crc32 != r["crc32"]:
             raise IntegrityError(f"stream {r['file']} CRC does not match the manifest")
-        streams.append(s)
-    codec = default_codec()
-    dev = [_device_bytes(s) for s in streams]
+    dev = [dev_all[o: o + n] for o, n in zip(offs, lens)]
     prev = None
     if prev_dir is not None:
         prev = []

@@ -233,3 +233,95 @@ def write_streams(tensors: Sequence, paths: Sequence, *, prev: Sequence | None =
         os.replace(tmp, paths[i])
 
     return StreamWriter(codec, **kw).run(items_from_tensors(tensors, prev, element_types), sink)
+
+
+_staging: dict = {}
+
+
+def _staging_slots(nslots: int, nbytes: int):
+    """Pinned staging slots, allocated once per process and reused (pinning
+    gigabytes for every restore would cost more than the reads)."""
+    import torch
+
+    key = (nslots, nbytes)
+    if key not in _staging:
+        _staging[key] = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(nslots)]
+    return _staging[key]
+
+
+def read_files_to_device(paths: Sequence, device, *, head: int = 64, slot_bytes: int = 64 << 20,
+                         threads: int = 8):
+    """Whole files into one device buffer (16-byte aligned offsets), read by
+    a thread pool into two reused pinned slots while the other slot's
+    host-to-device copy runs.  Returns ``(device uint8 tensor, offsets,
+    lengths, heads, errors)``: ``heads[i]`` are the first ``head`` bytes of
+    file i (for host-side header checks); an unreadable file has length 0
+    and its ``OSError`` in ``errors``."""
+    import os
+    from pathlib import Path
+
+    import torch
+
+    paths = [Path(p) for p in paths]
+    n = len(paths)
+    lengths, errors, heads = [0] * n, [None] * n, [b""] * n
+    for i, p in enumerate(paths):
+        try:
+            lengths[i] = os.stat(p).st_size
+        except OSError as exc:
+            errors[i] = exc
+    offsets, pos = [], 0
+    for L in lengths:
+        offsets.append(pos)
+        pos += (L + 15) & ~15
+    dev = torch.empty(max(pos, 16), dtype=torch.uint8, device=device)
+    slots = _staging_slots(2, slot_bytes)
+    copy = torch.cuda.Stream(device)
+    done = [None, None]
+
+    def fill(k: int, slot, lo: int, hi: int) -> None:
+        # the parts of every file inside device bytes [lo, hi)
+        mv = memoryview(slot.numpy())
+        jobs = [i for i in range(n) if lengths[i] and errors[i] is None and offsets[i] < hi and offsets[i] + lengths[i] > lo]
+
+        def read(i: int) -> None:
+            a, b = max(offsets[i], lo), min(offsets[i] + lengths[i], hi)
+            try:
+                fd = os.open(paths[i], os.O_RDONLY)
+                try:
+                    if a == offsets[i]:
+                        heads[i] = os.pread(fd, head, 0)
+                    got = 0
+                    while got < b - a:
+                        r = os.preadv(fd, [mv[a - lo + got: b - lo]], a - offsets[i] + got)
+                        if not r:
+                            raise OSError(f"{paths[i]}: file shrank while reading")
+                        got += r
+                finally:
+                    os.close(fd)
+            except OSError as exc:
+                errors[i] = exc
+
+        if threads > 1 and len(jobs) > 1:
+            list(pool.map(read, jobs))
+        else:
+            for i in jobs:
+                read(i)
+
+    with ThreadPoolExecutor(max(1, threads), thread_name_prefix="lmc-read") as pool:
+        for k, lo in enumerate(range(0, pos, slot_bytes)):
+            hi = min(lo + slot_bytes, pos)
+            s = k % 2
+            if done[s] is not None:
+                done[s].synchronize()   # this slot's previous copy has left it
+            fill(k, slots[s], lo, hi)
+            with torch.cuda.stream(copy):
+                dev[lo:hi].copy_(slots[s][: hi - lo], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy)
+            done[s] = ev
+    torch.cuda.current_stream(device).wait_stream(copy)
+    for i in range(n):
+        if errors[i] is not None:
+            lengths[i] = 0
+    return dev, offsets, lengths, heads, errors

@@ -312,3 +312,34 @@ def test_stream_writer_sink_error_propagates(tmp_path):
 
     with pytest.raises(OSError, match="disk full"):
         StreamWriter(group_bytes=200_000).run(items_from_tensors(ts), sink)
+
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("slot", [4096, 64 << 20])
+def test_read_files_to_device(tmp_path, slot):
+    """Files through the two reused pinned slots: sizes across slot edges,
+    empty and missing files, headers for the host-side checks."""
+    import torch
+
+    from paper_2505_09810_b200.pipeline import read_files_to_device
+
+    rng = np.random.default_rng(7)
+    paths, blobs = [], []
+    for i, n in enumerate([0, 1, 15, 16, 17, 4096, 100_003, 0, 333, 9000]):
+        b = rng.integers(0, 256, n, dtype=np.uint8).tobytes()
+        p = tmp_path / f"f{i}.lmc"
+        p.write_bytes(b)
+        paths.append(p)
+        blobs.append(b)
+    paths.insert(3, tmp_path / "missing.lmc")
+    blobs.insert(3, None)
+    dev, offs, lens, heads, errs = read_files_to_device(paths, torch.device("cuda", 0), slot_bytes=slot, threads=4)
+    data = dev.cpu().numpy()
+    for i, b in enumerate(blobs):
+        assert offs[i] % 16 == 0
+        if b is None:
+            assert isinstance(errs[i], FileNotFoundError) and lens[i] == 0
+        else:
+            assert errs[i] is None and lens[i] == len(b) and heads[i] == b[:64]
+            assert data[offs[i]: offs[i] + lens[i]].tobytes() == b
