@@ -30,6 +30,7 @@ struct lmcg_ctx {
     cudaEvent_t pin_done = nullptr;
     cudaStream_t side = nullptr;          // second stream for kernels that overlap the main chain
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaEvent_t dfork_ev = nullptr, djoin_ev = nullptr;   // decompress: large-record k_decrec on the side stream
     // last compress (block_info)
     uint64_t last_nb = 0;
     const BlockMeta* last_meta = nullptr;
@@ -318,6 +319,8 @@ lmcg_ctx* lmcg_create(int device) {
     cudaEventCreateWithFlags(&ctx->pin_done, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->dfork_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->djoin_ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (const char* e = getenv("LMCG_SERIAL")) ctx->serial = e[0] == '1';
     if (const char* e = getenv("LMCG_CRC_FORK")) ctx->crc_fork = atoi(e);
@@ -340,6 +343,8 @@ void lmcg_destroy(lmcg_ctx* ctx) {
         if (ctx->pin_done) cudaEventDestroy(ctx->pin_done);
         if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
         if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
+        if (ctx->dfork_ev) cudaEventDestroy(ctx->dfork_ev);
+        if (ctx->djoin_ev) cudaEventDestroy(ctx->djoin_ev);
         if (ctx->side) cudaStreamDestroy(ctx->side);
     }
     delete ctx;
@@ -925,7 +930,8 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     CK(cudaMemsetAsync(d_st, 0, (n + 1) * sizeof(uint32_t), st));
     CK(cudaMemsetAsync(d_sfail, 0, (nseg + 1) * sizeof(uint32_t), st));
     if (!n) return LMCG_OK;
-    const size_t dsm = sizeof(DecSmem);
+    const size_t dsm = dec_smem_bytes(kStageLarge), dsm_small = dec_smem_bytes(kStageSmall);
+    constexpr uint64_t kDecSplitFrom = 1024;   // record slots: below, one k_decrec launch
     if (!ctx->dec_attr) {
         CK(cudaFuncSetAttribute(k_decrec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         CK(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
@@ -952,7 +958,23 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         { PROF(k_resolve); k_resolve<<<(unsigned)std::min<uint64_t>(nseg, 148 * 2), kThreads, kResSmem, st>>>(
             d_seg, nseg, d_cand, d_ccnt, d_cpre, d_scnt, d_sfail, d_rpos, d_rnext); }
         PROF(k_decrec);
-        k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr);
+        if (nrec < kDecSplitFrom) {
+            k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 2);
+        } else {
+            // the records too large for the small staging area decode on the
+            // side stream (3 CTAs per SM) while the rest run at 4 CTAs per SM
+            cudaStream_t sst = ctx->serial ? st : ctx->side;
+            if (!ctx->serial) {
+                CK(cudaEventRecord(ctx->dfork_ev, st));
+                CK(cudaStreamWaitEvent(sst, ctx->dfork_ev, 0));
+            }
+            k_decrec<<<(unsigned)nrec, kThreads, dsm, sst>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 1);
+            k_decrec<<<(unsigned)nrec, kThreads, dsm_small, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 0);
+            if (!ctx->serial) {
+                CK(cudaEventRecord(ctx->djoin_ev, sst));
+                CK(cudaStreamWaitEvent(st, ctx->djoin_ev, 0));
+            }
+        }
     }
     if (nseg) {
         const int grid = (int)std::min<uint64_t>(nseg, 148 * 2);

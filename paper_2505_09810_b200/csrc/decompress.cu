@@ -228,11 +228,14 @@ __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __res
 // self-synchronise within a few codewords); pass 2 re-decodes every chunk
 // from its exact start and writes the symbols.  The decoder consumes up to
 // three symbols per table lookup.
-constexpr int kStage = 40960;
-constexpr int kCheckpoints = 3;  // at 128, 256 and 512 bits into a chunk  // bitstream bytes staged in shared memory (longer ones are read from global)
+// Bitstream bytes staged in shared memory (longer payloads are read from
+// global memory).  k_decrec runs twice: records whose payload fits
+// kStageSmall at 4 CTAs per SM, then the larger ones with kStageLarge at 3
+// (the staging area is the tail of the dynamic shared memory).
+constexpr int kStageSmall = 30720, kStageLarge = 40960;
+constexpr int kCheckpoints = 3;  // at 128, 256 and 512 bits into a chunk
 
 struct DecSmem {
-    uint32_t bits[kStage / 4 + 4];      // staged bitstream (TMA of the 16-byte aligned cover), big-endian words
     uint32_t lut3[1 << kLut];           // n(2)|tl(4)|pad(2)|s3(8)|s2(8)|s1(8); n == 0: slow path
     uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0
     uint8_t lutc[1 << kCntLut];         // count passes: n(4) | tl(4) of the whole codewords in a 12-bit window
@@ -247,7 +250,11 @@ struct DecSmem {
     uint32_t kraft;
     int minlen, maxlen, lgcd;
     uint64_t mbar;                      // TMA staging of the payload
+    alignas(16) uint32_t bits[4];       // staged bitstream (TMA of the 16-byte aligned cover), big-endian
+                                        // words; extends to the end of the dynamic shared memory
 };
+// dynamic shared memory of k_decrec / k_fallback for a staging capacity
+__host__ __device__ constexpr size_t dec_smem_bytes(uint32_t stage) { return sizeof(DecSmem) + stage + 16; }
 
 // Payload bit source: big-endian words, bit i of the payload is bit
 // 31 - ((i + sh) & 31) of word (i + sh) >> 5; staged in shared memory when
@@ -691,7 +698,15 @@ __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
 // bits) into dst[0, len).  Returns false on any corruption the reference
 // would report (malformed codebook, zero bit count, invalid prefix, wrong end
 // position or symbol count).
-__device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t* dst) {
+__device__ __forceinline__ uint64_t stage_cover(const uint8_t* pl) {   // staged bytes of a Huffman payload
+    const uint32_t bits0 = rd32(pl + 128);
+    const uint8_t* data0 = pl + kHuffOverhead;
+    const uint64_t a16 = reinterpret_cast<uint64_t>(data0) & ~15ull;
+    const uint64_t e16 = (reinterpret_cast<uint64_t>(data0) + ((uint64_t)bits0 + 7) / 8 + 15) & ~15ull;
+    return e16 - a16;
+}
+
+__device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t* dst, uint32_t stage_cap) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     DBG_T0(t_setup);
     __syncthreads();
@@ -701,7 +716,7 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     const uint8_t* data0 = pl + kHuffOverhead;
     const uint64_t a16 = reinterpret_cast<uint64_t>(data0) & ~15ull;
     const uint64_t e16 = (reinterpret_cast<uint64_t>(data0) + ((uint64_t)bits0 + 7) / 8 + 15) & ~15ull;
-    const bool staged = bits0 != 0 && e16 - a16 <= (uint64_t)kStage;
+    const bool staged = bits0 != 0 && e16 - a16 <= (uint64_t)stage_cap;
     if (staged && tid == 0) {
         mbar_init1(&s.mbar);
         tma_load_1d(s.bits, reinterpret_cast<const void*>(a16), (uint32_t)(e16 - a16), &s.mbar);
@@ -877,7 +892,8 @@ __device__ void copy_bytes(uint8_t* dst, const uint8_t* src, uint32_t n) {
 
 // Decode one record (mode u8 | len u32 | payload) at rec into dst.  The caller
 // has validated the header and the payload bounds.  CTA-wide.
-__device__ bool decode_record(DecSmem& s, const uint8_t* rec, uint32_t mode, uint32_t len, uint8_t* dst) {
+__device__ bool decode_record(DecSmem& s, const uint8_t* rec, uint32_t mode, uint32_t len, uint8_t* dst,
+                              uint32_t stage_cap) {
     const uint8_t* pl = rec + 5;
     if (mode == MODE_RLE) {
         const uint32_t v = pl[0] * 0x01010101u;
@@ -890,7 +906,7 @@ __device__ bool decode_record(DecSmem& s, const uint8_t* rec, uint32_t mode, uin
         copy_bytes(dst, pl, len);
         return true;
     }
-    return huff_decode(s, pl, len, dst);
+    return huff_decode(s, pl, len, dst, stage_cap);
 }
 
 // payload size of the record at pos (stream.py:258-268); false when the
@@ -1238,9 +1254,13 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
 // copy or CTA-wide Huffman decode into the grouped scratch.  A failure marks
 // the segment for k_fallback, which re-walks it serially and reports the
 // reference's error.
-__global__ void __launch_bounds__(kThreads, 3) k_decrec(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
+// cls 0: every record whose Huffman payload (if any) stages in kStageSmall;
+// cls 1: the larger Huffman records (kStageLarge, or read from global memory);
+// cls 2: every record (kStageLarge: one launch for small inputs).
+__global__ void __launch_bounds__(kThreads, 4) k_decrec(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
                                                    uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
-                                                   const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch) {
+                                                   const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch,
+                                                   int cls) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
     const uint64_t g = blockIdx.x;
@@ -1251,7 +1271,12 @@ __global__ void __launch_bounds__(kThreads, 3) k_decrec(const DecSeg* __restrict
     const uint32_t r = (uint32_t)(g - sg.rec0);
     const uint8_t* rec = sg.base + rec_pos[g];
     const uint32_t mode = rec[0], len = rd32(rec + 1);
-    const bool ok = decode_record(s, rec, mode, len, scratch + sg.goff + (uint64_t)r * sg.block);
+    if (cls != 2) {
+        const bool large = mode == MODE_HUFFMAN && stage_cover(rec + 5) > (uint64_t)kStageSmall;
+        if (large != (cls == 1)) return;
+    }
+    const bool ok = decode_record(s, rec, mode, len, scratch + sg.goff + (uint64_t)r * sg.block,
+                                  cls ? kStageLarge : kStageSmall);
     if (!ok && threadIdx.x == 0) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(16, 1); }
 }
 
@@ -1473,7 +1498,7 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
             const uint32_t okv = sh_ok;
             if (okv == 2) break;
             if (okv == 0) { corrupt = true; break; }
-            if (!decode_record(s, sg.base + sh_pos, sh_mode, sh_len, scratch + sg.goff + sh_got)) { corrupt = true; break; }
+            if (!decode_record(s, sg.base + sh_pos, sh_mode, sh_len, scratch + sg.goff + sh_got, kStageLarge)) { corrupt = true; break; }
             __syncthreads();
             if (threadIdx.x == 0) { sh_pos += 5 + sh_ps; sh_got += sh_len; }
             __syncthreads();
