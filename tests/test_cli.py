@@ -343,3 +343,31 @@ def test_read_files_to_device(tmp_path, slot):
         else:
             assert errs[i] is None and lens[i] == len(b) and heads[i] == b[:64]
             assert data[offs[i]: offs[i] + lens[i]].tobytes() == b
+
+
+@pytest.mark.gpu
+def test_batch_delta_and_prev_dir(runner, tmp_path):
+    """batch compress --delta (XOR against the previous step's manifest) and
+    batch decompress --prev-dir (decode fused with xor_apply) restore step 1."""
+    steps = _trajectory(50_000, 2, seed=9)
+    for i, s in enumerate(steps):
+        (tmp_path / f"a{i}.bin").write_bytes(s)
+        (tmp_path / f"b{i}.bin").write_bytes(s[::-1])
+        (tmp_path / f"m{i}.jsonl").write_text(
+            json.dumps({"name": "a", "dtype": "bf16", "path": f"a{i}.bin"}) + "\n"
+            + json.dumps({"name": "b", "dtype": "bf16", "path": f"b{i}.bin"}) + "\n")
+    out = tmp_path / "d"
+    r = _run(runner, ["batch", "compress", str(tmp_path / "m1.jsonl"), str(out), "--delta", str(tmp_path / "m0.jsonl")])
+    assert r.exit_code == 0, r.output
+    rows = {x["name"]: x for x in map(json.loads, (out / "streams.jsonl").read_text().splitlines())}
+    for name, s0, s1 in (("a", steps[0], steps[1]), ("b", steps[0][::-1], steps[1][::-1])):
+        x = (np.frombuffer(s0, np.uint8) ^ np.frombuffer(s1, np.uint8)).tobytes()
+        assert rows[name]["delta"] and (out / rows[name]["file"]).read_bytes() == oracle.compress(x, 1, delta=True)
+    prev = tmp_path / "prev"
+    prev.mkdir()
+    (prev / "a").write_bytes(steps[0])
+    (prev / "b").write_bytes(steps[0][::-1])
+    back = tmp_path / "back"
+    r = _run(runner, ["batch", "decompress", str(out / "streams.jsonl"), str(back), "--prev-dir", str(prev)])
+    assert r.exit_code == 0, r.output
+    assert (back / "a").read_bytes() == steps[1] and (back / "b").read_bytes() == steps[1][::-1]
