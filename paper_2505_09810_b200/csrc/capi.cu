@@ -31,6 +31,7 @@ struct lmcg_ctx {
     cudaStream_t side = nullptr;          // second stream for kernels that overlap the main chain
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t dfork_ev = nullptr, djoin_ev = nullptr;   // decompress: large-record k_decrec on the side stream
+    int sms = 148;                        // multiprocessors of the device
     // last compress (block_info)
     uint64_t last_nb = 0;
     const BlockMeta* last_meta = nullptr;
@@ -320,6 +321,7 @@ lmcg_ctx* lmcg_create(int device) {
     cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->join_ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ctx->dfork_ev, cudaEventDisableTiming);
+    cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device);
     cudaEventCreateWithFlags(&ctx->djoin_ev, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (const char* e = getenv("LMCG_SERIAL")) ctx->serial = e[0] == '1';
@@ -876,7 +878,7 @@ int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
 
 namespace {
 // Workspace layout of one decompress (offsets into the workspace).
-enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CAND, D_CCNT, D_CTOT, D_CPRE, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_TC, D_MAPS, D_SCR, D_NOFF };
+enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CAND, D_CCNT, D_CTOT, D_CPRE, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_LARGE, D_TC, D_MAPS, D_SCR, D_NOFF };
 size_t dec_layout(const DPlan& P, int n, size_t* o) {
     Arena a;
     o[D_IN] = a.take<DecStreamIn>(n + 1);
@@ -893,6 +895,7 @@ size_t dec_layout(const DPlan& P, int n, size_t* o) {
     o[D_SFAIL] = a.take<uint32_t>(P.nseg + 1);
     o[D_RPOS] = a.take<uint64_t>(P.nrec + 1);
     o[D_RNEXT] = a.take<uint64_t>(P.nrec + 1);
+    o[D_LARGE] = a.take<uint32_t>(P.nrec + 2);   // k_classify: count | record slots
     o[D_TC] = a.take<uint32_t>(P.ntile + 1);
     o[D_MAPS] = a.take<uint32_t>(P.nchunk + P.nrec + P.ntile + 3);   // chunk2seg | rec2seg | tile2win
     o[D_SCR] = a.take<uint8_t>(P.scratch + 64);
@@ -919,6 +922,7 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     auto* d_sfail = reinterpret_cast<uint32_t*>(ws + o[D_SFAIL]);
     auto* d_rpos = reinterpret_cast<uint64_t*>(ws + o[D_RPOS]);
     auto* d_rnext = reinterpret_cast<uint64_t*>(ws + o[D_RNEXT]);
+    auto* d_large = reinterpret_cast<uint32_t*>(ws + o[D_LARGE]);
     auto* d_tc = reinterpret_cast<uint32_t*>(ws + o[D_TC]);
     auto* d_c2s = reinterpret_cast<uint32_t*>(ws + o[D_MAPS]);
     uint32_t* d_r2s = d_c2s + nchunk + 1;
@@ -934,6 +938,7 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     constexpr uint64_t kDecSplitFrom = 1024;   // record slots: below, one k_decrec launch
     if (!ctx->dec_attr) {
         CK(cudaFuncSetAttribute(k_decrec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        CK(cudaFuncSetAttribute(k_decrec_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         CK(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         ctx->dec_attr = true;
     }
@@ -958,18 +963,26 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         { PROF(k_resolve); k_resolve<<<(unsigned)std::min<uint64_t>(nseg, 148 * 2), kThreads, kResSmem, st>>>(
             d_seg, nseg, d_cand, d_ccnt, d_cpre, d_scnt, d_sfail, d_rpos, d_rnext); }
         PROF(k_decrec);
-        if (nrec < kDecSplitFrom) {
-            k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 2);
+        // the split pays off inside CUDA graphs (plans); launched eagerly the
+        // two kernels overlap worse than one, so eager calls take one launch
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        CK(cudaStreamIsCapturing(st, &cap));
+        if (nrec < kDecSplitFrom || cap != cudaStreamCaptureStatusActive) {
+            k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 0);
         } else {
-            // the records too large for the small staging area decode on the
-            // side stream (3 CTAs per SM) while the rest run at 4 CTAs per SM
+            // records whose payload does not stage in kStageSmall are listed and
+            // decoded by persistent CTAs (3 per SM) on the side stream while the
+            // rest run at 4 CTAs per SM
+            CK(cudaMemsetAsync(d_large, 0, sizeof(uint32_t), st));
+            k_classify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_large + 1, d_large);
             cudaStream_t sst = ctx->serial ? st : ctx->side;
             if (!ctx->serial) {
                 CK(cudaEventRecord(ctx->dfork_ev, st));
                 CK(cudaStreamWaitEvent(sst, ctx->dfork_ev, 0));
             }
-            k_decrec<<<(unsigned)nrec, kThreads, dsm, sst>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 1);
-            k_decrec<<<(unsigned)nrec, kThreads, dsm_small, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 0);
+            k_decrec_large<<<(unsigned)std::min<uint64_t>(nrec, (uint64_t)ctx->sms * 3), kThreads, dsm, sst>>>(
+                d_seg, d_r2s, d_large + 1, d_large, d_sfail, d_rpos, d_scr);
+            k_decrec<<<(unsigned)nrec, kThreads, dsm_small, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 1);
             if (!ctx->serial) {
                 CK(cudaEventRecord(ctx->djoin_ev, sst));
                 CK(cudaStreamWaitEvent(st, ctx->djoin_ev, 0));

@@ -1254,30 +1254,68 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
 // copy or CTA-wide Huffman decode into the grouped scratch.  A failure marks
 // the segment for k_fallback, which re-walks it serially and reports the
 // reference's error.
-// cls 0: every record whose Huffman payload (if any) stages in kStageSmall;
-// cls 1: the larger Huffman records (kStageLarge, or read from global memory);
-// cls 2: every record (kStageLarge: one launch for small inputs).
-__global__ void __launch_bounds__(kThreads, 4) k_decrec(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
-                                                   uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
-                                                   const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch,
-                                                   int cls) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
-    const uint64_t g = blockIdx.x;
-    if (g >= nrec_total) return;
+__device__ __forceinline__ bool is_large(const uint8_t* rec) {
+    return rec[0] == MODE_HUFFMAN && stage_cover(rec + 5) > (uint64_t)kStageSmall;
+}
+
+// Decode record slot g into grouped scratch (CTA-wide).
+__device__ __forceinline__ void decrec_one(DecSmem& s, const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
+                                           uint64_t g, uint32_t* __restrict__ seg_fail, const uint64_t* __restrict__ rec_pos,
+                                           uint8_t* __restrict__ scratch, bool skip_large, uint32_t stage_cap) {
     const uint32_t lo = rec2seg[g];
     if (lo == ~0u || seg_fail[lo]) return;
     const DecSeg sg = segs[lo];
     const uint32_t r = (uint32_t)(g - sg.rec0);
     const uint8_t* rec = sg.base + rec_pos[g];
+    if (skip_large && is_large(rec)) return;   // (k_decrec_large has it)
     const uint32_t mode = rec[0], len = rd32(rec + 1);
-    if (cls != 2) {
-        const bool large = mode == MODE_HUFFMAN && stage_cover(rec + 5) > (uint64_t)kStageSmall;
-        if (large != (cls == 1)) return;
-    }
-    const bool ok = decode_record(s, rec, mode, len, scratch + sg.goff + (uint64_t)r * sg.block,
-                                  cls ? kStageLarge : kStageSmall);
+    const bool ok = decode_record(s, rec, mode, len, scratch + sg.goff + (uint64_t)r * sg.block, stage_cap);
     if (!ok && threadIdx.x == 0) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(16, 1); }
+}
+
+// CTA per record slot.  split: records listed by k_classify (Huffman payloads
+// that do not stage in kStageSmall) are left to k_decrec_large, and this
+// launch runs at 4 CTAs per SM with kStageSmall; otherwise (few records) it
+// decodes everything with kStageLarge.
+__global__ void __launch_bounds__(kThreads, 4) k_decrec(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
+                                                   uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
+                                                   const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch,
+                                                   int split) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
+    const uint64_t g = blockIdx.x;
+    if (g >= nrec_total) return;
+    decrec_one(s, segs, rec2seg, g, seg_fail, rec_pos, scratch, split != 0, split ? kStageSmall : kStageLarge);
+}
+
+// The large records (k_classify's list), persistent CTAs with kStageLarge;
+// runs on the side stream next to k_decrec.
+__global__ void __launch_bounds__(kThreads, 3) k_decrec_large(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
+                                                         const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
+                                                         uint32_t* __restrict__ seg_fail, const uint64_t* __restrict__ rec_pos,
+                                                         uint8_t* __restrict__ scratch) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
+    const uint32_t n = *count;
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        decrec_one(s, segs, rec2seg, list[i], seg_fail, rec_pos, scratch, false, kStageLarge);
+        __syncthreads();
+    }
+}
+
+// Thread per record slot (after discovery): list the records for
+// k_decrec_large.
+__global__ void k_classify(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg, uint64_t nrec_total,
+                           const uint32_t* __restrict__ seg_fail, const uint64_t* __restrict__ rec_pos,
+                           uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (g >= nrec_total) return;
+    const uint32_t lo = rec2seg[g];
+    if (lo == ~0u || seg_fail[lo]) return;
+    const DecSeg sg = segs[lo];
+    const uint64_t pos = rec_pos[g];
+    if (pos + 5 + kHuffOverhead > sg.comp) return;
+    if (is_large(sg.base + pos)) list[atomicAdd(count, 1u)] = (uint32_t)g;
 }
 
 // --------------------------------------------------------------- k_verify

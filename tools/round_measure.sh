@@ -6,6 +6,7 @@ set -u
 O=gpurun_out/final
 mkdir -p $O/configs
 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $O/rc.log
+python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > $O/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $O/rc.log
 timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" | tee -a $O/rc.log
 timeout 900 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?" | tee -a $O/rc.log
 for c in cfg1 cfg2 cfg3 cfg4 cfg5; do
