@@ -735,28 +735,38 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     for (int o = 16; o; o >>= 1) ku += __shfl_xor_sync(0xFFFFFFFFu, ku, o);
     if (lane == 0) atomicAdd(&s.kraft, ku);
     __syncthreads();
-    if (tid == 0) {
-        uint32_t left = 0, idx = 0;
-        int mn = 16, mx = 0, gl = 0;
-        for (int q = 1; q <= kMaxLen; q++) {
-            uint32_t c = 0;
-            for (int w = 0; w < kWarps; w++) c += s.cnt_w[w][q];
-            s.bl_count[q] = c;
-            s.first_left[q] = left;
-            s.first_idx[q] = idx;
-            left += c << (kMaxLen - q);
-            idx += c;
-            if (c) {
-                mn = min(mn, q);
-                mx = max(mx, q);
-                int a = gl, b = q;  // gcd of the code lengths in use
+    if (warp == 0) {
+        // lane q = code length q (1..15): its count, then exclusive scans of
+        // the Kraft units (first_left) and of the counts (first_idx)
+        const bool isq = lane >= 1 && lane <= kMaxLen;
+        uint32_t c = 0;
+        if (isq)
+#pragma unroll
+            for (int w = 0; w < kWarps; w++) c += s.cnt_w[w][lane];
+        const uint32_t lf = isq ? c << (kMaxLen - lane) : 0u;
+        uint32_t il = lf, ii = c;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const uint32_t yl = __shfl_up_sync(0xFFFFFFFFu, il, o), yi = __shfl_up_sync(0xFFFFFFFFu, ii, o);
+            if (lane >= o) { il += yl; ii += yi; }
+        }
+        if (isq) {
+            s.bl_count[lane] = c;
+            s.first_left[lane] = il - lf;
+            s.first_idx[lane] = ii - c;
+        }
+        const uint32_t used = __ballot_sync(0xFFFFFFFFu, c != 0);   // bit q: length q in use
+        if (lane == 0) {
+            int gl = 0;   // gcd of the code lengths in use
+            for (uint32_t u = used; u; u &= u - 1) {
+                int a = gl, b = __ffs(u) - 1;
                 while (b) { const int t = a % b; a = b; b = t; }
                 gl = a;
             }
+            s.minlen = used ? __ffs(used) - 1 : 16;
+            s.maxlen = used ? 31 - __clz(used) : 0;
+            s.lgcd = gl ? gl : 1;
         }
-        s.minlen = mn;
-        s.maxlen = mx;
-        s.lgcd = gl ? gl : 1;
     }
     __syncthreads();
     const uint32_t bits = rd32(pl + 128);
