@@ -372,3 +372,64 @@ def test_mode_decision_boundary(codec, rng, block):
     assert len(set(modes.tolist())) >= 2   # both sides of the boundary are present
     r = codec.decompress(b)
     assert r.status == [0] and host_bytes(r.payload(0)) == data
+
+
+def _length_set_block(kind: str, block: int, rng) -> np.ndarray:
+    """One block whose optimal code has a chosen set of lengths."""
+    if kind.startswith("uniform"):          # k symbols, all of length log2(k)
+        k = int(kind[7:])
+        counts = {s: block // k for s in range(k)}
+    elif kind == "len3_len6":                # lengths {3, 6}: gcd 3
+        counts = {s: block * 7 // 56 for s in range(7)}
+        counts.update({40 + s: block // 64 for s in range(8)})
+    elif kind == "geometric":                # lengths 1, 2, 3, ... (run path + codes > 11 bits)
+        counts, left, c, s = {}, block, block // 2, 200
+        while c >= 1 and left > c:
+            counts[s] = c
+            left -= c
+            c //= 2
+            s -= 7
+        counts[s] = left
+    elif kind == "fibonacci":                # deeper than 15: package-merge
+        a, b, counts, s = 1, 1, {}, 3
+        while sum(counts.values()) + a <= block * 3 // 4:
+            counts[s] = a
+            a, b, s = b, a + b, s + 11
+        counts[255] = block - sum(counts.values())
+    else:
+        raise ValueError(kind)
+    x = np.concatenate([np.full(c, sym, np.uint8) for sym, c in counts.items()])
+    assert len(x) == block
+    return rng.permutation(x)
+
+
+@pytest.mark.parametrize("block,kinds", [
+    (4096, ["uniform2", "uniform4", "uniform8", "uniform16", "uniform64", "uniform128", "len3_len6", "geometric"]),
+    (65536, ["uniform4", "len3_len6", "geometric", "fibonacci"]),
+])
+def test_code_length_sets(codec, block, kinds):
+    """Huffman blocks with one code length (gcd = that length), two lengths
+    with gcd 3, lengths 1..15 (run path plus codes longer than the 11-bit
+    table) and package-merge-limited Fibonacci counts: the decoder's per-record
+    length counts, canonical offsets, min / max length and gcd (one warp,
+    shuffle scans) and the encoder, against the oracle byte for byte."""
+    rng = np.random.default_rng(block + len(kinds))
+    data = np.concatenate([_length_set_block(k, block, rng) for k in kinds]).tobytes()
+    modes, _, _, lengths, pm = O.analyze_blocks(data, block)
+    assert (modes == 0).all(), modes   # every block is a Huffman record (MODE_HUFFMAN)
+    want = {"len3_len6": [3, 6], "geometric": list(range(1, 13)) if block == 4096 else None}
+    for k, l in zip(kinds, lengths):
+        got = sorted(set(l[l > 0].tolist()))
+        if k.startswith("uniform"):
+            assert got == [int(k[7:]).bit_length() - 1]
+        elif want.get(k):
+            assert got == want[k]
+        else:   # 64 KiB geometric / fibonacci: limited to 15 bits
+            assert got[0] <= 2 and got[-1] == 15
+    ref = O.compress(data, 0, block_size=block)
+    b = codec.compress([dev_bytes(data)], element_types=[0], block_size=block)
+    assert b.to_bytes()[0] == ref
+    fallback_segments(codec)
+    for r in (codec.decompress(b), codec.decompress([dev_bytes(ref)])):
+        assert r.status == [0] and host_bytes(r.payload(0)) == data
+    assert fallback_segments(codec) == 0
