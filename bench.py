@@ -1,15 +1,20 @@
 #!/usr/bin/env python
-"""LMC hot-path benchmark (BASELINE.json metric on configs[1], GPT-2-small).
+"""LMC hot-path benchmark: BASELINE.json's metric on its largest single-GPU
+config, cfg5 (Llama-7B-shaped bf16 checkpoint, 291 tensors, 12.55 GiB).
 
-One step = compress every tensor of a synthetic GPT-2-small bf16 checkpoint
-(148 tensors, 237 MiB) into LMC1 streams and decompress them again, on each
-rank's GPU.  ``value`` is whole-job GiB/s of uncompressed checkpoint bytes
-through compress + decompress (inputs resident in HBM, streams kept in HBM);
-``e2e`` is the same round trip through the public API with pinned host
-buffers (host->device copy of the checkpoint, device->host copy of the
-streams, and back).  See DESIGN.md "Measurement".
+One step = compress every tensor of the checkpoint into its own LMC1 stream
+and decompress the streams again.  ``value`` is whole-job GiB/s of
+uncompressed checkpoint bytes through compress + decompress (inputs resident
+in HBM, streams kept in HBM); ``e2e`` is the same round trip through the
+public plan API with pinned host buffers (host->device copy of the
+checkpoint, device->host copy of the streams, and back); ``delta_step`` is
+cfg5's second step in delta mode (step t+1 compressed against the resident
+step t, fused XOR).  With N GPUs (torchrun) the ONE checkpoint is sharded
+across the ranks (whole tensors, largest first; each rank holds only its
+own tensors) and the only exchange is the all-gather of the per-stream
+compressed lengths: strong scaling.  See DESIGN.md "Measurement".
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg5]
 """
 from __future__ import annotations
 
@@ -31,10 +36,11 @@ METRIC = "lmc compress+decompress round-trip throughput (uncompressed checkpoint
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
+    ap.add_argument("--no-delta", action="store_true", help="skip the delta-mode second step (cfg5)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch kernels directly instead of replaying CUDA graphs")
@@ -137,10 +143,11 @@ def dist_setup(args):
 
 # --------------------------------------------------------- reference arm
 def run_reference(args, ws, rank):
-    """Time the reference's algorithm on the host cores (C oracle port)."""
+    """Time the reference's algorithm on the host cores (C oracle port, all
+    threads) on a bounded sample of the same workload."""
     if rank != 0:
         return
-    import numpy as np
+    import torch
 
     from oracle import oracle as O
     from paper_2505_09810_b200 import synth
@@ -148,24 +155,30 @@ def run_reference(args, ws, rank):
     cores = os.cpu_count() or 1
     specs = synth.CONFIGS[args.config]()
     delta = args.config in DELTA
-    raws = _host_checkpoint(specs, seed=1000, delta=delta)
-    nbytes = sum(len(r) for r in raws)
-    # bounded sample: whole checkpoint when it fits ~60 s of total work
-    t0 = time.perf_counter()
-    s = [O.compress(r, 1, delta=delta, threads=cores) for r in raws[:8]]
-    [O.decompress(x, threads=cores) for x in s]
-    probe = time.perf_counter() - t0
-    probe_bytes = sum(len(r) for r in raws[:8])
-    est_step = probe / max(probe_bytes, 1) * nbytes
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+
+    def host_bytes(i):
+        t = synth.make_tensor(specs[i], 1000, i, device=dev)
+        x = t.view(torch.uint8).reshape(-1)
+        if delta:
+            x = x ^ synth.next_step(t, 1000, i).view(torch.uint8).reshape(-1)
+        return x.cpu().numpy().tobytes()
+
+    # bounded sample: tensors in checkpoint order until ~60 s of total work
+    # (warm-up + timed steps), estimated from a probe of the first tensors
     budget = 60.0 / max(args.steps + args.warmup, 1)
-    if est_step > budget:
-        keep, acc = [], 0
-        for r in raws:
-            keep.append(r)
-            acc += len(r)
-            if probe / max(probe_bytes, 1) * acc > budget:
-                break
-        raws = keep
+    raws, acc, t_probe, b_probe = [], 0, 0.0, 0
+    for i in range(len(specs)):
+        r = host_bytes(i)
+        raws.append(r)
+        acc += len(r)
+        if b_probe < (32 << 20):
+            t0 = time.perf_counter()
+            O.decompress(O.compress(r, 1, delta=delta, threads=cores), threads=cores)
+            t_probe += time.perf_counter() - t0
+            b_probe += len(r)
+        if t_probe / max(b_probe, 1) * acc > budget:
+            break
     sample_bytes = sum(len(r) for r in raws)
     sample = (f"{args.config} synthetic bf16 checkpoint: {len(raws)} of {len(specs)} tensors, "
               f"{sample_bytes / 2**20:.1f} MiB per step (compress + decompress, oracle C port, {cores} threads)")
@@ -187,7 +200,7 @@ def run_reference(args, ws, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GiB/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
         "config": {"workload": workload(args.config), "sample_tensors": len(raws)},
         "compression_ratio": round(ratio, 6),
         "cpu_baseline": {"value": round(value, 4), "unit": "GiB/s", "cores": cores, "kind": "port", "sample": sample},
@@ -196,27 +209,9 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
-def _host_checkpoint(specs, seed, delta=False):
-    """Host bytes of the synthetic checkpoint (generated with torch, CPU or GPU);
-    with delta, the XOR of step t+1 and step t (what a DeltaBuffer holds)."""
-    import torch
-
-    from paper_2505_09810_b200 import synth
-
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    out = []
-    for i, s in enumerate(specs):
-        t = synth.make_tensor(s, seed, i, device=dev)
-        x = t.view(torch.uint8).reshape(-1)
-        if delta:
-            x = x ^ synth.next_step(t, seed, i).view(torch.uint8).reshape(-1)
-        out.append(x.cpu().numpy().tobytes())
-        del t, x
-    return out
-
-
-# Workload names of BASELINE.json's configs (bench default: cfg2, the one the
-# metric is quoted on; the others are parity cases and optional bench runs).
+# Workload names of BASELINE.json's configs.  The bench line is cfg5, the
+# largest config that fits one GPU (BASELINE's metric names no config); the
+# others are parity cases and optional bench runs (--config).
 WORKLOAD = {
     "cfg1": "single bf16 tensor 4096x4096 ~ N(0, 0.02) (32 MiB)",
     "cfg2": "GPT-2-small bf16 checkpoint (148 tensors, 237.4 MiB)",
@@ -226,71 +221,93 @@ WORKLOAD = {
     "cfg5": "Llama-7B bf16 checkpoint (291 tensors, 12.55 GiB)",
 }
 DELTA = {"cfg4"}
+SEED = 1000
 L2_FLUSH_BELOW = 126_000_000   # bytes: the L2 size (inputs must be larger, or flushed)
 
 
-def workload(cfg: str, nbytes: float | None = None) -> str:
+def workload(cfg: str) -> str:
     return (f"{cfg}: {WORKLOAD[cfg]}, every tensor its own LMC1 stream, byte_group=True, block_size=65536, "
             "segment_count=1, buffer_size=128MiB")
 
 
 # ----------------------------------------------------------------- ours
-# Algorithmic bytes per launch as multiples of (N_in, N_stream); one launch per
-# batch.  k_hist_crc reads the checkpoint; k_encode reads it again and writes
-# the streams; k_cand scans the streams; k_decrec reads them again and writes the grouped planes;
-# k_ungroup reads the planes and writes the payload ("Kernels").
-ALGO = {
-    "k_hist_crc": (1, 0), "k_encode": (1, 1), "k_decrec": (1, 1), "k_cand": (0, 1), "k_ungroup": (2, 0),
-}
+# Algorithmic bytes per launch: what the kernel must move in
+# this pipeline, from the input bytes N_in (x2 with the fused delta: the
+# previous step is read too) and the stream bytes N_stream.
+COMPRESS_KERNELS = ("k_slotmap", "k_crc", "k_hist", "k_codebook", "k_pkgmerge", "k_scan", "k_layout", "k_frame",
+                    "k_encode", "k_recsizes", "k_crc_join")
 
 
-def run_ours(args, ws, rank, local):
+def is_compress_kernel(name: str) -> bool:
+    return any(name == k or name.startswith(k + "<") or name.startswith(k + "_") for k in COMPRESS_KERNELS)
+
+
+def algo_bytes(kernel: str, n_in: int, n_stream: int, delta: bool):
+    rd = n_in * (2 if delta else 1)
+    base = kernel.split("<")[0]
+    return {
+        "k_hist": rd, "k_hist_crc": rd, "k_crc": rd,       # read the input (and prev)
+        "k_encode": rd + n_stream,                          # read the input, write the streams
+        "k_cand": n_stream,                                 # scan the streams
+        "k_decrec": n_stream + n_in,                        # read the streams, write the planes
+        "k_decpair": n_stream + n_in,                       # read the streams, write the payload
+        "k_ungroup": 2 * n_in,                              # read the planes, write the payload
+    }.get(base)
+
+
+def roofline_of(prof: dict, nprof: int, n_in: int, n_stream: int, delta: bool, peak: float, peak_src: str,
+                config: str, kernels=None):
+    """Roofline object of the dominant kernel (by time) among `kernels`."""
+    cand = [(k, v) for k, v in prof.items() if algo_bytes(k, n_in, n_stream, delta) is not None
+            and (kernels is None or kernels(k))]
+    if not cand:
+        return None
+    dname, (dcnt, dms) = max(cand, key=lambda kv: kv[1][1])
+    avg_ms = dms / dcnt
+    ab = algo_bytes(dname, n_in, n_stream, delta)
+    achieved = ab / (avg_ms / 1e3) / 1e9
+    tot = sum(v[1] for k, v in prof.items() if kernels is None or kernels(k))
+    return {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, config), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": ab, "avg_launch_ms": round(avg_ms, 4),
+            "share_of_step": round(dms / max(tot, 1e-9), 4)}
+
+
+def exchange_lengths(batch, owned, n_total, dist):
+    """Container assembly across ranks: all-gather of every stream's compressed
+    length (device tensors, NCCL); nothing else crosses GPUs."""
+    from paper_2505_09810_b200 import shard
+
+    if dist is None:
+        return None
+    return shard.gather_device_lengths(batch.lengths, owned, n_total)
+
+
+def measure(codec, ts, prev, args, ws, dist, owned, n_total, local, with_clocks=True):
+    """Device-timed round trips (compress + length exchange + decompress) of
+    one rank's tensors; returns the timings (max over ranks) and the per-kernel
+    launch times of an untimed profiling pass."""
     import torch
 
-    import paper_2505_09810_b200 as lmcb
-    from paper_2505_09810_b200 import synth
-
-    torch.cuda.set_device(local)
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    specs, ts = synth.make_checkpoint(args.config, seed=1000 + rank, device="cuda")
-    prev = None
-    if args.config in DELTA:   # compress step t+1 against step t (fused XOR)
-        prev = ts
-        ts = [synth.next_step(w, 1000 + rank, i) for i, w in enumerate(prev)]
-    nbytes = sum(t.numel() * t.element_size() for t in ts)
-    codec = lmcb.Codec(local)
     stream = torch.cuda.current_stream()
-    # The checkpoint's tensors are registered once (CompressPlan): every step
-    # re-compresses their current contents.  Runs replay captured CUDA graphs.
+    nbytes = sum(t.numel() * t.element_size() for t in ts)
+    # the tensors are registered once (CompressPlan): every step re-compresses
+    # their current contents; runs replay captured CUDA graphs
     cplan = codec.compress_plan(ts, prev=prev, graph=not args.no_graph)
     dplan = cplan.decompress_plan(graph=not args.no_graph)
-    status_log = torch.zeros((args.steps + args.warmup + 8, len(ts)), dtype=torch.int32, device="cuda")
-
-    def exchange(batch):
-        # container assembly across ranks: all-gather of per-stream sizes
-        if dist is None:
-            return None
-        lens = batch.lengths
-        g = [torch.empty_like(lens) for _ in range(ws)]
-        dist.all_gather(g, lens)
-        return torch.stack(g)
-
+    status_log = torch.zeros((args.steps + args.warmup + 8, max(len(ts), 1)), dtype=torch.int32, device="cuda")
     step_no = [0]
 
     def step(ev=None):
         if ev:
             ev[0].record(stream)
         b = cplan.run()
-        exchange(b)
+        exchange_lengths(b, owned, n_total, dist)
         if ev:
             ev[1].record(stream)
         r = dplan.run(b)
-        # keep every step's decode status on the device; verified after the timed region
-        status_log[step_no[0] % status_log.shape[0]].copy_(r._status_dev)
+        # every step's decode status stays on the device; verified after the timed region
+        status_log[step_no[0] % status_log.shape[0], : len(ts)].copy_(r._status_dev)
         step_no[0] += 1
         if ev:
             ev[2].record(stream)
@@ -304,9 +321,8 @@ def run_ours(args, ws, rank, local):
         if prev is not None:
             want = want ^ prev[i].view(torch.uint8).reshape(-1)
         if not torch.equal(r.payload(i), want):
-            raise SystemExit(f"round trip mismatch on {specs[i].name}")
+            raise SystemExit(f"round trip mismatch on tensor {owned[i]}")
     stream_bytes = b.total_bytes()
-    ratio = stream_bytes / nbytes
     for _ in range(max(args.warmup - 1, 0)):
         step()
 
@@ -318,26 +334,29 @@ def run_ours(args, ws, rank, local):
         # per-kernel events never include host launch gaps
         torch.cuda._sleep(4_000_000)
         pb = codec.compress(ts, prev=prev)
-        exchange(pb)
         pb.host_layout()          # (synchronises: the decode below needs the layout)
         torch.cuda._sleep(4_000_000)
         codec.decompress(pb)
     prof = codec.ctx.profile_report()
     codec.ctx.profile(False)
+    del pb
     launches_per_step = sum(c for c, _ in prof.values()) / nprof
 
     # timed region
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    flush = None
+    if nbytes * ws < L2_FLUSH_BELOW:
+        # inputs smaller than the 126 MB L2: flush it between timed steps (a
+        # 512 MB write outside the per-step events) and time the steps alone
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler = ClockSampler(local) if with_clocks else None
+    if sampler:
+        sampler.start()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    # inputs smaller than the 126 MB L2: flush it between timed steps
-    # (a 512 MB write outside the per-step events) and time the steps alone
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if nbytes < L2_FLUSH_BELOW else None
     start.record(stream)
     for k in range(args.steps):
         if flush is not None:
@@ -345,7 +364,7 @@ def run_ours(args, ws, rank, local):
         step(evs[k])
     end.record(stream)
     torch.cuda.synchronize()
-    clocks = sampler.stop()
+    clocks = sampler.stop() if sampler else None
     if int(status_log.abs().sum().item()) != 0:
         raise SystemExit("a timed step reported a decode error")
     if dist is not None:
@@ -355,70 +374,128 @@ def run_ours(args, ws, rank, local):
     dec_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
     if flush is not None:
         total_ms = sum(e[0].elapsed_time(e[2]) for e in evs)
-    t = torch.tensor([total_ms, comp_ms, dec_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms, comp_ms, dec_ms, float(stream_bytes)], dtype=torch.float64, device="cuda")
     if dist is not None:
+        sb = t[3:].clone()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, comp_ms, dec_ms = t.tolist()
-    value = ws * nbytes * args.steps / (total_ms / 1e3) / GIB
+        dist.all_reduce(sb, op=dist.ReduceOp.SUM)
+        t[3] = sb[0]
+    total_ms, comp_ms, dec_ms, all_stream = t.tolist()
+    del cplan, dplan, b, r
+    return {"total_ms": total_ms, "comp_ms": comp_ms, "dec_ms": dec_ms, "stream_bytes": int(stream_bytes),
+            "all_stream_bytes": int(all_stream), "prof": prof, "nprof": nprof,
+            "launches_per_step": launches_per_step, "clocks": clocks, "flush": flush is not None, "nbytes": nbytes}
+
+
+def run_ours(args, ws, rank, local):
+    import gc
+
+    import torch
+
+    import paper_2505_09810_b200 as lmcb
+    from paper_2505_09810_b200 import shard, synth
+
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    specs = synth.CONFIGS[args.config]()
+    sizes = [s.numel * 2 for s in specs]
+    total_bytes = sum(sizes)
+    # ONE checkpoint sharded across the ranks: whole tensors, largest first
+    # onto the least-loaded rank (every rank computes the same table)
+    owner = shard.assign_tensors(sizes, ws)
+    owned = [i for i, r in enumerate(owner) if r == rank]
+    ts = [synth.make_tensor(specs[i], SEED, i) for i in owned]
+    prev = None
+    if args.config in DELTA:   # compress step t+1 against step t (fused XOR)
+        prev = ts
+        ts = [synth.next_step(w, SEED, i) for i, w in zip(owned, prev)]
+    codec = lmcb.Codec(local)
+    m = measure(codec, ts, prev, args, ws, dist, owned, len(specs), local)
+    gc.collect()
+    torch.cuda.empty_cache()
+
+    # cfg5's second step in delta mode: step t+1 against the resident step t
+    delta_step = None
+    if args.config == "cfg5" and not args.no_delta:
+        nxt = [synth.next_step(w, SEED, i) for i, w in zip(owned, ts)]
+        md = measure(codec, nxt, ts, args, ws, dist, owned, len(specs), local, with_clocks=False)
+        peak, peak_src = measured_peaks()
+        cs, ds = md["comp_ms"] / args.steps / 1e3, md["dec_ms"] / args.steps / 1e3
+        delta_step = {
+            "value": round(total_bytes * args.steps / (md["total_ms"] / 1e3) / GIB, 3), "unit": "GiB/s",
+            "workload": "cfg5 step t+1 = bf16(w_t + N(0,1)(1e-3|w_t| + 1e-6)) compressed against the resident step t "
+                        "(fused XOR, FLAG_DELTA streams) and decompressed to the XOR payload",
+            "ms_per_step": round(md["total_ms"] / args.steps, 4),
+            "compression_ratio": round(md["all_stream_bytes"] / total_bytes, 6),
+            "compress_gib_s": round(total_bytes / cs / GIB, 3), "decompress_gib_s": round(total_bytes / ds / GIB, 3),
+            "compress_hbm_frac": round((2 * total_bytes + md["all_stream_bytes"]) / cs / 1e9 / peak, 4),
+            "decompress_hbm_frac": round((total_bytes + md["all_stream_bytes"]) / ds / 1e9 / peak, 4),
+            "kernels_ms_per_step": {k: round(v[1] / md["nprof"], 4) for k, v in sorted(md["prof"].items())},
+        }
+        del nxt, md
+        gc.collect()
+        torch.cuda.empty_cache()
 
     # end-to-end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        # the device-resident plans are done: free them for the e2e buffer sets
-        del cplan, dplan, b, r, pb
-        import gc
-        gc.collect()
-        torch.cuda.empty_cache()
-        e2e = measure_e2e(codec, ts, args, ws, dist, prev=prev)
+        e2e = measure_e2e(codec, ts, args, ws, dist, total_bytes, owned, len(specs), prev=prev)
 
-    # roofline of the dominant kernel
     peak, peak_src = measured_peaks()
-    dom = max(prof.items(), key=lambda kv: kv[1][1])
-    dname, (dcnt, dms) = dom
-    avg_ms = dms / dcnt
-    a_in, a_st = ALGO.get(dname, (1, 1))
-    algo_bytes = a_in * nbytes + a_st * stream_bytes   # per launch (one launch per batch)
-    achieved = algo_bytes / (avg_ms / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dname, "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(dname, args.config), "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": algo_bytes, "avg_launch_ms": round(avg_ms, 4),
-                "share_of_step": round(dms / sum(v[1] for v in prof.values()), 4)}
-    # pipeline-level fractions (compress: in + stream, decompress: stream + out)
-    comp_s, dec_s = comp_ms / args.steps / 1e3, dec_ms / args.steps / 1e3
+    n_in, n_st = m["nbytes"], m["stream_bytes"]
+    delta = prev is not None
+    prof, nprof = m["prof"], m["nprof"]
+    roofline = roofline_of(prof, nprof, n_in, n_st, delta, peak, peak_src, args.config)
+    roof_c = roofline_of(prof, nprof, n_in, n_st, delta, peak, peak_src, args.config, is_compress_kernel)
+    roof_d = roofline_of(prof, nprof, n_in, n_st, delta, peak, peak_src, args.config,
+                         lambda k: not is_compress_kernel(k))
+    steps = args.steps
+    comp_s, dec_s = m["comp_ms"] / steps / 1e3, m["dec_ms"] / steps / 1e3
+    in_all = total_bytes * (2 if delta else 1)
     pipeline = {
-        "compress_gib_s": round(ws * nbytes / comp_s / GIB, 3),
-        "decompress_gib_s": round(ws * nbytes / dec_s / GIB, 3),
-        "compress_hbm_frac": round((nbytes + stream_bytes) / comp_s / 1e9 / peak, 4),
-        "decompress_hbm_frac": round((nbytes + stream_bytes) / dec_s / 1e9 / peak, 4),
+        "compress_gib_s": round(total_bytes / comp_s / GIB, 3),
+        "decompress_gib_s": round(total_bytes / dec_s / GIB, 3),
+        "compress_hbm_frac": round((in_all + m["all_stream_bytes"]) / comp_s / 1e9 / peak / ws, 4),
+        "decompress_hbm_frac": round((total_bytes + m["all_stream_bytes"]) / dec_s / 1e9 / peak / ws, 4),
         "compress_ms": round(comp_s * 1e3, 4), "decompress_ms": round(dec_s * 1e3, 4),
     }
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(ts, prev)
     if rank == 0:
+        value = total_bytes * steps / (m["total_ms"] / 1e3) / GIB
         line = {
-            "metric": METRIC, "value": round(value, 3), "unit": "GiB/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "metric": METRIC, "value": round(value, 3), "unit": "GiB/s", "n_gpus": ws, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": round(m["total_ms"] / steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
             "config": {"workload": workload(args.config),
-                       "l2": (f"inputs {nbytes / 1e6:.0f} MB > 126 MB L2 per step; no flush needed" if flush is None
-                              else f"inputs {nbytes / 1e6:.0f} MB: 512 MB L2 flush between timed steps, steps timed alone"),
-                       "parallelism": f"dp{ws} (independent checkpoints per rank + all-gather of stream sizes)"},
-            "compression_ratio": round(ratio, 6),
+                       "l2": (f"inputs {total_bytes / 1e6:.0f} MB > 126 MB L2 per step; no flush needed"
+                              if not m["flush"] else
+                              f"inputs {total_bytes / 1e6:.0f} MB: 512 MB L2 flush between timed steps, steps timed alone"),
+                       "parallelism": (f"dp{ws}: one checkpoint sharded by whole tensors across {ws} GPU(s), "
+                                       "all-gather of stream lengths only")},
+            "compression_ratio": round(m["all_stream_bytes"] / total_bytes, 6),
             "pipeline": pipeline,
             "kernels_ms_per_step": {k: round(v[1] / nprof, 4) for k, v in sorted(prof.items())},
             "roofline": roofline,
+            "roofline_compress": roof_c,
+            "roofline_decompress": roof_d,
+            "delta_step": delta_step,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": int(round(launches_per_step * args.steps)),
-            "clocks": clocks,
+            "gpu_launches": int(round(m["launches_per_step"] * steps)),
+            "clocks": m["clocks"],
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
 
 
-def measure_e2e(codec, ts, args, ws, dist, prev=None):
+def measure_e2e(codec, ts, args, ws, dist, total_bytes, owned, n_total, prev=None):
     """Round trip through the public plan API with pinned host buffers, every
     step: H2D of the checkpoint into the registered tensors, CompressPlan.run,
     D2H of the streams; H2D of the streams, DecompressPlan.run, D2H of the
@@ -443,7 +520,6 @@ def measure_e2e(codec, ts, args, ws, dist, prev=None):
     for t, o in zip(ts, offs):
         host_all[o:o + t.numel() * t.element_size()].copy_(t.view(torch.uint8).reshape(-1).cpu())
     host = [host_all[o:o + t.numel() * t.element_size()] for t, o in zip(ts, offs)]
-    nbytes = sum(h.numel() for h in host)
     sets = []
     for _ in range(2):
         dev_all = torch.empty(pos, dtype=torch.uint8, device="cuda")
@@ -488,7 +564,8 @@ def measure_e2e(codec, ts, args, ws, dist, prev=None):
             s_cmp.wait_event(ev["in"])
             if S["used"]:
                 s_cmp.wait_event(ev["d2h_s"])      # streams of step k-2 have left cp.out
-            cp.run()
+            b = cp.run()
+            exchange_lengths(b, owned, n_total, dist)
             S["ret"].meta.copy_(cp.meta)
             ev["cmp"].record(s_cmp)
             cp.layout_to_host(S["host_meta"], s_cmp)
@@ -570,12 +647,14 @@ def measure_e2e(codec, ts, args, ws, dist, prev=None):
     if dist is not None:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = ms.item()
+    nbytes = sum(h.numel() for h in host)
     sb = max(sizes)
-    return {"value": round(ws * nbytes * args.steps / (ms / 1e3) / GIB, 3), "unit": "GiB/s",
+    del sets
+    return {"value": round(total_bytes * args.steps / (ms / 1e3) / GIB, 3), "unit": "GiB/s",
             "h2d_bytes_per_step": nbytes + sb, "d2h_bytes_per_step": sb + nbytes,
             "path": "pinned host checkpoint -> H2D -> CompressPlan.run -> D2H streams -> H2D streams -> "
                     "DecompressPlan.run -> D2H payload; two buffer sets pipelined across steps on H2D / compute / "
-                    "D2H streams"}
+                    "D2H streams" + (" (per rank: its own tensors; bytes per step are rank 0's)" if ws > 1 else "")}
 
 
 def cpu_baseline(ts, prev=None):

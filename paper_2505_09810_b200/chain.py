@@ -158,6 +158,14 @@ class DeviceChain:
         self._step = -1           # step held in _buf (-1: nothing valid)
         self._chain_id = None     # manifest the resident step came from
 
+    def release(self) -> None:
+        """Free the resident step's HBM buffer (the next add_step restores
+        the previous step from the files again)."""
+        self._buf = None
+        self._layout = {}
+        self._step = -1
+        self._chain_id = None
+
     # ------------------------------------------------------------ resident
     def _view(self, name: str):
         off, n, _ = self._layout[name]
@@ -343,9 +351,21 @@ def _chain_for(chain_dir, block_size: int, byte_group: bool, segment_count: int)
     key = (os.path.realpath(os.fspath(chain_dir)), codec.ctx.device, block_size, bool(byte_group), segment_count)
     ch = _chains.get(key)
     if ch is None:
+        # one resident step per chain directory: entries of the same directory
+        # with other options hold a stale step, drop them
+        for k in [k for k in _chains if k[0] == key[0]]:
+            _chains.pop(k).release()
         ch = _chains[key] = DeviceChain(chain_dir, codec=codec, block_size=block_size, byte_group=byte_group,
                                         segment_count=segment_count)
     return ch
+
+
+def release_chains(chain_dir=None) -> None:
+    """Free the HBM that module-level ``add_step`` keeps resident (every chain,
+    or only ``chain_dir``'s).  Later calls restore from the files."""
+    path = None if chain_dir is None else os.path.realpath(os.fspath(chain_dir))
+    for k in [k for k in _chains if path is None or k[0] == path]:
+        _chains.pop(k).release()
 
 
 def add_step(chain_dir, shards: dict, *, step: int | None = None, block_size: int = DEFAULT_BLOCK_SIZE,

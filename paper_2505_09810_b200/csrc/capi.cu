@@ -31,6 +31,7 @@ struct lmcg_ctx {
     cudaStream_t side = nullptr;          // second stream for kernels that overlap the main chain
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t dfork_ev = nullptr, djoin_ev = nullptr;   // decompress: large-record k_decrec on the side stream
+    cudaEvent_t dec_done = nullptr;       // end of the last eager decompress (lmcg_decompress_result waits on it)
     int sms = 148;                        // multiprocessors of the device
     // last compress (block_info)
     uint64_t last_nb = 0;
@@ -323,6 +324,7 @@ lmcg_ctx* lmcg_create(int device) {
     cudaEventCreateWithFlags(&ctx->dfork_ev, cudaEventDisableTiming);
     cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, ctx->device);
     cudaEventCreateWithFlags(&ctx->djoin_ev, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ctx->dec_done, cudaEventDisableTiming);
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (const char* e = getenv("LMCG_SERIAL")) ctx->serial = e[0] == '1';
     if (const char* e = getenv("LMCG_CRC_FORK")) ctx->crc_fork = atoi(e);
@@ -347,6 +349,7 @@ void lmcg_destroy(lmcg_ctx* ctx) {
         if (ctx->join_ev) cudaEventDestroy(ctx->join_ev);
         if (ctx->dfork_ev) cudaEventDestroy(ctx->dfork_ev);
         if (ctx->djoin_ev) cudaEventDestroy(ctx->djoin_ev);
+        if (ctx->dec_done) cudaEventDestroy(ctx->dec_done);
         if (ctx->side) cudaStreamDestroy(ctx->side);
     }
     delete ctx;
@@ -1037,7 +1040,12 @@ static int decompress_impl(lmcg_ctx* ctx, const void* const* d_streams, const ui
                            cudaMemcpyHostToDevice, st));
         CK(cudaEventRecord(ctx->pin_done, st));
     }
-    return decompress_launch(ctx, n, P.nwin, P.nseg, P.nrec, P.nchunk, P.ntile, ws, o, d_out, nullptr, st);
+    if (int r = decompress_launch(ctx, n, P.nwin, P.nseg, P.nrec, P.nchunk, P.ntile, ws, o, d_out, nullptr, st)) return r;
+    // lmcg_decompress_result reads the per-stream results after this event: the
+    // caller's stream may be a non-blocking one that the legacy default stream
+    // (a plain cudaMemcpy) would not wait for
+    CK(cudaEventRecord(ctx->dec_done, st));
+    return LMCG_OK;
 }
 
 int lmcg_decompress(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t* lens, int n,
@@ -1097,6 +1105,7 @@ int lmcg_decompress_result(lmcg_ctx* ctx, int n, int32_t* h_status, uint64_t* h_
     std::vector<DecStreamOut> so(n);
     std::vector<uint32_t> st(n);
     if (n) {
+        CK(cudaEventSynchronize(ctx->dec_done));   // the decompress this reports on has finished
         CK(cudaMemcpy(so.data(), ctx->d_sout, n * sizeof(DecStreamOut), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(st.data(), ctx->d_dstatus, n * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     }

@@ -321,6 +321,11 @@ def read_files_to_device(paths: Sequence, device, *, head: int = 64, slot_bytes:
                 ev.record(copy)
             done[s] = ev
     torch.cuda.current_stream(device).wait_stream(copy)
+    # the staging slots are process-global: the next call (or another thread)
+    # may refill them as soon as this returns, so their copies must be done
+    for ev in done:
+        if ev is not None:
+            ev.synchronize()
     for i in range(n):
         if errors[i] is not None:
             lengths[i] = 0

@@ -181,10 +181,11 @@ def test_split_single_process_matches_oracle():
         data = _tensors()[6]
         full, part = _oracle_part_fn(data, **opts)
         got = shard.compress_split(data, element_type=BF16, part_fn=part, **opts)
-        assert got == full
+        assert got.length == len(full)
+        assert got.to_bytes() == full
 
 
-def _split_worker(rank, world, port, q):
+def _split_worker(rank, world, port, q, path):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -192,23 +193,66 @@ def _split_worker(rank, world, port, q):
         opts = {"block_size": 4096, "segment_count": 3, "buffer_size": 40000}
         full, part = _oracle_part_fn(data, **opts)
         got = shard.compress_split(data, element_type=BF16, part_fn=part, **opts)
-        q.put((rank, got == full))
+        # each rank writes only its own records (rank 0 also the frame) into
+        # the shared file; records never cross ranks on this path
+        fd = os.open(path, os.O_RDWR)
+        try:
+            got.write_into(fd)
+        finally:
+            os.close(fd)
+        dist.barrier()
+        with open(path, "rb") as f:
+            on_disk = f.read()
+        q.put((rank, on_disk == full and got.to_bytes() == full and got.length == len(full)))
     finally:
         dist.destroy_process_group()
 
 
 def test_gloo_world2_split_one_tensor():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    got = sorted(q.get(timeout=120) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    data = _tensors()[6]
+    full, _ = _oracle_part_fn(data, block_size=4096, segment_count=3, buffer_size=40000)
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "split.lmc")
+        with open(path, "wb") as f:
+            f.truncate(len(full))
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_split_worker, args=(r, 2, port, q, path)) for r in range(2)]
+        for p in procs:
+            p.start()
+        got = sorted(q.get(timeout=120) for _ in procs)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
     assert got == [(0, True), (1, True)]
+
+
+def test_pwrite_all_loops_until_written(tmp_path, monkeypatch):
+    # os.pwrite may write fewer bytes than asked (Linux caps one call near 2 GiB)
+    real = os.pwrite
+    calls = []
+
+    def short(fd, data, off):
+        calls.append(off)
+        return real(fd, bytes(data)[:3], off)
+
+    monkeypatch.setattr(shard.os, "pwrite", short)
+    p = tmp_path / "f"
+    p.write_bytes(b"\0" * 20)
+    fd = os.open(p, os.O_RDWR)
+    try:
+        shard._pwrite_all(fd, b"abcdefghij", 5)
+    finally:
+        os.close(fd)
+    assert p.read_bytes() == b"\0" * 5 + b"abcdefghij" + b"\0" * 5
+    assert calls == [5, 8, 11, 14]
+
+
+def test_collective_device_defaults():
+    import torch
+    assert shard.collective_device() == torch.device("cpu")
+    assert shard.collective_device(device="cpu") == torch.device("cpu")
 
 
 @pytest.mark.gpu
