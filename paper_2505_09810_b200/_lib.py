@@ -53,6 +53,7 @@ EXPORTS = [
     "lmcg_decompress", "lmcg_decompress_apply", "lmcg_decompress_result", "lmcg_compress_host", "lmcg_decompress_host", "lmcg_build_codebooks",
     "lmcg_block_info", "lmcg_profile", "lmcg_profile_report", "lmcg_compress_plan_create", "lmcg_compress_plan_run",
     "lmcg_decompress_plan_create", "lmcg_decompress_plan_run", "lmcg_plan_output_bytes", "lmcg_plan_destroy", "lmcg_copy_to_host", "lmcg_fallback_segments", "lmcg_compress_part",
+    "lmcg_set_decode_fusion",
 ]
 
 _lib = None
@@ -102,6 +103,8 @@ def load(path: str = SO_PATH):
         L.lmcg_build_codebooks.argtypes = [vp, vp, ctypes.c_int, vp, vp]
         L.lmcg_block_info.restype = ctypes.c_int64
         L.lmcg_block_info.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int64]
+        L.lmcg_set_decode_fusion.restype = ctypes.c_int
+        L.lmcg_set_decode_fusion.argtypes = [vp, ctypes.c_int]
         L.lmcg_profile.restype = ctypes.c_int
         L.lmcg_profile.argtypes = [vp, ctypes.c_int]
         L.lmcg_profile_report.restype = ctypes.c_int64
@@ -137,6 +140,10 @@ class Context:
         self.ptr = self.lib.lmcg_create(device)
         if not self.ptr:
             raise DeviceError("lmcg_create failed")
+
+    def set_decode_fusion(self, enable: bool) -> None:
+        """Fused decode + ungroup + CRC (k_decpair) on or off; same bytes either way."""
+        self.check(self.lib.lmcg_set_decode_fusion(self.ptr, int(enable)))
 
     def profile(self, enable: bool) -> None:
         self.lib.lmcg_profile(self.ptr, int(enable))

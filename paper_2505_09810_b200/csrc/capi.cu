@@ -60,6 +60,8 @@ struct lmcg_ctx {
     uint8_t* part_ws = nullptr;
     size_t part_ws_cap = 0;
     bool res_attr = false;
+    int pair_grid = 0;                    // persistent k_decpair CTAs (each owns a kPairRing slot)
+    bool fuse = true;                     // fused decode + ungroup + CRC (k_decpair) for eligible windows
     uint32_t* d_sh992 = nullptr;
     int crc_occ = 1;
     bool enc_attr = false;
@@ -328,6 +330,7 @@ lmcg_ctx* lmcg_create(int device) {
     cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking);
     if (const char* e = getenv("LMCG_SERIAL")) ctx->serial = e[0] == '1';
     if (const char* e = getenv("LMCG_CRC_FORK")) ctx->crc_fork = atoi(e);
+    if (const char* e = getenv("LMCG_NOFUSE")) ctx->fuse = e[0] != '1';
     return ctx;
 }
 
@@ -723,6 +726,12 @@ void lmcg_plan_destroy(lmcg_plan* pl) {
     delete pl;
 }
 
+int lmcg_set_decode_fusion(lmcg_ctx* ctx, int enable) {
+    if (!ctx) return LMCG_ERR_ARGUMENT;
+    ctx->fuse = enable != 0;
+    return LMCG_OK;
+}
+
 int lmcg_profile(lmcg_ctx* ctx, int enable) {
     if (!ctx) return LMCG_ERR_ARGUMENT;
     ctx->prof = enable != 0;
@@ -861,7 +870,7 @@ int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
     for (int i = 0; i < n; i++) in[i] = DecStreamIn{static_cast<const uint8_t*>(d_streams[i]), lens[i], nullptr, 0};
     CK(cudaMemcpyAsync(d_in, in.data(), n * sizeof(DecStreamIn), cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(d_caps, 0, n * sizeof(DecCaps), st));
-    k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, nullptr, nullptr);
+    k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, nullptr, nullptr, nullptr, 0);
     CK(cudaGetLastError());
     std::vector<DecStreamOut> so(n);
     CK(cudaMemcpyAsync(so.data(), d_sout, n * sizeof(DecStreamOut), cudaMemcpyDeviceToHost, st));
@@ -881,8 +890,8 @@ int lmcg_read_hints(lmcg_ctx* ctx, const void* const* d_streams, const uint64_t*
 
 namespace {
 // Workspace layout of one decompress (offsets into the workspace).
-enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CAND, D_CCNT, D_CTOT, D_CPRE, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_LARGE, D_TC, D_MAPS, D_SCR, D_NOFF };
-size_t dec_layout(const DPlan& P, int n, size_t* o) {
+enum { D_IN, D_CAPS, D_SOUT, D_ST, D_WIN, D_SEG, D_CAND, D_CCNT, D_CTOT, D_CPRE, D_SCNT, D_SFAIL, D_RPOS, D_RNEXT, D_LARGE, D_TC, D_MAPS, D_PAIRS, D_RING, D_SCR, D_NOFF };
+size_t dec_layout(const DPlan& P, int n, size_t* o, uint64_t ring_bytes) {
     Arena a;
     o[D_IN] = a.take<DecStreamIn>(n + 1);
     o[D_CAPS] = a.take<DecCaps>(n + 1);
@@ -901,10 +910,22 @@ size_t dec_layout(const DPlan& P, int n, size_t* o) {
     o[D_LARGE] = a.take<uint32_t>(P.nrec + 2);   // k_classify: count | record slots
     o[D_TC] = a.take<uint32_t>(P.ntile + 1);
     o[D_MAPS] = a.take<uint32_t>(P.nchunk + P.nrec + P.ntile + 3);   // chunk2seg | rec2seg | tile2win
+    o[D_PAIRS] = a.take<uint32_t>(P.nrec / 2 + 4);   // k_pairs: count | ticket | pad | pad | low-plane record slots
+    o[D_RING] = a.take<uint8_t>(ring_bytes + 256);
     o[D_SCR] = a.take<uint8_t>(P.scratch + 64);
     return a.off + 256;
 }
 }  // namespace
+
+// Persistent k_decpair grid (resident CTAs; each owns a kPairRing slot of the workspace).
+static int ensure_pair_grid(lmcg_ctx* ctx) {
+    if (!ctx->pair_grid) {
+        const size_t dsm = dec_smem_bytes(kStageSmall);
+        CK(cudaFuncSetAttribute(k_decpair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+        ctx->pair_grid = occupancy(ctx, (const void*)k_decpair, kThreads, dsm);
+    }
+    return LMCG_OK;
+}
 
 // Kernel sequence of one decompress; DecStreamIn and DecCaps are already on
 // the device.  No host synchronisation: capturable in a CUDA graph.
@@ -930,6 +951,8 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     auto* d_c2s = reinterpret_cast<uint32_t*>(ws + o[D_MAPS]);
     uint32_t* d_r2s = d_c2s + nchunk + 1;
     uint32_t* d_t2w = d_r2s + nrec + 1;
+    auto* d_pairs = reinterpret_cast<uint32_t*>(ws + o[D_PAIRS]);
+    uint8_t* d_ring = ws + o[D_RING];
     uint8_t* d_scr = ws + o[D_SCR];
     ctx->d_sout = d_sout;
     ctx->d_dstatus = d_st;
@@ -945,7 +968,9 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         CK(cudaFuncSetAttribute(k_fallback, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
         ctx->dec_attr = true;
     }
-    { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg); }
+    if (int r = ensure_pair_grid(ctx)) return r;
+    { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg,
+                                                            static_cast<const uint8_t*>(d_out), ctx->fuse ? 1 : 0); }
     CK(cudaMemsetAsync(d_c2s, 0xFF, (nchunk + nrec + ntile + 3) * sizeof(uint32_t), st));
     if (nseg + nwin) { PROF(k_maps); k_maps<<<(unsigned)(nseg + nwin), 256, 0, st>>>(d_seg, nseg, d_win, nwin, d_c2s, d_r2s, d_t2w); }
     if (nchunk) { PROF(k_cand); k_cand<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, d_c2s, nchunk, d_cand, d_ccnt, d_ctot); }
@@ -971,25 +996,33 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         CK(cudaStreamIsCapturing(st, &cap));
         if (nrec < kDecSplitFrom || cap != cudaStreamCaptureStatusActive) {
-            k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 0);
+            k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, d_win, nrec, d_sfail, d_rpos, d_scr, 0);
         } else {
             // records whose payload does not stage in kStageSmall are listed and
             // decoded by persistent CTAs (3 per SM) on the side stream while the
             // rest run at 4 CTAs per SM
             CK(cudaMemsetAsync(d_large, 0, sizeof(uint32_t), st));
-            k_classify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_large + 1, d_large);
+            k_classify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, d_win, nrec, d_sfail, d_rpos, d_large + 1, d_large);
             cudaStream_t sst = ctx->serial ? st : ctx->side;
             if (!ctx->serial) {
                 CK(cudaEventRecord(ctx->dfork_ev, st));
                 CK(cudaStreamWaitEvent(sst, ctx->dfork_ev, 0));
             }
             k_decrec_large<<<(unsigned)std::min<uint64_t>(nrec, (uint64_t)ctx->sms * 3), kThreads, dsm, sst>>>(
-                d_seg, d_r2s, d_large + 1, d_large, d_sfail, d_rpos, d_scr);
-            k_decrec<<<(unsigned)nrec, kThreads, dsm_small, st>>>(d_seg, d_r2s, nrec, d_sfail, d_rpos, d_scr, 1);
+                d_seg, d_r2s, d_win, d_large + 1, d_large, d_sfail, d_rpos, d_scr);
+            k_decrec<<<(unsigned)nrec, kThreads, dsm_small, st>>>(d_seg, d_r2s, d_win, nrec, d_sfail, d_rpos, d_scr, 1);
             if (!ctx->serial) {
                 CK(cudaEventRecord(ctx->djoin_ev, sst));
                 CK(cudaStreamWaitEvent(st, ctx->djoin_ev, 0));
             }
+        }
+        if (ctx->fuse) {
+            PROF(k_decpair);
+            CK(cudaMemsetAsync(d_pairs, 0, 4 * sizeof(uint32_t), st));
+            k_pairs<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, nrec, d_win, d_sfail, d_pairs + 4, d_pairs);
+            k_decpair<<<(unsigned)ctx->pair_grid, kThreads, dsm_small, st>>>(d_seg, d_r2s, d_win, d_pairs + 4, d_pairs, d_sfail,
+                                                                            d_rpos, d_ring, static_cast<uint8_t*>(d_out),
+                                                                            ctx->d_crc, ctx->d_sh992, d_tc);
         }
     }
     if (nseg) {
@@ -1004,7 +1037,7 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         }
         PROF(k_ungroup);
         k_ungroup<<<(unsigned)std::min<uint64_t>(ntile, (uint64_t)ctx->ung_occ), kUngThreads, kUngSmem, st>>>(
-            d_win, d_t2w, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, ctx->d_sh992, d_tc, d_st);
+            d_win, d_t2w, ntile, d_scr, static_cast<uint8_t*>(d_out), ctx->d_crc, ctx->d_sh992, d_tc, d_st, d_sfail);
     }
     { PROF(k_finalize); k_finalize<<<n, kThreads, 0, st>>>(d_sout, d_caps, d_win, n, d_tc, ctx->d_crc, d_st, d_in); }
     if (d_codes) k_status<<<(n + 255) / 256, 256, 0, st>>>(d_sout, d_st, n, d_codes);
@@ -1023,7 +1056,8 @@ static int decompress_impl(lmcg_ctx* ctx, const void* const* d_streams, const ui
     DPlan P;
     make_dplan(lens, n, hints, h_out_offsets, out_capacity, P);
     size_t o[D_NOFF];
-    const size_t need = dec_layout(P, n, o);
+    if (int r = ensure_pair_grid(ctx)) return r;
+    const size_t need = dec_layout(P, n, o, (uint64_t)ctx->pair_grid * kPairRing);
     if (int r = grow(ctx, &ctx->dws, &ctx->dws_cap, need)) return r;
     uint8_t* ws = ctx->dws;
     const size_t hb = (size_t)n * (sizeof(DecStreamIn) + sizeof(DecCaps)) + 64;
@@ -1076,7 +1110,8 @@ lmcg_plan* lmcg_decompress_plan_create(lmcg_ctx* ctx, int n, const lmcg_stream_h
     for (int i = 0; i < n; i++) out += (hints[i].orig + 15) & ~15ull;
     pl->out_bytes = out;
     pl->dn_win = P.nwin; pl->dn_seg = P.nseg; pl->dn_rec = P.nrec; pl->dn_chunk = P.nchunk; pl->dn_tile = P.ntile;
-    pl->ws_bytes = dec_layout(P, n, pl->doffs);
+    if (ensure_pair_grid(ctx)) { delete pl; return nullptr; }
+    pl->ws_bytes = dec_layout(P, n, pl->doffs, (uint64_t)ctx->pair_grid * kPairRing);
     if (cudaMalloc(&pl->ws, pl->ws_bytes) != cudaSuccess) {
         fail(ctx, LMCG_ERR_CUDA, "cudaMalloc of %zu bytes for a decompress plan failed", pl->ws_bytes);
         delete pl;

@@ -88,8 +88,11 @@ struct DecWin {
     uint64_t ooff;            // absolute output offset
     uint64_t soff;            // window start within the stream payload
     uint64_t tile0;           // global first tile
-    uint32_t ntile, w, stream, pad;
+    uint32_t ntile, w, stream;
+    uint32_t fuse;            // 1: k_decpair decodes the window straight into the output (see there)
     const uint8_t* prev;      // xor_apply source of this window's output (nullptr: none)
+    uint64_t rec0, seg0;      // global first record slot / segment of the window
+    uint32_t nseg, pad;
 };
 
 struct DecSeg {
@@ -99,6 +102,7 @@ struct DecSeg {
     uint64_t rec0, chunk0;    // global first record slot / chunk
     uint32_t nrec, nchunk;    // canonical records, scan chunks
     uint32_t block, stream;
+    uint32_t win, pad;        // global window index
 };
 
 __device__ __forceinline__ uint32_t rd32(const uint8_t* p) {
@@ -108,8 +112,14 @@ __device__ __forceinline__ uint64_t rd64(const uint8_t* p) { return (uint64_t)rd
 __device__ __forceinline__ bool valid_block(uint32_t b) { return b >= 4096 && b <= (1u << 20) && (b & (b - 1)) == 0; }
 
 // ---------------------------------------------------------------- k_parse
+// Fused windows (DecWin.fuse, decoded by k_decpair): two byte planes (bf16 /
+// fp16 byte-grouped), blocks of 16, 32 or 64 KiB, planes a whole number of
+// blocks and every segment a whole number of blocks (so every record is a full
+// block and low-plane record k pairs with high-plane record n / B + k), and
+// 16-byte aligned output (and xor_apply source).
 __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __restrict__ caps, int ns,
-                        DecStreamOut* __restrict__ sout, DecWin* __restrict__ wins, DecSeg* __restrict__ segs) {
+                        DecStreamOut* __restrict__ sout, DecWin* __restrict__ wins, DecSeg* __restrict__ segs,
+                        const uint8_t* out, int fuse_ok) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ns) return;
     const uint8_t* p = in[s].p;
@@ -140,11 +150,12 @@ __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __res
             while (remaining > 0 && !bad) {
                 if (table > len - off) { bad = true; break; }
                 uint64_t wsum = 0;
-                bool over = false;
+                bool over = false, seg_aligned = true;
                 for (uint64_t i = 0; i < S; i++) {
                     const uint64_t o = rd64(p + off + i * kSegEntry);
                     if (o > remaining - wsum) over = true;
                     else wsum += o;
+                    if (o % B) seg_aligned = false;
                 }
                 const uint64_t toff = off;
                 off += table;
@@ -159,6 +170,10 @@ __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __res
                     d.tile0 = cp.tile0 + ntile; d.ntile = (uint32_t)wtiles;
                     // xor_apply only with a prev of the payload's length (else k_finalize reports the mismatch)
                     d.prev = (in[s].prev && in[s].prev_len == h.orig) ? in[s].prev + opos : nullptr;
+                    d.rec0 = cp.rec0 + nrec; d.seg0 = cp.seg0 + nseg; d.nseg = S;
+                    d.fuse = fuse_ok && wdt == 2 && B >= 16384 && B <= 65536 && d.n >= B && d.n % B == 0 && seg_aligned &&
+                             ((reinterpret_cast<uint64_t>(out) + d.ooff) & 15) == 0 &&
+                             (reinterpret_cast<uint64_t>(d.prev) & 15) == 0;
                     wins[cp.win0 + nwin] = d;
                 }
                 uint64_t gpos = 0;
@@ -177,6 +192,7 @@ __global__ void k_parse(const DecStreamIn* __restrict__ in, const DecCaps* __res
                         d.goff = cp.scratch0 + scr + gpos;
                         d.rec0 = cp.rec0 + nrec; d.chunk0 = cp.chunk0 + nchunk;
                         d.nrec = (uint32_t)r; d.nchunk = (uint32_t)ch; d.block = B; d.stream = (uint32_t)s;
+                        d.win = (uint32_t)(cp.win0 + nwin); d.pad = 0;
                         segs[cp.seg0 + nseg] = d;
                     }
                     nrec += r;
@@ -1270,11 +1286,13 @@ __device__ __forceinline__ bool is_large(const uint8_t* rec) {
 
 // Decode record slot g into grouped scratch (CTA-wide).
 __device__ __forceinline__ void decrec_one(DecSmem& s, const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
-                                           uint64_t g, uint32_t* __restrict__ seg_fail, const uint64_t* __restrict__ rec_pos,
-                                           uint8_t* __restrict__ scratch, bool skip_large, uint32_t stage_cap) {
+                                           const DecWin* __restrict__ wins, uint64_t g, uint32_t* __restrict__ seg_fail,
+                                           const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch,
+                                           bool skip_large, uint32_t stage_cap) {
     const uint32_t lo = rec2seg[g];
     if (lo == ~0u || seg_fail[lo]) return;
     const DecSeg sg = segs[lo];
+    if (wins[sg.win].fuse) return;   // (k_decpair has it)
     const uint32_t r = (uint32_t)(g - sg.rec0);
     const uint8_t* rec = sg.base + rec_pos[g];
     if (skip_large && is_large(rec)) return;   // (k_decrec_large has it)
@@ -1288,44 +1306,241 @@ __device__ __forceinline__ void decrec_one(DecSmem& s, const DecSeg* __restrict_
 // launch runs at 4 CTAs per SM with kStageSmall; otherwise (few records) it
 // decodes everything with kStageLarge.
 __global__ void __launch_bounds__(kThreads, 4) k_decrec(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
-                                                   uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
+                                                   const DecWin* __restrict__ wins, uint64_t nrec_total, uint32_t* __restrict__ seg_fail,
                                                    const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch,
                                                    int split) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
     const uint64_t g = blockIdx.x;
     if (g >= nrec_total) return;
-    decrec_one(s, segs, rec2seg, g, seg_fail, rec_pos, scratch, split != 0, split ? kStageSmall : kStageLarge);
+    decrec_one(s, segs, rec2seg, wins, g, seg_fail, rec_pos, scratch, split != 0, split ? kStageSmall : kStageLarge);
 }
 
 // The large records (k_classify's list), persistent CTAs with kStageLarge;
 // runs on the side stream next to k_decrec.
 __global__ void __launch_bounds__(kThreads, 3) k_decrec_large(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
-                                                         const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
+                                                         const DecWin* __restrict__ wins, const uint32_t* __restrict__ list, const uint32_t* __restrict__ count,
                                                          uint32_t* __restrict__ seg_fail, const uint64_t* __restrict__ rec_pos,
                                                          uint8_t* __restrict__ scratch) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
     const uint32_t n = *count;
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        decrec_one(s, segs, rec2seg, list[i], seg_fail, rec_pos, scratch, false, kStageLarge);
+        decrec_one(s, segs, rec2seg, wins, list[i], seg_fail, rec_pos, scratch, false, kStageLarge);
         __syncthreads();
     }
 }
 
 // Thread per record slot (after discovery): list the records for
 // k_decrec_large.
-__global__ void k_classify(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg, uint64_t nrec_total,
-                           const uint32_t* __restrict__ seg_fail, const uint64_t* __restrict__ rec_pos,
+__global__ void k_classify(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg, const DecWin* __restrict__ wins,
+                           uint64_t nrec_total, const uint32_t* __restrict__ seg_fail, const uint64_t* __restrict__ rec_pos,
                            uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
     const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (g >= nrec_total) return;
     const uint32_t lo = rec2seg[g];
     if (lo == ~0u || seg_fail[lo]) return;
     const DecSeg sg = segs[lo];
+    if (wins[sg.win].fuse) return;
     const uint64_t pos = rec_pos[g];
     if (pos + 5 + kHuffOverhead > sg.comp) return;
     if (is_large(sg.base + pos)) list[atomicAdd(count, 1u)] = (uint32_t)g;
+}
+
+// ------------------------------------------------------------- k_decpair
+// Fused decode + inverse byte-grouping + CRC for the fused windows (k_parse):
+// the element range [kB, (k+1)B) of a two-plane window is low-plane record
+// k and high-plane record n/B + k, and its 2B output bytes are
+// out[2e] = low[e], out[2e+1] = high[e] (bytegroup.py:53-62,
+// stream.py:392-403).  One persistent CTA per pair at a time (ticket order):
+// Huffman planes are decoded (huff_decode, as k_decrec) into the CTA's 128 KiB
+// ring slot in global memory -- written and read back by the same CTA within
+// one pair, so the slot stays in L2 -- stored planes are read in place from
+// the record, RLE planes are one byte; then the CTA writes the interleaved
+// output with 16-byte streaming stores (XOR of the previous step for
+// lmcg_decompress_apply) and folds the raw CRC-32 of each 32 KiB tile from the
+// registers (byte table, 32-fold replicated so lane l reads its own bank, laid
+// over the decoder's shared memory).  No grouped scratch, no k_ungroup pass:
+// decompress moves the stream once and the output once.  Any failure (a
+// segment of the window that failed discovery, or a record that does not
+// decode) marks every segment of the window failed, so k_fallback re-walks it
+// into scratch and k_ungroup assembles it: the authoritative path decides.
+constexpr uint32_t kPairRing = 2 * 65536;   // ring bytes per k_decpair CTA: low | high plane
+constexpr int kCrcRep1Words = 256 * 32;     // byte table, entry i of copy l at [32 i + l]
+
+// k_decpair's work list: the low-plane record slots of fused windows
+// (ctl[0] = count, ctl[1] = k_decpair's ticket).
+__global__ void k_pairs(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg, uint64_t nrec_total,
+                        const DecWin* __restrict__ wins, const uint32_t* __restrict__ seg_fail,
+                        uint32_t* __restrict__ list, uint32_t* __restrict__ ctl) {
+    const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    bool is = false;
+    if (g < nrec_total) {
+        const uint32_t lo = rec2seg[g];
+        if (lo != ~0u) {
+            const uint32_t wi = segs[lo].win;
+            const uint32_t B = segs[lo].block;
+            if (wins[wi].fuse) is = (g - wins[wi].rec0) < wins[wi].n / B;
+        }
+    }
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, is);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == lead) base = atomicAdd(&ctl[0], (uint32_t)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, lead);
+    if (is) list[base + __popc(m & ((1u << lane) - 1))] = (uint32_t)g;
+}
+
+// 16 plane bytes at element offset e (a multiple of 16) of a pair's plane
+__device__ __forceinline__ uint4 plane16(const uint8_t* p, uint32_t mode, uint32_t rle, uint32_t e, uint32_t B) {
+    if (mode == MODE_RLE) return make_uint4(rle, rle, rle, rle);
+    if (mode == MODE_HUFFMAN) return *reinterpret_cast<const uint4*>(p + e);   // ring slot (L2)
+    const uint64_t a = reinterpret_cast<uint64_t>(p) + e;                      // stored payload, any alignment
+    if ((a & 15) == 0) return __ldcs(reinterpret_cast<const uint4*>(a));
+    const uint32_t sh = (uint32_t)(a & 3) * 8;
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~3ull);
+    const uint32_t x0 = __ldcs(w), x1 = __ldcs(w + 1), x2 = __ldcs(w + 2), x3 = __ldcs(w + 3);
+    uint32_t x4 = 0;
+    if (sh) {
+        if (e + 20 <= B) {
+            x4 = __ldcs(w + 4);
+        } else {   // the payload ends inside word 4: no read past the record
+            const uint8_t* b4 = reinterpret_cast<const uint8_t*>(w + 4);
+            const uint32_t have = (uint32_t)(reinterpret_cast<uint64_t>(p) + B - reinterpret_cast<uint64_t>(b4));
+            for (uint32_t q = 0; q < 4 && q < have; q++) x4 |= (uint32_t)b4[q] << (8 * q);
+        }
+    }
+    return make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh), __funnelshift_r(x2, x3, sh),
+                      __funnelshift_r(x3, x4, sh));
+}
+
+// raw CRC of one little-endian word, byte by byte through the replicated table
+__device__ __forceinline__ uint32_t crc_word_rep1(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
+    uint32_t c = crc ^ w;
+#pragma unroll
+    for (int b = 0; b < 4; b++) c = (c >> 8) ^ tl[(c & 0xFF) * 32];
+    return c;
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
+                                                    const DecWin* __restrict__ wins, const uint32_t* __restrict__ list,
+                                                    uint32_t* __restrict__ ctl, uint32_t* __restrict__ seg_fail,
+                                                    const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ ring,
+                                                    uint8_t* out /* may alias a window's prev */,
+                                                    const CrcTables* __restrict__ ct, const uint32_t* __restrict__ sh992,
+                                                    uint32_t* __restrict__ tile_crc) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
+    uint32_t* crctab = reinterpret_cast<uint32_t*>(smem_raw);   // after the decode: byte table | 992-byte shift
+    uint32_t* st992 = crctab + kCrcRep1Words;
+    __shared__ uint32_t sh_p;
+    __shared__ uint32_t wcrc[kWarps];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint8_t* slot = ring + (uint64_t)blockIdx.x * kPairRing;
+    const uint32_t npairs = ctl[0];
+    const uint32_t* tl = crctab + lane;
+    for (;;) {
+        __syncthreads();   // the previous pair is done with sh_p and the shared memory
+        if (tid == 0) sh_p = atomicAdd(&ctl[1], 1u);
+        __syncthreads();
+        const uint32_t p = sh_p;
+        if (p >= npairs) break;
+        const uint64_t gL = list[p];
+        const DecSeg sgL = segs[rec2seg[gL]];
+        const DecWin wd = wins[sgL.win];
+        const uint32_t B = sgL.block;
+        const uint64_t np = wd.n / B, k = gL - wd.rec0;
+        const uint64_t gH = gL + np;
+        const DecSeg sgH = segs[rec2seg[gH]];
+        bool f = false;
+        for (uint32_t i = tid; i < wd.nseg; i += kThreads) f |= seg_fail[wd.seg0 + i] != 0;
+        bool ok = !__syncthreads_or(f);
+        const uint8_t* recL = ok ? sgL.base + rec_pos[gL] : nullptr;   // (record positions are valid once discovery passed)
+        const uint8_t* recH = ok ? sgH.base + rec_pos[gH] : nullptr;
+        const uint32_t mL = ok ? recL[0] : 0u, mH = ok ? recH[0] : 0u;
+        uint8_t* dL = slot;
+        uint8_t* dH = slot + 65536;
+        if (ok && mH == MODE_HUFFMAN) ok = huff_decode(s, recH + 5, B, dH, kStageSmall);
+        if (ok && mL == MODE_HUFFMAN) ok = huff_decode(s, recL + 5, B, dL, kStageSmall);
+        if (!ok) {
+            for (uint32_t i = tid; i < wd.nseg; i += kThreads) seg_fail[wd.seg0 + i] = 1u;
+            DBG_ADD(21, tid == 0);
+            continue;
+        }
+        __syncthreads();   // decoded planes visible to the CTA; the decoder's shared memory is free
+        DBG_T0(t_tab);
+        for (int i = tid; i < kCrcRep1Words; i += kThreads) crctab[i] = __ldg(&ct->slice[0][i >> 5]);
+        for (int i = tid; i < 1024; i += kThreads) st992[i] = __ldg(sh992 + i);
+        __syncthreads();
+        DBG_TADD(23, t_tab);
+        DBG_T0(t_il);
+        const uint8_t* pL = mL == MODE_HUFFMAN ? dL : recL + 5;
+        const uint8_t* pH = mH == MODE_HUFFMAN ? dH : recH + 5;
+        const uint32_t rL = recL[5] * 0x01010101u, rH = recH[5] * 0x01010101u;
+        const uint64_t e0 = k * B;
+        uint8_t* o = out + wd.ooff + 2 * e0;
+        const uint8_t* pv = wd.prev ? wd.prev + 2 * e0 : nullptr;
+        // warp w writes output rows [w R, (w + 1) R) of 1 KiB (lane l: bytes
+        // 32 l .. 32 l + 31 of each row) as four chains of R / 4 rows
+        const uint32_t R = B >> 12, Rc = R >> 2;
+        uint32_t ch[4] = {0u, 0u, 0u, 0u};
+        for (uint32_t r = 0; r < Rc; r++) {
+            uint4 lo[4], hi[4];
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const uint32_t e = (warp * R + c * Rc + r) * 512u + 16u * lane;
+                lo[c] = plane16(pL, mL, rL, e, B);
+                hi[c] = plane16(pH, mH, rH, e, B);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const uint32_t e = (warp * R + c * Rc + r) * 512u + 16u * lane;
+                const uint32_t l4[4] = {lo[c].x, lo[c].y, lo[c].z, lo[c].w}, h4[4] = {hi[c].x, hi[c].y, hi[c].z, hi[c].w};
+                uint32_t v[8];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    v[2 * q] = __byte_perm(l4[q], h4[q], 0x5140);
+                    v[2 * q + 1] = __byte_perm(l4[q], h4[q], 0x7362);
+                }
+                uint4 s0 = make_uint4(v[0], v[1], v[2], v[3]), s1 = make_uint4(v[4], v[5], v[6], v[7]);
+                if (pv) {
+                    const uint4 a0 = __ldcs(reinterpret_cast<const uint4*>(pv + 2 * e));
+                    const uint4 a1 = __ldcs(reinterpret_cast<const uint4*>(pv + 2 * e + 16));
+                    s0.x ^= a0.x; s0.y ^= a0.y; s0.z ^= a0.z; s0.w ^= a0.w;
+                    s1.x ^= a1.x; s1.y ^= a1.y; s1.z ^= a1.z; s1.w ^= a1.w;
+                }
+                __stcs(reinterpret_cast<uint4*>(o + 2 * e), s0);
+                __stcs(reinterpret_cast<uint4*>(o + 2 * e + 16), s1);
+                uint32_t x = ch[c];
+                if (r) x = st992[x & 0xFF] ^ st992[256 + ((x >> 8) & 0xFF)] ^ st992[512 + ((x >> 16) & 0xFF)] ^ st992[768 + (x >> 24)];
+#pragma unroll
+                for (int q = 0; q < 8; q++) x = crc_word_rep1(tl, x, v[q]);
+                ch[c] = x;
+            }
+        }
+        // chain c's last piece ends (3 - c) Rc KiB + 32 (31 - lane) bytes before the warp's rows end
+        const int lc = 31 - __clz(Rc * 1024u);
+        const uint32_t* tc = &ct->pow2[lc][0][0];
+        uint32_t x = ch[0];
+        x = crc_shift_tab(tc, x) ^ ch[1];
+        x = crc_shift_tab(tc, x) ^ ch[2];
+        x = crc_shift_tab(tc, x) ^ ch[3];
+        x = crc_shift_bytes(ct, x, 32u * (31 - lane));
+#pragma unroll
+        for (int q = 16; q; q >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, q);
+        if (lane == 0) wcrc[warp] = x;
+        __syncthreads();
+        // tiles of 32 KiB: 32 / R warps each
+        const uint32_t T = (2 * B) / kOutTile, wpt = kWarps / T;
+        if ((uint32_t)tid < T) {
+            const uint32_t* tw = &ct->pow2[31 - __clz(R * 1024u)][0][0];
+            uint32_t acc = 0;
+            for (uint32_t j = 0; j < wpt; j++) acc = crc_shift_tab(tw, acc) ^ wcrc[tid * wpt + j];
+            tile_crc[wd.tile0 + k * T + tid] = acc;
+        }
+        DBG_TADD(22, t_il);
+    }
 }
 
 // --------------------------------------------------------------- k_verify
@@ -1575,7 +1790,7 @@ __global__ void __launch_bounds__(kUngThreads, 1) k_ungroup(const DecWin* __rest
                                                     uint64_t ntile_total, const uint8_t* __restrict__ scratch,
                                                     uint8_t* out /* may alias a window's prev */, const CrcTables* __restrict__ ct,
                                                     const uint32_t* __restrict__ sh992, uint32_t* __restrict__ tile_crc,
-                                                    const uint32_t* __restrict__ status) {
+                                                    const uint32_t* __restrict__ status, const uint32_t* __restrict__ seg_fail) {
     extern __shared__ uint32_t ung_tab[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     load_rep4(ung_tab, ct);
@@ -1600,6 +1815,11 @@ __global__ void __launch_bounds__(kUngThreads, 1) k_ungroup(const DecWin* __rest
         if (status[wd.stream]) {
             if (lane == 0) tile_crc[tile] = 0;
             continue;
+        }
+        if (wd.fuse) {   // k_decpair wrote it, unless a segment of the window failed (then k_fallback decoded it to scratch)
+            bool f = false;
+            for (uint32_t i = lane; i < wd.nseg; i += 32) f |= seg_fail[wd.seg0 + i] != 0;
+            if (!__any_sync(0xFFFFFFFFu, f)) continue;
         }
         const uint64_t t0 = (tile - wd.tile0) * kOutTile;
         const uint32_t L = (uint32_t)min((uint64_t)kOutTile, wd.W - t0);

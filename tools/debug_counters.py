@@ -26,8 +26,8 @@ print("first decompress: fallback segs", cnt[11], "dense", cnt[12], "r>=R", cnt[
 r = codec.decompress(b)
 L.lmcg_debug_counters(cnt, 1)
 names = ["count calls", "count syms", "rec-bm calls", "rec-bm syms", "emit calls", "emit syms", "fix nosync", "fix syms", "fixup rounds", "nosync last", "nosync p0bad", "fallback segs",
-         "dense", "r>=R", "rec fail", "verify fail", "huff setup cyc", "staged recs", "pass0 cyc", "fixup cyc", "emit cyc", "chunks", "scan cyc",
-         "lookback cyc", "huff rec cyc", "rle rec cyc", "stored rec cyc", "nosync e2bad", "huff recs", "rle recs", "stored recs"]
+         "dense", "r>=R", "rec fail", "verify fail", "huff setup cyc", "staged recs", "pass0 cyc", "fixup cyc", "emit cyc", "pair fail", "interleave+crc cyc",
+         "crc table cyc", "huff rec cyc", "rle rec cyc", "stored rec cyc", "nosync e2bad", "huff recs", "rle recs", "stored recs"]
 for i, n in enumerate(names):
     print(f"{n:14s} {cnt[i]}")
 print("status", set(r.status))
