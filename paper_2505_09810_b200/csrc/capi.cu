@@ -123,6 +123,9 @@ void build_crc_tables(CrcTables& t) {
     }
     for (int k = 1; k < 4; k++)
         for (int i = 0; i < 256; i++) t.slice[k][i] = (t.slice[k - 1][i] >> 8) ^ t.slice[0][t.slice[k - 1][i] & 0xFF];
+    for (int i = 0; i < 256; i++)
+        for (int tt = 0; tt < 4; tt++)
+            for (int c = 0; c < 8; c++) t.rep4x8[32 * i + 8 * tt + c] = t.slice[tt][i];
     t.x2n[0] = 1u << 30;  // x^1
     for (int k = 1; k < 64; k++) t.x2n[k] = h_multmodp(t.x2n[k - 1], t.x2n[k - 1]);
     for (int lvl = 0; lvl < 11; lvl++) {
@@ -910,7 +913,7 @@ size_t dec_layout(const DPlan& P, int n, size_t* o, uint64_t ring_bytes) {
     o[D_LARGE] = a.take<uint32_t>(P.nrec + 2);   // k_classify: count | record slots
     o[D_TC] = a.take<uint32_t>(P.ntile + 1);
     o[D_MAPS] = a.take<uint32_t>(P.nchunk + P.nrec + P.ntile + 3);   // chunk2seg | rec2seg | tile2win
-    o[D_PAIRS] = a.take<uint32_t>(P.nrec / 2 + 4);   // k_pairs: count | ticket | pad | pad | low-plane record slots
+    o[D_PAIRS] = a.take<uint32_t>(P.nrec + P.nrec / 2 + 8);   // k_pairs: ctl[4] | pairs | singles
     o[D_RING] = a.take<uint8_t>(ring_bytes + 256);
     o[D_SCR] = a.take<uint8_t>(P.scratch + 64);
     return a.off + 256;
@@ -990,14 +993,17 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         }
         { PROF(k_resolve); k_resolve<<<(unsigned)std::min<uint64_t>(nseg, 148 * 2), kThreads, kResSmem, st>>>(
             d_seg, nseg, d_cand, d_ccnt, d_cpre, d_scnt, d_sfail, d_rpos, d_rnext); }
-        PROF(k_decrec);
         // the split pays off inside CUDA graphs (plans); launched eagerly the
         // two kernels overlap worse than one, so eager calls take one launch
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         CK(cudaStreamIsCapturing(st, &cap));
-        if (nrec < kDecSplitFrom || cap != cudaStreamCaptureStatusActive) {
+        if (ctx->fuse) {
+            // k_decpair takes every record: fused pairs, then the records of the other windows
+        } else if (nrec < kDecSplitFrom || cap != cudaStreamCaptureStatusActive) {
+            PROF(k_decrec);
             k_decrec<<<(unsigned)nrec, kThreads, dsm, st>>>(d_seg, d_r2s, d_win, nrec, d_sfail, d_rpos, d_scr, 0);
         } else {
+            PROF(k_decrec);
             // records whose payload does not stage in kStageSmall are listed and
             // decoded by persistent CTAs (3 per SM) on the side stream while the
             // rest run at 4 CTAs per SM
@@ -1019,10 +1025,12 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         if (ctx->fuse) {
             PROF(k_decpair);
             CK(cudaMemsetAsync(d_pairs, 0, 4 * sizeof(uint32_t), st));
-            k_pairs<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, nrec, d_win, d_sfail, d_pairs + 4, d_pairs);
-            k_decpair<<<(unsigned)ctx->pair_grid, kThreads, dsm_small, st>>>(d_seg, d_r2s, d_win, d_pairs + 4, d_pairs, d_sfail,
-                                                                            d_rpos, d_ring, static_cast<uint8_t*>(d_out),
-                                                                            ctx->d_crc, ctx->d_sh992, d_tc);
+            uint32_t* d_plist = d_pairs + 4;
+            uint32_t* d_slist = d_plist + nrec / 2 + 2;
+            k_pairs<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, nrec, d_win, d_sfail, d_plist, d_slist, d_pairs);
+            k_decpair<<<(unsigned)ctx->pair_grid, kThreads, dsm_small, st>>>(d_seg, d_r2s, d_win, d_plist, d_slist, d_pairs,
+                                                                            d_sfail, d_rpos, d_ring, static_cast<uint8_t*>(d_out),
+                                                                            ctx->d_crc, ctx->d_sh992, d_tc, d_scr);
         }
     }
     if (nseg) {

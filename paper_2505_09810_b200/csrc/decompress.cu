@@ -252,7 +252,7 @@ constexpr int kStageSmall = 30720, kStageLarge = 40960;
 constexpr int kCheckpoints = 3;  // at 128, 256 and 512 bits into a chunk
 
 struct DecSmem {
-    uint32_t lut3[1 << kLut];           // n(2)|tl(4)|pad(2)|s3(8)|s2(8)|s1(8); n == 0: slow path
+    uint32_t lut3[1 << kLut];           // tl(4)|pad(2)|n(2)|s3(8)|s2(8)|s1(8); 0: slow path (long or invalid prefix)
     uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0
     uint8_t lutc[1 << kCntLut];         // count passes: n(4) | tl(4) of the whole codewords in a 12-bit window
     uint32_t bm[2][kThreads];           // pass-0 boundary bitmaps (first 64 bits of each chunk)
@@ -434,7 +434,11 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         // the 64-bit bitmap
 #pragma unroll 1
         for (int k = 0; k < kCheckpoints; k++) {
-            const uint32_t T = p0 + (128u << k);
+            // pass 0 (bm == 1) records the first boundary at or after p0 + (128 << k);
+            // a fix-up path (bm == 2) walks to the recorded boundary (whichever pass 0
+            // recorded it) and is synchronised iff it lands on it
+            const uint32_t cpk = bm == 2 ? s.cp[k][tid] : 0u;
+            const uint32_t T = bm == 2 ? (cpk == ~0u ? lim : p0 + (cpk >> 16)) : p0 + (128u << k);
             const bool on = bm != 0 && !bad && !done && T < lim;
             constexpr int kCW = RUN ? kLut : kCntLut;
             bool a2 = on && pos + kCW <= T;
@@ -444,7 +448,7 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
                     uint32_t n, tl;
                     if (RUN) {
                         const uint32_t e = s.lut3[wv >> (32 - kLut)];
-                        n = e >> 30; tl = (e >> 26) & 15;
+                        n = (e >> 24) & 3; tl = e >> 28;
                     } else {
                         const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
                         n = e >> 4; tl = e & 15;
@@ -516,7 +520,7 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         PackT packed = 0;
         if (EMIT) {
             const uint32_t e = s.lut3[wv >> (32 - kLut)];
-            n = e >> 30; tl = (e >> 26) & 15; packed = e & 0xFFFFFF;
+            n = (e >> 24) & 3; tl = e >> 28; packed = e & 0xFFFFFF;
             if (run1) {   // up to 8 run symbols: one 8-byte store at most
                 const uint32_t z = min((uint32_t)__clz(wv), 8u);
                 if (z > n) { n = z; tl = z; packed = rep8 >> (64 - 8 * z); }
@@ -524,7 +528,7 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         } else {
             if (RUN) {   // counting with the 3-symbol table (run records build no count LUT)
                 const uint32_t e = s.lut3[wv >> (32 - kLut)];
-                n = e >> 30; tl = (e >> 26) & 15;
+                n = (e >> 24) & 3; tl = e >> 28;
             } else {
                 const uint32_t e = s.lutc[wv >> (32 - kCntLut)];
                 n = e >> 4; tl = e & 15;
@@ -596,6 +600,194 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
     return bad ? ~0u : pos;
 }
 
+// ------------------------------------------------ lean passes (staged, no 1-bit code)
+// Records whose payload is staged in shared memory and whose code has no
+// 1-bit codeword (the weight exponent planes) take these loops: a two-word
+// register bit buffer refilled branch-free after every lookup, K table
+// lookups per warp vote, no branch per lookup (a window whose first codeword
+// is longer than the table, or invalid, reads entry 0: the lookups of that
+// lane consume nothing and one codeword is decoded by step1 after the vote),
+// inactive lanes mask their lookups to no-ops.
+struct BitBuf {
+    uint32_t hi, lo, boff, j;   // window = funnelshift_l(lo, hi, boff); sw[j] is the next word
+};
+__device__ __forceinline__ void bb_init(BitBuf& b, const uint32_t* sw, uint32_t a) {
+    b.j = a >> 5;
+    b.boff = a & 31;
+    b.hi = sw[b.j];
+    b.lo = sw[b.j + 1];
+    b.j += 2;
+}
+__device__ __forceinline__ uint32_t bb_win(const BitBuf& b) { return __funnelshift_l(b.lo, b.hi, b.boff); }
+__device__ __forceinline__ void bb_adv(BitBuf& b, const uint32_t* sw, uint32_t l) {   // l <= 32
+    b.boff += l;
+    const bool rf = b.boff >= 32;
+    const uint32_t nw = sw[b.j];
+    b.hi = rf ? b.lo : b.hi;
+    b.lo = rf ? nw : b.lo;
+    b.j += rf ? 1u : 0u;
+    b.boff -= rf ? 32u : 0u;
+}
+
+// Pass 0 of one chunk [p0, lim): the codeword boundaries of its first 64
+// bits into the bitmap, checkpoints (the first lookup end at or after
+// p0 + 128 / 256 / 512 bits, with the symbol count there) for the fix-up
+// rounds, and the count.  Returns the first boundary >= lim (~0u: invalid).
+template <int K>
+__device__ __forceinline__ uint32_t pass0_lean(DecSmem& s, const uint32_t* sw, uint32_t sh, uint32_t p0, uint32_t lim,
+                                               uint32_t& count) {
+    constexpr unsigned mask = 0xFFFFFFFFu;   // called by every thread (an empty chunk: p0 == lim)
+    const int tid = threadIdx.x;
+    BitBuf b;
+    bb_init(b, sw, p0 + sh);
+    uint32_t pos = p0, c = 0, m0 = 0, m1 = 0;
+    bool bad = false;
+    const uint32_t la = min(lim, p0 + 64);
+    bool act = pos < la;
+    while (__any_sync(mask, act)) {
+        if (act) {
+            uint32_t sym;
+            const uint32_t l = step1(s, bb_win(b), sym);
+            bad = l == 0;
+            bb_adv(b, sw, l);
+            pos += l;
+            c += l ? 1u : 0u;
+            const uint32_t rel = pos - p0;
+            if (l && rel < 32) m0 |= 1u << rel;
+            else if (l && rel < 64) m1 |= 1u << (rel - 32);
+            act = !bad && pos < la;
+        }
+    }
+    s.bm[0][tid] = m0;
+    s.bm[1][tid] = m1;
+    uint32_t k = 0, T = p0 + 128;
+    auto bulk = [&](auto kk) {
+        constexpr int KK = decltype(kk)::value;
+        bool a = !bad && pos + KK * kCntLut <= lim;
+        while (__any_sync(mask, a)) {
+            uint32_t tl = 0;
+#pragma unroll
+            for (int q = 0; q < KK; q++) {
+                const uint32_t e = a ? (uint32_t)s.lutc[bb_win(b) >> (32 - kCntLut)] : 0u;
+                tl = e & 15;
+                c += e >> 4;
+                pos += tl;
+                bb_adv(b, sw, tl);
+            }
+            const bool st = a && tl == 0;   // a long (or invalid) codeword at the window
+            if (__any_sync(mask, st)) {
+                if (st) {
+                    uint32_t sym;
+                    const uint32_t l = step1(s, bb_win(b), sym);
+                    bad = l == 0;
+                    bb_adv(b, sw, l);
+                    pos += l;
+                    c += l ? 1u : 0u;
+                }
+            }
+            if (a && k < kCheckpoints && pos >= T) {
+                s.cp[k][tid] = ((pos - p0) << 16) | c;
+                k++;
+                T = p0 + (128u << k);
+            }
+            a = !bad && pos + KK * kCntLut <= lim;
+        }
+    };
+    bulk(std::integral_constant<int, K>());
+    bulk(std::integral_constant<int, 1>());
+    act = !bad && pos < lim;
+    while (__any_sync(mask, act)) {
+        if (act) {
+            uint32_t sym;
+            const uint32_t l = step1(s, bb_win(b), sym);
+            bad = l == 0;
+            bb_adv(b, sw, l);
+            pos += l;
+            c += l ? 1u : 0u;
+            act = !bad && pos < lim;
+        }
+    }
+    count = c;
+    return bad ? ~0u : pos;
+}
+
+// Emit pass of one chunk: the codewords starting in [pos, lim) (validated by
+// pass 0 and the fix-up rounds) as symbols at dst.  Up to three symbols per
+// lookup are packed into a 32-bit accumulator that leaves with 4-byte stores.
+template <int K>
+__device__ __forceinline__ void emit_lean(DecSmem& s, const uint32_t* sw, uint32_t sh, uint32_t pos, uint32_t lim,
+                                          uint8_t* dst) {
+    constexpr unsigned mask = 0xFFFFFFFFu;   // called by every thread (nothing to emit: pos == lim)
+    BitBuf b;
+    bb_init(b, sw, pos + sh);
+    uint8_t* d = dst;
+    // head: single symbols until the destination is 4-byte aligned
+    bool act = pos < lim && (reinterpret_cast<uint64_t>(d) & 3);
+    while (__any_sync(mask, act)) {
+        if (act) {
+            uint32_t sym;
+            const uint32_t l = step1(s, bb_win(b), sym);
+            bb_adv(b, sw, l);
+            pos += l;
+            *d++ = (uint8_t)sym;
+            act = l && pos < lim && (reinterpret_cast<uint64_t>(d) & 3);
+        }
+    }
+    uint32_t* w = reinterpret_cast<uint32_t*>(d);
+    uint32_t acc = 0, nb = 0;   // accumulated bits (0, 8, 16 or 24)
+    auto put = [&](uint32_t packed, uint32_t nbits) {   // packed: up to 3 symbols, nbits = 8 * count
+        acc |= packed << nb;
+        const uint32_t ovf = __funnelshift_lc(packed, 0u, nb);   // the bytes beyond the word (packed >> (32 - nb))
+        nb += nbits;
+        const bool full = nb >= 32;
+        if (full) *w = acc;
+        w += full ? 1 : 0;
+        acc = full ? ovf : acc;
+        nb -= full ? 32u : 0u;
+    };
+    auto bulk = [&](auto kk) {
+        constexpr int KK = decltype(kk)::value;
+        bool a = pos + KK * kLut <= lim;
+        while (__any_sync(mask, a)) {
+            uint32_t tl = 0;
+#pragma unroll
+            for (int q = 0; q < KK; q++) {
+                const uint32_t e = a ? s.lut3[bb_win(b) >> (32 - kLut)] : 0u;
+                tl = e >> 28;
+                pos += tl;
+                bb_adv(b, sw, tl);
+                put(e & 0xFFFFFF, (e >> 21) & 0x18);
+            }
+            const bool st = a && tl == 0;   // a codeword longer than the table
+            if (__any_sync(mask, st)) {
+                if (st) {
+                    uint32_t sym;
+                    const uint32_t l = step1(s, bb_win(b), sym);
+                    bb_adv(b, sw, l);
+                    pos += l;
+                    put(sym, 8);
+                }
+            }
+            a = pos + KK * kLut <= lim;
+        }
+    };
+    bulk(std::integral_constant<int, K>());   // (every lane of the mask runs the votes)
+    bulk(std::integral_constant<int, 1>());
+    act = pos < lim;
+    while (__any_sync(mask, act)) {
+        if (act) {
+            uint32_t sym;
+            const uint32_t l = step1(s, bb_win(b), sym);
+            bb_adv(b, sw, l);
+            pos += l;
+            put(sym, 8);
+            act = l && pos < lim;
+        }
+    }
+    uint8_t* tb = reinterpret_cast<uint8_t*>(w);
+    for (uint32_t q = 0; q < nb / 8; q++) tb[q] = (uint8_t)(acc >> (8 * q));
+}
+
 // All passes over the chunks of one record (see huff_decode).
 template <bool STAGED, bool RUN>
 __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t bits, uint32_t len, uint8_t* dst) {
@@ -612,7 +804,22 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
     DBG_T0(t_p0);
 #pragma unroll
     for (int k = 0; k < kCheckpoints; k++) s.cp[k][tid] = ~0u;
-    if (c < nch) {
+    if (STAGED && !RUN) {
+        // the lean loops vote over full warps: every thread runs them, empty chunks as [0, 0)
+        if (c < nch) {
+            p0 = c * S;
+            if (gq > 1) p0 = ((p0 + gq - 1) / gq) * gq;
+            my_start = p0;
+        }
+        const bool work = c < nch && my_start < lim;
+        uint32_t cnt = 0;
+        const uint32_t e = pass0_lean<2>(s, src.sw, src.sh, work ? my_start : 0u, work ? lim : 0u, cnt);
+        if (c < nch) {
+            my_end = work ? e : my_start;
+            my_cnt = cnt;
+            s.end[c] = my_end;
+        }
+    } else if (c < nch) {
         p0 = c * S;
         if (gq > 1) p0 = ((p0 + gq - 1) / gq) * gq;
         my_start = p0;
@@ -685,7 +892,10 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
     DBG_TADD(19, t_fix);
     if (bad) return false;
     DBG_T0(t_emit);
-    if (c < nch && my_cnt) {
+    if (STAGED && !RUN) {
+        const bool has = c < nch && my_cnt;
+        emit_lean<2>(s, src.sw, src.sh, has ? my_start : 0u, has ? lim : 0u, dst + (has ? pre + incl - v : 0u));
+    } else if (c < nch && my_cnt) {
         uint32_t cc;
         decode_span<true, STAGED, RUN>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
     }
@@ -734,6 +944,10 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     const uint64_t e16 = (reinterpret_cast<uint64_t>(data0) + ((uint64_t)bits0 + 7) / 8 + 15) & ~15ull;
     const bool staged = bits0 != 0 && e16 - a16 <= (uint64_t)stage_cap;
     if (staged && tid == 0) {
+        // the staging area was last written through the generic proxy (byte
+        // swaps, k_decpair's CRC tables): order those writes before the bulk
+        // copy's async-proxy writes (the __syncthreads above ordered the CTA's)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_init1(&s.mbar);
         tma_load_1d(s.bits, reinterpret_cast<const void*>(a16), (uint32_t)(e16 - a16), &s.mbar);
     }
@@ -806,17 +1020,22 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     G.nwords_full = G.glimit / 4;
     __syncthreads();
     // single-symbol LUT over kLut-bit prefixes
-    for (int e = tid; e < (1 << kLut); e += kThreads) {
-        const uint32_t v = (uint32_t)e << (kMaxLen - kLut);
-        uint16_t ent = 0;
-        for (int q = s.minlen; q <= min(s.maxlen, kLut); q++) {
-            const uint32_t fl = s.first_left[q], endq = fl + (s.bl_count[q] << (kMaxLen - q));
-            if (v < endq) {
-                if (v >= fl) ent = (uint16_t)((q << 8) | s.csym[s.first_idx[q] + ((v - fl) >> (kMaxLen - q))]);
-                break;
+    // (canonical codes of one length occupy one interval of the code space,
+    // the intervals in length order: a thread's increasing entries walk the
+    // lengths forward once)
+    {
+        const int qmax = min(s.maxlen, kLut);
+        int q = s.minlen;
+        uint32_t fl = 0, endq = 0, base = 0;
+        if (q <= qmax) { fl = s.first_left[q]; endq = fl + (s.bl_count[q] << (kMaxLen - q)); base = s.first_idx[q]; }
+        for (int e = tid; e < (1 << kLut); e += kThreads) {
+            const uint32_t v = (uint32_t)e << (kMaxLen - kLut);
+            while (q <= qmax && v >= endq) {
+                q++;
+                if (q <= qmax) { fl = s.first_left[q]; endq = fl + (s.bl_count[q] << (kMaxLen - q)); base = s.first_idx[q]; }
             }
+            s.lut1[e] = q <= qmax ? (uint16_t)((q << 8) | s.csym[base + ((v - fl) >> (kMaxLen - q))]) : (uint16_t)0;
         }
-        s.lut1[e] = ent;
     }
     __syncthreads();
     // three-symbol LUT: greedy codewords fully inside the kLut-bit prefix
@@ -832,7 +1051,7 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
             tl += la;
             rest = (uint32_t)e << tl;
         }
-        if (n) ent = (n << 30) | (tl << 26) | syms;
+        if (n) ent = (tl << 28) | (n << 24) | syms;
         s.lut3[e] = ent;
     }
     // count LUT: every whole codeword of a 12-bit window (greedy, continued
@@ -842,7 +1061,7 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     if (!s.bl_count[1])
     for (int e = tid; e < (1 << kCntLut); e += kThreads) {
         const uint32_t e3 = s.lut3[e >> (kCntLut - kLut)];
-        uint32_t n = e3 >> 30, tl = (e3 >> 26) & 15;
+        uint32_t n = (e3 >> 24) & 3, tl = e3 >> 28;
         for (;;) {
             const uint32_t rest = ((uint32_t)e << tl) & ((1u << kCntLut) - 1);
             const uint32_t a = s.lut1[rest >> (kCntLut - kLut)];
@@ -1290,7 +1509,8 @@ __device__ __forceinline__ void decrec_one(DecSmem& s, const DecSeg* __restrict_
                                            const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ scratch,
                                            bool skip_large, uint32_t stage_cap) {
     const uint32_t lo = rec2seg[g];
-    if (lo == ~0u || seg_fail[lo]) return;
+    if (lo == ~0u) return;
+    if (__syncthreads_or(threadIdx.x == 0 && seg_fail[lo])) return;   // (one read: another CTA may be setting it)
     const DecSeg sg = segs[lo];
     if (wins[sg.win].fuse) return;   // (k_decpair has it)
     const uint32_t r = (uint32_t)(g - sg.rec0);
@@ -1359,37 +1579,50 @@ __global__ void k_classify(const DecSeg* __restrict__ segs, const uint32_t* __re
 // the record, RLE planes are one byte; then the CTA writes the interleaved
 // output with 16-byte streaming stores (XOR of the previous step for
 // lmcg_decompress_apply) and folds the raw CRC-32 of each 32 KiB tile from the
-// registers (byte table, 32-fold replicated so lane l reads its own bank, laid
-// over the decoder's shared memory).  No grouped scratch, no k_ungroup pass:
+// registers (slice-by-4 in the conflict-free 32 KiB layout rep4x8, laid over
+// the decoder's shared memory).  No grouped scratch, no k_ungroup pass:
 // decompress moves the stream once and the output once.  Any failure (a
 // segment of the window that failed discovery, or a record that does not
 // decode) marks every segment of the window failed, so k_fallback re-walks it
 // into scratch and k_ungroup assembles it: the authoritative path decides.
 constexpr uint32_t kPairRing = 2 * 65536;   // ring bytes per k_decpair CTA: low | high plane
-constexpr int kCrcRep1Words = 256 * 32;     // byte table, entry i of copy l at [32 i + l]
+constexpr int kCrcRepWords = 256 * 32;      // CrcTables::rep4x8 in shared memory
 
-// k_decpair's work list: the low-plane record slots of fused windows
-// (ctl[0] = count, ctl[1] = k_decpair's ticket).
+// k_decpair's work lists: the low-plane record slots of fused windows
+// (pairs) and the records of the other windows (singles, decoded into the
+// grouped scratch for k_ungroup).  ctl[0] = pairs, ctl[1] = k_decpair's
+// ticket, ctl[2] = singles.
+__device__ __forceinline__ void warp_append(bool is, uint32_t v, uint32_t* list, uint32_t* counter) {
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, is);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == lead) base = atomicAdd(counter, (uint32_t)__popc(m));
+    base = __shfl_sync(0xFFFFFFFFu, base, lead);
+    if (is) list[base + __popc(m & ((1u << lane) - 1))] = v;
+}
 __global__ void k_pairs(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg, uint64_t nrec_total,
                         const DecWin* __restrict__ wins, const uint32_t* __restrict__ seg_fail,
-                        uint32_t* __restrict__ list, uint32_t* __restrict__ ctl) {
+                        uint32_t* __restrict__ pairs, uint32_t* __restrict__ singles, uint32_t* __restrict__ ctl) {
     const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    bool is = false;
+    bool is_pair = false, is_single = false;
     if (g < nrec_total) {
         const uint32_t lo = rec2seg[g];
         if (lo != ~0u) {
             const uint32_t wi = segs[lo].win;
             const uint32_t B = segs[lo].block;
-            if (wins[wi].fuse) is = (g - wins[wi].rec0) < wins[wi].n / B;
+            if (wins[wi].fuse) is_pair = (g - wins[wi].rec0) < wins[wi].n / B;
+            else is_single = !seg_fail[lo];
         }
     }
-    const unsigned m = __ballot_sync(0xFFFFFFFFu, is);
-    if (!m) return;
-    const int lane = threadIdx.x & 31, lead = __ffs(m) - 1;
-    uint32_t base = 0;
-    if (lane == lead) base = atomicAdd(&ctl[0], (uint32_t)__popc(m));
-    base = __shfl_sync(0xFFFFFFFFu, base, lead);
-    if (is) list[base + __popc(m & ((1u << lane) - 1))] = (uint32_t)g;
+    warp_append(is_pair, (uint32_t)g, pairs, &ctl[0]);
+    warp_append(is_single, (uint32_t)g, singles, &ctl[2]);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {   // TMA prefetch into L2
+    const uint64_t a = reinterpret_cast<uint64_t>(p) & ~15ull;
+    const uint64_t e = (reinterpret_cast<uint64_t>(p) + bytes + 15) & ~15ull;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
 }
 
 // 16 plane bytes at element offset e (a multiple of 16) of a pair's plane
@@ -1415,37 +1648,43 @@ __device__ __forceinline__ uint4 plane16(const uint8_t* p, uint32_t mode, uint32
                       __funnelshift_r(x3, x4, sh));
 }
 
-// raw CRC of one little-endian word, byte by byte through the replicated table
-__device__ __forceinline__ uint32_t crc_word_rep1(const uint32_t* __restrict__ tl, uint32_t crc, uint32_t w) {
-    uint32_t c = crc ^ w;
-#pragma unroll
-    for (int b = 0; b < 4; b++) c = (c >> 8) ^ tl[(c & 0xFF) * 32];
-    return c;
-}
 
 __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restrict__ segs, const uint32_t* __restrict__ rec2seg,
                                                     const DecWin* __restrict__ wins, const uint32_t* __restrict__ list,
-                                                    uint32_t* __restrict__ ctl, uint32_t* __restrict__ seg_fail,
+                                                    const uint32_t* __restrict__ singles, uint32_t* __restrict__ ctl,
+                                                    uint32_t* __restrict__ seg_fail,
                                                     const uint64_t* __restrict__ rec_pos, uint8_t* __restrict__ ring,
                                                     uint8_t* out /* may alias a window's prev */,
                                                     const CrcTables* __restrict__ ct, const uint32_t* __restrict__ sh992,
-                                                    uint32_t* __restrict__ tile_crc) {
+                                                    uint32_t* __restrict__ tile_crc, uint8_t* __restrict__ scratch) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     DecSmem& s = *reinterpret_cast<DecSmem*>(smem_raw);
-    uint32_t* crctab = reinterpret_cast<uint32_t*>(smem_raw);   // after the decode: byte table | 992-byte shift
-    uint32_t* st992 = crctab + kCrcRep1Words;
+    uint32_t* crctab = reinterpret_cast<uint32_t*>(smem_raw);   // after the decode: rep4x8 | 992-byte shift
+    uint32_t* st992 = crctab + kCrcRepWords;
     __shared__ uint32_t sh_p;
     __shared__ uint32_t wcrc[kWarps];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     uint8_t* slot = ring + (uint64_t)blockIdx.x * kPairRing;
-    const uint32_t npairs = ctl[0];
-    const uint32_t* tl = crctab + lane;
+    const uint32_t npairs = ctl[0], nsingles = ctl[2];
+    Crc4x8Lane cl;
+    cl.init(crctab, lane);
     for (;;) {
         __syncthreads();   // the previous pair is done with sh_p and the shared memory
         if (tid == 0) sh_p = atomicAdd(&ctl[1], 1u);
         __syncthreads();
         const uint32_t p = sh_p;
-        if (p >= npairs) break;
+        if (p >= npairs + nsingles) break;
+        if (p >= npairs) {   // a record of a window that is not fused: into the grouped scratch (as k_decrec)
+            const uint64_t g = singles[p - npairs];
+            const uint32_t lo = rec2seg[g];
+            if (__syncthreads_or(tid == 0 && seg_fail[lo])) continue;   // (one read: another CTA may be setting it)
+            const DecSeg sg = segs[lo];
+            const uint8_t* rec = sg.base + rec_pos[g];
+            const bool ok = decode_record(s, rec, rec[0], rd32(rec + 1), scratch + sg.goff + (g - sg.rec0) * sg.block,
+                                          kStageSmall);
+            if (!ok && tid == 0) atomicOr(&seg_fail[lo], 1u);
+            continue;
+        }
         const uint64_t gL = list[p];
         const DecSeg sgL = segs[rec2seg[gL]];
         const DecWin wd = wins[sgL.win];
@@ -1459,6 +1698,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restric
         const uint8_t* recL = ok ? sgL.base + rec_pos[gL] : nullptr;   // (record positions are valid once discovery passed)
         const uint8_t* recH = ok ? sgH.base + rec_pos[gH] : nullptr;
         const uint32_t mL = ok ? recL[0] : 0u, mH = ok ? recH[0] : 0u;
+        if (ok && tid == 0) {   // stored planes are read at the end of the pair: have them in L2 by then
+            if (mL == MODE_STORED) prefetch_l2(recL + 5, B);
+            if (mH == MODE_STORED) prefetch_l2(recH + 5, B);
+        }
         uint8_t* dL = slot;
         uint8_t* dH = slot + 65536;
         if (ok && mH == MODE_HUFFMAN) ok = huff_decode(s, recH + 5, B, dH, kStageSmall);
@@ -1470,7 +1713,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restric
         }
         __syncthreads();   // decoded planes visible to the CTA; the decoder's shared memory is free
         DBG_T0(t_tab);
-        for (int i = tid; i < kCrcRep1Words; i += kThreads) crctab[i] = __ldg(&ct->slice[0][i >> 5]);
+        for (int i = tid; i < kCrcRepWords / 4; i += kThreads)
+            reinterpret_cast<uint4*>(crctab)[i] = __ldg(reinterpret_cast<const uint4*>(ct->rep4x8) + i);
         for (int i = tid; i < 1024; i += kThreads) st992[i] = __ldg(sh992 + i);
         __syncthreads();
         DBG_TADD(23, t_tab);
@@ -1515,7 +1759,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restric
                 uint32_t x = ch[c];
                 if (r) x = st992[x & 0xFF] ^ st992[256 + ((x >> 8) & 0xFF)] ^ st992[512 + ((x >> 16) & 0xFF)] ^ st992[768 + (x >> 24)];
 #pragma unroll
-                for (int q = 0; q < 8; q++) x = crc_word_rep1(tl, x, v[q]);
+                for (int q = 0; q < 8; q++) x = cl.word(x, v[q]);
                 ch[c] = x;
             }
         }

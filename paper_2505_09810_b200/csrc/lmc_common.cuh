@@ -80,6 +80,34 @@ struct CrcTables {
     uint32_t shift[11][4][256];            // shift by (16 << lvl) bytes
     uint32_t x2n[64];
     uint32_t pow2[kPow2Levels][4][256];    // shift by 2^m bytes
+    // slice-by-4 tables for shared memory without bank conflicts in 32 KiB:
+    // slice[t][i] at rep4x8[32 i + 8 t + c] for c = 0..7.  Lane l = c + 8 g
+    // takes table t = (s + g) & 3 at its s-th lookup of a word, so the 32
+    // lanes of every lookup instruction read 32 different banks.
+    uint32_t rep4x8[256 * 32];
+};
+
+// Per-lane view of rep4x8 for one word: tab[s] = table base of lookup s
+// (column 8 t + c), sel[s] = byte-perm selector of the byte that pairs with
+// table t (byte 3 - t, zero-extended).
+struct Crc4x8Lane {
+    const uint32_t* tab[4];
+    uint32_t sel[4];
+    __device__ __forceinline__ void init(const uint32_t* smem_rep4x8, int lane) {
+        const int c = lane & 7, g = lane >> 3;
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+            const int t = (s + g) & 3;
+            tab[s] = smem_rep4x8 + 8 * t + c;
+            sel[s] = 0x4440u | (uint32_t)(3 - t);
+        }
+    }
+    // raw CRC after one little-endian word
+    __device__ __forceinline__ uint32_t word(uint32_t crc, uint32_t w) const {
+        const uint32_t x = crc ^ w;
+        return tab[0][__byte_perm(x, 0, sel[0]) * 32] ^ tab[1][__byte_perm(x, 0, sel[1]) * 32] ^
+               tab[2][__byte_perm(x, 0, sel[2]) * 32] ^ tab[3][__byte_perm(x, 0, sel[3]) * 32];
+    }
 };
 
 __device__ __forceinline__ uint32_t crc_word(const uint32_t* __restrict__ sl, uint32_t crc, uint32_t word) {
