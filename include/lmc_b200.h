@@ -221,12 +221,13 @@ int lmcg_build_codebooks(lmcg_ctx* ctx, const uint32_t* d_hists, int nhist, uint
 int64_t lmcg_block_info(lmcg_ctx* ctx, int32_t* modes, uint32_t* bits, uint32_t* record_sizes,
                         uint8_t* codebook_wire /* cap x 128 */, uint32_t* pm_flags, int64_t cap);
 
-/* Decode fusion switch (default on; environment LMCG_NOFUSE=1 starts a
- * context with it off).  On: two-plane windows with 16-64 KiB blocks are
+/* Decode fusion switch (default on from 16384 record slots; environment
+ * LMCG_NOFUSE=1 / LMCG_FUSE_FROM=n set the defaults of a new context).  On:
+ * in decodes of at least min_records record slots, two-plane windows with 16-64 KiB blocks are
  * decoded, byte-interleaved and CRC-checked in one pass (k_decpair) instead
  * of decode -> grouped scratch -> k_ungroup.  Output and errors are identical
  * either way; the switch exists so the tests exercise both paths. */
-int lmcg_set_decode_fusion(lmcg_ctx* ctx, int enable);
+int lmcg_set_decode_fusion(lmcg_ctx* ctx, int enable, uint64_t min_records);
 
 /* Measurement hooks (bench.py): bracket every kernel launch with CUDA events
  * while enabled; lmcg_profile_report synchronises, writes lines

@@ -104,7 +104,7 @@ def load(path: str = SO_PATH):
         L.lmcg_block_info.restype = ctypes.c_int64
         L.lmcg_block_info.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int64]
         L.lmcg_set_decode_fusion.restype = ctypes.c_int
-        L.lmcg_set_decode_fusion.argtypes = [vp, ctypes.c_int]
+        L.lmcg_set_decode_fusion.argtypes = [vp, ctypes.c_int, u64]
         L.lmcg_profile.restype = ctypes.c_int
         L.lmcg_profile.argtypes = [vp, ctypes.c_int]
         L.lmcg_profile_report.restype = ctypes.c_int64
@@ -141,9 +141,10 @@ class Context:
         if not self.ptr:
             raise DeviceError("lmcg_create failed")
 
-    def set_decode_fusion(self, enable: bool) -> None:
-        """Fused decode + ungroup + CRC (k_decpair) on or off; same bytes either way."""
-        self.check(self.lib.lmcg_set_decode_fusion(self.ptr, int(enable)))
+    def set_decode_fusion(self, enable: bool, min_records: int = 16384) -> None:
+        """Fused decode + ungroup + CRC (k_decpair) on or off (on: for decodes of at
+        least min_records record slots); same bytes and errors either way."""
+        self.check(self.lib.lmcg_set_decode_fusion(self.ptr, int(enable), int(min_records)))
 
     def profile(self, enable: bool) -> None:
         self.lib.lmcg_profile(self.ptr, int(enable))

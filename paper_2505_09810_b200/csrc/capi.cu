@@ -62,6 +62,7 @@ struct lmcg_ctx {
     bool res_attr = false;
     int pair_grid = 0;                    // persistent k_decpair CTAs (each owns a kPairRing slot)
     bool fuse = true;                     // fused decode + ungroup + CRC (k_decpair) for eligible windows
+    uint64_t fuse_from = 16384;           // ... in decodes of at least this many record slots (LMCG_FUSE_FROM)
     uint32_t* d_sh992 = nullptr;
     int crc_occ = 1;
     bool enc_attr = false;
@@ -334,6 +335,7 @@ lmcg_ctx* lmcg_create(int device) {
     if (const char* e = getenv("LMCG_SERIAL")) ctx->serial = e[0] == '1';
     if (const char* e = getenv("LMCG_CRC_FORK")) ctx->crc_fork = atoi(e);
     if (const char* e = getenv("LMCG_NOFUSE")) ctx->fuse = e[0] != '1';
+    if (const char* e = getenv("LMCG_FUSE_FROM")) ctx->fuse_from = strtoull(e, nullptr, 10);
     return ctx;
 }
 
@@ -729,9 +731,10 @@ void lmcg_plan_destroy(lmcg_plan* pl) {
     delete pl;
 }
 
-int lmcg_set_decode_fusion(lmcg_ctx* ctx, int enable) {
+int lmcg_set_decode_fusion(lmcg_ctx* ctx, int enable, uint64_t min_records) {
     if (!ctx) return LMCG_ERR_ARGUMENT;
     ctx->fuse = enable != 0;
+    ctx->fuse_from = min_records;
     return LMCG_OK;
 }
 
@@ -972,8 +975,11 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         ctx->dec_attr = true;
     }
     if (int r = ensure_pair_grid(ctx)) return r;
+    // fusion pays off when the pairs fill the persistent grid many times over;
+    // a small decode keeps more CTAs busy as record-per-CTA + k_ungroup
+    const bool fuse = ctx->fuse && nrec >= ctx->fuse_from;
     { PROF(k_parse); k_parse<<<(n + 127) / 128, 128, 0, st>>>(d_in, d_caps, n, d_sout, d_win, d_seg,
-                                                            static_cast<const uint8_t*>(d_out), ctx->fuse ? 1 : 0); }
+                                                            static_cast<const uint8_t*>(d_out), fuse ? 1 : 0); }
     CK(cudaMemsetAsync(d_c2s, 0xFF, (nchunk + nrec + ntile + 3) * sizeof(uint32_t), st));
     if (nseg + nwin) { PROF(k_maps); k_maps<<<(unsigned)(nseg + nwin), 256, 0, st>>>(d_seg, nseg, d_win, nwin, d_c2s, d_r2s, d_t2w); }
     if (nchunk) { PROF(k_cand); k_cand<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, d_c2s, nchunk, d_cand, d_ccnt, d_ctot); }
@@ -997,7 +1003,7 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
         // two kernels overlap worse than one, so eager calls take one launch
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
         CK(cudaStreamIsCapturing(st, &cap));
-        if (ctx->fuse) {
+        if (fuse) {
             // k_decpair takes every record: fused pairs, then the records of the other windows
         } else if (nrec < kDecSplitFrom || cap != cudaStreamCaptureStatusActive) {
             PROF(k_decrec);
@@ -1022,7 +1028,7 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
                 CK(cudaStreamWaitEvent(st, ctx->djoin_ev, 0));
             }
         }
-        if (ctx->fuse) {
+        if (fuse) {
             PROF(k_decpair);
             CK(cudaMemsetAsync(d_pairs, 0, 4 * sizeof(uint32_t), st));
             uint32_t* d_plist = d_pairs + 4;

@@ -629,7 +629,7 @@ __device__ __forceinline__ void bb_adv(BitBuf& b, const uint32_t* sw, uint32_t l
     b.boff -= rf ? 32u : 0u;
 }
 
-// Pass 0 of one chunk [p0, lim): the codeword boundaries of its first 64
+// Pass 0 of one chunk [p0, lim): the codeword boundaries of its first 32
 // bits into the bitmap, checkpoints (the first lookup end at or after
 // p0 + 128 / 256 / 512 bits, with the symbol count there) for the fix-up
 // rounds, and the count.  Returns the first boundary >= lim (~0u: invalid).
@@ -642,7 +642,9 @@ __device__ __forceinline__ uint32_t pass0_lean(DecSmem& s, const uint32_t* sw, u
     bb_init(b, sw, p0 + sh);
     uint32_t pos = p0, c = 0, m0 = 0, m1 = 0;
     bool bad = false;
-    const uint32_t la = min(lim, p0 + 64);
+    // (32 bits: the weight planes resynchronise within 20 bits; longer paths
+    // meet a checkpoint)
+    const uint32_t la = min(lim, p0 + 32);
     bool act = pos < la;
     while (__any_sync(mask, act)) {
         if (act) {
@@ -654,7 +656,6 @@ __device__ __forceinline__ uint32_t pass0_lean(DecSmem& s, const uint32_t* sw, u
             c += l ? 1u : 0u;
             const uint32_t rel = pos - p0;
             if (l && rel < 32) m0 |= 1u << rel;
-            else if (l && rel < 64) m1 |= 1u << (rel - 32);
             act = !bad && pos < la;
         }
     }
@@ -813,7 +814,7 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
         }
         const bool work = c < nch && my_start < lim;
         uint32_t cnt = 0;
-        const uint32_t e = pass0_lean<2>(s, src.sw, src.sh, work ? my_start : 0u, work ? lim : 0u, cnt);
+        const uint32_t e = pass0_lean<3>(s, src.sw, src.sh, work ? my_start : 0u, work ? lim : 0u, cnt);
         if (c < nch) {
             my_end = work ? e : my_start;
             my_cnt = cnt;
@@ -894,7 +895,7 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
     DBG_T0(t_emit);
     if (STAGED && !RUN) {
         const bool has = c < nch && my_cnt;
-        emit_lean<2>(s, src.sw, src.sh, has ? my_start : 0u, has ? lim : 0u, dst + (has ? pre + incl - v : 0u));
+        emit_lean<3>(s, src.sw, src.sh, has ? my_start : 0u, has ? lim : 0u, dst + (has ? pre + incl - v : 0u));
     } else if (c < nch && my_cnt) {
         uint32_t cc;
         decode_span<true, STAGED, RUN>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
@@ -1663,51 +1664,69 @@ __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restric
     uint32_t* st992 = crctab + kCrcRepWords;
     __shared__ uint32_t sh_p;
     __shared__ uint32_t wcrc[kWarps];
+    // the pair's descriptor, set up by thread 0 (nothing of it stays in
+    // registers across the decoder calls)
+    struct PairInfo {
+        const uint8_t* rec[2];   // low, high record
+        const uint8_t* prev;
+        uint64_t ooff, tile0, k, seg0;
+        uint32_t mode[2], B, nseg, ok;
+    };
+    __shared__ PairInfo pi;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    uint8_t* slot = ring + (uint64_t)blockIdx.x * kPairRing;
-    const uint32_t npairs = ctl[0], nsingles = ctl[2];
-    Crc4x8Lane cl;
-    cl.init(crctab, lane);
     for (;;) {
         __syncthreads();   // the previous pair is done with sh_p and the shared memory
         if (tid == 0) sh_p = atomicAdd(&ctl[1], 1u);
         __syncthreads();
         const uint32_t p = sh_p;
-        if (p >= npairs + nsingles) break;
+        const uint32_t npairs = ctl[0];
+        if (p >= npairs + ctl[2]) break;
         if (p >= npairs) {   // a record of a window that is not fused: into the grouped scratch (as k_decrec)
             const uint64_t g = singles[p - npairs];
             const uint32_t lo = rec2seg[g];
             if (__syncthreads_or(tid == 0 && seg_fail[lo])) continue;   // (one read: another CTA may be setting it)
-            const DecSeg sg = segs[lo];
+            const DecSeg& sg = segs[lo];
             const uint8_t* rec = sg.base + rec_pos[g];
             const bool ok = decode_record(s, rec, rec[0], rd32(rec + 1), scratch + sg.goff + (g - sg.rec0) * sg.block,
                                           kStageSmall);
             if (!ok && tid == 0) atomicOr(&seg_fail[lo], 1u);
             continue;
         }
-        const uint64_t gL = list[p];
-        const DecSeg sgL = segs[rec2seg[gL]];
-        const DecWin wd = wins[sgL.win];
-        const uint32_t B = sgL.block;
-        const uint64_t np = wd.n / B, k = gL - wd.rec0;
-        const uint64_t gH = gL + np;
-        const DecSeg sgH = segs[rec2seg[gH]];
-        bool f = false;
-        for (uint32_t i = tid; i < wd.nseg; i += kThreads) f |= seg_fail[wd.seg0 + i] != 0;
-        bool ok = !__syncthreads_or(f);
-        const uint8_t* recL = ok ? sgL.base + rec_pos[gL] : nullptr;   // (record positions are valid once discovery passed)
-        const uint8_t* recH = ok ? sgH.base + rec_pos[gH] : nullptr;
-        const uint32_t mL = ok ? recL[0] : 0u, mH = ok ? recH[0] : 0u;
-        if (ok && tid == 0) {   // stored planes are read at the end of the pair: have them in L2 by then
-            if (mL == MODE_STORED) prefetch_l2(recL + 5, B);
-            if (mH == MODE_STORED) prefetch_l2(recH + 5, B);
+        if (tid == 0) {
+            const uint64_t gL = list[p];
+            const DecSeg& sgL = segs[rec2seg[gL]];
+            const DecWin& wd = wins[sgL.win];
+            const uint32_t B = sgL.block;
+            const uint64_t gH = gL + wd.n / B;
+            const DecSeg& sgH = segs[rec2seg[gH]];
+            pi.rec[0] = sgL.base + rec_pos[gL];
+            pi.rec[1] = sgH.base + rec_pos[gH];
+            pi.prev = wd.prev;
+            pi.ooff = wd.ooff;
+            pi.tile0 = wd.tile0;
+            pi.k = gL - wd.rec0;
+            pi.seg0 = wd.seg0;
+            pi.nseg = wd.nseg;
+            pi.B = B;
         }
-        uint8_t* dL = slot;
-        uint8_t* dH = slot + 65536;
-        if (ok && mH == MODE_HUFFMAN) ok = huff_decode(s, recH + 5, B, dH, kStageSmall);
-        if (ok && mL == MODE_HUFFMAN) ok = huff_decode(s, recL + 5, B, dL, kStageSmall);
+        __syncthreads();
+        bool f = false;
+        for (uint32_t i = tid; i < pi.nseg; i += kThreads) f |= seg_fail[pi.seg0 + i] != 0;
+        bool ok = !__syncthreads_or(f);
+        if (ok && tid == 0) {   // (record positions are valid once discovery passed)
+            const uint32_t B = pi.B;
+            pi.mode[0] = pi.rec[0][0];
+            pi.mode[1] = pi.rec[1][0];
+            // stored planes are read at the end of the pair: have them in L2 by then
+            if (pi.mode[0] == MODE_STORED) prefetch_l2(pi.rec[0] + 5, B);
+            if (pi.mode[1] == MODE_STORED) prefetch_l2(pi.rec[1] + 5, B);
+        }
+        __syncthreads();
+        uint8_t* slot = ring + (uint64_t)blockIdx.x * kPairRing;   // low plane | high plane
+        if (ok && pi.mode[1] == MODE_HUFFMAN) ok = huff_decode(s, pi.rec[1] + 5, pi.B, slot + 65536, kStageSmall);
+        if (ok && pi.mode[0] == MODE_HUFFMAN) ok = huff_decode(s, pi.rec[0] + 5, pi.B, slot, kStageSmall);
         if (!ok) {
-            for (uint32_t i = tid; i < wd.nseg; i += kThreads) seg_fail[wd.seg0 + i] = 1u;
+            for (uint32_t i = tid; i < pi.nseg; i += kThreads) seg_fail[pi.seg0 + i] = 1u;
             DBG_ADD(21, tid == 0);
             continue;
         }
@@ -1719,12 +1738,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restric
         __syncthreads();
         DBG_TADD(23, t_tab);
         DBG_T0(t_il);
+        Crc4x8Lane cl;
+        cl.init(crctab, lane);
+        const uint32_t B = pi.B, mL = pi.mode[0], mH = pi.mode[1];
+        const uint8_t* recL = pi.rec[0];
+        const uint8_t* recH = pi.rec[1];
+        const uint64_t k = pi.k;
+        const uint8_t* dL = slot;
+        const uint8_t* dH = slot + 65536;
         const uint8_t* pL = mL == MODE_HUFFMAN ? dL : recL + 5;
         const uint8_t* pH = mH == MODE_HUFFMAN ? dH : recH + 5;
         const uint32_t rL = recL[5] * 0x01010101u, rH = recH[5] * 0x01010101u;
         const uint64_t e0 = k * B;
-        uint8_t* o = out + wd.ooff + 2 * e0;
-        const uint8_t* pv = wd.prev ? wd.prev + 2 * e0 : nullptr;
+        uint8_t* o = out + pi.ooff + 2 * e0;
+        const uint8_t* pv = pi.prev ? pi.prev + 2 * e0 : nullptr;
         // warp w writes output rows [w R, (w + 1) R) of 1 KiB (lane l: bytes
         // 32 l .. 32 l + 31 of each row) as four chains of R / 4 rows
         const uint32_t R = B >> 12, Rc = R >> 2;
@@ -1781,7 +1808,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restric
             const uint32_t* tw = &ct->pow2[31 - __clz(R * 1024u)][0][0];
             uint32_t acc = 0;
             for (uint32_t j = 0; j < wpt; j++) acc = crc_shift_tab(tw, acc) ^ wcrc[tid * wpt + j];
-            tile_crc[wd.tile0 + k * T + tid] = acc;
+            tile_crc[pi.tile0 + k * T + tid] = acc;
         }
         DBG_TADD(22, t_il);
     }

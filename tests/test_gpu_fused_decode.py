@@ -21,6 +21,7 @@ def codec():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     c = lmcb.Codec()
+    c.ctx.set_decode_fusion(True, 0)    # fused at every size (the default starts at 16384 records)
     yield c
     c.ctx.set_decode_fusion(True)
 
@@ -40,11 +41,11 @@ def host_bytes(t) -> bytes:
 def both_paths(codec, streams, **kw):
     out = []
     for fuse in (True, False):
-        codec.ctx.set_decode_fusion(fuse)
+        codec.ctx.set_decode_fusion(fuse, 0)
         try:
             out.append(codec.decompress(streams, **kw))
         finally:
-            codec.ctx.set_decode_fusion(True)
+            codec.ctx.set_decode_fusion(True, 0)
     return out
 
 
@@ -85,11 +86,11 @@ def test_fused_kernel_runs_and_ungroup_skips(codec):
     b = codec.compress(ts)
     rep = _profiled(codec, lambda: codec.decompress(b).raise_for_status())
     assert "k_decpair" in rep
-    codec.ctx.set_decode_fusion(False)
+    codec.ctx.set_decode_fusion(False, 0)
     try:
         rep2 = _profiled(codec, lambda: codec.decompress(b).raise_for_status())
     finally:
-        codec.ctx.set_decode_fusion(True)
+        codec.ctx.set_decode_fusion(True, 0)
     assert "k_decpair" not in rep2
 
 
@@ -103,7 +104,7 @@ def test_fused_delta_both_planes_huffman_and_apply(codec):
         x = host_bytes((p.view(torch.uint8) ^ q.view(torch.uint8)).reshape(-1))
         assert s == O.compress(x, 1, delta=True, threads=8)
     for fuse in (True, False):
-        codec.ctx.set_decode_fusion(fuse)
+        codec.ctx.set_decode_fusion(fuse, 0)
         try:
             outs = [p.clone() for p in prev]
             r = codec.decompress(b, prev=outs, out=None)
@@ -111,7 +112,7 @@ def test_fused_delta_both_planes_huffman_and_apply(codec):
             for i, (p, q) in enumerate(zip(prev, nxt)):
                 assert torch.equal(r.payload(i), q.view(torch.uint8).reshape(-1)), (fuse, specs[i].name)
         finally:
-            codec.ctx.set_decode_fusion(True)
+            codec.ctx.set_decode_fusion(True, 0)
 
 
 def test_fused_misaligned_output_offsets(codec):
