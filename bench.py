@@ -366,7 +366,9 @@ def measure(codec, ts, prev, args, ws, dist, owned, n_total, local, with_clocks=
     torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
     if int(status_log.abs().sum().item()) != 0:
-        raise SystemExit("a timed step reported a decode error")
+        bad = status_log.nonzero().tolist()
+        codes = [int(status_log[i, j]) for i, j in bad[:8]]
+        raise SystemExit(f"a timed step reported a decode error: (step slot, stream) {bad[:8]} codes {codes}")
     if dist is not None:
         dist.barrier()
     total_ms = start.elapsed_time(end)

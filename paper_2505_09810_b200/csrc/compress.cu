@@ -56,26 +56,29 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
 // The warp reads 1 KiB rows (lane l: the 32 bytes at 1024 r + 32 l, two
 // 16-byte loads that together cover whole lines) and lane l folds its
 // pieces in order: shift by the 992 bytes of the other lanes' pieces (4
-// lookups), then the piece by slicing-by-4 through 32-fold replicated
-// tables (crc4_rep: lane l reads copy l, no bank conflicts).  Lane l's value ends 32 (31 - l)
+// lookups), then the piece by slicing-by-4 through the 32 KiB conflict-free
+// layout (CrcTables::rep4x8, Crc4x8Lane: the 32 lanes of every lookup read
+// 32 different banks).  Lane l's value ends 32 (31 - l)
 // bytes before the chunk end: shift and XOR-reduce.  A short last chunk is
 // treated as left-padded with zero bytes, which leave a raw CRC unchanged.
 // k_frame combines the chunks (stream.py:329).
-constexpr int kCrcThreads = 512;   // one CTA per SM (128 KiB of replicated slicing tables), leaving
+constexpr int kCrcThreads = 512;   // up to two CTAs per SM (36 KiB of tables each), leaving
                                    // registers and threads for the histogram / encode CTAs it overlaps
 constexpr int kCrcWarps = kCrcThreads / 32;
-constexpr size_t kCrcSmem = (kRep4Words + 1024) * sizeof(uint32_t);
+constexpr size_t kCrcSmem = (256 * 32 + 1024) * sizeof(uint32_t);
 
-__global__ void __launch_bounds__(kCrcThreads, 1) k_crc(const WinDesc* __restrict__ wins, const uint32_t* __restrict__ crc2win, uint64_t nchunk,
+__global__ void __launch_bounds__(kCrcThreads, 2) k_crc(const WinDesc* __restrict__ wins, const uint32_t* __restrict__ crc2win, uint64_t nchunk,
                                                 const CrcTables* __restrict__ ct, const uint32_t* __restrict__ sh992,
                                                 uint32_t* __restrict__ out) {
     extern __shared__ uint32_t tab[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    load_rep4(tab, ct);
-    uint32_t* st = tab + kRep4Words;
+    for (int i = tid; i < 256 * 32 / 4; i += kCrcThreads)
+        reinterpret_cast<uint4*>(tab)[i] = __ldg(reinterpret_cast<const uint4*>(ct->rep4x8) + i);
+    uint32_t* st = tab + 256 * 32;
     for (int i = tid; i < 1024; i += kCrcThreads) st[i] = sh992[i];
     __syncthreads();
-    const uint32_t* tl = tab + lane;
+    Crc4x8Lane cl;
+    cl.init(tab, lane);
     constexpr uint32_t kRows = kCrcChunk / 1024;
     // chunks dealt CTA-major (c = blockIdx.x + gridDim.x * j): small inputs still use every SM
     for (uint64_t j = warp, c = blockIdx.x + (uint64_t)warp * gridDim.x; c < nchunk;
@@ -126,14 +129,14 @@ __global__ void __launch_bounds__(kCrcThreads, 1) k_crc(const WinDesc* __restric
             load_piece(i + kHalf, b);
             ca = shift992(ca);
             cb = shift992(cb);
-            ca = crc4_rep(tl, ca, a[0].x); cb = crc4_rep(tl, cb, b[0].x);
-            ca = crc4_rep(tl, ca, a[0].y); cb = crc4_rep(tl, cb, b[0].y);
-            ca = crc4_rep(tl, ca, a[0].z); cb = crc4_rep(tl, cb, b[0].z);
-            ca = crc4_rep(tl, ca, a[0].w); cb = crc4_rep(tl, cb, b[0].w);
-            ca = crc4_rep(tl, ca, a[1].x); cb = crc4_rep(tl, cb, b[1].x);
-            ca = crc4_rep(tl, ca, a[1].y); cb = crc4_rep(tl, cb, b[1].y);
-            ca = crc4_rep(tl, ca, a[1].z); cb = crc4_rep(tl, cb, b[1].z);
-            ca = crc4_rep(tl, ca, a[1].w); cb = crc4_rep(tl, cb, b[1].w);
+            ca = cl.word(ca, a[0].x); cb = cl.word(cb, b[0].x);
+            ca = cl.word(ca, a[0].y); cb = cl.word(cb, b[0].y);
+            ca = cl.word(ca, a[0].z); cb = cl.word(cb, b[0].z);
+            ca = cl.word(ca, a[0].w); cb = cl.word(cb, b[0].w);
+            ca = cl.word(ca, a[1].x); cb = cl.word(cb, b[1].x);
+            ca = cl.word(ca, a[1].y); cb = cl.word(cb, b[1].y);
+            ca = cl.word(ca, a[1].z); cb = cl.word(cb, b[1].z);
+            ca = cl.word(ca, a[1].w); cb = cl.word(cb, b[1].w);
         }
         // chain a ends 16 rows (16 KiB) before chain b
         uint32_t crc = crc_shift_tab(&ct->pow2[14][0][0], ca) ^ cb;
@@ -942,6 +945,45 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
             put(t1, 0u);
             put(z - t1, 0u);
         };
+        if (!RUN && fast) {
+            // lean run: whole pieces of one plane, 16-byte loads one piece
+            // ahead, every symbol pair unconditional, the private slot
+            // addressed by a running pointer
+            const uint4* sp = reinterpret_cast<const uint4*>(srcp);
+            const uint4* pp = reinterpret_cast<const uint4*>(prvp);
+            const uint32_t npc = (uint32_t)((q1 - q0) / per);
+            auto ld = [&](uint32_t j) {
+                uint4 a = __ldg(sp + j);
+                if (pp) {
+                    const uint4 c = __ldg(pp + j);
+                    a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
+                }
+                return a;
+            };
+            uint32_t* pw = priv;
+            uint4 cur = ld(0);
+#pragma unroll 2
+            for (uint32_t j = 0; j < npc; j++) {
+                const uint4 nxt = j + 1 < npc ? ld(j + 1) : make_uint4(0, 0, 0, 0);
+                uint32_t sy[4];
+                piece_symbols(cur, W, (uint32_t)g, sy);
+#pragma unroll
+                for (int i = 0; i < per; i += 2) {
+                    const uint32_t e1 = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
+                    const uint32_t e2 = sh_code[(sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF];
+                    const uint32_t l2 = e2 >> 16;
+                    const uint32_t pl = (e1 >> 16) + l2;
+                    acc = (acc << pl) | (((e1 & 0xFFFF) << l2) | (e2 & 0xFFFF));
+                    n += pl;
+                    const bool fl = n >= 32;
+                    n -= fl ? 32 : 0;
+                    if (fl) *pw = (uint32_t)(acc >> n);
+                    pw += fl ? 1 : 0;
+                }
+                cur = nxt;
+            }
+            wi = (uint32_t)(pw - priv);
+        } else {
         // fast runs: the loads run kAhead pieces ahead of the packing (the
         // kernel is otherwise bound by load latency at its occupancy)
         constexpr int kAhead = 2;
@@ -1015,6 +1057,7 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
                     wi += fl ? 1 : 0;
                 }
             }
+        }
         }
         if (RUN) zeros(pend);
         const uint32_t nwp = wi + (n ? 1 : 0);
@@ -1247,6 +1290,12 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     }
     const uint32_t w = wd.w;
     const uint64_t p0 = k * B, p1 = min(wd.W, p0 + B);
+    if (tid == 32 && p1 <= (plane_of(p0, wd.n, w) + 1) * wd.n) {
+        // the block's source elements (one plane): in L2 before the first loads
+        const uint64_t e0 = p0 - plane_of(p0, wd.n, w) * wd.n;
+        prefetch_l2(wd.src + e0 * w, (uint32_t)((p1 - p0) * w));
+        if (wd.prev) prefetch_l2(wd.prev + e0 * w, (uint32_t)((p1 - p0) * w));
+    }
     if (!huff) {  // stored record: the block's bytes verbatim after the 5-byte header
         const uint64_t g0 = plane_of(p0, wd.n, w);
         if (wd.vec && ((p1 - p0) & 15) == 0 && p1 <= (g0 + 1) * wd.n) {

@@ -936,6 +936,11 @@ __device__ __forceinline__ uint64_t stage_cover(const uint8_t* pl) {   // staged
 __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t* dst, uint32_t stage_cap) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     DBG_T0(t_setup);
+    // the staging area below is rewritten by the bulk copy (async proxy);
+    // every thread's earlier generic writes to this shared memory (byte swaps
+    // of the last payload, k_decpair's CRC tables) must be ordered before it:
+    // a proxy fence by each writer, then the barrier
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     // stage the payload in shared memory with one TMA bulk copy of its
     // 16-byte aligned cover, issued first so it lands while the tables are built
@@ -945,10 +950,6 @@ __device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t
     const uint64_t e16 = (reinterpret_cast<uint64_t>(data0) + ((uint64_t)bits0 + 7) / 8 + 15) & ~15ull;
     const bool staged = bits0 != 0 && e16 - a16 <= (uint64_t)stage_cap;
     if (staged && tid == 0) {
-        // the staging area was last written through the generic proxy (byte
-        // swaps, k_decpair's CRC tables): order those writes before the bulk
-        // copy's async-proxy writes (the __syncthreads above ordered the CTA's)
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_init1(&s.mbar);
         tma_load_1d(s.bits, reinterpret_cast<const void*>(a16), (uint32_t)(e16 - a16), &s.mbar);
     }
@@ -1620,11 +1621,7 @@ __global__ void k_pairs(const DecSeg* __restrict__ segs, const uint32_t* __restr
     warp_append(is_single, (uint32_t)g, singles, &ctl[2]);
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {   // TMA prefetch into L2
-    const uint64_t a = reinterpret_cast<uint64_t>(p) & ~15ull;
-    const uint64_t e = (reinterpret_cast<uint64_t>(p) + bytes + 15) & ~15ull;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
-}
+
 
 // 16 plane bytes at element offset e (a multiple of 16) of a pair's plane
 __device__ __forceinline__ uint4 plane16(const uint8_t* p, uint32_t mode, uint32_t rle, uint32_t e, uint32_t B) {

@@ -336,4 +336,12 @@ __device__ __forceinline__ uint64_t plane_of(uint64_t p, uint64_t n, uint32_t w)
 
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
+// TMA prefetch of [p, p + bytes) into L2 (16-byte aligned cover; nothing is
+// written, a prefetch never faults the kernel)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    const uint64_t a = reinterpret_cast<uint64_t>(p) & ~15ull;
+    const uint64_t e = (reinterpret_cast<uint64_t>(p) + bytes + 15) & ~15ull;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+
 }  // namespace lmcg
