@@ -486,8 +486,8 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         if (int r = launch_crc()) return r;
 
     if (nslots) {
-        PROF(k_hist_crc);
-        k_hist_crc<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta,
+        PROF(k_hist);
+        k_hist<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta,
                                                           part ? part_lo : 0, part ? part_hi : ~0ull);
     }
     if (fork && ctx->crc_fork == 1)

@@ -1,10 +1,12 @@
 // compress.cu -- B200 kernels of the LMC compress path.
 //
 //   k_slotmap    slot -> window map (planes interleaved per window)
-//   k_hist_crc   K1: fused XOR delta + byte-group gather + per-block 256-bin
-//                histogram + raw CRC-32 of the plane-0 element range
-//                (entropy.py:53-59, bytegroup.py:39-50, delta.py:18-26,
-//                stream.py:329)
+//   k_crc        raw CRC-32 of every 32 KiB chunk of the payload (XOR delta
+//                applied), on the side stream next to k_hist / k_codebook
+//                (stream.py:329); k_frame combines the chunks
+//   k_hist       K1: fused XOR delta + byte-group gather + per-block 256-bin
+//                histogram (entropy.py:53-59, bytegroup.py:39-50,
+//                delta.py:18-26)
 //   k_codebook   K2: per-block mode + canonical length-limited Huffman lengths
 //                (stream.py:161-177, huffman.py:79-137), one warp per block
 //   k_pkgmerge   K2b: package-merge for blocks whose Huffman tree exceeds 15
@@ -36,7 +38,7 @@ __global__ void k_small_copy(uint8_t* __restrict__ dst, const uint8_t* __restric
 constexpr uint32_t kCrcChunk = 32768;   // k_crc's unit
 
 // ------------------------------------------------------------------ slotmap
-// Owner maps: block slot -> window (k_hist_crc, k_encode) and CRC chunk ->
+// Owner maps: block slot -> window (k_hist, k_encode) and CRC chunk ->
 // window (k_crc); one load per unit instead of a search.
 __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* __restrict__ slot2win,
                           uint32_t* __restrict__ crc2win) {
@@ -189,7 +191,7 @@ __device__ __forceinline__ void hist_tiles(const WinDesc& wd, uint64_t p0, uint6
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_hist_crc(
+__global__ void __launch_bounds__(kThreads, 3) k_hist(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
     uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta, uint64_t part_lo, uint64_t part_hi) {
     __shared__ uint32_t sh_hist[kWarps][256];

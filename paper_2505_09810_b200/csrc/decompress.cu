@@ -8,21 +8,31 @@
 //
 //   k_parse     one thread per stream: header + window/segment-table walk
 //               with the reference's exact validation (stream.py:114-142,
-//               358-389); writes window / segment descriptors (or RETRY when
-//               a stream does not fit the hinted capacities)
-//   k_scandec   persistent, ticket-ordered CTAs over 64 KiB chunks of segment
-//               payload: find record-header candidates "mode<=2|len==block",
-//               number them with a segmented decoupled look-back, and decode
-//               every candidate record straight away (RLE fill, stored copy,
-//               self-synchronising parallel Huffman decode, stream.py:190-215,
-//               huffman.py:258-349) into the grouped scratch
+//               358-389); window / segment descriptors (or RETRY when a
+//               stream does not fit the hinted capacities); marks the windows
+//               k_decpair decodes fused
+//   k_maps      chunk -> segment, record slot -> segment, tile -> window
+//   k_cand      record-header candidates "mode<=2|len==block" per 8 KiB span
+//   k_number    per segment: exclusive scan of the chunk candidate counts
+//   k_assign    record slot of every candidate (+ the tail record)
 //   k_verify    one thread per record slot: candidates must chain exactly
 //               (p -> p + record size) with the canonical record lengths
-//   k_fallback  segments that failed verification are re-walked serially,
-//               exactly like decompress_segment (stream.py:234-268), and
-//               re-decoded -- the authoritative path for any stream
-//   k_ungroup   inverse byte-grouping per window (bytegroup.py:53-62) + raw
-//               CRC-32 of each 16 KiB output tile
+//   k_resolve   segments with false candidates: the path from the segment
+//               start by pointer doubling
+//   k_pairs +   (large decodes) persistent CTAs: low/high record pairs of
+//   k_decpair   two-plane windows decoded into an L2 ring slot, interleaved
+//               into the output with the tile CRCs in the same pass
+//               (stream.py:190-215,392-403, huffman.py:258-349,
+//               bytegroup.py:53-62); then the other windows' records into
+//               the grouped scratch
+//   k_decrec    (small decodes) CTA per record slot into the grouped scratch;
+//               k_classify / k_decrec_large take the records whose payload
+//               does not stage in kStageSmall
+//   k_fallback  segments that failed discovery or decode are re-walked
+//               serially, exactly like decompress_segment (stream.py:234-268)
+//               -- the authoritative path for any stream
+//   k_ungroup   inverse byte-grouping of the windows k_decpair did not write
+//               (bytegroup.py:53-62) + raw CRC-32 of each 32 KiB output tile
 //   k_finalize  per-stream CRC combine and status (stream.py:416-423)
 #include <type_traits>
 
@@ -271,6 +281,13 @@ struct DecSmem {
 };
 // dynamic shared memory of k_decrec / k_fallback for a staging capacity
 __host__ __device__ constexpr size_t dec_smem_bytes(uint32_t stage) { return sizeof(DecSmem) + stage + 16; }
+
+// Every kernel that decodes records keeps DecSmem at the start of its dynamic
+// shared memory; the decoder addresses it through this symbol, so table and
+// staging lookups are [register + constant] shared-memory loads (a DecSmem&
+// handed through a call would cost a base-register add per lookup).
+extern __shared__ __align__(16) uint8_t g_dsmem[];
+__device__ __forceinline__ DecSmem& dec_smem() { return *reinterpret_cast<DecSmem*>(g_dsmem); }
 
 // Payload bit source: big-endian words, bit i of the payload is bit
 // 31 - ((i + sh) & 31) of word (i + sh) >> 5; staged in shared memory when
@@ -933,7 +950,9 @@ __device__ __forceinline__ uint64_t stage_cover(const uint8_t* pl) {   // staged
     return e16 - a16;
 }
 
-__device__ bool huff_decode(DecSmem& s, const uint8_t* pl, uint32_t len, uint8_t* dst, uint32_t stage_cap) {
+__device__ bool huff_decode(DecSmem& /* the caller's view of dec_smem() */, const uint8_t* pl, uint32_t len, uint8_t* dst,
+                            uint32_t stage_cap) {
+    DecSmem& s = dec_smem();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     DBG_T0(t_setup);
     // the staging area below is rewritten by the bulk copy (async proxy);

@@ -22,5 +22,5 @@ timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --mast
 ARGS="--steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv python bench.py $ARGS > $O/ncu_launch.log 2>&1; echo "launch rc=$?" | tee -a $O/rc.log
 for c in cfg2 cfg5; do
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_decrec|k_encode|k_hist_crc|k_crc|k_ungroup|k_codebook|k_cand" -c 7 -o $O/prof_$c python bench.py $ARGS --config $c > $O/ncu_full_$c.log 2>&1; echo "full $c rc=$?" | tee -a $O/rc.log
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"k_decrec|k_encode|k_hist|k_decpair|k_crc|k_ungroup|k_codebook|k_cand" -c 7 -o $O/prof_$c python bench.py $ARGS --config $c > $O/ncu_full_$c.log 2>&1; echo "full $c rc=$?" | tee -a $O/rc.log
 done
