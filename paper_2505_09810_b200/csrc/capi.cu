@@ -66,6 +66,7 @@ struct lmcg_ctx {
     uint32_t* d_sh992 = nullptr;
     int crc_occ = 1;
     bool enc_attr = false;
+    bool hist_attr = false;
     // per-kernel event timing (lmcg_profile)
     bool prof = false;
     std::vector<std::pair<const char*, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
@@ -127,6 +128,13 @@ void build_crc_tables(CrcTables& t) {
     for (int i = 0; i < 256; i++)
         for (int tt = 0; tt < 4; tt++)
             for (int c = 0; c < 8; c++) t.rep4x8[32 * i + 8 * tt + c] = t.slice[tt][i];
+    auto shift_table = [&](uint64_t nbytes, uint32_t (*out)[256]) {   // [k][b] = (b << 8k) * x^(8 nbytes)
+        uint32_t p = 1u << 31;
+        for (uint64_t nn = nbytes, k = 3; nn; nn >>= 1, k++)
+            if (nn & 1) p = h_multmodp(t.x2n[k & 63], p);
+        for (int k = 0; k < 4; k++)
+            for (uint32_t b = 0; b < 256; b++) out[k][b] = b ? h_multmodp(p, b << (8 * k)) : 0;
+    };
     t.x2n[0] = 1u << 30;  // x^1
     for (int k = 1; k < 64; k++) t.x2n[k] = h_multmodp(t.x2n[k - 1], t.x2n[k - 1]);
     for (int lvl = 0; lvl < 11; lvl++) {
@@ -154,6 +162,8 @@ void build_crc_tables(CrcTables& t) {
                 t.pow2[m][byte][b] = c ? h_multmodp(p, c) : 0;
             }
     }
+    shift_table(496, t.sh496);
+    shift_table(kHistTileGap, t.shtile);
 }
 
 int ensure_ctx(lmcg_ctx* ctx) {
@@ -238,6 +248,7 @@ struct CPlan {
     std::vector<StreamDesc> streams;
     std::vector<WinDesc> wins;
     uint64_t nb = 0, nslots = 0, ncrc = 0;
+    uint64_t ncrc_k = 0;   // CRC chunks k_crc computes (windows k_hist does not fold)
     uint32_t min_w = 4;
 };
 
@@ -280,9 +291,14 @@ void make_plan(const lmcg_tensor* t, int n, const lmcg_options* o, CPlan& P) {
             const bool al = ((uint64_t)wd.src % 16 == 0) && ((uint64_t)wd.prev % 16 == 0);
             wd.vec = al && (w == 1 || wd.W % 16 == 0);
             wd.al16 = al ? 1u : 0u;
-            wd.pad = 0;
+            // k_hist folds the CRC when every plane-0 block is whole and on
+            // the vector path (its tiles then hold every source byte of the
+            // block's element range); k_crc takes the other windows
+            wd.hcrc = (wd.vec && wd.W % ((uint64_t)w * B) == 0) ? 1u : 0u;
+            wd.cunit = wd.hcrc ? (uint64_t)w * B : kCrcChunk;
             wd.crc0 = P.ncrc;
-            P.ncrc += (wd.W + kCrcChunk - 1) / kCrcChunk;
+            P.ncrc += (wd.W + wd.cunit - 1) / wd.cunit;
+            if (!wd.hcrc) P.ncrc_k += (wd.W + kCrcChunk - 1) / kCrcChunk;
             P.nb += wd.nblocks;
             P.nslots += wd.nslots;
             P.min_w = std::min(P.min_w, w);
@@ -438,7 +454,8 @@ static int check_compress_args(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const
 // Part mode (part_out != null, lmcg_compress_part): only blocks [part_lo,
 // part_hi) are compressed, their records land back to back in part_out and
 // their sizes in d_rec_sizes; no header, segment tables or CRC.
-static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t nslots, uint64_t ncrc, uint32_t min_w,
+static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t nslots, uint64_t ncrc, uint64_t ncrc_k,
+                           uint32_t min_w,
                            const lmcg_options* o, uint8_t* ws, const size_t* offs, void* d_out, uint64_t* d_offsets,
                            uint64_t* d_lengths, cudaStream_t st, uint64_t part_lo = 0, uint64_t part_hi = ~0ull,
                            uint8_t* part_out = nullptr, uint32_t* d_rec_sizes = nullptr) {
@@ -463,7 +480,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
     if (nwin) { PROF(k_slotmap); k_slotmap<<<nwin, 256, 0, st>>>(d_wins, nwin, d_slot2win, ncrc ? d_crc2win : nullptr); }
     // k_crc only reads the tensors: it runs on the side stream, overlapping
     // the histogram / codebook / encode chain, and joins before k_frame
-    const bool fork = ncrc && n && !part;
+    const bool fork = ncrc_k && n && !part;   // (k_hist folds the CRC of the other windows)
     auto launch_crc = [&]() -> int {
         if (!ctx->crc_attr) {
             CK(cudaFuncSetAttribute(k_crc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCrcSmem));
@@ -487,8 +504,13 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
 
     if (nslots) {
         PROF(k_hist);
-        k_hist<<<(unsigned)nslots, kThreads, 0, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta,
-                                                          part ? part_lo : 0, part ? part_hi : ~0ull);
+        if (!ctx->hist_attr) {   // (static + dynamic shared memory above 48 KiB)
+            CK(cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kHistSmem));
+            ctx->hist_attr = true;
+        }
+        k_hist<<<(unsigned)nslots, kThreads, kHistSmem, st>>>(d_wins, d_slot2win, nslots, o->block_size, d_hist, d_meta,
+                                                          part ? part_lo : 0, part ? part_hi : ~0ull, ctx->d_crc,
+                                                          part ? nullptr : d_crcp);
     }
     if (fork && ctx->crc_fork == 1)
         if (int r = launch_crc()) return r;
@@ -566,7 +588,8 @@ int lmcg_compress(lmcg_ctx* ctx, const lmcg_tensor* t, int n, const lmcg_options
     if (wbytes) CK(cudaMemcpyAsync(ws + offs[0], ctx->pin, wbytes, cudaMemcpyHostToDevice, st));
     if (sbytes) CK(cudaMemcpyAsync(ws + offs[1], ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(ctx->pin_done, st));
-    return compress_launch(ctx, n, (int)P.wins.size(), P.nb, P.nslots, P.ncrc, P.min_w, o, ws, offs, d_out, d_offsets, d_lengths, st);
+    return compress_launch(ctx, n, (int)P.wins.size(), P.nb, P.nslots, P.ncrc, P.ncrc_k, P.min_w, o, ws, offs, d_out, d_offsets,
+                           d_lengths, st);
 }
 
 int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* o, uint64_t blk_begin,
@@ -599,7 +622,7 @@ int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* 
     if (sbytes) CK(cudaMemcpyAsync(ws + offs[1], ctx->pin + wbytes, sbytes, cudaMemcpyHostToDevice, st));
     CK(cudaEventRecord(ctx->pin_done, st));
     if (blk_end > blk_begin) {
-        if (int r = compress_launch(ctx, 1, (int)P.wins.size(), P.nb, P.nslots, P.ncrc, P.min_w, o, ws, offs, nullptr,
+        if (int r = compress_launch(ctx, 1, (int)P.wins.size(), P.nb, P.nslots, P.ncrc, P.ncrc_k, P.min_w, o, ws, offs, nullptr,
                                     nullptr, nullptr, st, blk_begin, blk_end, static_cast<uint8_t*>(d_out), d_rec_sizes))
             return r;
     }
@@ -620,6 +643,7 @@ int lmcg_compress_part(lmcg_ctx* ctx, const lmcg_tensor* t, const lmcg_options* 
     cw.n = L;
     cw.w = 1;
     cw.crc0 = 0;
+    cw.cunit = kCrcChunk;
     cw.al16 = ((uint64_t)cw.src % 16 == 0) && ((uint64_t)cw.prev % 16 == 0);
     CK(cudaStreamSynchronize(st));
     CK(cudaMemcpy(ctx->part_ws, &cw, sizeof(WinDesc), cudaMemcpyHostToDevice));
@@ -647,7 +671,7 @@ struct lmcg_plan {
     // compress
     lmcg_options opts{};
     int nwin = 0;
-    uint64_t nb = 0, nslots = 0, ncrc = 0, bound = 0;
+    uint64_t nb = 0, nslots = 0, ncrc = 0, ncrc_k = 0, bound = 0;
     uint32_t min_w = 4;
     size_t offs[16] = {};
     // decompress
@@ -668,6 +692,7 @@ lmcg_plan* lmcg_compress_plan_create(lmcg_ctx* ctx, const lmcg_tensor* t, int n,
     pl->nb = P.nb;
     pl->nslots = P.nslots;
     pl->ncrc = P.ncrc;
+    pl->ncrc_k = P.ncrc_k;
     pl->min_w = P.min_w;
     pl->bound = lmcg_compress_bound(t, n, o);
     pl->ws_bytes = compress_layout(P, n, pl->offs);
@@ -718,7 +743,7 @@ int lmcg_compress_plan_run(lmcg_ctx* ctx, lmcg_plan* pl, void* d_out, uint64_t o
     if (!ctx || !pl || pl->kind != 1) return fail(ctx, LMCG_ERR_ARGUMENT, "not a compress plan");
     if (out_capacity < pl->bound) return fail(ctx, LMCG_ERR_CAPACITY, "output capacity below the plan's bound");
     if (int r = ensure_ctx(ctx)) return r;
-    return compress_launch(ctx, pl->n, pl->nwin, pl->nb, pl->nslots, pl->ncrc, pl->min_w, &pl->opts, pl->ws, pl->offs, d_out,
+    return compress_launch(ctx, pl->n, pl->nwin, pl->nb, pl->nslots, pl->ncrc, pl->ncrc_k, pl->min_w, &pl->opts, pl->ws, pl->offs, d_out,
                            d_offsets, d_lengths, static_cast<cudaStream_t>(cuda_stream));
 }
 

@@ -47,7 +47,7 @@ __global__ void k_slotmap(const WinDesc* __restrict__ wins, int nwin, uint32_t* 
     const WinDesc wd = wins[wi];
     for (uint32_t i = threadIdx.x; i < wd.nslots; i += blockDim.x) slot2win[wd.slot0 + i] = (uint32_t)wi;
     if (crc2win) {
-        const uint64_t nc = (wd.W + kCrcChunk - 1) / kCrcChunk;
+        const uint64_t nc = (wd.W + wd.cunit - 1) / wd.cunit;
         for (uint64_t i = threadIdx.x; i < nc; i += blockDim.x) crc2win[wd.crc0 + i] = (uint32_t)wi;
     }
 }
@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(kCrcThreads, 2) k_crc(const WinDesc* __restric
     for (uint64_t j = warp, c = blockIdx.x + (uint64_t)warp * gridDim.x; c < nchunk;
          j += kCrcWarps, c = blockIdx.x + j * gridDim.x) {
         const WinDesc wd = wins[crc2win[c]];
+        if (wd.hcrc) continue;   // (k_hist folds this window's CRC)
         const uint64_t off = (c - wd.crc0) * kCrcChunk;
         const uint32_t L = (uint32_t)min((uint64_t)kCrcChunk, wd.W - off);
         const uint32_t Z = kCrcChunk - L;   // leading zero bytes of the padded chunk
@@ -159,8 +160,20 @@ __global__ void __launch_bounds__(kCrcThreads, 2) k_crc(const WinDesc* __restric
 // pieces, then the four rows in order).
 // The warp-tiles of one block for element width W (compile-time: the plane
 // gather and the per-piece symbol count are then static).
-template <int W>
-__device__ __forceinline__ void hist_tiles(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_t* hist, int lane, int warp) {
+// CRC: (plane-0 blocks of hcrc windows) lane l folds its pieces -- 16 bytes
+// at 512 q + 16 l of each of the warp's tiles, in byte order -- into one
+// chain: a 496-byte shift between the pieces of a tile, kHistTileGap between
+// the warp's tiles; *last = the warp's last tile.  (One 64-byte run per lane
+// and tile instead -- one shift per tile -- measured slower: 8.98 vs 8.74 ms
+// on cfg5, the strided loads cost more than the shifts.)
+template <int W, bool CRC>
+__device__ __forceinline__ uint32_t hist_tiles(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_t* hist, int lane, int warp,
+                                               const Crc4x8Lane& cl, const uint32_t* s496, const uint32_t* sgap,
+                                               uint32_t* last) {
+    uint32_t ch = 0;
+    auto shift = [](const uint32_t* t, uint32_t x) {
+        return t[x & 0xFF] ^ t[256 + ((x >> 8) & 0xFF)] ^ t[512 + ((x >> 16) & 0xFF)] ^ t[768 + (x >> 24)];
+    };
     constexpr uint32_t lw = W == 1 ? 0 : (W == 2 ? 1 : 2);
     constexpr uint64_t T = kTileBytes >> lw;    // positions per warp-tile
     constexpr int per = 16 / W;                 // symbols per 16-byte piece
@@ -175,6 +188,18 @@ __device__ __forceinline__ void hist_tiles(const WinDesc& wd, uint64_t p0, uint6
             uint4 a[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, base + 512ull * q);
+            if (CRC) {
+                ch = shift(sgap, ch);   // (no-op on the warp's first tile: ch == 0)
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    if (q) ch = shift(s496, ch);
+                    ch = cl.word(ch, a[q].x);
+                    ch = cl.word(ch, a[q].y);
+                    ch = cl.word(ch, a[q].z);
+                    ch = cl.word(ch, a[q].w);
+                }
+                *last = (uint32_t)t;
+            }
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 uint32_t sy[4];
@@ -189,12 +214,19 @@ __device__ __forceinline__ void hist_tiles(const WinDesc& wd, uint64_t p0, uint6
             for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p)], 1u);
         }
     }
+    return ch;
 }
+
+// k_hist's dynamic shared memory: rep4x8 | sh496 | shtile (CRC folding)
+constexpr size_t kHistSmem = (256 * 32 + 2 * 1024) * sizeof(uint32_t);
 
 __global__ void __launch_bounds__(kThreads, 3) k_hist(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
-    uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta, uint64_t part_lo, uint64_t part_hi) {
+    uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta, uint64_t part_lo, uint64_t part_hi,
+    const CrcTables* __restrict__ ct, uint32_t* __restrict__ crcpart) {
+    extern __shared__ __align__(16) uint32_t crc_tab[];
     __shared__ uint32_t sh_hist[kWarps][256];
+    __shared__ uint32_t sh_crc;
     const uint64_t slot = blockIdx.x;
     if (slot >= nslots) return;
     const WinDesc wd = wins[slot2win[slot]];
@@ -208,10 +240,37 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist(
 
     const uint64_t p0 = k * B;
     const uint64_t p1 = min(wd.W, p0 + B);
-    if (wd.w == 1) hist_tiles<1>(wd, p0, p1, sh_hist[warp], lane, warp);
-    else if (wd.w == 2) hist_tiles<2>(wd, p0, p1, sh_hist[warp], lane, warp);
-    else hist_tiles<4>(wd, p0, p1, sh_hist[warp], lane, warp);
+    // the plane-0 block of an hcrc window folds the raw CRC of its element
+    // range (every source byte of it passes through its tiles); part runs
+    // (lmcg_compress_part) take their CRC from k_crc
+    const bool crc = wd.hcrc && p1 <= wd.n && crcpart != nullptr;
+    Crc4x8Lane cl;
+    uint32_t ch = 0, last = 0;
+    if (crc) {
+        for (int i = tid; i < (256 * 32 + 2 * 1024) / 4; i += kThreads)
+            reinterpret_cast<uint4*>(crc_tab)[i] = i < 256 * 32 / 4 ? __ldg(reinterpret_cast<const uint4*>(ct->rep4x8) + i)
+                                                                   : __ldg(reinterpret_cast<const uint4*>(&ct->sh496[0][0]) + (i - 256 * 32 / 4));
+        if (tid == 0) sh_crc = 0;
+        __syncthreads();
+        cl.init(crc_tab, lane);
+        const uint32_t* s496 = crc_tab + 256 * 32;
+        const uint32_t* sgap = s496 + 1024;
+        if (wd.w == 1) ch = hist_tiles<1, true>(wd, p0, p1, sh_hist[warp], lane, warp, cl, s496, sgap, &last);
+        else if (wd.w == 2) ch = hist_tiles<2, true>(wd, p0, p1, sh_hist[warp], lane, warp, cl, s496, sgap, &last);
+        else ch = hist_tiles<4, true>(wd, p0, p1, sh_hist[warp], lane, warp, cl, s496, sgap, &last);
+        // lane l's chain ends 1552 + 16 l bytes into the warp's last tile
+        const uint32_t Lb = (uint32_t)((p1 - p0) * wd.w);
+        uint32_t x = crc_shift_bytes(ct, ch, Lb - (last * kTileBytes + 1552u + 16u * lane));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, o);
+        if (lane == 0 && x) atomicXor(&sh_crc, x);
+    } else {
+        if (wd.w == 1) hist_tiles<1, false>(wd, p0, p1, sh_hist[warp], lane, warp, cl, nullptr, nullptr, &last);
+        else if (wd.w == 2) hist_tiles<2, false>(wd, p0, p1, sh_hist[warp], lane, warp, cl, nullptr, nullptr, &last);
+        else hist_tiles<4, false>(wd, p0, p1, sh_hist[warp], lane, warp, cl, nullptr, nullptr, &last);
+    }
     __syncthreads();
+    if (crc && tid == 0) crcpart[wd.crc0 + k] = sh_crc;
     // block histogram
     const uint64_t b = wd.blk0 + k;
     {
@@ -824,14 +883,15 @@ __global__ void __launch_bounds__(kThreads) k_frame(const StreamDesc* __restrict
     const int s = blockIdx.x;
     const StreamDesc sd = streams[s];
     const uint64_t base = soff[s];
-    // --- CRC: the plane-0 parts of a window are the raw CRCs of consecutive
-    // B*w-byte element ranges (the last one shorter): fold them CTA-wide with
-    // byte-shift tables, then chain the windows.
+    // --- CRC: a window's parts are the raw CRCs of consecutive cunit-byte
+    // ranges (the last one shorter; k_crc's 32 KiB chunks or k_hist's
+    // plane-0 element ranges): fold them CTA-wide with byte-shift tables,
+    // then chain the windows.
     uint32_t acc = 0;
     for (uint32_t wl = 0; wl < sd.nwin; wl++) {
         const WinDesc wd = wins[sd.win0 + wl];
-        const uint64_t unit = kCrcChunk;
-        const uint64_t nfull = wd.W / kCrcChunk, rem = wd.W % kCrcChunk;
+        const uint64_t unit = wd.cunit;
+        const uint64_t nfull = wd.W / unit, rem = wd.W % unit;
         const uint32_t* cp = crcpart + wd.crc0;
         uint32_t wc = crc_combine_uniform(ct, nfull, unit, [&](uint64_t i) { return cp[i]; }, sh_red);
         if (threadIdx.x == 0) {

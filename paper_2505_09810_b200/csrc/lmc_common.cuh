@@ -35,9 +35,10 @@ struct WinDesc {
     uint32_t stream;      // owning stream
     uint32_t win_local;   // window index inside the stream
     uint32_t vec;         // 16-byte vector loads allowed (alignment of src/prev/W)
-    uint64_t crc0;        // global index of the window's first CRC chunk (k_crc)
+    uint64_t crc0;        // global index of the window's first CRC part
     uint32_t al16;        // src / prev 16-byte aligned
-    uint32_t pad;
+    uint32_t hcrc;        // 1: k_hist folds the CRC (parts = plane-0 blocks' element ranges, cunit bytes)
+    uint64_t cunit;       // bytes per CRC part (kCrcChunk for k_crc, w * B for k_hist)
 };
 
 // One stream of the batch.
@@ -85,7 +86,13 @@ struct CrcTables {
     // takes table t = (s + g) & 3 at its s-th lookup of a word, so the 32
     // lanes of every lookup instruction read 32 different banks.
     uint32_t rep4x8[256 * 32];
+    // byte-sliced shift operators for k_hist's lane chains: 496 bytes (the
+    // other lanes' pieces of a 512-byte row) and kHistTileGap bytes (the
+    // other warps' tiles between two tiles of one warp)
+    uint32_t sh496[4][256];
+    uint32_t shtile[4][256];
 };
+constexpr uint32_t kHistTileGap = (kWarps - 1) * kTileBytes + 496;
 
 // Per-lane view of rep4x8 for one word: tab[s] = table base of lookup s
 // (column 8 t + c), sel[s] = byte-perm selector of the byte that pairs with
