@@ -634,7 +634,8 @@ def measure_e2e(codec, ts, args, ws, dist, total_bytes, owned, n_total, prev=Non
     e1.record(s_d2h)
     torch.cuda.synchronize()
     if int(status.abs().sum().item()) != 0:
-        raise SystemExit("e2e decode error")
+        bad = status.nonzero().tolist()
+        raise SystemExit(f"e2e decode error: (step slot, stream) {bad[:8]} codes {[int(status[i, j]) for i, j in bad[:8]]}")
     # the payload that came back is the checkpoint
     S = sets[(args.steps - 1) % 2]
     for i, h in enumerate(host):

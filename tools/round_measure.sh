@@ -3,7 +3,7 @@
 # config, chain + pipeline benches, torchrun N=1, ncu launch list and full
 # captures (cfg2, cfg5).  Output: gpurun_out/final/
 set -u
-O=gpurun_out/final
+O=gpurun_out/${1:-final}
 mkdir -p $O/configs
 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" | tee -a $O/rc.log
 python -c "import __graft_entry__ as g; g.smoke(); print(\"smoke ok\")" > $O/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $O/rc.log
