@@ -536,7 +536,7 @@ static int compress_launch(lmcg_ctx* ctx, int n, int nwin, uint64_t nb, uint64_t
         { PROF(k_layout); k_layout<<<1, 1024, 0, st>>>(d_streams, n, o->segment_count, d_scan, d_soff, d_slen); }
     }
     if (nslots) {
-        const size_t smem = (size_t)(kStageWords + kThreads * kSlot) * sizeof(uint32_t);
+        const size_t smem = kEncSmem;
         if (smem > 48 * 1024 && !ctx->enc_attr) {
             CK(cudaFuncSetAttribute(k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             ctx->enc_attr = true;

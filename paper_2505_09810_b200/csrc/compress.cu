@@ -968,6 +968,22 @@ __device__ __forceinline__ int tile_piece(const WinDesc& wd, uint64_t tp, uint64
 // coalesced 32-bit stores.
 constexpr int kSlot = (kEncRun * kMaxLen + 31) / 32 + 1;   // private words per run
 constexpr int kStageWords = (kEncRun * kThreads * kMaxLen) / 32 + 8;
+// k_encode's dynamic shared memory: code table (256 words: len << 16 | code) |
+// staging | private slots.  The packing loops address the code table through
+// this symbol, so a lookup is one [register + constant] shared-memory load
+// (a pointer handed through the call costs a base add per lookup).
+extern __shared__ __align__(1024) uint32_t g_enc_smem[];
+// Code table entry of byte `b` (0..3) of word `w`: the table is 1 KiB aligned,
+// so base | (index * 4) is its shared-memory address -- one shift, one LOP3
+// and the load per symbol.
+__device__ __forceinline__ uint32_t code_at(uint32_t cb, uint32_t w, int b) {
+    const uint32_t a = cb | ((b == 0 ? w << 2 : w >> (8 * b - 2)) & 0x3FCu);
+    uint32_t e;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(a));
+    return e;
+}
+constexpr int kEncCodeWords = 256;
+constexpr size_t kEncSmem = (size_t)(kEncCodeWords + kStageWords + kThreads * kSlot) * sizeof(uint32_t);
 
 // RUN: the block's code has a 1-bit codeword, which canonical assignment
 // makes '0' (huffman.py:213-225), for symbol `runsym`.  Each thread then only
@@ -975,7 +991,7 @@ constexpr int kStageWords = (kEncRun * kThreads * kMaxLen) / 32 + 8;
 // bytes) and appends the run symbols between them as zero bits, instead of a
 // table lookup per symbol.
 template <int W, bool RUN>
-__device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const uint32_t* sh_code,
+__device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
                             uint32_t* sh_wsum, uint32_t* stg, uint32_t* gw, uint32_t lead,
                             uint32_t& bitpos, uint64_t& base_word, uint32_t runsym) {
     constexpr uint32_t lw = W == 1 ? 0 : (W == 2 ? 1 : 2);
@@ -1022,7 +1038,9 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
                 }
                 return a;
             };
-            uint32_t* pw = priv;
+            const uint32_t pw0 = (uint32_t)__cvta_generic_to_shared(priv);
+            uint32_t pw = pw0;   // running shared-memory address in the private slot
+            const uint32_t cb = (uint32_t)__cvta_generic_to_shared(g_enc_smem);
             uint4 cur = ld(0);
 #pragma unroll 2
             for (uint32_t j = 0; j < npc; j++) {
@@ -1031,20 +1049,21 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
                 piece_symbols(cur, W, (uint32_t)g, sy);
 #pragma unroll
                 for (int i = 0; i < per; i += 2) {
-                    const uint32_t e1 = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
-                    const uint32_t e2 = sh_code[(sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF];
+                    const uint32_t e1 = code_at(cb, sy[i >> 2], i & 3);
+                    const uint32_t e2 = code_at(cb, sy[(i + 1) >> 2], (i + 1) & 3);
                     const uint32_t l2 = e2 >> 16;
                     const uint32_t pl = (e1 >> 16) + l2;
                     acc = (acc << pl) | (((e1 & 0xFFFF) << l2) | (e2 & 0xFFFF));
                     n += pl;
-                    const bool fl = n >= 32;
-                    n -= fl ? 32 : 0;
-                    if (fl) *pw = (uint32_t)(acc >> n);
-                    pw += fl ? 1 : 0;
+                    if (n >= 32) {
+                        n -= 32;
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(pw), "r"((uint32_t)(acc >> n)) : "memory");
+                        pw += 4;
+                    }
                 }
                 cur = nxt;
             }
-            wi = (uint32_t)(pw - priv);
+            wi = (pw - pw0) >> 2;
         } else {
         // fast runs: the loads run kAhead pieces ahead of the packing (the
         // kernel is otherwise bound by load latency at its occupancy)
@@ -1097,7 +1116,7 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
                     uint32_t word = sy[0];
                     if (per > 4) word = (i >> 2) == 1 ? sy[1] : word;
                     if (per > 8) { word = (i >> 2) == 2 ? sy[2] : word; word = (i >> 2) == 3 ? sy[3] : word; }
-                    const uint32_t e = sh_code[(word >> (8 * (i & 3))) & 0xFF];
+                    const uint32_t e = g_enc_smem[(word >> (8 * (i & 3))) & 0xFF];
                     put(e >> 16, e & 0xFFFF);
                 }
                 pend += ns - last;
@@ -1107,8 +1126,8 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1, const u
 #pragma unroll
             for (int i = 0; i < per; i += 2) {
                 if (!RUN && i < ns) {
-                    const uint32_t e1 = sh_code[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
-                    const uint32_t e2 = (i + 1 < ns) ? sh_code[(sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF] : 0u;
+                    const uint32_t e1 = g_enc_smem[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
+                    const uint32_t e2 = (i + 1 < ns) ? g_enc_smem[(sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF] : 0u;
                     const uint32_t l2 = e2 >> 16;
                     const uint32_t pl = (e1 >> 16) + l2;
                     acc = (acc << pl) | (((e1 & 0xFFFF) << l2) | (e2 & 0xFFFF));
@@ -1234,8 +1253,8 @@ __device__ void store_plane(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_
 // 16 bytes, 16-byte source loads allowed.  Thread t owns payload piece k (16
 // bytes gathered from 16 W source bytes) and writes the 16-byte aligned
 // destination chunk k, which holds the end of piece k-1 (from the lane below
-// by shuffle; lane 0 gathers it again) and the start of piece k: aligned
-// 16-byte stores, no staging.  The record's first and last chunks share bytes
+// by shuffle; lane 0 takes the last piece of the warp's previous iteration)
+// and the start of piece k: aligned 16-byte stores, no staging.  The record's first and last chunks share bytes
 // with the header / the next record and are written bytewise.
 template <int W>
 __device__ __forceinline__ uint4 stored_piece(const WinDesc& wd, uint64_t sb, uint32_t g, uint32_t k) {
@@ -1269,15 +1288,22 @@ __device__ __forceinline__ uint4 chunk_of(uint4 Q, uint4 P, uint32_t lb) {
 
 template <int W>
 __device__ void store_plane_fast(const WinDesc& wd, uint64_t p0, uint64_t p1, uint8_t* d0) {
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t g = (uint32_t)plane_of(p0, wd.n, W);
     const uint64_t sb = (p0 - (uint64_t)g * wd.n) * W;   // source byte of payload byte 0
     const uint32_t K = (uint32_t)((p1 - p0) / 16);
     const uint32_t lb = (uint32_t)(reinterpret_cast<uint64_t>(d0) & 15);
     uint4* A = reinterpret_cast<uint4*>(reinterpret_cast<uint64_t>(d0) & ~15ull);
-    for (uint32_t k0 = 0; k0 < K; k0 += kThreads) {
-        const uint32_t k = k0 + tid;
-        const bool have = k < K;
+    // each warp owns a contiguous range of pieces, 32 per iteration: lane
+    // 0's neighbour piece is lane 31's of the iteration before (carried by a
+    // shuffle), gathered again only once per warp
+    const uint32_t Kw = (K + kWarps - 1) / kWarps;
+    const uint32_t ka = min(K, warp * Kw), kb = min(K, ka + Kw);
+    uint4 carry = make_uint4(0, 0, 0, 0);
+    if (lb && ka > 0 && ka < kb) carry = stored_piece<W>(wd, sb, g, ka - 1);   // (every lane: one broadcast gather)
+    for (uint32_t k0 = ka; k0 < kb; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool have = k < kb;
         const uint4 P = have ? stored_piece<W>(wd, sb, g, k) : make_uint4(0, 0, 0, 0);
         if (lb == 0) {
             if (have) A[k] = P;
@@ -1288,8 +1314,12 @@ __device__ void store_plane_fast(const WinDesc& wd, uint64_t p0, uint64_t p1, ui
         Q.y = __shfl_up_sync(0xFFFFFFFFu, P.y, 1);
         Q.z = __shfl_up_sync(0xFFFFFFFFu, P.z, 1);
         Q.w = __shfl_up_sync(0xFFFFFFFFu, P.w, 1);
+        if (lane == 0) Q = carry;
+        carry.x = __shfl_sync(0xFFFFFFFFu, P.x, 31);
+        carry.y = __shfl_sync(0xFFFFFFFFu, P.y, 31);
+        carry.z = __shfl_sync(0xFFFFFFFFu, P.z, 31);
+        carry.w = __shfl_sync(0xFFFFFFFFu, P.w, 31);
         if (!have) continue;
-        if (lane == 0 && k > 0) Q = stored_piece<W>(wd, sb, g, k - 1);
         if (k > 0) A[k] = chunk_of(Q, P, lb);
         if (k == 0 || k + 1 == K) {   // the partial chunks: bytewise
             const uint64_t lo = (uint64_t)P.x | ((uint64_t)P.y << 32), hi = (uint64_t)P.z | ((uint64_t)P.w << 32);
@@ -1313,8 +1343,8 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     uint32_t segs, const StreamDesc* __restrict__ streams, const BlockMeta* __restrict__ meta,
     const uint8_t* __restrict__ wire, const uint64_t* __restrict__ scan, const uint64_t* __restrict__ soff,
     uint8_t* __restrict__ out, uint64_t part_lo, uint64_t part_hi) {
-    extern __shared__ uint32_t stg[];
-    __shared__ uint32_t sh_code[256];
+    uint32_t* const sh_code = g_enc_smem;
+    uint32_t* const stg = g_enc_smem + kEncCodeWords;
     __shared__ uint32_t sh_cnt[kWarps][16];
     __shared__ uint32_t sh_first[16];
     __shared__ uint32_t sh_wsum[kWarps];
@@ -1417,13 +1447,13 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     // (<= 1.5 code bits per symbol on average: XOR deltas, sparse tensors)
     const uint32_t rs = ((uint64_t)m.bits * 2 <= (uint64_t)(p1 - p0) * 3) ? sh_run : 256u;
     if (rs < 256) {
-        if (w == 1) encode_runs<1, true>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
-        else if (w == 2) encode_runs<2, true>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
-        else encode_runs<4, true>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
+        if (w == 1) encode_runs<1, true>(wd, p0, p1, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
+        else if (w == 2) encode_runs<2, true>(wd, p0, p1, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
+        else encode_runs<4, true>(wd, p0, p1, sh_wsum, stg, gw, lead, bitpos, base_word, rs);
     } else {
-        if (w == 1) encode_runs<1, false>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
-        else if (w == 2) encode_runs<2, false>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
-        else encode_runs<4, false>(wd, p0, p1, sh_code, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
+        if (w == 1) encode_runs<1, false>(wd, p0, p1, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
+        else if (w == 2) encode_runs<2, false>(wd, p0, p1, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
+        else encode_runs<4, false>(wd, p0, p1, sh_wsum, stg, gw, lead, bitpos, base_word, 0);
     }
     // trailing partial word: bytes up to the record end
     if (tid == 0 && bitpos) {

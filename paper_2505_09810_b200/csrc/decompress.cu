@@ -1352,6 +1352,42 @@ __device__ bool warp_scan(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t& 
     return __all_sync(0xFFFFFFFFu, ok);
 }
 
+// Stored-grid shortcut for a span [pa, pe): a plane that does not compress
+// (the low byte plane of bf16 weights) is a run of full stored records, each
+// 5 + B bytes, so its records sit on the (B + 5)-byte grid from the segment
+// start.  If every grid position whose record would cover a byte of the span
+// holds a full stored header (mode 0, len B, payload inside the segment),
+// the span's candidates are the grid positions inside it and its payload
+// bytes are not read.  If those headers are not the segment's real records
+// (payload bytes that look like them), record starts inside the span are
+// missed, the chain does not verify (k_verify / k_resolve) and k_fallback
+// walks the segment: the result is the same, only slower.  Returns false
+// when the span is not of this shape (the caller scans it).
+template <class Emit>
+__device__ __forceinline__ bool stored_grid_span(const DecSeg& sg, uint64_t pa, uint64_t pe, uint32_t& cnt, int lane,
+                                                 Emit emit) {
+    const uint32_t B = sg.block;
+    const uint64_t G = (uint64_t)B + 5;
+    const uint64_t k_lo = pa / G, k_hi = (pe - 1) / G;
+    if (k_hi - k_lo >= 32) return false;
+    const uint64_t p = (k_lo + lane) * G;
+    const bool mine = k_lo + lane <= k_hi;
+    const uint32_t Ltail = (uint32_t)(sg.orig - (uint64_t)(sg.nrec - 1) * B);
+    // each of them a full candidate (is_cand: the successor header too), so
+    // that bit streams of delta payloads -- long zero runs with a stray 02 and
+    // 01 byte look like "stored | B" about once in 1e5 positions -- do not
+    // send segments to the serial walk
+    bool good = true;
+    if (mine) good = p + G <= sg.comp && sg.base[p] == MODE_STORED && is_cand(sg.base, sg.comp, p, B, Ltail);
+    if (!__all_sync(0xFFFFFFFFu, good)) return false;
+    // (position 0 is listed by the caller, as in warp_scan)
+    const bool in = mine && p >= max(pa, (uint64_t)1) && p < pe;
+    const uint32_t m = __ballot_sync(0xFFFFFFFFu, in);
+    if (in) emit(p, cnt + __popc(m & ((1u << lane) - 1)));
+    cnt += __popc(m);
+    return true;
+}
+
 // Owner maps (chunk -> segment, record slot -> segment, output tile ->
 // window): one load per CTA in the kernels below instead of a binary search
 // of dependent loads.  Unowned capacity slots keep the ~0u of the memset.
@@ -1401,7 +1437,10 @@ __global__ void __launch_bounds__(kThreads) k_cand(const DecSeg* __restrict__ se
         n = 1;
     }
     bool ok = true;
-    if (pa < pe) ok = warp_scan(sg, pa, pe, n, lane, [&](uint64_t p, uint32_t r) { if (r < kSpanCap) list[r] = (uint32_t)p; });
+    if (pa < pe) {
+        auto put = [&](uint64_t p, uint32_t r) { if (r < kSpanCap) list[r] = (uint32_t)p; };
+        if (!stored_grid_span(sg, pa, pe, n, lane, put)) ok = warp_scan(sg, pa, pe, n, lane, put);
+    }
     if (lane == 0) {
         ccnt[span] = ok ? n : kDense;
         wcnt[warp] = ok ? n : kDense;

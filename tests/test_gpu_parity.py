@@ -301,6 +301,41 @@ def test_false_candidates_inside_payload(codec):
     assert r.status == [0] and host_bytes(r.payload(0)) == data
 
 
+def test_false_stored_grid_inside_payload(codec):
+    # k_cand's stored-grid shortcut trusts full stored headers on the (B + 5)
+    # grid from the segment start.  Here the first record is RLE (6 bytes), so
+    # every real record is off the grid, while the stored payloads carry fake
+    # "stored | B" headers exactly on it: spans take the shortcut, miss the
+    # real record starts, the chain does not verify and the serial walk
+    # decides.  The payload must still come back exactly.
+    B = 4096
+    rng = np.random.default_rng(11)
+    data = bytearray(rng.integers(0, 256, 40 * B, dtype=np.uint8).tobytes())
+    data[0:B] = bytes(B)                               # block 0: RLE record
+    fake = bytes([2]) + B.to_bytes(4, "little")
+    for k in range(1, 40):
+        # grid position k (B + 5) lies 4095 bytes into record k: payload offset 4090
+        data[k * B + 4090: k * B + 4095] = fake
+    data = bytes(data)
+    s = O.compress(data, 0, byte_group=False, block_size=B)
+    G = B + 5
+    seg0 = s.index(bytes([1]) + B.to_bytes(4, "little") + b"\x00")   # the RLE record = segment start
+    assert all(s[seg0 + k * G: seg0 + k * G + 5] == fake for k in range(1, 39))
+    b = codec.compress([dev_bytes(data)], element_types=[0], byte_group=False, block_size=B)
+    assert b.to_bytes()[0] == s
+    fallback_segments(codec)
+    r = codec.decompress(b)
+    assert r.status == [0] and host_bytes(r.payload(0)) == data
+    assert fallback_segments(codec) == 1
+    # and the real shape of the shortcut: every block stored, records on the grid
+    data2 = rng.integers(0, 256, 40 * B, dtype=np.uint8).tobytes()
+    b2 = codec.compress([dev_bytes(data2)], element_types=[0], byte_group=False, block_size=B)
+    assert b2.to_bytes()[0] == O.compress(data2, 0, byte_group=False, block_size=B)
+    r2 = codec.decompress(b2)
+    assert r2.status == [0] and host_bytes(r2.payload(0)) == data2
+    assert fallback_segments(codec) == 0
+
+
 @pytest.mark.parametrize("et", [ET.RAW8, ET.BF16, ET.FP32])
 @pytest.mark.parametrize("density", [0.002, 0.03, 0.2])
 def test_run_symbol_paths(codec, et, density):
