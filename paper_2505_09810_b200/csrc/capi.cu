@@ -162,7 +162,7 @@ void build_crc_tables(CrcTables& t) {
                 t.pow2[m][byte][b] = c ? h_multmodp(p, c) : 0;
             }
     }
-    shift_table(496, t.sh496);
+    shift_table(512, t.sh512);
     shift_table(kHistTileGap, t.shtile);
 }
 

@@ -161,16 +161,18 @@ __global__ void __launch_bounds__(kCrcThreads, 2) k_crc(const WinDesc* __restric
 // The warp-tiles of one block for element width W (compile-time: the plane
 // gather and the per-piece symbol count are then static).
 // CRC: (plane-0 blocks of hcrc windows) lane l folds its pieces -- 16 bytes
-// at 512 q + 16 l of each of the warp's tiles, in byte order -- into one
-// chain: a 496-byte shift between the pieces of a tile, kHistTileGap between
-// the warp's tiles; *last = the warp's last tile.  (One 64-byte run per lane
-// and tile instead -- one shift per tile -- measured slower: 8.98 vs 8.74 ms
-// on cfg5, the strided loads cost more than the shifts.)
+// at 512 q + 16 l of each of the warp's tiles -- into four chains, one per
+// row q (independent table lookups in flight: one chain through all rows was
+// bound by the latency of its dependent lookups), each shifted by
+// kHistTileGap between the warp's tiles; the chains are merged with 512-byte
+// shifts at the end; *last = the warp's last tile.  (One 64-byte run per
+// lane and tile instead -- one shift per tile -- measured slower: the strided
+// loads cost more than the shifts.)
 template <int W, bool CRC>
 __device__ __forceinline__ uint32_t hist_tiles(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_t* hist, int lane, int warp,
-                                               const Crc4x8Lane& cl, const uint32_t* s496, const uint32_t* sgap,
+                                               const Crc4x8Lane& cl, const uint32_t* s512, const uint32_t* sgap,
                                                uint32_t* last) {
-    uint32_t ch = 0;
+    uint32_t ch[4] = {0u, 0u, 0u, 0u};
     auto shift = [](const uint32_t* t, uint32_t x) {
         return t[x & 0xFF] ^ t[256 + ((x >> 8) & 0xFF)] ^ t[512 + ((x >> 16) & 0xFF)] ^ t[768 + (x >> 24)];
     };
@@ -178,26 +180,30 @@ __device__ __forceinline__ uint32_t hist_tiles(const WinDesc& wd, uint64_t p0, u
     constexpr uint64_t T = kTileBytes >> lw;    // positions per warp-tile
     constexpr int per = 16 / W;                 // symbols per 16-byte piece
     const uint64_t ntiles = (p1 - p0 + T - 1) / T;
+    const uint64_t g0 = plane_of(p0, wd.n, W);
+    const bool one = p1 <= (g0 + 1) * wd.n;   // the block lies in one plane (the usual case)
     for (uint64_t t = warp; t < ntiles; t += kWarps) {
         const uint64_t tp = p0 + t * T;
         const uint64_t te = min(tp + T, p1);
-        const uint64_t g = plane_of(tp, wd.n, W);
-        const bool fast = wd.vec && (te - tp == T) && (te <= (g + 1) * wd.n);
+        const uint64_t g = one ? g0 : plane_of(tp, wd.n, W);
+        const bool fast = wd.vec && (te - tp == T) && (one || te <= (g + 1) * wd.n);
         if (fast) {
             const uint64_t base = ((tp - g * wd.n) << lw) + 16ull * lane;
             uint4 a[4];
 #pragma unroll
             for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, base + 512ull * q);
             if (CRC) {
-                ch = shift(sgap, ch);   // (no-op on the warp's first tile: ch == 0)
+                // four chains (one per row q): independent lookups in flight
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    if (q) ch = shift(s496, ch);
-                    ch = cl.word(ch, a[q].x);
-                    ch = cl.word(ch, a[q].y);
-                    ch = cl.word(ch, a[q].z);
-                    ch = cl.word(ch, a[q].w);
-                }
+                for (int q = 0; q < 4; q++) ch[q] = shift(sgap, ch[q]);   // (no-op on the warp's first tile: ch == 0)
+#pragma unroll
+                for (int q = 0; q < 4; q++) ch[q] = cl.word(ch[q], a[q].x);
+#pragma unroll
+                for (int q = 0; q < 4; q++) ch[q] = cl.word(ch[q], a[q].y);
+#pragma unroll
+                for (int q = 0; q < 4; q++) ch[q] = cl.word(ch[q], a[q].z);
+#pragma unroll
+                for (int q = 0; q < 4; q++) ch[q] = cl.word(ch[q], a[q].w);
                 *last = (uint32_t)t;
             }
 #pragma unroll
@@ -205,27 +211,35 @@ __device__ __forceinline__ uint32_t hist_tiles(const WinDesc& wd, uint64_t p0, u
                 uint32_t sy[4];
                 piece_symbols(a[q], W, (uint32_t)g, sy);
 #pragma unroll
-                for (int i = 0; i < per; i++) atomicAdd(&hist[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF], 1u);
+                for (int i = 0; i < per; i++) atomicAdd(&hist[((sy[i >> 2] >> (8 * (i & 3))) & 0xFF) << 5], 1u);
             }
         } else {
             // slow gather: lane owns positions [tp + lane*T/32, ...)
             constexpr uint64_t pl = T / 32;
             const uint64_t a = tp + lane * pl, bnd = min(a + pl, te);
-            for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p)], 1u);
+            for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p) << 5], 1u);
         }
     }
-    return ch;
+    // row q + 1's piece lies 512 bytes after row q's
+    return CRC ? shift(s512, shift(s512, shift(s512, ch[0]) ^ ch[1]) ^ ch[2]) ^ ch[3] : 0u;
 }
 
-// k_hist's dynamic shared memory: rep4x8 | sh496 | shtile (CRC folding)
-constexpr size_t kHistSmem = (256 * 32 + 2 * 1024) * sizeof(uint32_t);
+// k_hist's dynamic shared memory: rep4x8 | sh512 | shtile (CRC folding) |
+// the CTA's bins.  Bin of symbol s for lane l (of any warp): word 32 s + l, so
+// lane l only ever touches bank l: the shared atomics of a warp never
+// conflict, whatever the symbols (warp-private 256-word bins took 3.1
+// wavefronts per atomic on the near-uniform planes, 2 on the exponent planes
+// whose symbols 52.. and 180.. share banks).
+constexpr int kHistCrcWords = 256 * 32 + 2 * 1024;
+constexpr int kHistBinWords = 256 * 32;
+constexpr size_t kHistSmem = (size_t)(kHistCrcWords + kHistBinWords) * sizeof(uint32_t);
 
 __global__ void __launch_bounds__(kThreads, 3) k_hist(
     const WinDesc* __restrict__ wins, const uint32_t* __restrict__ slot2win, uint64_t nslots, uint32_t B,
     uint32_t* __restrict__ hist_out, BlockMeta* __restrict__ meta, uint64_t part_lo, uint64_t part_hi,
     const CrcTables* __restrict__ ct, uint32_t* __restrict__ crcpart) {
     extern __shared__ __align__(16) uint32_t crc_tab[];
-    __shared__ uint32_t sh_hist[kWarps][256];
+    uint32_t* const bins = crc_tab + kHistCrcWords;
     __shared__ uint32_t sh_crc;
     const uint64_t slot = blockIdx.x;
     if (slot >= nslots) return;
@@ -235,11 +249,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist(
     const uint64_t k = (uint64_t)kk;
     if (wd.blk0 + k < part_lo || wd.blk0 + k >= part_hi) return;   // outside the part (lmcg_compress_part)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int i = tid; i < kWarps * 256; i += kThreads) (&sh_hist[0][0])[i] = 0;
+    for (int i = tid; i < kHistBinWords / 4; i += kThreads) reinterpret_cast<uint4*>(bins)[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
 
     const uint64_t p0 = k * B;
     const uint64_t p1 = min(wd.W, p0 + B);
+    if (tid == 32 && p1 <= (plane_of(p0, wd.n, wd.w) + 1) * wd.n) {
+        // the block's source elements (one plane): on their way to L2 before the first loads
+        const uint64_t e0 = p0 - plane_of(p0, wd.n, wd.w) * wd.n;
+        prefetch_l2(wd.src + e0 * wd.w, (uint32_t)((p1 - p0) * wd.w));
+        if (wd.prev) prefetch_l2(wd.prev + e0 * wd.w, (uint32_t)((p1 - p0) * wd.w));
+    }
     // the plane-0 block of an hcrc window folds the raw CRC of its element
     // range (every source byte of it passes through its tiles); part runs
     // (lmcg_compress_part) take their CRC from k_crc
@@ -247,17 +267,17 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist(
     Crc4x8Lane cl;
     uint32_t ch = 0, last = 0;
     if (crc) {
-        for (int i = tid; i < (256 * 32 + 2 * 1024) / 4; i += kThreads)
+        for (int i = tid; i < kHistCrcWords / 4; i += kThreads)
             reinterpret_cast<uint4*>(crc_tab)[i] = i < 256 * 32 / 4 ? __ldg(reinterpret_cast<const uint4*>(ct->rep4x8) + i)
-                                                                   : __ldg(reinterpret_cast<const uint4*>(&ct->sh496[0][0]) + (i - 256 * 32 / 4));
+                                                                   : __ldg(reinterpret_cast<const uint4*>(&ct->sh512[0][0]) + (i - 256 * 32 / 4));
         if (tid == 0) sh_crc = 0;
         __syncthreads();
         cl.init(crc_tab, lane);
-        const uint32_t* s496 = crc_tab + 256 * 32;
-        const uint32_t* sgap = s496 + 1024;
-        if (wd.w == 1) ch = hist_tiles<1, true>(wd, p0, p1, sh_hist[warp], lane, warp, cl, s496, sgap, &last);
-        else if (wd.w == 2) ch = hist_tiles<2, true>(wd, p0, p1, sh_hist[warp], lane, warp, cl, s496, sgap, &last);
-        else ch = hist_tiles<4, true>(wd, p0, p1, sh_hist[warp], lane, warp, cl, s496, sgap, &last);
+        const uint32_t* s512 = crc_tab + 256 * 32;
+        const uint32_t* sgap = s512 + 1024;
+        if (wd.w == 1) ch = hist_tiles<1, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
+        else if (wd.w == 2) ch = hist_tiles<2, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
+        else ch = hist_tiles<4, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
         // lane l's chain ends 1552 + 16 l bytes into the warp's last tile
         const uint32_t Lb = (uint32_t)((p1 - p0) * wd.w);
         uint32_t x = crc_shift_bytes(ct, ch, Lb - (last * kTileBytes + 1552u + 16u * lane));
@@ -265,18 +285,18 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist(
         for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, o);
         if (lane == 0 && x) atomicXor(&sh_crc, x);
     } else {
-        if (wd.w == 1) hist_tiles<1, false>(wd, p0, p1, sh_hist[warp], lane, warp, cl, nullptr, nullptr, &last);
-        else if (wd.w == 2) hist_tiles<2, false>(wd, p0, p1, sh_hist[warp], lane, warp, cl, nullptr, nullptr, &last);
-        else hist_tiles<4, false>(wd, p0, p1, sh_hist[warp], lane, warp, cl, nullptr, nullptr, &last);
+        if (wd.w == 1) hist_tiles<1, false>(wd, p0, p1, bins + lane, lane, warp, cl, nullptr, nullptr, &last);
+        else if (wd.w == 2) hist_tiles<2, false>(wd, p0, p1, bins + lane, lane, warp, cl, nullptr, nullptr, &last);
+        else hist_tiles<4, false>(wd, p0, p1, bins + lane, lane, warp, cl, nullptr, nullptr, &last);
     }
     __syncthreads();
     if (crc && tid == 0) crcpart[wd.crc0 + k] = sh_crc;
     // block histogram
     const uint64_t b = wd.blk0 + k;
     {
-        uint32_t sum = 0;
+        uint32_t sum = 0;   // thread s sums symbol s's 32 lane counters, skewed across the banks
 #pragma unroll
-        for (int q = 0; q < kWarps; q++) sum += sh_hist[q][tid];
+        for (int q = 0; q < 32; q++) sum += bins[32 * tid + ((q + tid) & 31)];
         hist_out[b * 256 + tid] = sum;
     }
     if (tid == 0) {

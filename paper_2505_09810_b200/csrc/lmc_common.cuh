@@ -86,13 +86,13 @@ struct CrcTables {
     // takes table t = (s + g) & 3 at its s-th lookup of a word, so the 32
     // lanes of every lookup instruction read 32 different banks.
     uint32_t rep4x8[256 * 32];
-    // byte-sliced shift operators for k_hist's lane chains: 496 bytes (the
-    // other lanes' pieces of a 512-byte row) and kHistTileGap bytes (the
-    // other warps' tiles between two tiles of one warp)
-    uint32_t sh496[4][256];
+    // byte-sliced shift operators for k_hist's lane chains: 512 bytes (from
+    // one row's piece to the next row's) and kHistTileGap bytes (from the end
+    // of a piece to the piece of the same row in the warp's next tile)
+    uint32_t sh512[4][256];
     uint32_t shtile[4][256];
 };
-constexpr uint32_t kHistTileGap = (kWarps - 1) * kTileBytes + 496;
+constexpr uint32_t kHistTileGap = kWarps * kTileBytes - 16;
 
 // Per-lane view of rep4x8 for one word: tab[s] = table base of lookup s
 // (column 8 t + c), sel[s] = byte-perm selector of the byte that pairs with
