@@ -278,12 +278,20 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist(
         if (wd.w == 1) ch = hist_tiles<1, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
         else if (wd.w == 2) ch = hist_tiles<2, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
         else ch = hist_tiles<4, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
-        // lane l's chain ends 1552 + 16 l bytes into the warp's last tile
+        // lane l's chain ends 1552 + 16 (l + 1) bytes into the warp's last
+        // tile: a Horner tree over the lanes (fixed shifts of 16 << k bytes),
+        // then lane 31 shifts the warp's value to the end of the block
         const uint32_t Lb = (uint32_t)((p1 - p0) * wd.w);
-        uint32_t x = crc_shift_bytes(ct, ch, Lb - (last * kTileBytes + 1552u + 16u * lane));
+        uint32_t x = ch;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) x ^= __shfl_xor_sync(0xFFFFFFFFu, x, o);
-        if (lane == 0 && x) atomicXor(&sh_crc, x);
+        for (int q = 0; q < 5; q++) {
+            const uint32_t y = crc_shift_tab(&ct->shift[q][0][0], __shfl_xor_sync(0xFFFFFFFFu, x, 1 << q));
+            if (lane & (1 << q)) x ^= y;
+        }
+        if (lane == 31) {
+            x = crc_shift_bytes(ct, x, Lb - (last + 1) * kTileBytes);
+            if (x) atomicXor(&sh_crc, x);
+        }
     } else {
         if (wd.w == 1) hist_tiles<1, false>(wd, p0, p1, bins + lane, lane, warp, cl, nullptr, nullptr, &last);
         else if (wd.w == 2) hist_tiles<2, false>(wd, p0, p1, bins + lane, lane, warp, cl, nullptr, nullptr, &last);
