@@ -263,7 +263,7 @@ constexpr int kCheckpoints = 3;  // at 128, 256 and 512 bits into a chunk
 
 struct DecSmem {
     uint32_t lut3[1 << kLut];           // tl(4)|pad(2)|n(2)|s3(8)|s2(8)|s1(8); 0: slow path (long or invalid prefix)
-    uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0
+    uint16_t lut1[1 << kLut];           // (len << 8) | sym for codes <= kLut bits, else 0; entry i at lut1_at(i)
     uint8_t lutc[1 << kCntLut];         // count passes: n(4) | tl(4) of the whole codewords in a 12-bit window
     uint32_t bm[2][kThreads];           // pass-0 boundary bitmaps (first 64 bits of each chunk)
     uint32_t cp[kCheckpoints][kThreads];  // pass-0 checkpoints: (offset from p0) << 16 | symbol count
@@ -275,7 +275,6 @@ struct DecSmem {
     uint32_t wsum[kWarps];
     uint32_t kraft;
     int minlen, maxlen, lgcd;
-    uint64_t mbar;                      // TMA staging of the payload
     alignas(16) uint32_t bits[4];       // staged bitstream (TMA of the 16-byte aligned cover), big-endian
                                         // words; extends to the end of the dynamic shared memory
 };
@@ -286,8 +285,26 @@ __host__ __device__ constexpr size_t dec_smem_bytes(uint32_t stage) { return siz
 // shared memory; the decoder addresses it through this symbol, so table and
 // staging lookups are [register + constant] shared-memory loads (a DecSmem&
 // handed through a call would cost a base-register add per lookup).
+// lut1 is stored swizzled: entry i at i ^ (((i >> 6) & 31) << 1), i.e. the
+// bank of an entry is bits 1..5 XOR bits 6..10 of its index.  The table
+// builds look it up at (e << tl) & mask for the consecutive e of a warp (a
+// power-of-two stride: up to 32 lanes in one bank of the plain layout, 8-11
+// wavefronts per lookup measured); any five consecutive index bits now select
+// five different bank bits, so those lookups are conflict-free.
+__device__ __forceinline__ uint32_t lut1_at(uint32_t i) { return i ^ ((i >> 5) & 0x3Eu); }
 extern __shared__ __align__(16) uint8_t g_dsmem[];
 __device__ __forceinline__ DecSmem& dec_smem() { return *reinterpret_cast<DecSmem*>(g_dsmem); }
+// The mbarrier of the payload bulk copy lives in the last 16 bytes of the
+// dynamic shared memory (after the staging area: nothing else ever uses
+// them) and is invalidated after every wait.  It used to sit inside DecSmem,
+// which k_decpair overlays with its CRC tables after the decode: about one
+// decompress in 300 then found the 8 bytes of barrier state written back over
+// the table words in many CTAs at once (CRC-only IntegrityErrors on correct
+// payloads) -- PTX requires mbarrier.inval before the memory of a barrier
+// object is used for anything else.
+__device__ __forceinline__ uint64_t* tma_bar(uint32_t stage_cap) {
+    return reinterpret_cast<uint64_t*>(g_dsmem + sizeof(DecSmem) + stage_cap);
+}
 
 // Payload bit source: big-endian words, bit i of the payload is bit
 // 31 - ((i + sh) & 31) of word (i + sh) >> 5; staged in shared memory when
@@ -326,7 +343,7 @@ struct Src {
 
 // One codeword at the window: returns its length (0 = invalid prefix).
 __device__ __forceinline__ uint32_t step1(const DecSmem& s, uint32_t win, uint32_t& sym) {
-    const uint32_t e = s.lut1[win >> (32 - kLut)];
+    const uint32_t e = s.lut1[lut1_at(win >> (32 - kLut))];
     if (e) {
         sym = e & 0xFF;
         return e >> 8;
@@ -866,7 +883,7 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
                 uint32_t h = ~0u, cnt2 = 0;
                 const uint32_t e2 = decode_span<false, STAGED, RUN>(s, src, my_start, lim, p0, 2, cnt2, nullptr, &h);
                 DBG_ADD(6, h == ~0u);
-#ifdef LMCG_DEBUG
+#if defined(LMCG_DEBUG) && !defined(LMCG_CHECK_TABLES)
                 if (h == ~0u) {
                     const unsigned long long k = atomicAdd(&lmcg_dbg[10], 1ull);
                     if (k < 512) {
@@ -933,6 +950,9 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
+__device__ __forceinline__ void mbar_inval(uint64_t* bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait0(uint64_t* bar) {
     asm volatile("{\n .reg .pred P;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P, [%0], 0;\n @!P bra WAIT_%=;\n}\n"
                  ::"r"(smem_u32(bar)) : "memory");
@@ -969,8 +989,8 @@ __device__ bool huff_decode(DecSmem& /* the caller's view of dec_smem() */, cons
     const uint64_t e16 = (reinterpret_cast<uint64_t>(data0) + ((uint64_t)bits0 + 7) / 8 + 15) & ~15ull;
     const bool staged = bits0 != 0 && e16 - a16 <= (uint64_t)stage_cap;
     if (staged && tid == 0) {
-        mbar_init1(&s.mbar);
-        tma_load_1d(s.bits, reinterpret_cast<const void*>(a16), (uint32_t)(e16 - a16), &s.mbar);
+        mbar_init1(tma_bar(stage_cap));
+        tma_load_1d(s.bits, reinterpret_cast<const void*>(a16), (uint32_t)(e16 - a16), tma_bar(stage_cap));
     }
     const uint8_t wb = pl[tid >> 1];
     const uint32_t l = (tid & 1) ? (wb >> 4) : (wb & 15);
@@ -1023,7 +1043,11 @@ __device__ bool huff_decode(DecSmem& /* the caller's view of dec_smem() */, cons
     const uint32_t bits = rd32(pl + 128);
     // _validate_codebook (huffman.py:191-210) and decode_block's bit-length check (:275)
     if (s.maxlen == 0 || s.kraft > (1u << kMaxLen) || bits == 0) {
-        if (staged) mbar_wait0(&s.mbar);   // no bulk copy left in flight
+        if (staged) {   // no bulk copy left in flight, no live barrier object
+            mbar_wait0(tma_bar(stage_cap));
+            __syncthreads();
+            if (tid == 0) mbar_inval(tma_bar(stage_cap));
+        }
         return false;
     }
     if (l) {
@@ -1055,7 +1079,7 @@ __device__ bool huff_decode(DecSmem& /* the caller's view of dec_smem() */, cons
                 q++;
                 if (q <= qmax) { fl = s.first_left[q]; endq = fl + (s.bl_count[q] << (kMaxLen - q)); base = s.first_idx[q]; }
             }
-            s.lut1[e] = q <= qmax ? (uint16_t)((q << 8) | s.csym[base + ((v - fl) >> (kMaxLen - q))]) : (uint16_t)0;
+            s.lut1[lut1_at((uint32_t)e)] = q <= qmax ? (uint16_t)((q << 8) | s.csym[base + ((v - fl) >> (kMaxLen - q))]) : (uint16_t)0;
         }
     }
     __syncthreads();
@@ -1064,7 +1088,7 @@ __device__ bool huff_decode(DecSmem& /* the caller's view of dec_smem() */, cons
         uint32_t ent = 0, n = 0, tl = 0, syms = 0;
         uint32_t rest = (uint32_t)e;
         while (n < 3) {
-            const uint32_t a = s.lut1[rest & ((1u << kLut) - 1)];
+            const uint32_t a = s.lut1[lut1_at(rest & ((1u << kLut) - 1))];
             const uint32_t la = a >> 8;
             if (!a || tl + la > kLut) break;
             syms |= (a & 0xFF) << (8 * n);
@@ -1085,7 +1109,7 @@ __device__ bool huff_decode(DecSmem& /* the caller's view of dec_smem() */, cons
         uint32_t n = (e3 >> 24) & 3, tl = e3 >> 28;
         for (;;) {
             const uint32_t rest = ((uint32_t)e << tl) & ((1u << kCntLut) - 1);
-            const uint32_t a = s.lut1[rest >> (kCntLut - kLut)];
+            const uint32_t a = s.lut1[lut1_at(rest >> (kCntLut - kLut))];
             const uint32_t la = a >> 8;
             if (!a || tl + la > kCntLut) break;
             n++;
@@ -1099,10 +1123,11 @@ __device__ bool huff_decode(DecSmem& /* the caller's view of dec_smem() */, cons
     if (staged) {
         // the staged words in memory order -> big-endian words (bit i of the
         // payload is bit 31 - ((i + sh) & 31) of word (i + sh) >> 5)
-        mbar_wait0(&s.mbar);
+        mbar_wait0(tma_bar(stage_cap));
         const uint32_t nw = (uint32_t)((e16 - a16) / 4);
         for (uint32_t j = tid; j < nw; j += kThreads) s.bits[j] = bswap32(s.bits[j]);
         __syncthreads();
+        if (tid == 0) mbar_inval(tma_bar(stage_cap));   // (every thread is past its wait)
         Src St;
         St.sw = s.bits;
         St.gbase = reinterpret_cast<const uint8_t*>(a16);
@@ -1684,7 +1709,7 @@ __global__ void k_pairs(const DecSeg* __restrict__ segs, const uint32_t* __restr
 // 16 plane bytes at element offset e (a multiple of 16) of a pair's plane
 __device__ __forceinline__ uint4 plane16(const uint8_t* p, uint32_t mode, uint32_t rle, uint32_t e, uint32_t B) {
     if (mode == MODE_RLE) return make_uint4(rle, rle, rle, rle);
-    if (mode == MODE_HUFFMAN) return *reinterpret_cast<const uint4*>(p + e);   // ring slot (L2)
+    if (mode == MODE_HUFFMAN) return __ldcg(reinterpret_cast<const uint4*>(p + e));   // ring slot (L2; never through L1)
     const uint64_t a = reinterpret_cast<uint64_t>(p) + e;                      // stored payload, any alignment
     if ((a & 15) == 0) return __ldcs(reinterpret_cast<const uint4*>(a));
     const uint32_t sh = (uint32_t)(a & 3) * 8;
@@ -1866,6 +1891,28 @@ __global__ void __launch_bounds__(kThreads, 4) k_decpair(const DecSeg* __restric
             tile_crc[pi.tile0 + k * T + tid] = acc;
         }
         DBG_TADD(22, t_il);
+#ifdef LMCG_CHECK_TABLES
+        {   // experiment: are the CRC tables in shared memory still intact after the interleave?
+            uint32_t badw = 0, first = ~0u, got = 0, want = 0;
+            for (int i = tid; i < kCrcRepWords + 1024; i += kThreads) {
+                const uint32_t wv = i < kCrcRepWords ? __ldg(ct->rep4x8 + i) : __ldg(sh992 + (i - kCrcRepWords));
+                if (crctab[i] != wv) {
+                    if (!badw) { first = i; got = crctab[i]; want = wv; }
+                    badw++;
+                }
+            }
+            if (badw) {
+                atomicAdd(&lmcg_fallback_segs, (unsigned long long)badw);
+#ifdef LMCG_DEBUG
+                const unsigned long long kq = atomicAdd(&lmcg_dbg[31], 1ull);
+                if (kq < 512) {
+                    unsigned long long* e = lmcg_dbg_ev + 8 * kq;
+                    e[0] = blockIdx.x; e[1] = tid; e[2] = first; e[3] = badw; e[4] = got; e[5] = want; e[6] = p; e[7] = clock64();
+                }
+#endif
+            }
+        }
+#endif
     }
 }
 
