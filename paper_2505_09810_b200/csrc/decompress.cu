@@ -667,9 +667,15 @@ __device__ __forceinline__ void bb_adv(BitBuf& b, const uint32_t* sw, uint32_t l
 // bits into the bitmap, checkpoints (the first lookup end at or after
 // p0 + 128 / 256 / 512 bits, with the symbol count there) for the fix-up
 // rounds, and the count.  Returns the first boundary >= lim (~0u: invalid).
+// After its chunk the thread keeps decoding single codewords and marks the
+// boundaries of its path inside the first 32 bits of the next chunk (np0 =
+// that chunk's speculative start, ~0u: none) in `ov`, stopping at the first
+// one that is also a boundary of the next chunk's own pass-0 path (its bitmap
+// comes from lane + 1 by shuffle; lane 31 walks the 32 bits): the fix-up of the
+// next chunk is then bit arithmetic on the two bitmaps (huff_passes).
 template <int K>
 __device__ __forceinline__ uint32_t pass0_lean(DecSmem& s, const uint32_t* sw, uint32_t sh, uint32_t p0, uint32_t lim,
-                                               uint32_t& count) {
+                                               uint32_t& count, uint32_t np0, uint32_t bits, uint32_t& ov) {
     constexpr unsigned mask = 0xFFFFFFFFu;   // called by every thread (an empty chunk: p0 == lim)
     const int tid = threadIdx.x;
     BitBuf b;
@@ -743,6 +749,32 @@ __device__ __forceinline__ uint32_t pass0_lean(DecSmem& s, const uint32_t* sw, u
         }
     }
     count = c;
+    {
+        const int lane = tid & 31;
+        // the next chunk's speculative boundaries (bit 0: its start), relative to np0
+        uint32_t mnext = __shfl_down_sync(mask, m0 | 1u, 1);
+        if (lane == 31) mnext = 0;
+        const uint32_t pend = pos;
+        uint32_t o = 0;
+        const uint32_t stop = np0 == ~0u ? 0u : min(np0 + 32, bits);
+        act = !bad && np0 != ~0u && pos < stop;
+        while (__any_sync(mask, act)) {
+            if (act) {
+                bool hit = false;
+                if (pos >= np0) {
+                    o |= 1u << (pos - np0);
+                    hit = (mnext >> (pos - np0)) & 1u;
+                }
+                uint32_t sym;
+                const uint32_t l = hit ? 0u : step1(s, bb_win(b), sym);
+                bb_adv(b, sw, l);
+                pos += l;
+                act = l != 0 && pos < stop;
+            }
+        }
+        ov = o;
+        pos = pend;
+    }
     return bad ? ~0u : pos;
 }
 
@@ -847,13 +879,18 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
             my_start = p0;
         }
         const bool work = c < nch && my_start < lim;
-        uint32_t cnt = 0;
-        const uint32_t e = pass0_lean<3>(s, src.sw, src.sh, work ? my_start : 0u, work ? lim : 0u, cnt);
+        uint32_t cnt = 0, ov = 0, np0 = ~0u;
+        if (work && c + 1 < nch) {
+            np0 = (c + 1) * S;
+            if (gq > 1) np0 = ((np0 + gq - 1) / gq) * gq;
+        }
+        const uint32_t e = pass0_lean<3>(s, src.sw, src.sh, work ? my_start : 0u, work ? lim : 0u, cnt, np0, bits, ov);
         if (c < nch) {
             my_end = work ? e : my_start;
             my_cnt = cnt;
             s.end[c] = my_end;
         }
+        s.bm[1][tid] = ov;   // (for the bitmap fix-up below; zero again before the general rounds)
     } else if (c < nch) {
         p0 = c * S;
         if (gq > 1) p0 = ((p0 + gq - 1) / gq) * gq;
@@ -865,10 +902,36 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
     __syncthreads();
     DBG_TADD(18, t_p0);
     DBG_T0(t_fix);
+    const uint32_t p0_end = my_end, p0_cnt = my_cnt;   // the pass-0 path's end and count
+    if (STAGED && !RUN) {
+        // Bitmap fix-up: chunk c's true path starts at its predecessor's end
+        // pe.  A = the boundaries of c's pass-0 path in its first 32 bits (bit
+        // 0: its start), Bm = the predecessor's path there (pass0_lean's
+        // overshoot).  The paths merge at the first common boundary x: the
+        // codewords of the true path that start in [pe, x) replace those of
+        // the pass-0 path that start before x; the end stays.  Chunks that do
+        // not merge inside their 32 bits (or inside the chunk) are left to
+        // the general rounds below, which also re-check every start.
+        uint32_t pe = ~0u, Bm = 0;
+        if (c < nch && c > 0) { pe = s.end[c - 1]; Bm = s.bm[1][tid - 1]; }
+        __syncthreads();
+        s.bm[1][tid] = 0;
+        if (c < nch && c > 0 && pe != ~0u && pe != my_start && my_end != ~0u && pe >= p0 && my_start < lim) {
+            const uint32_t A = s.bm[0][tid] | 1u;
+            const uint32_t X = A & Bm;
+            if (X) {
+                const uint32_t x = __ffs(X) - 1;
+                if (p0 + x < lim) {
+                    const uint32_t below = (1u << x) - 1;
+                    my_cnt = my_cnt - __popc(A & below) + __popc(Bm & below);
+                    my_start = pe;
+                }
+            }
+        }
+    }
     // fix-up rounds until every chunk starts where its predecessor ended; a
     // re-decoded path that meets the pass-0 path (bitmap or checkpoint) takes
     // the rest of its count and its end from pass 0
-    const uint32_t p0_end = my_end, p0_cnt = my_cnt;
     for (;;) {
         uint32_t pe = 0;
         if (c < nch && c > 0) pe = s.end[c - 1];
