@@ -1001,6 +1001,14 @@ constexpr int kStageWords = (kEncRun * kThreads * kMaxLen) / 32 + 8;
 // this symbol, so a lookup is one [register + constant] shared-memory load
 // (a pointer handed through the call costs a base add per lookup).
 extern __shared__ __align__(1024) uint32_t g_enc_smem[];
+// The code table is stored permuted: the entry of symbol s at enc_slot(s) = s
+// with bit 4 flipped when bit 7 is set.  The high planes of weights hold the
+// same exponents under both signs (symbols 52.. and 180.., 128 apart: the
+// same bank), which cost every table lookup a second wavefront; the flip
+// moves the negative half 16 banks away.  enc_slot4 maps the four symbols of
+// a word at once (two instructions per four symbols).
+__device__ __forceinline__ uint32_t enc_slot(uint32_t s) { return s ^ ((s >> 3) & 0x10u); }
+__device__ __forceinline__ uint32_t enc_slot4(uint32_t w) { return w ^ ((w >> 3) & 0x10101010u); }
 // Code table entry of byte `b` (0..3) of word `w`: the table is 1 KiB aligned,
 // so base | (index * 4) is its shared-memory address -- one shift, one LOP3
 // and the load per symbol.
@@ -1076,6 +1084,8 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
                 uint32_t sy[4];
                 piece_symbols(cur, W, (uint32_t)g, sy);
 #pragma unroll
+                for (int i = 0; i < (per + 3) / 4; i++) sy[i] = enc_slot4(sy[i]);
+#pragma unroll
                 for (int i = 0; i < per; i += 2) {
                     const uint32_t e1 = code_at(cb, sy[i >> 2], i & 3);
                     const uint32_t e2 = code_at(cb, sy[(i + 1) >> 2], (i + 1) & 3);
@@ -1144,7 +1154,7 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
                     uint32_t word = sy[0];
                     if (per > 4) word = (i >> 2) == 1 ? sy[1] : word;
                     if (per > 8) { word = (i >> 2) == 2 ? sy[2] : word; word = (i >> 2) == 3 ? sy[3] : word; }
-                    const uint32_t e = g_enc_smem[(word >> (8 * (i & 3))) & 0xFF];
+                    const uint32_t e = g_enc_smem[enc_slot((word >> (8 * (i & 3))) & 0xFF)];
                     put(e >> 16, e & 0xFFFF);
                 }
                 pend += ns - last;
@@ -1154,8 +1164,8 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
 #pragma unroll
             for (int i = 0; i < per; i += 2) {
                 if (!RUN && i < ns) {
-                    const uint32_t e1 = g_enc_smem[(sy[i >> 2] >> (8 * (i & 3))) & 0xFF];
-                    const uint32_t e2 = (i + 1 < ns) ? g_enc_smem[(sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF] : 0u;
+                    const uint32_t e1 = g_enc_smem[enc_slot((sy[i >> 2] >> (8 * (i & 3))) & 0xFF)];
+                    const uint32_t e2 = (i + 1 < ns) ? g_enc_smem[enc_slot((sy[(i + 1) >> 2] >> (8 * ((i + 1) & 3))) & 0xFF)] : 0u;
                     const uint32_t l2 = e2 >> 16;
                     const uint32_t pl = (e1 >> 16) + l2;
                     acc = (acc << pl) | (((e1 & 0xFFFF) << l2) | (e2 & 0xFFFF));
@@ -1457,9 +1467,9 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     if (my_len) {
         uint32_t r = my_rank_w;
         for (int q = 0; q < warp; q++) r += sh_cnt[q][my_len];
-        sh_code[tid] = (my_len << 16) | ((sh_first[my_len] >> (kMaxLen - my_len)) + r);
+        sh_code[enc_slot(tid)] = (my_len << 16) | ((sh_first[my_len] >> (kMaxLen - my_len)) + r);
     } else {
-        sh_code[tid] = 0;
+        sh_code[enc_slot(tid)] = 0;
     }
     const uint64_t gaddr = (uint64_t)(rp + hdr);
     const uint32_t lead = (uint32_t)(gaddr & 3) * 8;
@@ -1469,7 +1479,7 @@ __global__ void __launch_bounds__(kThreads) k_encode(
     if (tid == 0) stg[0] = 0;
     if (tid == 0) sh_run = 256;
     __syncthreads();
-    if (sh_code[tid] == (1u << 16)) sh_run = tid;
+    if (sh_code[enc_slot(tid)] == (1u << 16)) sh_run = tid;
     __syncthreads();
     // the run path pays off only when most symbols are the run symbol
     // (<= 1.5 code bits per symbol on average: XOR deltas, sparse tensors)
