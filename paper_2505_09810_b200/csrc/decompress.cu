@@ -788,8 +788,8 @@ __device__ __forceinline__ void emit_lean(DecSmem& s, const uint32_t* sw, uint32
     BitBuf b;
     bb_init(b, sw, pos + sh);
     uint8_t* d = dst;
-    // head: single symbols until the destination is 4-byte aligned
-    bool act = pos < lim && (reinterpret_cast<uint64_t>(d) & 3);
+    // head: single symbols until the destination is 16-byte aligned
+    bool act = pos < lim && (reinterpret_cast<uint64_t>(d) & 15);
     while (__any_sync(mask, act)) {
         if (act) {
             uint32_t sym;
@@ -797,20 +797,30 @@ __device__ __forceinline__ void emit_lean(DecSmem& s, const uint32_t* sw, uint32
             bb_adv(b, sw, l);
             pos += l;
             *d++ = (uint8_t)sym;
-            act = l && pos < lim && (reinterpret_cast<uint64_t>(d) & 3);
+            act = l && pos < lim && (reinterpret_cast<uint64_t>(d) & 15);
         }
     }
-    uint32_t* w = reinterpret_cast<uint32_t*>(d);
+    // Full words collect in a four-register queue (oldest in q0 when it is
+    // full) and leave as one 16-byte store: a warp's stores go to 32
+    // different lines whatever their width, so 4-byte stores cost four times
+    // the LSU wavefronts and L2 write sectors per byte (the kernel's LSU data
+    // pipe ran at 68%, half of it these stores).
+    uint4* w = reinterpret_cast<uint4*>(d);
     uint32_t acc = 0, nb = 0;   // accumulated bits (0, 8, 16 or 24)
+    uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0, wc = 0;
     auto put = [&](uint32_t packed, uint32_t nbits) {   // packed: up to 3 symbols, nbits = 8 * count
         acc |= packed << nb;
         const uint32_t ovf = __funnelshift_lc(packed, 0u, nb);   // the bytes beyond the word (packed >> (32 - nb))
         nb += nbits;
-        const bool full = nb >= 32;
-        if (full) *w = acc;
-        w += full ? 1 : 0;
-        acc = full ? ovf : acc;
-        nb -= full ? 32u : 0u;
+        if (nb >= 32) {
+            q0 = q1; q1 = q2; q2 = q3; q3 = acc;
+            acc = ovf;
+            nb -= 32;
+            if (++wc == 4) {
+                *w++ = make_uint4(q0, q1, q2, q3);
+                wc = 0;
+            }
+        }
     };
     auto bulk = [&](auto kk) {
         constexpr int KK = decltype(kk)::value;
@@ -851,7 +861,12 @@ __device__ __forceinline__ void emit_lean(DecSmem& s, const uint32_t* sw, uint32
             act = l && pos < lim;
         }
     }
-    uint8_t* tb = reinterpret_cast<uint8_t*>(w);
+    // the queue's wc words (the newest in q3), then the bytes of the open word
+    uint32_t* tw = reinterpret_cast<uint32_t*>(w);
+    if (wc == 3) { tw[0] = q1; tw[1] = q2; tw[2] = q3; }
+    else if (wc == 2) { tw[0] = q2; tw[1] = q3; }
+    else if (wc == 1) tw[0] = q3;
+    uint8_t* tb = reinterpret_cast<uint8_t*>(tw + wc);
     for (uint32_t q = 0; q < nb / 8; q++) tb[q] = (uint8_t)(acc >> (8 * q));
 }
 
