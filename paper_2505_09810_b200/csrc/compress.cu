@@ -1059,7 +1059,64 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
             put(t1, 0u);
             put(z - t1, 0u);
         };
-        if (!RUN && fast) {
+        // W == 2: when every lane of the warp has a full run in one plane, the
+        // warp's 4 KiB of source are read as eight fully coalesced 512-byte
+        // rows, the plane's symbols (slot-mapped) transposed through the idle
+        // staging area, and each lane reads its 64 symbols back as four
+        // 16-byte pieces.  (Each lane loading its own 128-byte run touched 32
+        // lines per load instruction: eight times the LSU wavefronts, and the
+        // kernel's LSU data pipe ran at 78%.)
+        bool warp_t = false;
+        if constexpr (W == 2 && !RUN) {
+            const uint64_t g_0 = __shfl_sync(0xFFFFFFFFu, g, 0);
+            warp_t = __all_sync(0xFFFFFFFFu, fast && q1 - q0 == (uint64_t)kEncRun && g == g_0);
+        }
+        if (warp_t) {
+            // staging word 0 carries the previous round's open word: the buffer starts 16 bytes in
+            uint8_t* tb = reinterpret_cast<uint8_t*>(stg) + 16 + warp * 2048;
+            const uint64_t wbase = (((r0 + (uint64_t)(warp * 32) * kEncRun) - g * wd.n) << lw);   // source byte of the warp's first run
+#pragma unroll
+            for (int hq = 0; hq < 2; hq++) {
+                uint4 a[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, wbase + 512ull * (4 * hq + q) + 16ull * lane);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    uint32_t sy[4];
+                    piece_symbols(a[q], W, (uint32_t)g, sy);
+                    // run and piece of source bytes 512 (4 hq + q) + 16 lane; 16-byte unit u of run r sits at unit u ^ ((r >> 1) & 3)
+                    const uint32_t r = 4 * (4 * hq + q) + (lane >> 3), pc = lane & 7;
+                    const uint32_t off = r * 64 + (((pc >> 1) ^ ((r >> 1) & 3)) << 4) + ((pc & 1) << 3);
+                    *reinterpret_cast<uint2*>(tb + off) = make_uint2(enc_slot4(sy[0]), enc_slot4(sy[1]));
+                }
+            }
+            __syncwarp();
+            const uint32_t pw0 = (uint32_t)__cvta_generic_to_shared(priv);
+            uint32_t pw = pw0;   // running shared-memory address in the private slot
+            const uint32_t cb = (uint32_t)__cvta_generic_to_shared(g_enc_smem);
+            const uint32_t sw = (lane >> 1) & 3;
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const uint4 c = *reinterpret_cast<const uint4*>(tb + lane * 64 + ((u ^ sw) << 4));
+                const uint32_t sy[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    const uint32_t e1 = code_at(cb, sy[i >> 2], i & 3);
+                    const uint32_t e2 = code_at(cb, sy[(i + 1) >> 2], (i + 1) & 3);
+                    const uint32_t l2 = e2 >> 16;
+                    const uint32_t pl = (e1 >> 16) + l2;
+                    acc = (acc << pl) | (((e1 & 0xFFFF) << l2) | (e2 & 0xFFFF));
+                    n += pl;
+                    if (n >= 32) {
+                        n -= 32;
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(pw), "r"((uint32_t)(acc >> n)) : "memory");
+                        pw += 4;
+                    }
+                }
+            }
+            wi = (pw - pw0) >> 2;
+            __syncwarp();   // (the staging area is rewritten after the CTA barrier below)
+        } else if (!RUN && fast) {
             // lean run: whole pieces of one plane, 16-byte loads one piece
             // ahead, every symbol pair unconditional, the private slot
             // addressed by a running pointer
