@@ -1788,23 +1788,24 @@ __global__ void k_pairs(const DecSeg* __restrict__ segs, const uint32_t* __restr
 __device__ __forceinline__ uint4 plane16(const uint8_t* p, uint32_t mode, uint32_t rle, uint32_t e, uint32_t B) {
     if (mode == MODE_RLE) return make_uint4(rle, rle, rle, rle);
     if (mode == MODE_HUFFMAN) return __ldcg(reinterpret_cast<const uint4*>(p + e));   // ring slot (L2; never through L1)
-    const uint64_t a = reinterpret_cast<uint64_t>(p) + e;                      // stored payload, any alignment
-    if ((a & 15) == 0) return __ldcs(reinterpret_cast<const uint4*>(a));
-    const uint32_t sh = (uint32_t)(a & 3) * 8;
-    const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~3ull);
-    const uint32_t x0 = __ldcs(w), x1 = __ldcs(w + 1), x2 = __ldcs(w + 2), x3 = __ldcs(w + 3);
-    uint32_t x4 = 0;
-    if (sh) {
-        if (e + 20 <= B) {
-            x4 = __ldcs(w + 4);
-        } else {   // the payload ends inside word 4: no read past the record
-            const uint8_t* b4 = reinterpret_cast<const uint8_t*>(w + 4);
-            const uint32_t have = (uint32_t)(reinterpret_cast<uint64_t>(p) + B - reinterpret_cast<uint64_t>(b4));
-            for (uint32_t q = 0; q < 4 && q < have; q++) x4 |= (uint32_t)b4[q] << (8 * q);
-        }
+    // stored payload, any alignment: the two aligned 16-byte chunks the piece
+    // spans (two requests of 32 sectors; five 4-byte loads took five requests
+    // of 16 sectors each).  The last piece's second chunk may reach up to 15
+    // bytes past the payload, inside the same aligned 16 bytes as payload
+    // bytes (as the bulk copy's aligned cover does).
+    const uint64_t a = reinterpret_cast<uint64_t>(p) + e;
+    const uint32_t lb = (uint32_t)(a & 15);   // (the same for every piece of a pair)
+    const uint4* A = reinterpret_cast<const uint4*>(a & ~15ull);
+    const uint4 P = __ldcs(A);
+    if (lb == 0) return P;
+    const uint4 N = __ldcs(A + 1);
+    const uint32_t r = 8 * (lb & 3);
+    switch (lb >> 2) {
+    case 0: return make_uint4(__funnelshift_r(P.x, P.y, r), __funnelshift_r(P.y, P.z, r), __funnelshift_r(P.z, P.w, r), __funnelshift_r(P.w, N.x, r));
+    case 1: return make_uint4(__funnelshift_r(P.y, P.z, r), __funnelshift_r(P.z, P.w, r), __funnelshift_r(P.w, N.x, r), __funnelshift_r(N.x, N.y, r));
+    case 2: return make_uint4(__funnelshift_r(P.z, P.w, r), __funnelshift_r(P.w, N.x, r), __funnelshift_r(N.x, N.y, r), __funnelshift_r(N.y, N.z, r));
+    default: return make_uint4(__funnelshift_r(P.w, N.x, r), __funnelshift_r(N.x, N.y, r), __funnelshift_r(N.y, N.z, r), __funnelshift_r(N.z, N.w, r));
     }
-    return make_uint4(__funnelshift_r(x0, x1, sh), __funnelshift_r(x1, x2, sh), __funnelshift_r(x2, x3, sh),
-                      __funnelshift_r(x3, x4, sh));
 }
 
 
