@@ -1067,7 +1067,7 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
         // lines per load instruction: eight times the LSU wavefronts, and the
         // kernel's LSU data pipe ran at 78%.)
         bool warp_t = false;
-        if constexpr (W == 2 && !RUN) {
+        if constexpr (W == 2) {
             const uint64_t g_0 = __shfl_sync(0xFFFFFFFFu, g, 0);
             warp_t = __all_sync(0xFFFFFFFFu, fast && q1 - q0 == (uint64_t)kEncRun && g == g_0);
         }
@@ -1087,7 +1087,8 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
                     // run and piece of source bytes 512 (4 hq + q) + 16 lane; 16-byte unit u of run r sits at unit u ^ ((r >> 1) & 3)
                     const uint32_t r = 4 * (4 * hq + q) + (lane >> 3), pc = lane & 7;
                     const uint32_t off = r * 64 + (((pc >> 1) ^ ((r >> 1) & 3)) << 4) + ((pc & 1) << 3);
-                    *reinterpret_cast<uint2*>(tb + off) = make_uint2(enc_slot4(sy[0]), enc_slot4(sy[1]));
+                    // (run blocks compare the raw symbols with the run symbol and map the slot per lookup)
+                    *reinterpret_cast<uint2*>(tb + off) = RUN ? make_uint2(sy[0], sy[1]) : make_uint2(enc_slot4(sy[0]), enc_slot4(sy[1]));
                 }
             }
             __syncwarp();
@@ -1099,6 +1100,31 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
             for (int u = 0; u < 4; u++) {
                 const uint4 c = *reinterpret_cast<const uint4*>(tb + lane * 64 + ((u ^ sw) << 4));
                 const uint32_t sy[4] = {c.x, c.y, c.z, c.w};
+                if (RUN) {
+                    // bit i: symbol i of the 16 is not the run symbol
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t r = __vcmpne4(sy[k], rep4) & 0x80808080u;
+                        m |= ((r * 0x00204081u) >> 28) << (4 * k);
+                    }
+                    uint32_t last = 0;
+                    while (m) {
+                        const uint32_t i = __ffs(m) - 1;
+                        m &= m - 1;
+                        zeros(pend + i - last);
+                        pend = 0;
+                        last = i + 1;
+                        uint32_t word = sy[0];
+                        word = (i >> 2) == 1 ? sy[1] : word;
+                        word = (i >> 2) == 2 ? sy[2] : word;
+                        word = (i >> 2) == 3 ? sy[3] : word;
+                        const uint32_t e = g_enc_smem[enc_slot((word >> (8 * (i & 3))) & 0xFF)];
+                        put(e >> 16, e & 0xFFFF);
+                    }
+                    pend += 16 - last;
+                    continue;
+                }
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
                     const uint32_t e1 = code_at(cb, sy[i >> 2], i & 3);
@@ -1114,7 +1140,7 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
                     }
                 }
             }
-            wi = (pw - pw0) >> 2;
+            if (!RUN) wi = (pw - pw0) >> 2;
             __syncwarp();   // (the staging area is rewritten after the CTA barrier below)
         } else if (!RUN && fast) {
             // lean run: whole pieces of one plane, 16-byte loads one piece
