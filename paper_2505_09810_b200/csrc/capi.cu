@@ -164,6 +164,8 @@ void build_crc_tables(CrcTables& t) {
     }
     shift_table(512, t.sh512);
     shift_table(kHistTileGap, t.shtile);
+    shift_table(1024, t.sh1024);
+    shift_table(kHistTileGap32, t.shtile32);
 }
 
 int ensure_ctx(lmcg_ctx* ctx) {

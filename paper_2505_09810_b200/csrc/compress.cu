@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kCrcThreads, 2) k_crc(const WinDesc* __restric
 // shifts at the end; *last = the warp's last tile.  (One 64-byte run per
 // lane and tile instead -- one shift per tile -- measured slower: the strided
 // loads cost more than the shifts.)
-template <int W, bool CRC>
+template <int W, bool CRC, bool P32 = false>
 __device__ __forceinline__ uint32_t hist_tiles(const WinDesc& wd, uint64_t p0, uint64_t p1, uint32_t* hist, int lane, int warp,
                                                const Crc4x8Lane& cl, const uint32_t* s512, const uint32_t* sgap,
                                                uint32_t* last) {
@@ -188,11 +188,34 @@ __device__ __forceinline__ uint32_t hist_tiles(const WinDesc& wd, uint64_t p0, u
         const uint64_t g = one ? g0 : plane_of(tp, wd.n, W);
         const bool fast = wd.vec && (te - tp == T) && (one || te <= (g + 1) * wd.n);
         if (fast) {
-            const uint64_t base = ((tp - g * wd.n) << lw) + 16ull * lane;
             uint4 a[4];
+            if (P32) {
+                // two 1 KiB rows, lane l holds bytes 32 l .. 32 l + 31 of each (one
+                // 256-bit load): one chain per row, one shift per 32 bytes
+                const uint64_t base = ((tp - g * wd.n) << lw) + 32ull * lane;
+                ldg32x(wd.src, wd.prev, base, a[0], a[1]);
+                ldg32x(wd.src, wd.prev, base + 1024, a[2], a[3]);
+            } else {
+                const uint64_t base = ((tp - g * wd.n) << lw) + 16ull * lane;
 #pragma unroll
-            for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, base + 512ull * q);
-            if (CRC) {
+                for (int q = 0; q < 4; q++) a[q] = ldg16x(wd.src, wd.prev, base + 512ull * q);
+            }
+            if (CRC && P32) {
+#pragma unroll
+                for (int q = 0; q < 2; q++) ch[q] = shift(sgap, ch[q]);   // (no-op on the warp's first tile: ch == 0)
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+#pragma unroll
+                    for (int q = 0; q < 2; q++) ch[q] = cl.word(ch[q], a[2 * q + h].x);
+#pragma unroll
+                    for (int q = 0; q < 2; q++) ch[q] = cl.word(ch[q], a[2 * q + h].y);
+#pragma unroll
+                    for (int q = 0; q < 2; q++) ch[q] = cl.word(ch[q], a[2 * q + h].z);
+#pragma unroll
+                    for (int q = 0; q < 2; q++) ch[q] = cl.word(ch[q], a[2 * q + h].w);
+                }
+                *last = (uint32_t)t;
+            } else if (CRC) {
                 // four chains (one per row q): independent lookups in flight
 #pragma unroll
                 for (int q = 0; q < 4; q++) ch[q] = shift(sgap, ch[q]);   // (no-op on the warp's first tile: ch == 0)
@@ -220,7 +243,8 @@ __device__ __forceinline__ uint32_t hist_tiles(const WinDesc& wd, uint64_t p0, u
             for (uint64_t p = a; p < bnd; p++) atomicAdd(&hist[gather_byte(wd, p) << 5], 1u);
         }
     }
-    // row q + 1's piece lies 512 bytes after row q's
+    // row q + 1's piece lies 512 bytes after row q's (32-byte pieces: two rows, 1024 bytes; s512 is then sh1024)
+    if (CRC && P32) return shift(s512, ch[0]) ^ ch[1];
     return CRC ? shift(s512, shift(s512, shift(s512, ch[0]) ^ ch[1]) ^ ch[2]) ^ ch[3] : 0u;
 }
 
@@ -264,28 +288,33 @@ __global__ void __launch_bounds__(kThreads, 3) k_hist(
     // range (every source byte of it passes through its tiles); part runs
     // (lmcg_compress_part) take their CRC from k_crc
     const bool crc = wd.hcrc && p1 <= wd.n && crcpart != nullptr;
+    // 16-bit elements at 32-byte aligned addresses: 32-byte lane pieces (256-bit loads, half the chain shifts)
+    const bool p32 = crc && wd.w == 2 && (reinterpret_cast<uint64_t>(wd.src) & 31) == 0 &&
+                     (!wd.prev || (reinterpret_cast<uint64_t>(wd.prev) & 31) == 0);
     Crc4x8Lane cl;
     uint32_t ch = 0, last = 0;
     if (crc) {
         for (int i = tid; i < kHistCrcWords / 4; i += kThreads)
             reinterpret_cast<uint4*>(crc_tab)[i] = i < 256 * 32 / 4 ? __ldg(reinterpret_cast<const uint4*>(ct->rep4x8) + i)
-                                                                   : __ldg(reinterpret_cast<const uint4*>(&ct->sh512[0][0]) + (i - 256 * 32 / 4));
+                                                                   : __ldg(reinterpret_cast<const uint4*>(p32 ? &ct->sh1024[0][0] : &ct->sh512[0][0]) + (i - 256 * 32 / 4));
         if (tid == 0) sh_crc = 0;
         __syncthreads();
         cl.init(crc_tab, lane);
         const uint32_t* s512 = crc_tab + 256 * 32;
         const uint32_t* sgap = s512 + 1024;
         if (wd.w == 1) ch = hist_tiles<1, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
-        else if (wd.w == 2) ch = hist_tiles<2, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
+        else if (wd.w == 2) ch = p32 ? hist_tiles<2, true, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last)
+                                     : hist_tiles<2, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
         else ch = hist_tiles<4, true>(wd, p0, p1, bins + lane, lane, warp, cl, s512, sgap, &last);
-        // lane l's chain ends 1552 + 16 (l + 1) bytes into the warp's last
-        // tile: a Horner tree over the lanes (fixed shifts of 16 << k bytes),
-        // then lane 31 shifts the warp's value to the end of the block
+        // lane l's chain ends 1536 + 16 (l + 1) (32-byte pieces: 1024 + 32 (l +
+        // 1)) bytes into the warp's last tile: a Horner tree over the lanes
+        // (fixed shifts of 16 << k or 32 << k bytes), then lane 31 shifts the
+        // warp's value to the end of the block
         const uint32_t Lb = (uint32_t)((p1 - p0) * wd.w);
         uint32_t x = ch;
 #pragma unroll
         for (int q = 0; q < 5; q++) {
-            const uint32_t y = crc_shift_tab(&ct->shift[q][0][0], __shfl_xor_sync(0xFFFFFFFFu, x, 1 << q));
+            const uint32_t y = crc_shift_tab(&ct->shift[q + (p32 ? 1 : 0)][0][0], __shfl_xor_sync(0xFFFFFFFFu, x, 1 << q));
             if (lane & (1 << q)) x ^= y;
         }
         if (lane == 31) {

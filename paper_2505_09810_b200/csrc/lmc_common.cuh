@@ -91,8 +91,13 @@ struct CrcTables {
     // of a piece to the piece of the same row in the warp's next tile)
     uint32_t sh512[4][256];
     uint32_t shtile[4][256];
+    // the same for 32-byte lane pieces (sources aligned to 32 bytes, 256-bit
+    // loads): two 1 KiB rows per tile, 1024 bytes apart, gap kHistTileGap32
+    uint32_t sh1024[4][256];
+    uint32_t shtile32[4][256];
 };
 constexpr uint32_t kHistTileGap = kWarps * kTileBytes - 16;
+constexpr uint32_t kHistTileGap32 = kWarps * kTileBytes - 32;
 
 // Per-lane view of rep4x8 for one word: tab[s] = table base of lookup s
 // (column 8 t + c), sel[s] = byte-perm selector of the byte that pairs with
@@ -260,6 +265,22 @@ __device__ __forceinline__ uint4 ldg16x(const uint8_t* src, const uint8_t* prev,
         a.x ^= b.x; a.y ^= b.y; a.z ^= b.z; a.w ^= b.w;
     }
     return a;
+}
+
+// 32 contiguous source bytes (32-byte aligned) XOR the previous step: one
+// 256-bit load per operand (sm_100: LDG.E.ENL2.256)
+__device__ __forceinline__ void ldg32x(const uint8_t* src, const uint8_t* prev, uint64_t off, uint4& a, uint4& b) {
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+        : "l"(src + off));
+    if (prev) {
+        uint4 c, d;
+        asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(c.x), "=r"(c.y), "=r"(c.z), "=r"(c.w), "=r"(d.x), "=r"(d.y), "=r"(d.z), "=r"(d.w)
+            : "l"(prev + off));
+        a.x ^= c.x; a.y ^= c.y; a.z ^= c.z; a.w ^= c.w;
+        b.x ^= d.x; b.y ^= d.y; b.z ^= d.z; b.w ^= d.w;
+    }
 }
 
 // ------------------------------------------------------------- gathers
