@@ -57,3 +57,29 @@ def test_header_crc_delta_and_unaligned_views(codec):
     view = base[8: 8 + (1 << 20)]
     b = codec.compress([view], element_types=[1])
     assert b.to_bytes()[0] == O.compress(host_bytes(view), 1, threads=8)
+
+
+@pytest.mark.parametrize("off", [16, 32, 48])
+def test_header_crc_views_at_16_byte_offsets(codec, off):
+    # 16-bit elements on the vector path at addresses that are / are not
+    # 32-byte aligned: k_hist folds the CRC with 32-byte (256-bit loads) or
+    # 16-byte lane pieces; plain and delta (the previous step at the same offset)
+    g = torch.Generator(device="cuda").manual_seed(off)
+    n = 1 << 20
+    base = torch.zeros(2 * n + 64, dtype=torch.uint8, device="cuda")
+    pbase = torch.zeros(2 * n + 64, dtype=torch.uint8, device="cuda")
+    w = (torch.randn(n, generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+    w2 = (w.float() + torch.randn(n, generator=g, device="cuda") * 1e-3 * w.float().abs()).to(torch.bfloat16)
+    pbase[off: off + 2 * n] = w.view(torch.uint8)
+    base[off: off + 2 * n] = w2.view(torch.uint8)
+    cur = base[off: off + 2 * n].view(torch.bfloat16)
+    prev = pbase[off: off + 2 * n].view(torch.bfloat16)
+    assert cur.data_ptr() % 32 == off % 32
+    b = codec.compress([cur])
+    assert b.to_bytes()[0] == O.compress(host_bytes(cur), 1, threads=8)
+    b = codec.compress([cur], prev=[prev])
+    x = host_bytes(cur.view(torch.uint8) ^ prev.view(torch.uint8))
+    assert b.to_bytes()[0] == O.compress(x, 1, delta=True, threads=8)
+    r = codec.decompress(b)
+    assert r.status == [0]
+    assert torch.equal(r.payload(0), cur.view(torch.uint8) ^ prev.view(torch.uint8))
