@@ -370,7 +370,7 @@ __device__ __forceinline__ uint32_t step1(const DecSmem& s, uint32_t win, uint32
 // three symbols.
 template <bool EMIT, bool STAGED, bool RUN>
 __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint32_t pos, uint32_t lim, uint32_t p0, int bm,
-                                uint32_t& count, uint8_t* dst, uint32_t* hit) {
+                                uint32_t& count, uint8_t* dst, uint32_t* hit, bool sparse = false) {
     // Lanes decode different chunks with different trip counts: every loop is
     // driven by a warp vote so the warp re-converges each iteration (instead of
     // drifting into independently scheduled, divergent lanes).
@@ -523,6 +523,36 @@ __device__ __forceinline__ uint32_t decode_span(DecSmem& s, const Src& src, uint
         }
     }
     uint8_t* d = dst;
+    if (EMIT && RUN && sparse) {
+        // The plane is already filled with the run symbol (huff_passes): walk
+        // the chunk, every leading zero bit of the window one run symbol (up to
+        // 32 per step, nothing to store), and store only the other symbols.
+        bool act = pos < lim;
+        while (__any_sync(mask, act)) {
+            if (act) {
+                const uint32_t wv = win();
+                const uint32_t z = min((uint32_t)__clz(wv), lim - pos);
+                if (z) {
+                    adv(z);
+                    d += z;
+                    c += z;
+                } else {
+                    uint32_t sym;
+                    const uint32_t l = step1(s, wv, sym);
+                    if (!l) {
+                        bad = true;
+                    } else {
+                        adv(l);
+                        *d++ = (uint8_t)sym;
+                        c++;
+                    }
+                }
+                act = !bad && pos < lim;
+            }
+        }
+        count = c;
+        return bad ? ~0u : pos;
+    }
     if (EMIT) {
         // head: single symbols until the destination is 8-byte aligned
         bool act = pos < lim && (reinterpret_cast<uint64_t>(d) & 7);
@@ -1008,9 +1038,27 @@ __device__ __forceinline__ bool huff_passes(DecSmem& s, const Src& src, uint32_t
     if (STAGED && !RUN) {
         const bool has = c < nch && my_cnt;
         emit_lean<3>(s, src.sw, src.sh, has ? my_start : 0u, has ? lim : 0u, dst + (has ? pre + incl - v : 0u));
-    } else if (c < nch && my_cnt) {
-        uint32_t cc;
-        decode_span<true, STAGED, RUN>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr);
+    } else {
+        // Records that are nearly all run symbol (<= 1.125 bits per symbol: the
+        // high planes of XOR deltas): the CTA fills the plane with the run
+        // symbol (coalesced 16-byte stores) and the emit pass stores only the
+        // other symbols, taking up to 32 run symbols per step instead of the 8
+        // that fill one store.
+        const bool sparse = RUN && bits <= len + (len >> 3);
+        if (sparse) {
+            const uint32_t rs = s.csym[s.first_idx[1]] * 0x01010101u;
+            const uint32_t head = min(len, (uint32_t)((16 - (reinterpret_cast<uint64_t>(dst) & 15)) & 15));
+            const uint32_t n16 = (len - head) >> 4;
+            if ((uint32_t)tid < head) dst[tid] = (uint8_t)rs;
+            uint4* d16 = reinterpret_cast<uint4*>(dst + head);
+            for (uint32_t i = tid; i < n16; i += kThreads) d16[i] = make_uint4(rs, rs, rs, rs);
+            for (uint32_t i = head + (n16 << 4) + tid; i < len; i += kThreads) dst[i] = (uint8_t)rs;
+            __syncthreads();
+        }
+        if (c < nch && my_cnt) {
+            uint32_t cc;
+            decode_span<true, STAGED, RUN>(s, src, my_start, lim, 0, 0, cc, dst + (pre + incl - v), nullptr, sparse);
+        }
     }
     __syncthreads();
     DBG_TADD(20, t_emit);
