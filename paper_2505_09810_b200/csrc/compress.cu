@@ -1152,10 +1152,9 @@ __device__ void encode_runs(const WinDesc& wd, uint64_t p0, uint64_t p1,
                         put(e >> 16, e & 0xFFFF);
                     }
                     pend += 16 - last;
-                    continue;
                 }
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) {
+                for (int i = 0; !RUN && i < 16; i += 2) {
                     const uint32_t e1 = code_at(cb, sy[i >> 2], i & 3);
                     const uint32_t e2 = code_at(cb, sy[(i + 1) >> 2], (i + 1) & 3);
                     const uint32_t l2 = e2 >> 16;
