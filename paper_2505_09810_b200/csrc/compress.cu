@@ -1,12 +1,13 @@
 // compress.cu -- B200 kernels of the LMC compress path.
 //
 //   k_slotmap    slot -> window map (planes interleaved per window)
-//   k_crc        raw CRC-32 of every 32 KiB chunk of the payload (XOR delta
-//                applied), on the side stream next to k_hist / k_codebook
-//                (stream.py:329); k_frame combines the chunks
+//   k_crc        raw CRC-32 of every 32 KiB chunk of the windows k_hist does
+//                not fold (XOR delta applied), on the side stream next to
+//                k_hist / k_codebook (stream.py:329); k_frame combines the parts
 //   k_hist       K1: fused XOR delta + byte-group gather + per-block 256-bin
 //                histogram (entropy.py:53-59, bytegroup.py:39-50,
-//                delta.py:18-26)
+//                delta.py:18-26); the plane-0 block of a whole-block window
+//                also folds the raw CRC of its element range
 //   k_codebook   K2: per-block mode + canonical length-limited Huffman lengths
 //                (stream.py:161-177, huffman.py:79-137), one warp per block
 //   k_pkgmerge   K2b: package-merge for blocks whose Huffman tree exceeds 15

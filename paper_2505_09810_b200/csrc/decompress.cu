@@ -810,7 +810,8 @@ __device__ __forceinline__ uint32_t pass0_lean(DecSmem& s, const uint32_t* sw, u
 
 // Emit pass of one chunk: the codewords starting in [pos, lim) (validated by
 // pass 0 and the fix-up rounds) as symbols at dst.  Up to three symbols per
-// lookup are packed into a 32-bit accumulator that leaves with 4-byte stores.
+// lookup are packed into a 32-bit accumulator; its full words queue in four
+// registers and leave as 16-byte stores.
 template <int K>
 __device__ __forceinline__ void emit_lean(DecSmem& s, const uint32_t* sw, uint32_t sh, uint32_t pos, uint32_t lim,
                                           uint8_t* dst) {
