@@ -1016,7 +1016,7 @@ static int decompress_launch(lmcg_ctx* ctx, int n, uint64_t nwin, uint64_t nseg,
     }
     if (nchunk) {
         PROF(k_assign);
-        k_assign<<<(unsigned)nchunk, kThreads, 0, st>>>(d_seg, d_c2s, nchunk, d_cand, d_ccnt, d_cpre, d_sfail, d_rpos, d_rnext);
+        k_assign<<<(unsigned)((nchunk + kWarps - 1) / kWarps), kThreads, 0, st>>>(d_seg, d_c2s, nchunk, d_cand, d_ccnt, d_cpre, d_sfail, d_rpos, d_rnext);
     }
     if (nrec) {
         { PROF(k_verify); k_verify<<<(unsigned)((nrec + 255) / 256), 256, 0, st>>>(d_seg, d_r2s, nrec, d_scnt, d_sfail, d_rpos, d_rnext); }

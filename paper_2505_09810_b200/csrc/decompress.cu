@@ -1653,31 +1653,28 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
                                                    const uint32_t* __restrict__ ccnt, const uint32_t* __restrict__ cpre,
                                                    uint32_t* __restrict__ seg_fail, uint64_t* __restrict__ rec_pos,
                                                    uint64_t* __restrict__ rec_next) {
-    __shared__ uint32_t spre[kWarps + 1];
+    // one warp per chunk (a CTA per chunk spent its time being launched: a
+    // chunk holds one to three records): lane w < kWarps holds span w's count
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t t = blockIdx.x;
+    const uint64_t t = (uint64_t)blockIdx.x * kWarps + warp;
     if (t >= nchunk_total) return;
     const uint32_t lo = chunk2seg[t];
     if (lo == ~0u) return;
     const DecSeg sg = segs[lo];
-    if (tid == 0) {
-        uint32_t acc = cpre[t];
-        bool dense = false;
-        for (int w = 0; w < kWarps; w++) {
-            spre[w] = acc;
-            const uint32_t c = ccnt[t * kWarps + w];
-            if (c == kDense) dense = true; else acc += c;
-        }
-        spre[kWarps] = dense ? 1u : 0u;
+    const uint32_t cw = lane < kWarps ? ccnt[t * kWarps + lane] : 0u;
+    if (__any_sync(0xFFFFFFFFu, cw == kDense)) return;  // k_number failed the segment
+    uint32_t incl = cw;
+#pragma unroll
+    for (int o = 1; o < kWarps; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += y;
     }
-    __syncthreads();
-    if (spre[kWarps]) return;  // k_number failed the segment
-    const uint64_t span = t * kWarps + warp;
-    const uint32_t c = ccnt[span];
+    const uint32_t base = cpre[t];
     const uint32_t R = sg.nrec, B = sg.block;
     const uint32_t Ltail = R ? (uint32_t)(sg.orig - (uint64_t)(R - 1) * B) : 0;
+    uint32_t pre = 0;   // record index of the current span's first candidate
     auto assign = [&](uint64_t pos, uint32_t k) {
-        uint32_t r = spre[warp] + k;
+        uint32_t r = pre + k;
         if (r >= R) { atomicOr(&seg_fail[lo], 1u); DBG_ADD(13, 1); return; }
         for (int part = 0; part < 2; part++) {
             uint32_t mode = 0, l = 0;
@@ -1691,19 +1688,24 @@ __global__ void __launch_bounds__(kThreads) k_assign(const DecSeg* __restrict__ 
             r = R - 1;
         }
     };
-    if (c <= kSpanCap) {
-        for (uint32_t k = lane; k < c; k += 32) assign(cand[span * kSpanCap + k], k);
-    } else {
-        // dense span (e.g. runs of 6-byte RLE records): enumerate it again
-        constexpr uint64_t kWarpSpan = kChunk / kWarps;
-        const uint64_t c0 = (t - sg.chunk0) * kChunk, c1 = min(c0 + kChunk, sg.comp);
-        const uint64_t pa = c0 + warp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
-        uint32_t n = 0;
-        if (pa == 0 && pa < pe) {
-            if (lane == 0) assign(0, 0);
-            n = 1;
+    for (int sp = 0; sp < kWarps; sp++) {
+        const uint32_t c = __shfl_sync(0xFFFFFFFFu, cw, sp);
+        pre = base + __shfl_sync(0xFFFFFFFFu, incl - cw, sp);
+        const uint64_t span = t * kWarps + sp;
+        if (c <= kSpanCap) {
+            for (uint32_t k = lane; k < c; k += 32) assign(cand[span * kSpanCap + k], k);
+        } else {
+            // dense span (e.g. runs of 6-byte RLE records): enumerate it again
+            constexpr uint64_t kWarpSpan = kChunk / kWarps;
+            const uint64_t c0 = (t - sg.chunk0) * kChunk, c1 = min(c0 + kChunk, sg.comp);
+            const uint64_t pa = c0 + sp * kWarpSpan, pe = min(pa + kWarpSpan, c1);
+            uint32_t n = 0;
+            if (pa == 0 && pa < pe) {
+                if (lane == 0) assign(0, 0);
+                n = 1;
+            }
+            if (pa < pe) warp_scan(sg, pa, pe, n, lane, assign);
         }
-        if (pa < pe) warp_scan(sg, pa, pe, n, lane, assign);
     }
 }
 
