@@ -2285,9 +2285,9 @@ __global__ void __launch_bounds__(kThreads) k_fallback(const DecSeg* __restrict_
 // the tile end and XOR-reduced.  A short last tile is treated as left-padded
 // with zero bytes, which leave a raw CRC unchanged.  lmcg_decompress_apply
 // XORs the previous step into the stores (the CRC stays the payload's).
-constexpr int kUngThreads = 1024;   // one CTA per SM shares the 128 KiB of replicated slicing tables
+constexpr int kUngThreads = 1024;   // one CTA per SM shares the 32 KiB of conflict-free slicing tables (rep4x8)
 constexpr int kUngWarps = kUngThreads / 32;
-constexpr size_t kUngSmem = (kRep4Words + 1024) * sizeof(uint32_t);
+constexpr size_t kUngSmem = (kCrcRepWords + 1024) * sizeof(uint32_t);   // rep4x8 | 992-byte shift
 
 __global__ void __launch_bounds__(kUngThreads, 1) k_ungroup(const DecWin* __restrict__ wins, const uint32_t* __restrict__ tile2win,
                                                     uint64_t ntile_total, const uint8_t* __restrict__ scratch,
@@ -2296,11 +2296,13 @@ __global__ void __launch_bounds__(kUngThreads, 1) k_ungroup(const DecWin* __rest
                                                     const uint32_t* __restrict__ status, const uint32_t* __restrict__ seg_fail) {
     extern __shared__ uint32_t ung_tab[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    load_rep4(ung_tab, ct);
-    uint32_t* st = ung_tab + kRep4Words;
+    for (int i = tid; i < kCrcRepWords / 4; i += kUngThreads)
+        reinterpret_cast<uint4*>(ung_tab)[i] = __ldg(reinterpret_cast<const uint4*>(ct->rep4x8) + i);
+    uint32_t* st = ung_tab + kCrcRepWords;
     for (int i = tid; i < 1024; i += kUngThreads) st[i] = sh992[i];
     __syncthreads();
-    const uint32_t* tl = ung_tab + lane;
+    Crc4x8Lane cl;
+    cl.init(ung_tab, lane);
     auto shift992 = [&](uint32_t x) {
         return st[x & 0xFF] ^ st[256 + ((x >> 8) & 0xFF)] ^ st[512 + ((x >> 16) & 0xFF)] ^ st[768 + (x >> 24)];
     };
@@ -2404,8 +2406,8 @@ __global__ void __launch_bounds__(kUngThreads, 1) k_ungroup(const DecWin* __rest
             cb = shift992(cb);
 #pragma unroll
             for (int q = 0; q < 8; q++) {
-                ca = crc4_rep(tl, ca, va[q]);
-                cb = crc4_rep(tl, cb, vb[q]);
+                ca = cl.word(ca, va[q]);
+                cb = cl.word(cb, vb[q]);
             }
         }
         // chain a ends 16 rows (16 KiB) before chain b; lane l's value ends
